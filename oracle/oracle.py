@@ -1,0 +1,269 @@
+"""CPU oracle binding (TEST INFRASTRUCTURE ONLY).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this module.  The product package
+``paper_1302_7014_b200`` never imports it, and this module imports nothing from
+the product package.
+
+Thin ctypes marshalling over ``peel_oracle.c`` (plain single-threaded C, built
+with gcc); every function cites the paper passage it follows in that file.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "peel_oracle.c")
+_LIB = os.path.join(_HERE, "_build", "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain -O2, no vectorisation pragmas)."""
+    os.makedirs(os.path.dirname(_LIB), exist_ok=True)
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            L = ctypes.CDLL(build())
+            u32, u64, i32, p = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
+            L.ora_philox4x32_10.argtypes = [p, p, p]
+            L.ora_gen_edge.argtypes = [u64, u64, u32, u64, p]
+            L.ora_gen_edge.restype = i32
+            L.ora_gen_hypergraph.argtypes = [u64, u64, u64, u32, p]
+            L.ora_gen_hypergraph.restype = i32
+            L.ora_mix64.argtypes = [u64]
+            L.ora_mix64.restype = u64
+            L.ora_gen_keys.argtypes = [u64, u64, p]
+            L.ora_seed_h.argtypes = [u64]
+            L.ora_seed_h.restype = u64
+            L.ora_seed_c.argtypes = [u64]
+            L.ora_seed_c.restype = u64
+            L.ora_checksum.argtypes = [u64, u64]
+            L.ora_checksum.restype = u32
+            L.ora_cells_of.argtypes = [u64, u64, u32, u64, p]
+            L.ora_cells_of.restype = i32
+            L.ora_sync_peel.argtypes = [p, u64, u64, u32, u32, p, p, p, p, u32, p]
+            L.ora_sync_peel.restype = i32
+            L.ora_queue_peel.argtypes = [p, u64, u64, u32, u32, p]
+            L.ora_queue_peel.restype = i32
+            L.ora_iblt_new.argtypes = [u64, u32, u64]
+            L.ora_iblt_new.restype = p
+            L.ora_iblt_free.argtypes = [p]
+            L.ora_iblt_seed_h.argtypes = [p]
+            L.ora_iblt_seed_h.restype = u64
+            L.ora_iblt_seed_c.argtypes = [p]
+            L.ora_iblt_seed_c.restype = u64
+            L.ora_iblt_insert.argtypes = [p, p, u64]
+            L.ora_iblt_insert.restype = i32
+            L.ora_iblt_delete.argtypes = [p, p, u64]
+            L.ora_iblt_delete.restype = i32
+            L.ora_iblt_dump.argtypes = [p, p, p, p]
+            L.ora_iblt_peel.argtypes = [p, p, u64, p, p, p, u32, p]
+            L.ora_iblt_peel.restype = i32
+            L.ora_iblt_serial_recover.argtypes = [p, p, u64, p, p]
+            L.ora_iblt_serial_recover.restype = i32
+            L.ora_iblt_to_hypergraph.argtypes = [p, p, u64, p]
+            _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+# ---------------------------------------------------------------------------
+# generator (restated in DESIGN.md §3)
+# ---------------------------------------------------------------------------
+def philox4x32_10(ctr, key) -> tuple:
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().ora_philox4x32_10(_ptr(c), _ptr(k), _ptr(out))
+    return tuple(int(x) for x in out)
+
+
+def gen_edge(seed: int, n: int, r: int, e: int) -> np.ndarray:
+    out = np.zeros(r, dtype=np.uint32)
+    if lib().ora_gen_edge(seed, n, r, e, _ptr(out)):
+        raise ValueError("bad generator arguments")
+    return out
+
+
+def gen_hypergraph(n: int, m: int, r: int, seed: int) -> np.ndarray:
+    """edges[m][r] u32, G^r_{n,cn} with m = cn edges."""
+    edges = np.zeros((m, r), dtype=np.uint32)
+    if lib().ora_gen_hypergraph(seed, n, m, r, _ptr(edges)):
+        raise ValueError("bad generator arguments (need r>=2, n>=r)")
+    return edges
+
+
+def mix64(z: int) -> int:
+    return int(lib().ora_mix64(z & 0xFFFFFFFFFFFFFFFF))
+
+
+def gen_keys(nkeys: int, seed: int) -> np.ndarray:
+    keys = np.zeros(nkeys, dtype=np.uint64)
+    lib().ora_gen_keys(seed, nkeys, _ptr(keys))
+    return keys
+
+
+def seed_h(seed: int) -> int:
+    return int(lib().ora_seed_h(seed))
+
+
+def seed_c(seed: int) -> int:
+    return int(lib().ora_seed_c(seed))
+
+
+def checksum(x: int, seed: int) -> int:
+    return int(lib().ora_checksum(x, seed_c(seed)))
+
+
+def cells_of(x: int, C: int, r: int, seed: int) -> np.ndarray:
+    out = np.zeros(r, dtype=np.uint64)
+    if lib().ora_cells_of(x, C, r, seed_h(seed), _ptr(out)):
+        raise ValueError("bad cell-hash arguments")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# k-core peels
+# ---------------------------------------------------------------------------
+class PeelResult:
+    def __init__(self, core_mask, rounds, survivors, killed, peel_round):
+        self.core_mask = core_mask
+        self.rounds = rounds
+        self.survivors = survivors
+        self.killed = killed
+        self.peel_round = peel_round
+
+    def __repr__(self):
+        return (f"PeelResult(rounds={self.rounds}, core={int(self.core_mask.sum())}, "
+                f"survivors={self.survivors.tolist()[:6]}...)")
+
+
+def sync_peel(edges: np.ndarray, n: int, k: int, cap: int = 1 << 16,
+              want_peel_round: bool = False) -> PeelResult:
+    """Literal round-synchronous peel."""
+    edges = np.ascontiguousarray(edges, dtype=np.uint32)
+    m = edges.shape[0]
+    r = edges.shape[1] if edges.ndim == 2 and m > 0 else (edges.shape[1] if edges.ndim == 2 else 0)
+    core = np.zeros(max(n, 1), dtype=np.uint8)
+    rounds = ctypes.c_uint32(0)
+    surv = np.zeros(cap, dtype=np.uint64)
+    killed = np.zeros(cap, dtype=np.uint64)
+    pr = np.zeros(max(n, 1), dtype=np.uint32) if want_peel_round else None
+    st = lib().ora_sync_peel(_ptr(edges) if m else None, n, m, r, k, _ptr(core),
+                             ctypes.addressof(rounds), _ptr(surv), _ptr(killed), cap,
+                             _ptr(pr) if pr is not None else None)
+    if st < 0:
+        raise ValueError("oracle sync_peel: bad input or out of memory")
+    if st == 1:
+        raise OverflowError("more rounds than cap")
+    t = rounds.value
+    return PeelResult(core[:n].copy(), t, surv[:t].copy(), killed[:t].copy(),
+                      pr[:n].copy() if pr is not None else None)
+
+
+def queue_peel(edges: np.ndarray, n: int, k: int) -> np.ndarray:
+    """Serial greedy peel; returns the k-core mask."""
+    edges = np.ascontiguousarray(edges, dtype=np.uint32)
+    m = edges.shape[0]
+    r = edges.shape[1]
+    core = np.zeros(max(n, 1), dtype=np.uint8)
+    if lib().ora_queue_peel(_ptr(edges) if m else None, n, m, r, k, _ptr(core)):
+        raise MemoryError("oracle queue_peel")
+    return core[:n].copy()
+
+
+# ---------------------------------------------------------------------------
+# IBLT
+# ---------------------------------------------------------------------------
+class IbltResult:
+    def __init__(self, keys, rounds, per_round, complete):
+        self.keys = keys
+        self.rounds = rounds
+        self.per_round = per_round
+        self.complete = complete
+
+
+class Iblt:
+    """IBLT with C cells and r hashes."""
+
+    def __init__(self, C: int, r: int, seed: int):
+        self.C, self.r, self.seed = C, r, seed
+        self._t = lib().ora_iblt_new(C, r, seed)
+        if not self._t:
+            raise ValueError("bad IBLT arguments (need r>=2, C>=r)")
+
+    def __del__(self):
+        t = getattr(self, "_t", None)
+        if t:
+            lib().ora_iblt_free(t)
+            self._t = None
+
+    def insert(self, keys: np.ndarray):
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        lib().ora_iblt_insert(self._t, _ptr(keys), keys.size)
+
+    def delete(self, keys: np.ndarray):
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        lib().ora_iblt_delete(self._t, _ptr(keys), keys.size)
+
+    def cells(self):
+        count = np.zeros(self.C, dtype=np.int64)
+        keysum = np.zeros(self.C, dtype=np.uint64)
+        hashsum = np.zeros(self.C, dtype=np.uint32)
+        lib().ora_iblt_dump(self._t, _ptr(count), _ptr(keysum), _ptr(hashsum))
+        return count, keysum, hashsum
+
+    def peel(self, cap_keys: int | None = None, cap: int = 1 << 16) -> IbltResult:
+        """Round-synchronous recovery, destructive."""
+        cap_keys = self.C * 2 if cap_keys is None else cap_keys
+        out = np.zeros(max(cap_keys, 1), dtype=np.uint64)
+        nrec = ctypes.c_uint64(0)
+        rounds = ctypes.c_uint32(0)
+        per_round = np.zeros(cap, dtype=np.uint64)
+        complete = ctypes.c_int(0)
+        st = lib().ora_iblt_peel(self._t, _ptr(out), cap_keys, ctypes.addressof(nrec),
+                                 ctypes.addressof(rounds), _ptr(per_round), cap,
+                                 ctypes.addressof(complete))
+        if st < 0:
+            raise MemoryError("oracle iblt_peel")
+        if st == 1:
+            raise OverflowError("cap exceeded")
+        t = rounds.value
+        return IbltResult(out[:nrec.value].copy(), t, per_round[:t].copy(), bool(complete.value))
+
+    def serial_recover(self):
+        """One-pure-cell-at-a-time recovery, destructive."""
+        cap_keys = self.C * 2
+        out = np.zeros(cap_keys, dtype=np.uint64)
+        nrec = ctypes.c_uint64(0)
+        complete = ctypes.c_int(0)
+        st = lib().ora_iblt_serial_recover(self._t, _ptr(out), cap_keys, ctypes.addressof(nrec),
+                                           ctypes.addressof(complete))
+        if st != 0:
+            raise MemoryError("oracle serial_recover")
+        return out[:nrec.value].copy(), bool(complete.value)
+
+    def to_hypergraph(self, keys: np.ndarray) -> np.ndarray:
+        """edge i = the r cells of key i."""
+        keys = np.ascontiguousarray(keys, dtype=np.uint64)
+        edges = np.zeros((keys.size, self.r), dtype=np.uint32)
+        lib().ora_iblt_to_hypergraph(self._t, _ptr(keys), keys.size, _ptr(edges))
+        return edges

@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""bench.py -- round-synchronous k-core peeling on B200 (BASELINE.json metric).
+
+One "step" = one full peel_kcore call (a2-a7: degree/state build, every
+round, core-mask output) over one synthetic G^r_{n,cn} instance already
+resident in HBM; the generator (a1) produces the input outside the timed
+region.  Default workload = BASELINE.json configs[4] at N=1: n=10^9, r=3,
+k=2, c=0.75 (m=7.5e8), seed 6 -- the north-star instance.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C5|C1|C3|C4a|C4b|C2]
+  python bench.py --impl reference ...   (the CPU oracle on the host cores)
+
+Multi-GPU (torchrun): every rank peels its own independent instance (seed +
+rank; weak scaling, no data-path collective); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (kind, n_or_cells, m_or_keys, r, k, seed, BASELINE.json config text)
+    "C1": ("kcore", 100_000, 70_000, 3, 2, 1, "k-core peel r=3 k=2 n=100,000 c=0.7"),
+    "C2": ("iblt", 10_000_000, 7_500_000, 3, 2, 2, "IBLT recovery r=3, 10^7 cells, 7.5e6 keys"),
+    "C3": ("kcore", 100_000_000, 75_000_000, 4, 2, 3, "k-core peel r=4 k=2 n=10^8 c=0.75"),
+    "C4a": ("kcore", 100_000_000, 85_000_000, 3, 2, 4, "above-threshold k-core r=3 k=2 c=0.85 n=10^8"),
+    "C4b": ("kcore", 100_000_000, 160_000_000, 3, 3, 5, "above-threshold k-core r=3 k=3 c=1.6 n=10^8"),
+    "C5": ("kcore", 1_000_000_000, 750_000_000, 3, 2, 6, "r=3 k=2 c=0.75 n=10^9 (north star)"),
+}
+METRIC = "hyperedges peeled/sec"
+
+
+def algorithmic_bytes(r, n, m, n_core, m_core, k):
+    """SURVEY §8 d0 compulsory traffic of a work-efficient synchronous peel, split by kernel.
+    k<=2 packed state: build = read edges 4rm + write state 8n; rounds = read state of removed
+    vertices 8(n-n_core) + per killed edge re-read its ids 4r and RMW r-1 endpoints 16(r-1),
+    plus the n-byte mask."""
+    if k <= 2:
+        build = 4 * r * m + 8 * n
+        rounds = 8 * (n - n_core) + (m - m_core) * (4 * r + 16 * (r - 1)) + n
+    else:  # CSR (u32 deg + offsets + adj): SURVEY §8 d0 general-k formula
+        build = (4 * r * m + 4 * n) + 8 * n + 8 * r * m
+        rounds = 12 * (n - n_core) + 4 * r * (m - m_core) + (m - m_core) * (4 * r + 8 * (r - 1)) + n
+    return build, rounds
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline_kcore(r, k, c, target_s=12.0):
+    """The oracle as it stands (single-threaded literal synchronous peel) on a bounded
+    sample: one instance of the same model (r, k, c) scaled down so it runs ~10-30 s."""
+    from oracle import oracle as O
+    n = 2_000_000
+    t_total = 0.0
+    peeled = 0
+    runs = 0
+    while True:
+        m = int(round(c * n))
+        e = O.gen_hypergraph(n, m, r, 1000 + runs)
+        t0 = time.perf_counter()
+        res = O.sync_peel(e, n, k)
+        dt = time.perf_counter() - t0
+        inside = res.core_mask[e].all(axis=1)
+        peeled += int(m - inside.sum())
+        t_total += dt
+        runs += 1
+        if t_total > target_s or runs >= 4:
+            break
+        if dt < target_s / 4:
+            n *= 2
+    return {"value": peeled / t_total, "unit": "edges/s", "cores": 1, "kind": "oracle",
+            "sample": f"{runs} instance(s) of G^{r}_(n,cn), c={c}, k={k}, largest n={n} "
+                      f"(literal synchronous oracle, single thread, {t_total:.1f} s of peel)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    kind, n_full, m_full, r, k, seed, text = CONFIGS[args.config]
+    c = m_full / n_full
+    # each step: one bounded sample instance of the workload (same r, k, c)
+    n = 1_000_000 if kind == "kcore" else 1 << 20
+    m = int(round(c * n))
+    times, units = [], 0
+    if kind == "kcore":
+        e = O.gen_hypergraph(n, m, r, seed)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = O.sync_peel(e, n, k)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+        inside = res.core_mask[e].all(axis=1)
+        per_step = int(m - inside.sum())
+        unit = "edges/s"
+    else:
+        keys = O.gen_keys(m, seed)
+        for i in range(args.warmup + args.steps):
+            t = O.Iblt(n, r, seed)
+            t0 = time.perf_counter()
+            t.insert(keys)
+            res = t.peel(cap_keys=m + 1)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+        per_step = int(res.keys.size)
+        unit = "keys/s"
+    T = sum(times)
+    val = per_step * len(times) / T
+    metric = METRIC if kind == "kcore" else "IBLT keys recovered/sec"
+    line = {
+        "impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
+        "data": "synthetic (counter-based G^r_{n,cn} generator, oracle implementation)",
+        "config": {"workload": f"{args.config}: {text}", "sample_n": n, "sample_m": m, "r": r, "k": k},
+        "cpu_baseline": {"value": val, "unit": unit, "cores": 1, "kind": "oracle",
+                         "sample": f"each step = oracle peel of one n={n} instance of the same model"},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", action="store_true",
+                    help="record per-kernel CUDA events inside the timed steps (default on)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1302_7014_b200 as pk
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    kind, n, m, r, k, seed, text = CONFIGS[args.config]
+    seed = seed + rank  # independent instance per rank (weak scaling)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    if kind != "kcore":
+        raise SystemExit("bench.py times the k-core configs; the IBLT is covered by tests/bench_iblt.py")
+
+    edges = pk.gen_hypergraph(n, m, r, seed, device=dev)
+    wsb = pk.kcore_workspace_bytes(n, m, r, k)
+    wsp = torch.empty((wsb,), dtype=torch.uint8, device=dev)
+    mask = torch.empty((n,), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        return pk.peel_kcore(edges, n, k, core_mask=mask, ws=wsp, cap=4096)
+
+    for _ in range(max(args.warmup, 3)):
+        res = step()
+    # results of this instance (deterministic): peeled edges = edges not wholly in the core
+    n_core = int(mask.sum().item())
+    if n_core:
+        inside = mask[edges.long()].all(dim=1)
+        m_core = int(inside.sum().item())
+        del inside
+    else:
+        m_core = 0
+    peeled = m - m_core
+    b_build, b_rounds = algorithmic_bytes(r, n, m, n_core, m_core, k)
+
+    pk.profile_enable(True)
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    t_ev0 = torch.cuda.Event(enable_timing=True)
+    t_ev1 = torch.cuda.Event(enable_timing=True)
+    per_kernel = {}
+    launches = 0
+    t_ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+        launches += pk.last_launches()
+        for name, ms, nl in pk.profile_read():
+            a = per_kernel.setdefault(name, [0.0, 0])
+            a[0] += ms
+            a[1] += nl
+    t_ev1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    pk.profile_enable(False)
+    ms_total = t_ev0.elapsed_time(t_ev1)
+    ms_step = ms_total / args.steps
+    t_max = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        tot = torch.tensor([float(peeled)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        total_peeled = tot.item()
+    else:
+        total_peeled = float(peeled)
+    t_max_s = t_max.item() / 1e3
+    value = total_peeled * args.steps / t_max_s
+
+    # roofline for the dominant kernel (algorithmic bytes per launch / avg launch time)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback (B200_PROFILING.md 6.65 TB/s)"
+    hbm = hbm or 6650.0
+    kb = {"build_packed": b_build, "build_deg": b_build, "peel_rounds_packed": b_rounds, "peel_rounds_csr": b_rounds}
+    dom = max(per_kernel.items(), key=lambda kv: kv[1][0]) if per_kernel else None
+    roof = None
+    if dom:
+        name, (ms_sum, nl) = dom
+        avg_ms = ms_sum / max(nl, 1)
+        alg = kb.get(name, b_build + b_rounds)
+        ach = alg / (avg_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
+                "alg_bytes_per_launch": alg, "avg_launch_ms": round(avg_ms, 4)}
+    step_alg = b_build + b_rounds
+    kernels = {nm: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
+               for nm, v in per_kernel.items()}
+
+    # e2e: through the C-ABI with HOST buffers (H2D of the edges + D2H of the mask inside)
+    e2e = None
+    if not args.no_e2e:
+        try:
+            e_host = torch.empty((m, r), dtype=torch.int32, pin_memory=True)
+            e_host.copy_(edges)
+            m_host = torch.empty((n,), dtype=torch.uint8, pin_memory=True)
+            hws = torch.empty((int(pk.lib().peel_kcore_host_workspace_bytes(n, m, r, k, 0)),),
+                              dtype=torch.uint8, device=dev)
+            del wsp
+            torch.cuda.empty_cache()
+            pk.peel_kcore_host(e_host, n, k, core_mask_host=m_host, ws=hws, cap=4096)  # warm-up
+            barrier()
+            h0 = torch.cuda.Event(enable_timing=True)
+            h1 = torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            for _ in range(args.e2e_steps):
+                pk.peel_kcore_host(e_host, n, k, core_mask_host=m_host, ws=hws, cap=4096)
+            h1.record(stream)
+            barrier()
+            te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+            if ws > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            assert int(m_host.sum().item()) == n_core
+            e2e = {"value": total_peeled * args.e2e_steps / (te.item() / 1e3), "unit": "edges/s",
+                   "h2d_bytes_per_step": 4 * r * m, "d2h_bytes_per_step": n, "steps": args.e2e_steps,
+                   "api": "peel_kcore_host (C-ABI, pinned host edges in, host core mask out)"}
+            del hws, e_host, m_host
+        except Exception as ex:  # pragma: no cover
+            e2e = {"value": None, "unit": "edges/s", "error": repr(ex)[:200],
+                   "h2d_bytes_per_step": 4 * r * m, "d2h_bytes_per_step": n}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_kcore(r, k, m / n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(t_max_s * 1e3 / args.steps, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
+            "data": "synthetic G^r_{n,cn} (counter-based Philox generator on device, seed per rank)",
+            "config": {"workload": f"{args.config}: {text}", "n": n, "m": m, "r": r, "k": k, "seed": seed - rank,
+                       "rounds": res.rounds, "core_vertices": n_core, "peeled_edges": peeled,
+                       "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                       "l2": "inputs (edges 4rm B, state 8n B) larger than L2; no flush needed"},
+            "rounds": res.rounds,
+            "hbm_roofline_step": {"alg_bytes": step_alg, "frac_of_measured": round(step_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
+                                  "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

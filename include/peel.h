@@ -1,0 +1,227 @@
+/*
+ * peel.h -- C-ABI of libpeel.so: round-synchronous parallel peeling of random
+ * r-uniform hypergraphs to the k-core, and IBLT recovery, on NVIDIA B200
+ * (sm_100a).  Plain pointers and sizes only; no torch or CUDA types.
+ *
+ * Citations: "P:n" = line n of the paper (Jiang, Mitzenmacher, Thaler,
+ * "Parallel Peeling Algorithms", arXiv 1302.7014, PAPER.md); "S:n" = SPEC.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - "dev" pointers are CUDA device pointers (e.g. torch tensor data_ptr());
+ *   "host" pointers are ordinary CPU memory.  The caller owns every buffer it
+ *   passes; the library never frees them.
+ * - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   Everything is stream-ordered on it.  Calls that return host scalars
+ *   (peel_kcore, iblt_peel, ...) synchronise `stream` before returning.
+ * - Errors are returned as peel_status; nothing is thrown or aborted across
+ *   the ABI.  Arguments are validated before any launch (PEEL_EINVAL).
+ *   Outputs are meaningful only on PEEL_OK (and on PEEL_ETRUNC, see below).
+ * - Vertex ids are u32 (n <= 2^32); edge ids are u32 (m < 2^32); 2 <= r <= 8.
+ * - Not thread-safe per stream: concurrent calls must use distinct streams and
+ *   workspaces.
+ */
+#ifndef PEEL_H_
+#define PEEL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PEEL_OK = 0,
+    PEEL_EINVAL = 1,    /* bad argument, or an input edge with a vertex id >= n or a repeated vertex */
+    PEEL_ENOMEM = 2,    /* workspace too small / allocation failed */
+    PEEL_ECUDA = 3,     /* a CUDA runtime error (peel_last_cuda_error() has the text) */
+    PEEL_ETRUNC = 4,    /* more rounds than the caller's `cap`; rounds and the first cap entries are valid */
+    PEEL_ENCCL = 5,     /* an NCCL error (multi-GPU entry points) */
+    PEEL_EOVERFLOW = 6  /* packed k<=2 state cannot hold this degree x edge-id range (see peel_kcore) */
+} peel_status;
+
+/* Human-readable name of a status code (static storage). */
+const char *peel_strerror(int status);
+/* Text of the last CUDA error seen by this process's library calls (static storage). */
+const char *peel_last_cuda_error(void);
+/* ABI version of this header (bumped on any signature change). */
+int peel_abi_version(void);
+#define PEEL_ABI_VERSION 1
+
+/* ======================================================================= */
+/* a1 -- generator: G^r_{n,cn} and IBLT keys (counter-based) */
+/* ======================================================================= */
+
+/*
+ * peel_gen_hypergraph -- fill edges[m][r] (dev, u32, row-major) with m
+ * independent hyperedges of r DISTINCT vertices chosen uniformly from [0,n)
+ * ("cn hyperedges, where each hyperedge consists of r distinct
+ * vertices"; "each edge is chosen independently and uniformly").
+ * Edge e is a pure function of (seed, n, r, e): draw j is half j%2 of
+ * Philox4x32-10(ctr = {e_lo, e_hi, j/2, 'EDGE'}, key = {seed_lo, seed_hi}),
+ * mapped to vertex umulhi64(draw, n), rejected if already in the edge.
+ * Vertex order within an edge is draw order.  Duplicate edges may occur
+ * (hashing model).
+ * EINVAL: r < 2, r > 8, n < r, n > 2^32, m >= 2^32, edges == NULL with m > 0.
+ */
+peel_status peel_gen_hypergraph(uint64_t n, uint64_t m, uint32_t r, uint64_t seed,
+                                uint32_t *edges, void *stream);
+
+/*
+ * peel_gen_keys -- keys[i] (dev, u64) = i-th output of a SplitMix64 stream
+ * with state `seed`: mix64(seed + (i+1) * 0x9E3779B97F4A7C15).  A bijection of
+ * i, so the nkeys keys are distinct (the IBLT stores a set).
+ */
+peel_status peel_gen_keys(uint64_t nkeys, uint64_t seed, uint64_t *keys, void *stream);
+
+/* ======================================================================= */
+/* a2-a7 -- k-core by round-synchronous parallel peeling                    */
+/* ======================================================================= */
+
+/* flags */
+#define PEEL_FLAG_CSR 1u /* force the general-k incidence (CSR) path even for k <= 2 */
+
+/*
+ * Bytes of device workspace peel_kcore needs for (n, m, r, k, flags).
+ * Returns 0 if the arguments are invalid.
+ */
+size_t peel_kcore_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k, uint32_t flags);
+
+/*
+ * peel_kcore -- round-synchronous parallel peeling to the k-core
+ * ("in each round, all vertices of degree less than k and their
+ * adjacent edges are removed in parallel"; an edge is peeled when
+ * an adjacent vertex is; the k-core is the maximal sub-hypergraph with all
+ * degrees >= k).
+ *
+ * Round t removes F_t = {alive v : deg_t(v) < k}, deg_t the number of alive
+ * edges at the START of round t (a snapshot; degree-0 vertices included),
+ * then every alive edge with an endpoint in F_t.  The loop stops at the first
+ * round with F_t empty; that terminal round is not counted.
+ *
+ * in:  edges     dev u32 [m][r], row-major, read-only.  Every id < n and the
+ *                r ids of an edge distinct, else PEEL_EINVAL (checked on device).
+ *                Edges are a multiset (duplicates allowed).
+ *      n, m, r, k  sizes; k = 0 peels nothing (rounds = 0).
+ *      flags     0 or PEEL_FLAG_CSR.
+ * out: core_mask dev u8 [n]: 1 iff v is in the k-core.
+ *      rounds    host u32: number of rounds with F_t non-empty.
+ *      survivors host u64 [cap] (nullable): survivors[t-1] = |alive vertices|
+ *                after round t, t = 1..min(rounds, cap).
+ *      killed    host u64 [cap] (nullable): edges removed in round t.
+ *      peel_round dev u32 [n] (nullable): round in which v was removed, 0 if
+ *                v is in the core (a schedule certificate for tests).
+ * workspace: dev, >= peel_kcore_workspace_bytes(n, m, r, k, flags) bytes,
+ *      any contents; clobbered.
+ * Blocking: synchronises `stream` before returning.
+ * Status: PEEL_ETRUNC if rounds > cap (or > 65536): rounds is exact, the
+ *      first cap entries are written.  PEEL_EOVERFLOW (k <= 2 packed path
+ *      only, impossible for random inputs) if some vertex degree d has
+ *      d * (m-1) >= 2^40; rerun with PEEL_FLAG_CSR.
+ */
+peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k,
+                       uint32_t flags, uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
+                       uint64_t *killed, uint32_t cap, uint32_t *peel_round, void *workspace,
+                       size_t ws_bytes, void *stream);
+
+/*
+ * peel_kcore_host -- the same computation with HOST input and output:
+ * edges_host u32 [m][r] and core_mask_host u8 [n] are CPU memory (pinned for
+ * full copy speed); the host->device copy of the edges and the device->host
+ * copy of the mask are part of the call.  workspace must hold
+ * peel_kcore_host_workspace_bytes(n, m, r, k, flags) bytes of device memory.
+ */
+size_t peel_kcore_host_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k, uint32_t flags);
+peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, uint64_t m, uint32_t r,
+                            uint32_t k, uint32_t flags, uint8_t *core_mask_host, uint32_t *rounds,
+                            uint64_t *survivors, uint64_t *killed, uint32_t cap, void *workspace,
+                            size_t ws_bytes, void *stream);
+
+/* ======================================================================= */
+/* IBLT -- cells {count, checksum, key} with XOR accumulators   */
+/* ======================================================================= */
+
+/*
+ * Cell layout in device memory (16 bytes, 16-byte aligned, array of structs):
+ *   struct { uint32_t count; uint32_t hashSum; uint64_t keySum; }
+ * keySum / hashSum are the paper's key and checksum fields,
+ * XOR accumulators; count is this build's count field (signed, two's
+ * complement), which makes "pure" exact: count == 1 and
+ * hashSum == checkSum(keySum).  The table and all peel scratch live
+ * in caller-owned device memory `mem` of iblt_mem_bytes(cells, r) bytes; the
+ * cell array is at offset 0.
+ *
+ * Hashes: seed_h = mix64((seed ^ 0x6A09E667F3BCC909) + G),
+ * seed_c = mix64((seed ^ 0xBB67AE8584CAA73B) + G), G = 0x9E3779B97F4A7C15;
+ * cell j-th candidate = umulhi64(mix64(x ^ seed_h ^ (j+1)*0xD1B54A32D192ED03), cells),
+ * duplicates rejected, until r distinct cells; checkSum(x) = mix64(x ^ seed_c) >> 32.
+ */
+typedef struct peel_iblt peel_iblt;
+
+size_t iblt_mem_bytes(uint64_t cells, uint32_t r);
+
+/* Zero the cells and create the handle.  EINVAL: r < 2, r > 8, cells < r,
+ * cells >= 2^32, mem NULL, mem_bytes too small, mem not 16-byte aligned. */
+peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, void *mem, size_t mem_bytes,
+                       void *stream, peel_iblt **out);
+
+/* Insert nkeys keys (dev u64): XOR x into keySum and checkSum(x) into
+ * hashSum of each of x's r cells, count += 1 (one thread per key
+ * with atomic XOR).  Keys must be distinct and not already in the
+ * table (XOR would cancel them; caller error, not detected). */
+peel_status iblt_insert(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, void *stream);
+
+/* Delete: the same XOR update with count -= 1 ("insertion and deletion
+ * procedures are identical"). */
+peel_status iblt_delete(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, void *stream);
+
+/*
+ * iblt_peel -- round-synchronous recovery (the 2-core peel of the
+ * IBLT's hypergraph).  Each round snapshots the pure cells, recovers
+ * each of their keys exactly once (the owner is the round-start-pure cell
+ * with the lowest hash index among the key's cells), deletes every recovered
+ * key from its r cells, and stops at the first round recovering nothing.
+ * DESTRUCTIVE: the table holds the unrecovered remainder afterwards.
+ * out: out_keys dev u64 [cap_keys], recovered keys in unspecified order;
+ *      nrecovered host u64 (may exceed cap_keys: then PEEL_ETRUNC and only
+ *      cap_keys were stored); rounds host u32; per_round host u64 [cap]
+ *      (nullable) keys recovered in round t; complete host int (nullable):
+ *      1 iff every cell is zero afterwards (success iff the 2-core is empty).
+ * Blocking.
+ */
+peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
+                      uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete,
+                      void *stream);
+
+/* Device pointer to the 16-byte cell array (for tests and serialisation). */
+void *iblt_cells(const peel_iblt *t);
+
+/* edges[i][j] (dev u32 [nkeys][r]) = j-th cell of keys[i]: the IBLT's
+ * hypergraph, cells = vertices, keys = edges. */
+peel_status iblt_to_hypergraph(const peel_iblt *t, const uint64_t *keys, uint64_t nkeys,
+                               uint32_t *edges, void *stream);
+
+/* Free the handle (not the caller's memory). */
+void iblt_destroy(peel_iblt *t);
+
+/* ======================================================================= */
+/* Measurement support                                                      */
+/* ======================================================================= */
+
+/*
+ * When enabled, every peel_kcore / iblt_peel / iblt_insert call records a
+ * CUDA event pair on `stream` around each kernel it launches; after the call
+ * peel_profile_read returns up to `cap` (name, milliseconds, launches)
+ * triples of the LAST call, in launch order.  Names are static strings.
+ * Returns the number of entries.  Disabled by default (no events recorded).
+ */
+void peel_profile_enable(int on);
+int peel_profile_read(const char **names, double *ms, uint32_t *launches, int cap);
+/* Kernel launches made by the last peel_kcore / iblt_* call (always counted). */
+uint32_t peel_last_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PEEL_H_ */

@@ -1,0 +1,301 @@
+"""paper_1302_7014_b200 -- parallel peeling (k-core / IBLT recovery) on B200.
+
+Thin Python binding over the C-ABI of ``libpeel.so`` (``include/peel.h``):
+argument marshalling only; every step of the method runs in the library's
+sm_100a kernels.  torch supplies device memory and streams.  There is no CPU
+fallback: if the library is missing, every call raises.
+
+Tensors: edges are int32 tensors holding u32 vertex ids, shape [m, r];
+keys are int64 tensors holding u64 bit patterns.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpeel.so")
+
+PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOVERFLOW = range(7)
+PEEL_FLAG_CSR = 1
+
+_lib = None
+
+
+class PeelError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        msg = _L().peel_strerror(status).decode()
+        if status == PEEL_ECUDA:
+            msg += " -- " + _L().peel_last_cuda_error().decode()
+        super().__init__(f"{what}: {msg}")
+
+
+def _L() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        u32, u64, i32, p, sz = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
+        L.peel_strerror.argtypes = [i32]
+        L.peel_strerror.restype = ctypes.c_char_p
+        L.peel_last_cuda_error.restype = ctypes.c_char_p
+        L.peel_abi_version.restype = i32
+        L.peel_gen_hypergraph.argtypes = [u64, u64, u32, u64, p, p]
+        L.peel_gen_keys.argtypes = [u64, u64, p, p]
+        L.peel_kcore_workspace_bytes.argtypes = [u64, u64, u32, u32, u32]
+        L.peel_kcore_workspace_bytes.restype = sz
+        L.peel_kcore.argtypes = [p, u64, u64, u32, u32, u32, p, p, p, p, u32, p, p, sz, p]
+        L.peel_kcore_host_workspace_bytes.argtypes = [u64, u64, u32, u32, u32]
+        L.peel_kcore_host_workspace_bytes.restype = sz
+        L.peel_kcore_host.argtypes = [p, u64, u64, u32, u32, u32, p, p, p, p, u32, p, sz, p]
+        L.iblt_mem_bytes.argtypes = [u64, u32]
+        L.iblt_mem_bytes.restype = sz
+        L.iblt_build.argtypes = [u64, u32, u64, p, sz, p, ctypes.POINTER(p)]
+        L.iblt_insert.argtypes = [p, p, u64, p]
+        L.iblt_delete.argtypes = [p, p, u64, p]
+        L.iblt_peel.argtypes = [p, p, u64, p, p, p, u32, p, p]
+        L.iblt_cells.argtypes = [p]
+        L.iblt_cells.restype = p
+        L.iblt_to_hypergraph.argtypes = [p, p, u64, p, p]
+        L.iblt_destroy.argtypes = [p]
+        L.peel_profile_enable.argtypes = [i32]
+        L.peel_profile_read.argtypes = [p, p, p, i32]
+        L.peel_profile_read.restype = i32
+        L.peel_last_launches.restype = u32
+        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "iblt_build",
+                  "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
+            getattr(L, f).restype = i32
+        _lib = L
+    return _lib
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libpeel.so (raises if not built)."""
+    return _L()
+
+
+def _check(st: int, what: str, ok=(PEEL_OK,)):
+    if st not in ok:
+        raise PeelError(st, what)
+    return st
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _dev(device):
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------------------
+# a1 generator
+# ---------------------------------------------------------------------------
+def gen_hypergraph(n: int, m: int, r: int, seed: int, out: torch.Tensor | None = None,
+                   device=None, stream=None) -> torch.Tensor:
+    """edges [m, r] (int32 storage of u32 ids) of G^r_{n,cn} (peel.h peel_gen_hypergraph)."""
+    if out is None:
+        out = torch.empty((m, r), dtype=torch.int32, device=_dev(device))
+    _check(_L().peel_gen_hypergraph(n, m, r, seed & (2**64 - 1), _ptr(out), _stream(stream)),
+           "peel_gen_hypergraph")
+    return out
+
+
+def gen_keys(nkeys: int, seed: int, out: torch.Tensor | None = None, device=None, stream=None) -> torch.Tensor:
+    """nkeys distinct u64 keys (int64 storage), SplitMix64 stream (peel.h peel_gen_keys)."""
+    if out is None:
+        out = torch.empty((nkeys,), dtype=torch.int64, device=_dev(device))
+    _check(_L().peel_gen_keys(nkeys, seed & (2**64 - 1), _ptr(out), _stream(stream)), "peel_gen_keys")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# k-core
+# ---------------------------------------------------------------------------
+class KcoreResult:
+    def __init__(self, core_mask, rounds, survivors, killed, peel_round, status):
+        self.core_mask = core_mask
+        self.rounds = rounds
+        self.survivors = survivors
+        self.killed = killed
+        self.peel_round = peel_round
+        self.status = status
+
+    def __repr__(self):
+        return f"KcoreResult(rounds={self.rounds}, survivors[-1]={self.survivors[-1] if len(self.survivors) else None})"
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """A cached uint8 device workspace of at least nbytes."""
+    key = str(device)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        _ws_cache.pop(key, None)
+        t = torch.empty((max(nbytes, 256),), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def kcore_workspace_bytes(n: int, m: int, r: int, k: int, flags: int = 0) -> int:
+    return int(_L().peel_kcore_workspace_bytes(n, m, r, k, flags))
+
+
+def peel_kcore(edges: torch.Tensor, n: int, k: int, flags: int = 0, cap: int = 65536,
+               core_mask: torch.Tensor | None = None, want_peel_round: bool = False,
+               ws: torch.Tensor | None = None, stream=None, allow_trunc: bool = False) -> KcoreResult:
+    """Round-synchronous peel of the hypergraph `edges` [m, r] to its k-core (peel.h peel_kcore)."""
+    assert edges.dim() == 2 and edges.dtype == torch.int32 and edges.is_cuda and edges.is_contiguous()
+    m, r = edges.shape
+    dev = edges.device
+    need = kcore_workspace_bytes(n, m, r, k, flags)
+    if need == 0:
+        raise PeelError(PEEL_EINVAL, "peel_kcore_workspace_bytes")
+    if ws is None:
+        ws = workspace(need, dev)
+    if core_mask is None:
+        core_mask = torch.empty((n,), dtype=torch.uint8, device=dev)
+    pr = torch.empty((n,), dtype=torch.int32, device=dev) if want_peel_round else None
+    rounds = ctypes.c_uint32(0)
+    surv = np.zeros(cap, dtype=np.uint64)
+    killed = np.zeros(cap, dtype=np.uint64)
+    st = _L().peel_kcore(_ptr(edges), n, m, r, k, flags, _ptr(core_mask), ctypes.addressof(rounds),
+                         surv.ctypes.data, killed.ctypes.data, cap, _ptr(pr), _ptr(ws), ws.numel(),
+                         _stream(stream))
+    _check(st, "peel_kcore", ok=(PEEL_OK, PEEL_ETRUNC) if allow_trunc else (PEEL_OK,))
+    t = rounds.value
+    nst = min(t, cap)
+    return KcoreResult(core_mask, t, surv[:nst].copy(), killed[:nst].copy(), pr, st)
+
+
+def peel_kcore_host(edges_host: np.ndarray, n: int, k: int, flags: int = 0, cap: int = 65536,
+                    core_mask_host: np.ndarray | None = None, ws: torch.Tensor | None = None,
+                    device=None, stream=None):
+    """peel_kcore with host (preferably pinned) input edges and output mask (peel.h peel_kcore_host).
+    edges_host: uint32/int32 numpy array or pinned CPU tensor [m, r]."""
+    if isinstance(edges_host, torch.Tensor):
+        m, r = edges_host.shape
+        eptr = edges_host.data_ptr()
+    else:
+        m, r = edges_host.shape
+        eptr = edges_host.ctypes.data
+    dev = _dev(device)
+    need = int(_L().peel_kcore_host_workspace_bytes(n, m, r, k, flags))
+    if need == 0:
+        raise PeelError(PEEL_EINVAL, "peel_kcore_host_workspace_bytes")
+    if ws is None:
+        ws = workspace(need, dev)
+    if core_mask_host is None:
+        core_mask_host = np.empty((n,), dtype=np.uint8)
+    mptr = core_mask_host.data_ptr() if isinstance(core_mask_host, torch.Tensor) else core_mask_host.ctypes.data
+    rounds = ctypes.c_uint32(0)
+    surv = np.zeros(cap, dtype=np.uint64)
+    killed = np.zeros(cap, dtype=np.uint64)
+    st = _L().peel_kcore_host(eptr, n, m, r, k, flags, mptr, ctypes.addressof(rounds), surv.ctypes.data,
+                              killed.ctypes.data, cap, _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "peel_kcore_host")
+    t = rounds.value
+    return KcoreResult(core_mask_host, t, surv[:min(t, cap)].copy(), killed[:min(t, cap)].copy(), None, st)
+
+
+# ---------------------------------------------------------------------------
+# IBLT
+# ---------------------------------------------------------------------------
+class IbltResult:
+    def __init__(self, keys, nrecovered, rounds, per_round, complete, status):
+        self.keys = keys
+        self.nrecovered = nrecovered
+        self.rounds = rounds
+        self.per_round = per_round
+        self.complete = complete
+        self.status = status
+
+
+class Iblt:
+    """IBLT of `cells` 16-byte cells and r hashes in a torch-owned device buffer (peel.h iblt_*)."""
+
+    def __init__(self, cells: int, r: int, seed: int, device=None, stream=None):
+        self.C, self.r, self.seed = cells, r, seed
+        self.device = _dev(device)
+        nb = int(_L().iblt_mem_bytes(cells, r))
+        if nb == 0:
+            raise PeelError(PEEL_EINVAL, "iblt_mem_bytes")
+        self.mem = torch.empty((nb,), dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p(0)
+        _check(_L().iblt_build(cells, r, seed & (2**64 - 1), _ptr(self.mem), nb, _stream(stream),
+                               ctypes.byref(h)), "iblt_build")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.iblt_destroy(h)
+            self._h = None
+
+    def insert(self, keys: torch.Tensor, stream=None):
+        assert keys.dtype == torch.int64 and keys.is_cuda and keys.is_contiguous()
+        _check(_L().iblt_insert(self._h, _ptr(keys), keys.numel(), _stream(stream)), "iblt_insert")
+
+    def delete(self, keys: torch.Tensor, stream=None):
+        assert keys.dtype == torch.int64 and keys.is_cuda and keys.is_contiguous()
+        _check(_L().iblt_delete(self._h, _ptr(keys), keys.numel(), _stream(stream)), "iblt_delete")
+
+    def cells(self) -> torch.Tensor:
+        """[C, 4] int32 view (count, hashSum, keySum_lo, keySum_hi) of the device cells."""
+        return self.mem[: 16 * self.C].view(torch.int32).view(self.C, 4)
+
+    def peel(self, cap_keys: int | None = None, cap: int = 65536, out: torch.Tensor | None = None,
+             stream=None) -> IbltResult:
+        cap_keys = self.C if cap_keys is None else cap_keys
+        if out is None:
+            out = torch.empty((max(cap_keys, 1),), dtype=torch.int64, device=self.device)
+        nrec = ctypes.c_uint64(0)
+        rounds = ctypes.c_uint32(0)
+        per_round = np.zeros(cap, dtype=np.uint64)
+        complete = ctypes.c_int(0)
+        st = _L().iblt_peel(self._h, _ptr(out), cap_keys, ctypes.addressof(nrec), ctypes.addressof(rounds),
+                            per_round.ctypes.data, cap, ctypes.addressof(complete), _stream(stream))
+        _check(st, "iblt_peel")
+        t = rounds.value
+        return IbltResult(out[: min(nrec.value, cap_keys)], nrec.value, t, per_round[:min(t, cap)].copy(),
+                          bool(complete.value), st)
+
+    def to_hypergraph(self, keys: torch.Tensor, stream=None) -> torch.Tensor:
+        edges = torch.empty((keys.numel(), self.r), dtype=torch.int32, device=self.device)
+        _check(_L().iblt_to_hypergraph(self._h, _ptr(keys), keys.numel(), _ptr(edges), _stream(stream)),
+               "iblt_to_hypergraph")
+        return edges
+
+
+# ---------------------------------------------------------------------------
+# measurement support
+# ---------------------------------------------------------------------------
+def profile_enable(on: bool = True):
+    _L().peel_profile_enable(1 if on else 0)
+
+
+def profile_read() -> list[tuple[str, float, int]]:
+    names = (ctypes.c_char_p * 64)()
+    ms = (ctypes.c_double * 64)()
+    nl = (ctypes.c_uint32 * 64)()
+    n = _L().peel_profile_read(ctypes.addressof(names), ctypes.addressof(ms), ctypes.addressof(nl), 64)
+    return [(names[i].decode(), ms[i], nl[i]) for i in range(min(n, 64))]
+
+
+def last_launches() -> int:
+    return int(_L().peel_last_launches())

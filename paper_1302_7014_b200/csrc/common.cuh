@@ -1,0 +1,90 @@
+// common.cuh -- shared device/host helpers of libpeel (product path; no oracle code).
+#pragma once
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "peel.h"
+
+namespace cg = cooperative_groups;
+
+namespace peel {
+
+typedef unsigned long long ull;
+
+// ---------------------------------------------------------------------------
+// host-side error plumbing
+// ---------------------------------------------------------------------------
+void set_cuda_error(cudaError_t e, const char *where);
+
+#define PEEL_CUDA(call)                                   \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) {                          \
+            ::peel::set_cuda_error(_e, #call);            \
+            return PEEL_ECUDA;                            \
+        }                                                 \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// per-call launch accounting + optional CUDA-event profiling (peel.h)
+// ---------------------------------------------------------------------------
+void prof_begin_call();                                   // resets the per-call tables
+void prof_pre(const char *name, cudaStream_t s);          // before a kernel launch
+void prof_post(const char *name, cudaStream_t s);         // after it (counts the launch)
+int prof_collect();                                       // after stream sync: resolve events
+
+struct ProfScope {
+    const char *name;
+    cudaStream_t s;
+    ProfScope(const char *n, cudaStream_t st) : name(n), s(st) { prof_pre(n, st); }
+    ~ProfScope() { prof_post(name, s); }
+};
+
+// number of SMs and cooperative occupancy helpers
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ ull ld_cg_u64(const ull *p) { return __ldcg(p); }
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t *p) { return __ldcg(p); }
+
+// SplitMix64 finalizer (Steele-Lea-Flood); the IBLT hash/checksum mixer.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Warp-aggregated append of `v` to list[counter++] for the threads that call
+// it (all calling threads must be converged at the call, e.g. inside `if`).
+template <typename T>
+__device__ __forceinline__ ull append(T *list, ull *counter, T v) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    ull base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(counter, (ull)g.size());
+    base = g.shfl(base, 0);
+    list[base + g.thread_rank()] = v;
+    return base + g.thread_rank();
+}
+
+// block-wide sum of a per-thread u64, one atomicAdd per block into *dst.
+template <int BLOCK>
+__device__ __forceinline__ void block_add(ull *dst, ull v) {
+    __shared__ ull red[BLOCK / 32];
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < BLOCK / 32 ? red[lane] : 0;
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(dst, v);
+    }
+    __syncthreads();
+}
+
+}  // namespace peel

@@ -1,0 +1,108 @@
+// gen.cu -- a1: counter-based generator of G^r_{n,cn} edges and IBLT keys.
+//
+// P:89-91 / P:363: m independent hyperedges, each r DISTINCT vertices chosen
+// uniformly.  Edge e is a pure function of (seed, n, r, e), so one thread per
+// edge needs no coordination: draw j = half (j%2) of Philox4x32-10 block
+// (ctr = {e_lo, e_hi, j/2, 'EDGE'}, key = {seed_lo, seed_hi}); vertex =
+// umulhi64(draw, n); rejected if already in the edge.
+#include "common.cuh"
+
+namespace peel {
+
+// Philox4x32-10 (Salmon et al. SC'11), 10 rounds with Weyl key schedule.
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+    #pragma unroll
+    for (int i = 0; i < 10; i++) {
+        uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
+        uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
+        uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, uint64_t seed,
+                                                        uint32_t *__restrict__ edges) {
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t acc[R];
+        int na = 0;
+        uint32_t w[4];
+        for (uint32_t j = 0; na < R; j++) {
+            if ((j & 1) == 0) {
+                w[0] = (uint32_t)e; w[1] = (uint32_t)(e >> 32); w[2] = j >> 1; w[3] = 0x45444745u;
+                philox4x32_10(w, k0, k1);
+            }
+            uint64_t d = (j & 1) ? (((uint64_t)w[3] << 32) | w[2]) : (((uint64_t)w[1] << 32) | w[0]);
+            uint32_t v = (uint32_t)__umul64hi(d, n);
+            bool dup = false;
+            #pragma unroll
+            for (int i = 0; i < R; i++) dup |= (i < na) && (acc[i] == v);
+            if (!dup) {
+                #pragma unroll
+                for (int i = 0; i < R; i++) if (i == na) acc[i] = v;
+                na++;
+            }
+        }
+        #pragma unroll
+        for (int i = 0; i < R; i++) edges[e * R + i] = acc[i];
+    }
+}
+
+__global__ void __launch_bounds__(256) gen_keys_kernel(uint64_t nkeys, uint64_t seed,
+                                                       uint64_t *__restrict__ keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nkeys;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = mix64(seed + (i + 1) * 0x9E3779B97F4A7C15ull);
+}
+
+static unsigned grid_for(uint64_t work, int per_sm = 16) {
+    uint64_t blocks = (work + 255) / 256;
+    uint64_t cap = (uint64_t)num_sms() * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) blocks = 1;
+    return (unsigned)blocks;
+}
+
+}  // namespace peel
+
+using namespace peel;
+
+extern "C" peel_status peel_gen_hypergraph(uint64_t n, uint64_t m, uint32_t r, uint64_t seed,
+                                           uint32_t *edges, void *stream) {
+    if (r < 2 || r > 8 || n < r || n > (1ull << 32) || m >= (1ull << 32)) return PEEL_EINVAL;
+    if (m == 0) return PEEL_OK;
+    if (!edges) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    unsigned g = grid_for(m);
+    {
+        ProfScope ps("gen_edges", s);
+        switch (r) {
+            case 2: gen_edges_kernel<2><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+            case 3: gen_edges_kernel<3><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+            case 4: gen_edges_kernel<4><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+            case 5: gen_edges_kernel<5><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+            case 6: gen_edges_kernel<6><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+            case 7: gen_edges_kernel<7><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+            case 8: gen_edges_kernel<8><<<g, 256, 0, s>>>(n, m, seed, edges); break;
+        }
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+
+extern "C" peel_status peel_gen_keys(uint64_t nkeys, uint64_t seed, uint64_t *keys, void *stream) {
+    if (nkeys == 0) return PEEL_OK;
+    if (!keys) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    {
+        ProfScope ps("gen_keys", s);
+        gen_keys_kernel<<<grid_for(nkeys), 256, 0, s>>>(nkeys, seed, keys);
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}

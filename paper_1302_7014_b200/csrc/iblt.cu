@@ -1,0 +1,428 @@
+// iblt.cu -- IBLT insert/delete and round-synchronous recovery on sm_100a
+// (P:474-513).
+//
+// Cells are 16 B {u32 count, u32 hashSum, u64 keySum}: two cells per 32-byte
+// sector, the three fields of one cell in one sector.  Insert/delete: one
+// thread per key, r x 3 atomics.  Recovery is the 2-core peel of
+// the IBLT's hypergraph, one cooperative persistent kernel:
+//
+//   round 1   scan all C cells; pure cells -> frontier entries (cell, key)
+//             (the key is snapshotted) + round-start "pure" bitmap.
+//   phase A   for each entry (c, x): x is recovered by this entry iff c is
+//             the LOWEST-index cell among h_1(x)..h_r(x) that was pure at round
+//             start (each round-start-pure cell holding x holds only x, so the
+//             owner is unique: exactly-once deletion without the paper's r
+//             serial subtable steps).  The owner XOR-deletes x from
+//             its r cells with atomics; a cell whose count drops
+//             2 -> 1 becomes a candidate (deduplicated by a bitmap).
+//   phase B   clear the round's pure bits; re-test candidates for purity
+//             (a candidate may have dropped to 0 in the same round) and emit
+//             the next frontier.
+//   stop      at the first round with an empty frontier.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace peel {
+
+static constexpr uint32_t ISTAT_CAP = 65536;
+static constexpr int IB_BLOCK = 256;
+
+struct __align__(16) Cell {
+    uint32_t count;
+    uint32_t hashSum;
+    ull keySum;
+};
+static_assert(sizeof(Cell) == 16, "cell is 16 bytes");
+
+struct IbltCtl {
+    ull fcnt[3];   // frontier sizes, F_t uses fcnt[(t-1)%3]
+    ull ccnt[2];   // candidate-list sizes, round t appends ccnt[t%2]
+    ull nrec;      // keys recovered so far
+    ull rounds;
+    uint32_t nonzero;
+    uint32_t pad;
+};
+
+struct ILayout {
+    size_t cells, ctl, per_round, pure0, pure1, cand, Fc0, Fc1, Fk0, Fk1, clist, total;
+};
+
+static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static ILayout ilayout(uint64_t C) {
+    ILayout L;
+    size_t o = 0;
+    L.cells = o; o += al(sizeof(Cell) * C);
+    L.ctl = o; o += al(sizeof(IbltCtl));
+    L.per_round = o; o += al(sizeof(ull) * (ISTAT_CAP + 1));
+    L.pure0 = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
+    L.pure1 = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
+    L.cand = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
+    L.Fc0 = o; o += al(sizeof(uint32_t) * C);
+    L.Fc1 = o; o += al(sizeof(uint32_t) * C);
+    L.Fk0 = o; o += al(sizeof(ull) * C);
+    L.Fk1 = o; o += al(sizeof(ull) * C);
+    L.clist = o; o += al(sizeof(uint32_t) * C);
+    L.total = o;
+    return L;
+}
+
+// h_1(x)..h_r(x): r distinct cells
+template <int R>
+__device__ __forceinline__ void cells_of(ull x, ull C, ull seed_h, uint32_t (&c)[R]) {
+    int na = 0;
+    for (ull j = 0; na < R; j++) {
+        ull z = mix64(x ^ seed_h ^ ((j + 1) * 0xD1B54A32D192ED03ull));
+        uint32_t v = (uint32_t)__umul64hi(z, C);
+        bool dup = false;
+        #pragma unroll
+        for (int i = 0; i < R; i++) dup |= (i < na) && (c[i] == v);
+        if (!dup) {
+            #pragma unroll
+            for (int i = 0; i < R; i++) if (i == na) c[i] = v;
+            na++;
+        }
+    }
+}
+
+// checkSum(x)
+__device__ __forceinline__ uint32_t checksum(ull x, ull seed_c) { return (uint32_t)(mix64(x ^ seed_c) >> 32); }
+
+__device__ __forceinline__ Cell ld_cell_cg(const Cell *p) {
+    uint4 v = __ldcg(reinterpret_cast<const uint4 *>(p));
+    Cell c;
+    c.count = v.x;
+    c.hashSum = v.y;
+    c.keySum = ((ull)v.w << 32) | v.z;
+    return c;
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ull seed_h, ull seed_c,
+                                                          const ull *__restrict__ keys, ull nkeys,
+                                                          uint32_t delta) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
+        const ull x = __ldg(keys + i);
+        uint32_t c[R];
+        cells_of<R>(x, C, seed_h, c);
+        const uint32_t h = checksum(x, seed_c);
+        #pragma unroll
+        for (int j = 0; j < R; j++) {
+            Cell *p = cells + c[j];
+            atomicAdd(&p->count, delta);
+            atomicXor(&p->keySum, x);
+            atomicXor(&p->hashSum, h);
+        }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) iblt_edges_kernel(ull C, ull seed_h, const ull *__restrict__ keys,
+                                                         ull nkeys, uint32_t *edges) {
+    for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
+        uint32_t c[R];
+        cells_of<R>(__ldg(keys + i), C, seed_h, c);
+        #pragma unroll
+        for (int j = 0; j < R; j++) edges[i * R + j] = c[j];
+    }
+}
+
+struct IPeelArgs {
+    Cell *cells;
+    ull C, seed_h, seed_c;
+    IbltCtl *ctl;
+    ull *per_round;
+    uint32_t *pure[2];  // round-start pure bitmaps: F_t's bits live in pure[(t-1)&1]
+    uint32_t *cand;
+    uint32_t *Fc[2];
+    ull *Fk[2];
+    uint32_t *clist;
+    ull *out;
+    ull cap_keys;
+};
+
+__device__ __forceinline__ bool is_pure(const Cell &c, ull seed_c) {
+    return c.count == 1u && c.hashSum == checksum(c.keySum, seed_c);
+}
+
+__device__ __forceinline__ void emit_entry(uint32_t *pure, uint32_t c, ull key, uint32_t *Fc, ull *Fk,
+                                           ull *cnt) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    ull base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(cnt, (ull)g.size());
+    base = g.shfl(base, 0) + g.thread_rank();
+    Fc[base] = c;
+    Fk[base] = key;
+    atomicOr(pure + (c >> 5), 1u << (c & 31));
+}
+
+template <int R>
+__global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    IbltCtl *ctl = a.ctl;
+    const ull tid = blockIdx.x * (ull)blockDim.x + threadIdx.x;
+    const ull nthr = (ull)gridDim.x * blockDim.x;
+
+    // ---- round 1: every pure cell ("a single thread to each cell") ----
+    for (ull c = tid; c < a.C; c += nthr) {
+        Cell v = ld_cell_cg(a.cells + c);
+        if (is_pure(v, a.seed_c)) emit_entry(a.pure[0], (uint32_t)c, v.keySum, a.Fc[0], a.Fk[0], &ctl->fcnt[0]);
+    }
+    grid.sync();
+
+    uint32_t t = 1;
+    for (;;) {
+        const ull nF = ld_cg_u64(&ctl->fcnt[(t - 1) % 3]);
+        if (nF == 0) break;
+        if (tid == 0) ctl->fcnt[(t + 1) % 3] = 0;
+        const uint32_t *Fc = a.Fc[(t - 1) & 1];
+        const ull *Fk = a.Fk[(t - 1) & 1];
+        ull *ccnt = &ctl->ccnt[t & 1];
+        const uint32_t *pure_cur = a.pure[(t - 1) & 1];
+        ull recovered = 0;
+        // ---- phase A: owner rule, XOR-delete, candidates ----
+        for (ull i = tid; i < nF; i += nthr) {
+            const uint32_t c = ld_cg_u32(Fc + i);
+            const ull x = __ldcg(Fk + i);
+            uint32_t h[R];
+            cells_of<R>(x, a.C, a.seed_h, h);
+            bool owner = false, found = false;
+            #pragma unroll
+            for (int j = 0; j < R; j++) {
+                if (!found && h[j] == c) { found = true; owner = true; }
+                if (!found && (ld_cg_u32(pure_cur + (h[j] >> 5)) >> (h[j] & 31) & 1u)) break;
+            }
+            if (!owner) continue;
+            recovered++;
+            {
+                cg::coalesced_group g = cg::coalesced_threads();
+                ull base = 0;
+                if (g.thread_rank() == 0) base = atomicAdd(&ctl->nrec, (ull)g.size());
+                base = g.shfl(base, 0) + g.thread_rank();
+                if (base < a.cap_keys) a.out[base] = x;
+            }
+            const uint32_t hx = checksum(x, a.seed_c);
+            #pragma unroll
+            for (int j = 0; j < R; j++) {
+                Cell *p = a.cells + h[j];
+                const uint32_t old = atomicAdd(&p->count, 0xFFFFFFFFu);
+                atomicXor(&p->keySum, x);
+                atomicXor(&p->hashSum, hx);
+                if (old == 2u) {
+                    const uint32_t bit = 1u << (h[j] & 31);
+                    if (!(atomicOr(a.cand + (h[j] >> 5), bit) & bit)) append<uint32_t>(a.clist, ccnt, h[j]);
+                }
+            }
+        }
+        block_add<IB_BLOCK>(&a.per_round[t <= ISTAT_CAP ? t - 1 : ISTAT_CAP], recovered);
+        grid.sync();
+        // ---- phase B: retire this round's pure bits, re-test candidates ----
+        for (ull i = tid; i < nF; i += nthr) {
+            const uint32_t c = ld_cg_u32(Fc + i);
+            atomicAnd(a.pure[(t - 1) & 1] + (c >> 5), ~(1u << (c & 31)));
+        }
+        if (tid == 0) ctl->ccnt[(t + 1) & 1] = 0;
+        const ull nC = ld_cg_u64(ccnt);
+        uint32_t *Fcn = a.Fc[t & 1];
+        ull *Fkn = a.Fk[t & 1];
+        for (ull i = tid; i < nC; i += nthr) {
+            const uint32_t c = ld_cg_u32(a.clist + i);
+            atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
+            Cell v = ld_cell_cg(a.cells + c);
+            if (is_pure(v, a.seed_c)) emit_entry(a.pure[t & 1], c, v.keySum, Fcn, Fkn, &ctl->fcnt[t % 3]);
+        }
+        grid.sync();
+        t++;
+    }
+    if (tid == 0) ctl->rounds = t - 1;
+    // ---- complete iff every cell is zero ----
+    uint32_t nz = 0;
+    for (ull c = tid; c < a.C; c += nthr) {
+        Cell v = ld_cell_cg(a.cells + c);
+        nz |= (v.count | v.hashSum) != 0u || v.keySum != 0ull;
+    }
+    if (__any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nonzero, 1u);
+}
+
+static unsigned grid_for(ull work, int per_sm = 16) {
+    ull blocks = (work + 255) / 256;
+    ull cap = (ull)num_sms() * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) blocks = 1;
+    return (unsigned)blocks;
+}
+
+}  // namespace peel
+
+using namespace peel;
+
+struct peel_iblt {
+    ull C;
+    uint32_t r;
+    ull seed, seed_h, seed_c;
+    char *mem;
+    ILayout L;
+};
+
+static ull host_mix64(ull z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+extern "C" size_t iblt_mem_bytes(uint64_t cells, uint32_t r) {
+    if (r < 2 || r > 8 || cells < r || cells >= (1ull << 32)) return 0;
+    return ilayout(cells).total;
+}
+
+extern "C" peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, void *mem, size_t mem_bytes,
+                                  void *stream, peel_iblt **out) {
+    if (!out || !mem || r < 2 || r > 8 || cells < r || cells >= (1ull << 32)) return PEEL_EINVAL;
+    if (((uintptr_t)mem & 15) != 0) return PEEL_EINVAL;
+    ILayout L = ilayout(cells);
+    if (mem_bytes < L.total) return PEEL_ENOMEM;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    PEEL_CUDA(cudaMemsetAsync(mem, 0, sizeof(Cell) * cells, s));
+    peel_iblt *t = new peel_iblt;
+    t->C = cells;
+    t->r = r;
+    t->seed = seed;
+    const ull G = 0x9E3779B97F4A7C15ull;
+    t->seed_h = host_mix64((seed ^ 0x6A09E667F3BCC909ull) + G);
+    t->seed_c = host_mix64((seed ^ 0xBB67AE8584CAA73Bull) + G);
+    t->mem = (char *)mem;
+    t->L = L;
+    *out = t;
+    return PEEL_OK;
+}
+
+static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, uint32_t delta,
+                               void *stream) {
+    if (!t) return PEEL_EINVAL;
+    if (nkeys == 0) return PEEL_OK;
+    if (!keys) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    Cell *cells = (Cell *)(t->mem + t->L.cells);
+    unsigned g = grid_for(nkeys);
+    {
+        ProfScope ps(delta == 1u ? "iblt_insert" : "iblt_delete", s);
+        switch (t->r) {
+            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+        }
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+
+extern "C" peel_status iblt_insert(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, void *stream) {
+    return iblt_update(t, keys, nkeys, 1u, stream);
+}
+
+extern "C" peel_status iblt_delete(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, void *stream) {
+    return iblt_update(t, keys, nkeys, 0xFFFFFFFFu, stream);
+}
+
+template <int R>
+static peel_status run_iblt_peel(peel_iblt *t, IPeelArgs &a, cudaStream_t s) {
+    auto kern = iblt_peel_kernel<R>;
+    int per_sm = 0;
+    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, IB_BLOCK, 0));
+    if (per_sm < 1) per_sm = 1;
+    unsigned grid = (unsigned)(num_sms() * per_sm);
+    void *args[] = {&a};
+    ProfScope ps("iblt_peel_rounds", s);
+    PEEL_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, IB_BLOCK, args, 0, s));
+    (void)t;
+    return PEEL_OK;
+}
+
+extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
+                                 uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete,
+                                 void *stream) {
+    if (!t || !nrecovered || !rounds || (cap_keys && !out_keys)) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    const ILayout &L = t->L;
+    char *m = t->mem;
+    // zero control, per-round stats and both bitmaps (contiguous)
+    PEEL_CUDA(cudaMemsetAsync(m + L.ctl, 0, L.Fc0 - L.ctl, s));
+    IPeelArgs a;
+    memset(&a, 0, sizeof a);
+    a.cells = (Cell *)(m + L.cells);
+    a.C = t->C;
+    a.seed_h = t->seed_h;
+    a.seed_c = t->seed_c;
+    a.ctl = (IbltCtl *)(m + L.ctl);
+    a.per_round = (ull *)(m + L.per_round);
+    a.pure[0] = (uint32_t *)(m + L.pure0);
+    a.pure[1] = (uint32_t *)(m + L.pure1);
+    a.cand = (uint32_t *)(m + L.cand);
+    a.Fc[0] = (uint32_t *)(m + L.Fc0);
+    a.Fc[1] = (uint32_t *)(m + L.Fc1);
+    a.Fk[0] = (ull *)(m + L.Fk0);
+    a.Fk[1] = (ull *)(m + L.Fk1);
+    a.clist = (uint32_t *)(m + L.clist);
+    a.out = (ull *)out_keys;
+    a.cap_keys = cap_keys;
+    peel_status st = PEEL_EINVAL;
+    switch (t->r) {
+        case 2: st = run_iblt_peel<2>(t, a, s); break;
+        case 3: st = run_iblt_peel<3>(t, a, s); break;
+        case 4: st = run_iblt_peel<4>(t, a, s); break;
+        case 5: st = run_iblt_peel<5>(t, a, s); break;
+        case 6: st = run_iblt_peel<6>(t, a, s); break;
+        case 7: st = run_iblt_peel<7>(t, a, s); break;
+        case 8: st = run_iblt_peel<8>(t, a, s); break;
+    }
+    if (st != PEEL_OK) return st;
+    IbltCtl h;
+    PEEL_CUDA(cudaMemcpyAsync(&h, a.ctl, sizeof h, cudaMemcpyDeviceToHost, s));
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    prof_collect();
+    *nrecovered = h.nrec;
+    *rounds = (uint32_t)h.rounds;
+    if (complete) *complete = h.nonzero ? 0 : 1;
+    uint64_t nstore = h.rounds < cap ? h.rounds : cap;
+    if (nstore > ISTAT_CAP) nstore = ISTAT_CAP;
+    if (per_round && nstore)
+        PEEL_CUDA(cudaMemcpy(per_round, a.per_round, sizeof(ull) * nstore, cudaMemcpyDeviceToHost));
+    if (h.nrec > cap_keys || h.rounds > cap || h.rounds > ISTAT_CAP) return PEEL_ETRUNC;
+    return PEEL_OK;
+}
+
+extern "C" void *iblt_cells(const peel_iblt *t) { return t ? (void *)(t->mem + t->L.cells) : nullptr; }
+
+extern "C" peel_status iblt_to_hypergraph(const peel_iblt *t, const uint64_t *keys, uint64_t nkeys,
+                                          uint32_t *edges, void *stream) {
+    if (!t) return PEEL_EINVAL;
+    if (nkeys == 0) return PEEL_OK;
+    if (!keys || !edges) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    unsigned g = grid_for(nkeys);
+    {
+        ProfScope ps("iblt_edges", s);
+        switch (t->r) {
+            case 2: iblt_edges_kernel<2><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 3: iblt_edges_kernel<3><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 4: iblt_edges_kernel<4><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 5: iblt_edges_kernel<5><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 6: iblt_edges_kernel<6><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 7: iblt_edges_kernel<7><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 8: iblt_edges_kernel<8><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+        }
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+
+extern "C" void iblt_destroy(peel_iblt *t) { delete t; }

@@ -1,0 +1,528 @@
+// kcore.cu -- a2-a7: round-synchronous parallel peeling to the k-core on sm_100a.
+//
+// The method: round t removes the snapshot
+// F_t = {alive v : deg_t(v) < k} and every alive edge with an endpoint in F_t;
+// stop at the first empty F_t.  This file computes exactly that schedule with
+// work proportional to the edges actually removed:
+//
+//  * build   -- per-vertex state from one coalesced pass over edges[m][r]:
+//               k <= 2 "packed": u64 {count:24 | idsum:40}, one 64-bit atomic per
+//               endpoint adds (1<<40) + e; when count == 1 the idsum IS the one
+//               alive incident edge, so no incidence lists are needed.
+//               k >= 3 "CSR": u32 degree histogram, exclusive scan, scatter of
+//               edge ids into adj[r m].
+//  * rounds  -- ONE cooperative persistent kernel runs every round with a grid
+//               barrier between rounds (no host round trips, P:505-506 done on
+//               device):
+//                 round 1 frontier = scan of all n vertices for count < k;
+//                 round t: each v in F_t finds its alive edges; an edge is killed
+//                 exactly once by test-and-clear of its alive bit (atomicAnd);
+//                 the winner decrements the other endpoints; the ONE decrement
+//                 that takes a count from k to k-1 appends that vertex to F_{t+1}
+//                 (a warp-aggregated append) -- so F_{t+1} is built without any
+//                 rescan, and each vertex is appended once.
+//               After the last round, core_mask[v] = (count(v) >= k): a removed
+//               vertex had count < k when removed and counts never increase.
+#include <string.h>
+
+#include "common.cuh"
+
+namespace peel {
+
+static constexpr uint32_t STAT_CAP = 65536;  // per-round statistics kept on device
+static constexpr int PEEL_BLOCK = 256;
+
+enum : uint32_t { ERR_BADVERTEX = 1u, ERR_OVERFLOW = 2u };
+
+struct Ctl {
+    ull cnt[3];       // frontier sizes, rotating: F_t uses cnt[(t-1)%3]
+    ull rounds;       // number of non-empty rounds
+    uint32_t err;     // ERR_* bits
+    uint32_t pad;
+    ull pad2[3];
+};
+
+struct Layout {
+    size_t ctl, fsize, killed, state, deg, off, bsum, adj, alive, F0, F1, total;
+};
+
+static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static constexpr uint32_t SCAN_TILE = 2048;  // 256 threads x 8 elements
+
+static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
+    Layout L;
+    size_t o = 0;
+    L.ctl = o; o += al(sizeof(Ctl));
+    L.fsize = o; o += al(sizeof(ull) * (STAT_CAP + 1));
+    L.killed = o; o += al(sizeof(ull) * (STAT_CAP + 1));
+    if (!csr) {
+        L.state = o; o += al(sizeof(ull) * n);
+        L.deg = L.off = L.bsum = L.adj = 0;
+    } else {
+        L.state = 0;
+        L.deg = o; o += al(sizeof(uint32_t) * n);
+        L.off = o; o += al(sizeof(uint32_t) * n);
+        L.bsum = o; o += al(sizeof(uint32_t) * ((n + SCAN_TILE - 1) / SCAN_TILE + 1));
+        L.adj = o; o += al(sizeof(uint32_t) * r * m);
+    }
+    L.alive = o; o += al(sizeof(uint32_t) * ((m + 31) / 32));
+    L.F0 = o; o += al(sizeof(uint32_t) * n);
+    L.F1 = o; o += al(sizeof(uint32_t) * n);
+    L.total = o;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+// build
+// ---------------------------------------------------------------------------
+template <int R>
+__device__ __forceinline__ bool load_edge(const uint32_t *__restrict__ edges, uint64_t e, uint64_t n,
+                                          uint32_t (&u)[R]) {
+    bool ok = true;
+    #pragma unroll
+    for (int j = 0; j < R; j++) {
+        u[j] = __ldg(edges + e * R + j);
+        ok &= (uint64_t)u[j] < n;
+    }
+    #pragma unroll
+    for (int i = 0; i < R; i++)
+        #pragma unroll
+        for (int j = i + 1; j < R; j++) ok &= u[i] != u[j];
+    return ok;
+}
+
+// packed k<=2 build: state[u] += (1<<40) + e for every endpoint (P:500-501's
+// atomic-update pattern, applied to the degree/id-sum accumulators).
+// CHECK (m > 2^23): use the returning atomic and flag the increment that takes a
+// count to ovf_count -- until then id-sums cannot have carried into the count
+// field, so the flag is exact even for degrees that would wrap the 24-bit count.
+// Without CHECK (m <= 2^23) counts stay below 2^24 and the round-1 scan's check
+// of the final count is exact.
+template <int R, bool CHECK>
+__global__ void __launch_bounds__(256) build_packed_kernel(const uint32_t *__restrict__ edges,
+                                                           uint64_t n, uint64_t m, ull *state,
+                                                           Ctl *ctl, ull ovf_count) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t u[R];
+        if (!load_edge<R>(edges, e, n, u)) {
+            atomicOr(&ctl->err, ERR_BADVERTEX);
+            continue;
+        }
+        const ull inc = (1ull << 40) + e;
+        if (CHECK) {
+            bool ovf = false;
+            #pragma unroll
+            for (int j = 0; j < R; j++) ovf |= (atomicAdd(state + u[j], inc) >> 40) + 1 >= ovf_count;
+            if (ovf) atomicOr(&ctl->err, ERR_OVERFLOW);
+        } else {
+            #pragma unroll
+            for (int j = 0; j < R; j++) atomicAdd(state + u[j], inc);
+        }
+    }
+}
+
+// CSR build, pass 1: degree histogram
+template <int R>
+__global__ void __launch_bounds__(256) build_deg_kernel(const uint32_t *__restrict__ edges, uint64_t n,
+                                                        uint64_t m, uint32_t *deg, Ctl *ctl) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t u[R];
+        if (!load_edge<R>(edges, e, n, u)) {
+            atomicOr(&ctl->err, ERR_BADVERTEX);
+            continue;
+        }
+        #pragma unroll
+        for (int j = 0; j < R; j++) atomicAdd(deg + u[j], 1u);
+    }
+}
+
+// exclusive scan of deg into off, tile pass: local exclusive scan + tile total
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *total) {
+    __shared__ uint32_t ws[PEEL_BLOCK / 32];
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+    #pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < PEEL_BLOCK / 32 ? ws[lane] : 0;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < PEEL_BLOCK / 32) ws[lane] = s;
+    }
+    __syncthreads();
+    uint32_t before = (w ? ws[w - 1] : 0) + x - v;
+    *total = ws[PEEL_BLOCK / 32 - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(PEEL_BLOCK) scan_tiles_kernel(const uint32_t *__restrict__ deg,
+                                                                uint64_t n, uint32_t *off,
+                                                                uint32_t *bsum) {
+    const int PER = SCAN_TILE / PEEL_BLOCK;
+    uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * PER;
+    uint32_t v[PER], s = 0;
+    #pragma unroll
+    for (int i = 0; i < PER; i++) {
+        v[i] = base + i < n ? deg[base + i] : 0;
+        s += v[i];
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan(s, &tot);
+    #pragma unroll
+    for (int i = 0; i < PER; i++) {
+        if (base + i < n) off[base + i] = ex;
+        ex += v[i];
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(PEEL_BLOCK) scan_bsum_kernel(uint32_t *bsum, uint64_t nb) {
+    uint32_t carry = 0;
+    for (uint64_t b0 = 0; b0 < nb; b0 += PEEL_BLOCK) {
+        uint64_t i = b0 + threadIdx.x;
+        uint32_t v = i < nb ? bsum[i] : 0, tot;
+        uint32_t ex = block_exclusive_scan(v, &tot);
+        if (i < nb) bsum[i] = carry + ex;
+        carry += tot;
+    }
+}
+
+__global__ void __launch_bounds__(PEEL_BLOCK) scan_add_kernel(uint32_t *off, uint64_t n,
+                                                              const uint32_t *__restrict__ bsum) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        off[i] += bsum[i / SCAN_TILE];
+}
+
+// CSR build, pass 2: scatter edge ids; afterwards off[u] = END of u's list
+template <int R>
+__global__ void __launch_bounds__(256) scatter_kernel(const uint32_t *__restrict__ edges, uint64_t n,
+                                                      uint64_t m, uint32_t *off, uint32_t *adj) {
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t u[R];
+        if (!load_edge<R>(edges, e, n, u)) continue;  // flagged by build_deg_kernel
+        #pragma unroll
+        for (int j = 0; j < R; j++) {
+            uint32_t pos = atomicAdd(off + u[j], 1u);
+            adj[pos] = (uint32_t)e;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the round loop: one cooperative persistent kernel
+// ---------------------------------------------------------------------------
+struct PeelArgs {
+    const uint32_t *edges;
+    uint64_t n, m;
+    uint32_t k;
+    uint32_t stat_cap;
+    ull *state;              // packed path
+    uint32_t *deg;           // CSR path
+    const uint32_t *off_end; // CSR path: end of u's adjacency list
+    const uint32_t *adj;     // CSR path
+    uint32_t *alive;
+    uint32_t *F[2];
+    Ctl *ctl;
+    ull *fsize;
+    ull *killed;
+    uint8_t *core_mask;
+    uint32_t *peel_round;
+    ull ovf_count;           // packed path: a count >= this may have overflowed idsum
+};
+
+__device__ __forceinline__ void on_crossing(const PeelArgs &a, uint32_t u, uint32_t *Fn, ull *cn,
+                                            uint32_t next_round) {
+    append<uint32_t>(Fn, cn, u);
+    if (a.peel_round) a.peel_round[u] = next_round;
+}
+
+template <int R, bool CSR>
+__global__ void __launch_bounds__(PEEL_BLOCK) peel_rounds_kernel(PeelArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    Ctl *ctl = a.ctl;
+    if (ld_cg_u32(&ctl->err) & ERR_BADVERTEX) return;  // uniform across the grid
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t k = a.k;
+
+    // ---- round 1 frontier: F_1 = {v : deg(v) < k} (a full scan) ----
+    for (uint64_t v = tid; v < a.n; v += nthr) {
+        uint32_t c;
+        if (CSR) {
+            c = a.deg[v];
+        } else {
+            ull s = a.state[v];
+            c = (uint32_t)(s >> 40);
+            if (c >= a.ovf_count) atomicOr(&ctl->err, ERR_OVERFLOW);  // exact for m <= 2^23
+        }
+        if (c < k) on_crossing(a, (uint32_t)v, a.F[0], &ctl->cnt[0], 1);
+    }
+    grid.sync();
+    if (ld_cg_u32(&ctl->err) & ERR_OVERFLOW) return;
+
+    // ---- rounds ----
+    uint32_t t = 1;
+    for (;;) {
+        const ull nF = ld_cg_u64(&ctl->cnt[(t - 1) % 3]);
+        if (nF == 0) break;
+        if (tid == 0) {
+            a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
+            ctl->cnt[(t + 1) % 3] = 0;  // F_{t+2}'s counter; its last reader finished a barrier ago
+        }
+        const uint32_t *Fc = a.F[(t - 1) & 1];
+        uint32_t *Fn = a.F[t & 1];
+        ull *cn = &ctl->cnt[t % 3];
+        ull kills = 0;
+        for (uint64_t i = tid; i < nF; i += nthr) {
+            const uint32_t v = ld_cg_u32(Fc + i);
+            if (!CSR) {
+                // packed: count <= 1 here; if 1, the id-sum is the one alive edge
+                const ull s = ld_cg_u64(a.state + v);
+                if ((s >> 40) != 1) continue;
+                const uint32_t e = (uint32_t)(s & ((1ull << 40) - 1));
+                const uint32_t bit = 1u << (e & 31);
+                if (!(atomicAnd(a.alive + (e >> 5), ~bit) & bit)) continue;  // exactly-once kill
+                kills++;
+                const ull dec = 0ull - ((1ull << 40) + e);
+                #pragma unroll
+                for (int j = 0; j < R; j++) {
+                    const uint32_t u = __ldg(a.edges + (uint64_t)e * R + j);
+                    if (u == v) continue;
+                    const ull old = atomicAdd(a.state + u, dec);
+                    if ((uint32_t)(old >> 40) == k) on_crossing(a, u, Fn, cn, t + 1);
+                }
+            } else {
+                const uint32_t b = v ? ld_cg_u32(a.off_end + v - 1) : 0u;
+                const uint32_t eend = ld_cg_u32(a.off_end + v);
+                for (uint32_t p = b; p < eend; p++) {
+                    const uint32_t e = __ldg(a.adj + p);
+                    const uint32_t bit = 1u << (e & 31);
+                    if (!(ld_cg_u32(a.alive + (e >> 5)) & bit)) continue;
+                    if (!(atomicAnd(a.alive + (e >> 5), ~bit) & bit)) continue;
+                    kills++;
+                    #pragma unroll
+                    for (int j = 0; j < R; j++) {
+                        const uint32_t u = __ldg(a.edges + (uint64_t)e * R + j);
+                        if (u == v) continue;
+                        const uint32_t old = atomicSub(a.deg + u, 1u);
+                        if (old == k) on_crossing(a, u, Fn, cn, t + 1);
+                    }
+                }
+            }
+        }
+        block_add<PEEL_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
+        grid.sync();
+        t++;
+    }
+    if (tid == 0) ctl->rounds = t - 1;
+
+    // ---- outputs: core_mask[v] = count(v) >= k (counts only decrease) ----
+    for (uint64_t v = tid; v < a.n; v += nthr) {
+        uint32_t c = CSR ? ld_cg_u32(a.deg + v) : (uint32_t)(ld_cg_u64(a.state + v) >> 40);
+        a.core_mask[v] = c >= k ? 1 : 0;
+    }
+}
+
+static unsigned grid_for(uint64_t work, int per_sm = 16) {
+    uint64_t blocks = (work + 255) / 256;
+    uint64_t cap = (uint64_t)num_sms() * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks == 0) blocks = 1;
+    return (unsigned)blocks;
+}
+
+template <int R>
+static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr,
+                             uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
+                             uint64_t *killed, uint32_t cap, uint32_t *peel_round, char *ws,
+                             const Layout &L, cudaStream_t s) {
+    Ctl *ctl = (Ctl *)(ws + L.ctl);
+    ull *fsize = (ull *)(ws + L.fsize);
+    ull *kil = (ull *)(ws + L.killed);
+    uint32_t *alive = (uint32_t *)(ws + L.alive);
+    PEEL_CUDA(cudaMemsetAsync(ws + L.ctl, 0, L.state ? L.state - L.ctl : L.deg - L.ctl, s));
+    PEEL_CUDA(cudaMemsetAsync(alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s));
+
+    PeelArgs a;
+    memset(&a, 0, sizeof a);
+    a.edges = edges; a.n = n; a.m = m; a.k = k;
+    a.stat_cap = STAT_CAP;
+    a.alive = alive;
+    a.F[0] = (uint32_t *)(ws + L.F0);
+    a.F[1] = (uint32_t *)(ws + L.F1);
+    a.ctl = ctl; a.fsize = fsize; a.killed = kil;
+    a.core_mask = core_mask; a.peel_round = peel_round;
+    if (peel_round) PEEL_CUDA(cudaMemsetAsync(peel_round, 0, sizeof(uint32_t) * n, s));
+
+    if (!csr) {
+        ull *state = (ull *)(ws + L.state);
+        PEEL_CUDA(cudaMemsetAsync(state, 0, sizeof(ull) * n, s));
+        a.state = state;
+        a.ovf_count = m > 1 ? ((1ull << 40) + (m - 1) - 1) / (m - 1) : (1ull << 24);
+        if (a.ovf_count > (1ull << 24) - 1) a.ovf_count = (1ull << 24) - 1;
+        if (m > (1ull << 23)) {
+            ProfScope ps("build_packed", s);
+            build_packed_kernel<R, true><<<grid_for(m), 256, 0, s>>>(edges, n, m, state, ctl, a.ovf_count);
+        } else if (m) {
+            ProfScope ps("build_packed", s);
+            build_packed_kernel<R, false><<<grid_for(m), 256, 0, s>>>(edges, n, m, state, ctl, a.ovf_count);
+        }
+    } else {
+        uint32_t *deg = (uint32_t *)(ws + L.deg);
+        uint32_t *off = (uint32_t *)(ws + L.off);
+        uint32_t *bsum = (uint32_t *)(ws + L.bsum);
+        uint32_t *adj = (uint32_t *)(ws + L.adj);
+        PEEL_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * n, s));
+        if (m) {
+            ProfScope ps("build_deg", s);
+            build_deg_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, deg, ctl);
+        }
+        uint64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+        {
+            ProfScope ps("scan_tiles", s);
+            scan_tiles_kernel<<<(unsigned)nb, PEEL_BLOCK, 0, s>>>(deg, n, off, bsum);
+        }
+        {
+            ProfScope ps("scan_bsum", s);
+            scan_bsum_kernel<<<1, PEEL_BLOCK, 0, s>>>(bsum, nb);
+        }
+        {
+            ProfScope ps("scan_add", s);
+            scan_add_kernel<<<grid_for(n), PEEL_BLOCK, 0, s>>>(off, n, bsum);
+        }
+        if (m) {
+            ProfScope ps("scatter", s);
+            scatter_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, off, adj);
+        }
+        a.deg = deg; a.off_end = off; a.adj = adj;
+        a.ovf_count = ~0ull;
+    }
+    PEEL_CUDA(cudaGetLastError());
+
+    // cooperative persistent round loop: every block must be co-resident
+    auto kern = csr ? peel_rounds_kernel<R, true> : peel_rounds_kernel<R, false>;
+    int per_sm = 0;
+    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PEEL_BLOCK, 0));
+    if (per_sm < 1) per_sm = 1;
+    unsigned grid = (unsigned)(num_sms() * per_sm);
+    void *args[] = {&a};
+    {
+        ProfScope ps(csr ? "peel_rounds_csr" : "peel_rounds_packed", s);
+        PEEL_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, PEEL_BLOCK, args, 0, s));
+    }
+
+    // results
+    Ctl hctl;
+    PEEL_CUDA(cudaMemcpyAsync(&hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    prof_collect();
+    if (hctl.err & ERR_BADVERTEX) return PEEL_EINVAL;
+    if (hctl.err & ERR_OVERFLOW) return PEEL_EOVERFLOW;
+    uint64_t T = hctl.rounds;
+    *rounds = (uint32_t)T;
+    uint64_t nstore = T < cap ? T : cap;
+    if (nstore > STAT_CAP) nstore = STAT_CAP;
+    if (nstore && (survivors || killed)) {
+        ull *hf = new ull[nstore];
+        cudaError_t e1 = cudaMemcpy(hf, fsize, sizeof(ull) * nstore, cudaMemcpyDeviceToHost);
+        if (e1 != cudaSuccess) { delete[] hf; set_cuda_error(e1, "copy fsize"); return PEEL_ECUDA; }
+        if (survivors) {
+            uint64_t alive_v = n;
+            for (uint64_t t = 0; t < nstore; t++) { alive_v -= hf[t]; survivors[t] = alive_v; }
+        }
+        delete[] hf;
+        if (killed) PEEL_CUDA(cudaMemcpy(killed, kil, sizeof(ull) * nstore, cudaMemcpyDeviceToHost));
+    }
+    return (T > cap || T > STAT_CAP) ? PEEL_ETRUNC : PEEL_OK;
+}
+
+static bool kcore_args_ok(uint64_t n, uint64_t m, uint32_t r, uint32_t k, bool csr) {
+    if (r < 2 || r > 8 || n > (1ull << 32) || m >= (1ull << 32)) return false;
+    if (csr && (uint64_t)r * m >= (1ull << 32)) return false;
+    (void)k;
+    return true;
+}
+
+static bool use_csr(uint32_t k, uint32_t flags) { return (flags & PEEL_FLAG_CSR) || k >= 3; }
+
+}  // namespace peel
+
+using namespace peel;
+
+extern "C" size_t peel_kcore_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k,
+                                             uint32_t flags) {
+    bool csr = use_csr(k, flags);
+    if (!kcore_args_ok(n, m, r, k, csr)) return 0;
+    return layout(n, m, r, csr).total;
+}
+
+extern "C" peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r,
+                                  uint32_t k, uint32_t flags, uint8_t *core_mask, uint32_t *rounds,
+                                  uint64_t *survivors, uint64_t *killed, uint32_t cap,
+                                  uint32_t *peel_round, void *workspace, size_t ws_bytes,
+                                  void *stream) {
+    bool csr = use_csr(k, flags);
+    if (!kcore_args_ok(n, m, r, k, csr) || !rounds) return PEEL_EINVAL;
+    if ((m && !edges) || (n && !core_mask) || !workspace) return PEEL_EINVAL;
+    Layout L = layout(n, m, r, csr);
+    if (ws_bytes < L.total) return PEEL_ENOMEM;
+    prof_begin_call();
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        *rounds = 0;
+        return PEEL_OK;
+    }
+    char *ws = (char *)workspace;
+    switch (r) {
+        case 2: return run_kcore<2>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 3: return run_kcore<3>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 4: return run_kcore<4>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 5: return run_kcore<5>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 6: return run_kcore<6>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 7: return run_kcore<7>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 8: return run_kcore<8>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+    }
+    return PEEL_EINVAL;
+}
+
+extern "C" size_t peel_kcore_host_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k,
+                                                  uint32_t flags) {
+    size_t w = peel_kcore_workspace_bytes(n, m, r, k, flags);
+    if (!w) return 0;
+    return w + al(sizeof(uint32_t) * r * m) + al(n);
+}
+
+extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, uint64_t m,
+                                       uint32_t r, uint32_t k, uint32_t flags,
+                                       uint8_t *core_mask_host, uint32_t *rounds,
+                                       uint64_t *survivors, uint64_t *killed, uint32_t cap,
+                                       void *workspace, size_t ws_bytes, void *stream) {
+    size_t w = peel_kcore_workspace_bytes(n, m, r, k, flags);
+    if (!w || !rounds || !workspace || (m && !edges_host) || (n && !core_mask_host)) return PEEL_EINVAL;
+    if (ws_bytes < peel_kcore_host_workspace_bytes(n, m, r, k, flags)) return PEEL_ENOMEM;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *base = (char *)workspace;
+    uint32_t *d_edges = (uint32_t *)(base + w);
+    uint8_t *d_mask = (uint8_t *)(base + w + al(sizeof(uint32_t) * r * m));
+    if (m) PEEL_CUDA(cudaMemcpyAsync(d_edges, edges_host, sizeof(uint32_t) * r * m, cudaMemcpyHostToDevice, s));
+    peel_status st = peel_kcore(d_edges, n, m, r, k, flags, d_mask, rounds, survivors, killed, cap,
+                                nullptr, workspace, w, stream);
+    if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
+    if (n) PEEL_CUDA(cudaMemcpyAsync(core_mask_host, d_mask, n, cudaMemcpyDeviceToHost, s));
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    return st;
+}

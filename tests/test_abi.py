@@ -1,0 +1,79 @@
+"""The C-ABI library loads and exports every entry point include/peel.h declares;
+host-side argument validation and workspace queries (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1302_7014_b200 as pk
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "peel.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^[A-Za-z_][\w \*]*?\b([a-z_][a-z0-9_]*)\s*\(", src, flags=re.M)
+    return sorted(set(n for n in names if n not in ("if", "while")))
+
+
+def test_header_declares_the_north_star_entry_points():
+    fns = header_functions()
+    for f in ("peel_kcore", "iblt_build", "iblt_insert", "iblt_peel", "peel_gen_hypergraph"):
+        assert f in fns
+
+
+def test_library_exports_every_header_symbol():
+    L = pk.lib()
+    missing = [f for f in header_functions() if not hasattr(L, f)]
+    assert not missing, missing
+
+
+def test_abi_version_and_strerror():
+    L = pk.lib()
+    assert L.peel_abi_version() == 1
+    for s in range(7):
+        assert L.peel_strerror(s).decode().startswith("PEEL_")
+
+
+def test_workspace_queries():
+    L = pk.lib()
+    n, m = 10**9, 750 * 10**6
+    ws = L.peel_kcore_workspace_bytes(n, m, 3, 2, 0)
+    # packed k=2 layout: 8n state + 2 x 4n frontiers + m/8 alive bits + stats
+    assert 16 * n < ws < 16 * n + m // 8 + (4 << 20)
+    assert L.peel_kcore_workspace_bytes(n, m, 3, 3, 0) > ws  # CSR adds the incidence lists
+    assert L.peel_kcore_workspace_bytes(10, 10, 1, 2, 0) == 0  # r < 2
+    assert L.peel_kcore_workspace_bytes(10, 10, 9, 2, 0) == 0  # r > 8
+    assert L.peel_kcore_workspace_bytes(2**32 + 1, 10, 3, 2, 0) == 0
+    assert L.iblt_mem_bytes(10**7, 3) >= 16 * 10**7
+    assert L.iblt_mem_bytes(2, 3) == 0
+
+
+def test_invalid_arguments_rejected_before_any_launch():
+    L = pk.lib()
+    r = ctypes.c_uint32(0)
+    # r = 1
+    assert L.peel_kcore(None, 10, 0, 1, 2, 0, None, ctypes.addressof(r), None, None, 0, None, None, 0,
+                        None) == pk.PEEL_EINVAL
+    # null workspace
+    assert L.peel_kcore(None, 10, 0, 3, 2, 0, 1, ctypes.addressof(r), None, None, 0, None, None, 0,
+                        None) == pk.PEEL_EINVAL
+    # workspace too small
+    assert L.peel_kcore(None, 10, 0, 3, 2, 0, 1, ctypes.addressof(r), None, None, 0, None, 1, 16,
+                        None) == pk.PEEL_ENOMEM
+    assert L.peel_gen_hypergraph(2, 10, 3, 1, None, None) == pk.PEEL_EINVAL  # n < r
+    h = ctypes.c_void_p(0)
+    assert L.iblt_build(10, 1, 0, 16, 1 << 20, None, ctypes.byref(h)) == pk.PEEL_EINVAL
+    assert L.iblt_build(100, 3, 0, 8, 1 << 20, None, ctypes.byref(h)) == pk.PEEL_EINVAL  # misaligned
+
+
+def test_library_does_not_link_the_oracle():
+    # the product library and the oracle share no code: no oracle symbol is exported
+    L = pk.lib()
+    for sym in ("ora_sync_peel", "ora_gen_edge", "ora_iblt_peel"):
+        assert not hasattr(L, sym)
+    import subprocess
+    out = subprocess.run(["nm", "-D", pk.LIB_PATH], capture_output=True, text=True).stdout
+    assert "ora_" not in out

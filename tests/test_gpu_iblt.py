@@ -1,0 +1,121 @@
+"""GPU parity for the IBLT through the C-ABI against the oracle:
+cell contents after insert/delete (bit-exact), sorted recovered key set,
+rounds, per-round counts, completeness; the C2 config at full size."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1302_7014_b200 as pk
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+
+
+def keys_dev(k: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(k, dtype=np.uint64).view(np.int64)).to(DEV)
+
+
+def dev_cells(t: pk.Iblt):
+    c = t.cells().cpu().numpy()
+    count = c[:, 0].astype(np.int64)
+    hashsum = c[:, 1].view(np.uint32)
+    keysum = c[:, 2:4].copy().view(np.uint64).ravel()
+    return count, keysum, hashsum
+
+
+def compare(C, r, seed, keys, deletes=None):
+    t = pk.Iblt(C, r, seed, device=DEV)
+    o = O.Iblt(C, r, seed)
+    t.insert(keys_dev(keys))
+    o.insert(keys)
+    if deletes is not None:
+        t.delete(keys_dev(deletes))
+        o.delete(deletes)
+    cnt, ks, hs = dev_cells(t)
+    ocnt, oks, ohs = o.cells()
+    assert np.array_equal(cnt.astype(np.int32), ocnt.astype(np.int32))
+    assert np.array_equal(ks, oks) and np.array_equal(hs, ohs)
+    res = t.peel()
+    ref = o.peel()
+    got = np.sort(res.keys.cpu().numpy().view(np.uint64))
+    assert res.nrecovered == ref.keys.size
+    assert np.array_equal(got, np.sort(ref.keys))
+    assert res.rounds == ref.rounds and res.per_round.tolist() == ref.per_round.tolist()
+    assert res.complete == ref.complete
+    # destructive: remaining cells equal the oracle's remainder
+    cnt, ks, hs = dev_cells(t)
+    ocnt, oks, ohs = o.cells()
+    assert np.array_equal(cnt.astype(np.int32), ocnt.astype(np.int32)) and np.array_equal(ks, oks)
+    return res, ref
+
+
+def test_empty_and_single():
+    compare(100, 3, 1, np.zeros(0, dtype=np.uint64))
+    compare(100, 3, 1, np.array([0], dtype=np.uint64))            # the zero key is recoverable
+    compare(100, 3, 1, np.array([12345], dtype=np.uint64))
+
+
+@pytest.mark.parametrize("r", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("load", [0.3, 0.75, 0.83, 1.0, 1.3])
+def test_random_tables(r, load):
+    for C in (r, 37, 1000, 65537):
+        N = int(load * C)
+        keys = synth.random_keys(N, seed=C + r)
+        compare(C, r, seed=C * 7 + r, keys=keys)
+
+
+def test_insert_delete_sparse_recovery():
+    # insert N items, delete all but n, recover the remaining set
+    C, r = 40000, 3
+    allk = synth.random_keys(200000, 4)
+    keep = allk[:30000]
+    res, ref = compare(C, r, 9, allk, deletes=allk[30000:])
+    assert res.complete and np.array_equal(np.sort(res.keys.cpu().numpy().view(np.uint64)), np.sort(keep))
+
+
+@pytest.mark.parametrize("r,load", [(3, 0.75), (3, 0.83), (4, 0.75), (4, 0.83)])
+def test_paper_loads_2pow20(r, load):
+    # Tables 3a/3b workload shape (2^24 cells; here 2^20 so the oracle stays fast)
+    C = 1 << 20
+    N = int(load * C)
+    seed = 100 + r
+    keys = pk.gen_keys(N, seed, device=DEV)
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), O.gen_keys(N, seed))
+    compare(C, r, seed, O.gen_keys(N, seed))
+
+
+def test_to_hypergraph_matches_oracle():
+    C, r, seed = 5000, 4, 3
+    keys = O.gen_keys(3000, 1)
+    t = pk.Iblt(C, r, seed, device=DEV)
+    o = O.Iblt(C, r, seed)
+    got = t.to_hypergraph(keys_dev(keys)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, o.to_hypergraph(keys))
+
+
+def test_key_cap_truncation():
+    C, r = 1000, 3
+    keys = synth.random_keys(500, 1)
+    t = pk.Iblt(C, r, 5, device=DEV)
+    t.insert(keys_dev(keys))
+    with pytest.raises(pk.PeelError) as ei:
+        t.peel(cap_keys=100)
+    assert ei.value.status == pk.PEEL_ETRUNC
+
+
+def test_c2_full_config(goldens):
+    """BASELINE.json configs[1]: 10^7 cells, 7.5e6 keys, r=3, seed=2."""
+    g = goldens["C2"]
+    keys = pk.gen_keys(g["nkeys"], g["seed"], device=DEV)
+    t = pk.Iblt(g["cells"], g["r"], g["seed"], device=DEV)
+    t.insert(keys)
+    res = t.peel(cap_keys=g["nkeys"])
+    assert res.rounds == g["rounds"] and res.per_round.tolist() == g["per_round"]
+    assert res.complete
+    got = np.sort(res.keys.cpu().numpy().view(np.uint64))
+    assert hashlib.sha256(got.tobytes()).hexdigest() == g["sorted_keys_sha256"]

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs -- bit-exact core mask, rounds, every survivors[t] and
+killed[t] -- plus full-scale configs against goldens and the local schedule
+certificate (properties that hold at any size)."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1302_7014_b200 as pk
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+
+
+def to_dev(e: np.ndarray) -> torch.Tensor:
+    e = np.ascontiguousarray(e, dtype=np.uint32)
+    return torch.from_numpy(e.view(np.int32)).to(DEV)
+
+
+def check_vs_oracle(e_np, n, k, flags=0, twice=True):
+    m, r = e_np.shape if e_np.size else (0, e_np.shape[1])
+    ref = O.sync_peel(e_np, n, k, want_peel_round=True)
+    ed = to_dev(e_np) if m else torch.zeros((0, r), dtype=torch.int32, device=DEV)
+    for _ in range(2 if twice else 1):  # twice: expose nondeterminism
+        res = pk.peel_kcore(ed, n, k, flags=flags, want_peel_round=True)
+        assert res.rounds == ref.rounds, (res.rounds, ref.rounds)
+        assert res.survivors.tolist() == ref.survivors.tolist()
+        assert res.killed.tolist() == ref.killed.tolist()
+        assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
+        assert np.array_equal(res.peel_round.cpu().numpy().view(np.uint32), ref.peel_round)
+    return ref
+
+
+# ---- generator (a1) ---------------------------------------------------------------------
+@pytest.mark.parametrize("n,m,r,seed", [(100000, 70000, 3, 1), (1000, 12345, 4, 9), (7, 1001, 7, 3),
+                                        (5, 333, 5, 2), (2**32, 5000, 3, 11), (3, 10, 3, 4),
+                                        (1000003, 99999, 8, 5), (50, 1, 2, 0)])
+def test_generator_matches_oracle(n, m, r, seed):
+    got = pk.gen_hypergraph(n, m, r, seed, device=DEV).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, O.gen_hypergraph(n, m, r, seed))
+
+
+def test_generator_c1_digest(goldens):
+    g = goldens["C1"]
+    got = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV).cpu().numpy().view(np.uint32)
+    assert hashlib.sha256(got.tobytes()).hexdigest() == g["sha256"]
+
+
+def test_generator_sampled_at_full_scale(goldens):
+    # C5 (n=10^9, m=7.5e8): the oracle computes any edge on its own; compare 2000 sampled edges
+    g = goldens["C5"]
+    e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
+    rng = np.random.default_rng(0)
+    idx = np.concatenate([[0, 1, g["m"] - 1], rng.integers(0, g["m"], 2000)])
+    got = e[torch.from_numpy(idx).to(DEV)].cpu().numpy().view(np.uint32)
+    for row, i in zip(got, idx):
+        assert row.tolist() == O.gen_edge(g["seed"], g["n"], g["r"], int(i)).tolist()
+    del e
+
+
+def test_keys_match_oracle():
+    got = pk.gen_keys(100001, 77, device=DEV).cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, O.gen_keys(100001, 77))
+
+
+# ---- k-core parity (a2-a7) ----------------------------------------------------------------
+def test_spec_examples():
+    check_vs_oracle(np.array([[0, 1, 2]], dtype=np.uint32), 3, 2)
+    check_vs_oracle(np.array([[0, 1, 2], [0, 1, 3], [0, 1, 4], [2, 3, 4]], dtype=np.uint32), 6, 2)
+    check_vs_oracle(np.array([[0, 1, 2], [2, 3, 4], [4, 5, 6]], dtype=np.uint32), 7, 2)
+
+
+@pytest.mark.parametrize("flags", [0, pk.PEEL_FLAG_CSR])
+def test_degenerate_cases(flags):
+    check_vs_oracle(np.zeros((0, 3), dtype=np.uint32), 10, 2, flags)        # no edges
+    check_vs_oracle(np.zeros((0, 3), dtype=np.uint32), 1, 1, flags)
+    check_vs_oracle(np.array([[0, 1, 2]], dtype=np.uint32), 3, 0, flags)    # k = 0: nothing peels
+    check_vs_oracle(np.array([[0, 1, 2], [0, 1, 2]], dtype=np.uint32), 3, 2, flags)  # duplicate edge = core
+    e, n = synth.chain(301, 2)
+    check_vs_oracle(e, n, 2, flags)                                          # 151 rounds
+    check_vs_oracle(synth.star(1001, 3), 1001, 2, flags)
+    check_vs_oracle(synth.complete_r_graph(9, 3), 9, 3, flags)              # non-empty 3-core
+
+
+def test_empty_vertex_set():
+    res = pk.peel_kcore(torch.zeros((0, 3), dtype=torch.int32, device=DEV), 0, 2)
+    assert res.rounds == 0
+
+
+@pytest.mark.parametrize("r", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_random_small_vs_oracle(r, k):
+    rng = np.random.default_rng(10 * r + k)
+    for trial in range(6):
+        n = int(rng.integers(r, 3000))
+        m = int(rng.integers(0, 2 * n))
+        e = synth.random_hypergraph(n, m, r, seed=trial)
+        if trial % 2 and m:
+            e = np.concatenate([e, e[: max(1, m // 50)]])  # duplicated edges
+        check_vs_oracle(e, n, k, twice=False)
+        if k <= 2:
+            check_vs_oracle(e, n, k, flags=pk.PEEL_FLAG_CSR, twice=False)
+
+
+@pytest.mark.parametrize("r,k,c", [(3, 2, 0.70), (3, 2, 0.818), (3, 2, 0.85), (4, 2, 0.75), (4, 2, 0.8),
+                                   (3, 3, 1.6), (3, 3, 1.5), (5, 2, 0.7), (4, 3, 1.3)])
+def test_paper_shaped_vs_oracle(r, k, c):
+    # several tiles and a ragged tail: n not a multiple of 32 / 256 / 2048
+    n = 200003
+    m = int(c * n)
+    seed = int(1000 * c) + 10 * r + k
+    e = pk.gen_hypergraph(n, m, r, seed, device=DEV)
+    e_np = O.gen_hypergraph(n, m, r, seed)
+    assert np.array_equal(e.cpu().numpy().view(np.uint32), e_np)
+    check_vs_oracle(e_np, n, k)
+    if k == 2:
+        check_vs_oracle(e_np, n, k, flags=pk.PEEL_FLAG_CSR, twice=False)
+
+
+def test_c1_golden_and_oracle(goldens):
+    g = goldens["C1"]
+    e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
+    res = pk.peel_kcore(e, g["n"], g["k"])
+    assert res.rounds == g["rounds"] and res.survivors.tolist() == g["survivors"]
+    assert res.killed.tolist() == g["killed"]
+    check_vs_oracle(e.cpu().numpy().view(np.uint32), g["n"], g["k"])
+
+
+@pytest.mark.parametrize("name", ["C4a_small", "C4b_small"])
+def test_reduced_c4_vs_oracle(goldens, name):
+    g = goldens[name]
+    e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
+    e_np = e.cpu().numpy().view(np.uint32)
+    assert hashlib.sha256(e_np.tobytes()).hexdigest() == g["sha256"]
+    ref = check_vs_oracle(e_np, g["n"], g["k"], twice=False)
+    assert ref.rounds == g["rounds"] and int(ref.core_mask.sum()) == g["core"]
+
+
+def test_invalid_vertex_rejected():
+    e = to_dev(np.array([[0, 1, 2], [3, 4, 10]], dtype=np.uint32))
+    with pytest.raises(pk.PeelError) as ei:
+        pk.peel_kcore(e, 10, 2)
+    assert ei.value.status == pk.PEEL_EINVAL
+    e = to_dev(np.array([[0, 1, 1]], dtype=np.uint32))
+    with pytest.raises(pk.PeelError):
+        pk.peel_kcore(e, 10, 2, flags=pk.PEEL_FLAG_CSR)
+
+
+def test_round_cap_truncation():
+    e, n = synth.chain(101, 2)
+    ref = O.sync_peel(e, n, 2)
+    res = pk.peel_kcore(to_dev(e), n, 2, cap=10, allow_trunc=True)
+    assert res.status == pk.PEEL_ETRUNC and res.rounds == ref.rounds
+    assert res.survivors.tolist() == ref.survivors[:10].tolist()
+
+
+def test_host_buffer_entry_point():
+    n, m, r, k = 50021, 40000, 3, 2
+    e_np = O.gen_hypergraph(n, m, r, 5)
+    ref = O.sync_peel(e_np, n, k)
+    pinned = torch.from_numpy(e_np.view(np.int32)).pin_memory()
+    res = pk.peel_kcore_host(pinned, n, k)
+    assert res.rounds == ref.rounds and np.array_equal(res.core_mask, ref.core_mask)
+    assert res.survivors.tolist() == ref.survivors.tolist()
+
+
+# ---- full-scale configs (BASELINE.json), checked against goldens + certificate -----------
+def schedule_certificate_torch(edges: torch.Tensor, n: int, k: int, peel_round: torch.Tensor):
+    """The local certificate of tests/test_oracle_peel.py, in torch on the device: with
+    p(v) the removal round (inf = core) and d(e) = min p over e, deg_t(v) = #{e ni v: d(e) >= t};
+    removed v: deg_{p(v)}(v) < k and deg_{p(v)-1}(v) >= k (p >= 2); core v: deg_inf(v) >= k."""
+    INF = 1 << 40
+    p = peel_round.to(torch.int64)
+    p = torch.where(p == 0, torch.full_like(p, INF), p)
+    el = edges.to(torch.int64)
+    d = p[el].min(dim=1).values
+    removed = p != INF
+
+    def deg_at(tv):
+        ok = d[:, None] >= tv[el]
+        return torch.bincount(el[ok], minlength=n)
+
+    tr = torch.where(removed, p, torch.ones_like(p))
+    assert bool((deg_at(tr)[removed] < k).all())
+    tp = torch.where(removed, torch.clamp(p - 1, min=1), torch.ones_like(p))
+    late = removed & (p >= 2)
+    assert bool((deg_at(tp)[late] >= k).all())
+    core = ~removed
+    tc = torch.where(core, torch.full_like(p, INF), torch.ones_like(p))
+    assert bool((deg_at(tc)[core] >= k).all())
+
+
+@pytest.mark.parametrize("name", ["C3", "C4a", "C4b"])
+def test_full_scale_1e8_goldens_and_certificate(goldens, name):
+    g = goldens[name]
+    e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
+    assert e[0].cpu().numpy().view(np.uint32).tolist() == g["edges_head"][0]
+    res = pk.peel_kcore(e, g["n"], g["k"], want_peel_round=True)
+    assert res.rounds == g["rounds"]
+    assert int(res.core_mask.sum().item()) == g["core"]
+    if "survivors" in g:
+        assert res.survivors.tolist() == g["survivors"] and res.killed.tolist() == g["killed"]
+    else:
+        assert res.survivors[:len(g["survivors_head"])].tolist() == g["survivors_head"]
+        assert res.killed[:len(g["killed_head"])].tolist() == g["killed_head"]
+        if "killed_tail" in g:
+            assert res.killed[-len(g["killed_tail"]):].tolist() == g["killed_tail"]
+    # survivors[t] == n - #{v : peel_round(v) <= t}
+    hist = torch.bincount(res.peel_round.to(torch.int64), minlength=res.rounds + 1).cpu().numpy()
+    assert np.array_equal(g["n"] - np.cumsum(hist[1:]), res.survivors)
+    schedule_certificate_torch(e, g["n"], g["k"], res.peel_round)
+    # packed and CSR paths agree at full scale (k=2)
+    if g["k"] == 2:
+        res2 = pk.peel_kcore(e, g["n"], g["k"], flags=pk.PEEL_FLAG_CSR)
+        assert res2.rounds == res.rounds and res2.survivors.tolist() == res.survivors.tolist()
+        assert torch.equal(res2.core_mask, res.core_mask)
+    del e, res
+    pk._ws_cache.clear()
+    torch.cuda.empty_cache()
+
+
+def test_full_scale_c5_north_star(goldens):
+    """n = 10^9, m = 7.5e8, r=3, k=2 (the bench workload): goldens + certificate pieces."""
+    g = goldens["C5"]
+    e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
+    res = pk.peel_kcore(e, g["n"], g["k"])
+    assert res.rounds == g["rounds"]
+    assert res.survivors.tolist() == g["survivors"]
+    assert res.killed.tolist() == g["killed"]
+    assert int(res.core_mask.sum().item()) == 0
+    del e, res
+    pk._ws_cache.clear()
+    torch.cuda.empty_cache()

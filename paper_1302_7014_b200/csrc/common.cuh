@@ -87,4 +87,63 @@ __device__ __forceinline__ void block_add(ull *dst, ull v) {
     __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Block-aggregated append queue (double-buffered in shared memory).
+// Threads push with one shared-memory atomic per warp; at the end of every
+// block-uniform iteration the block reserves space in the global list with ONE
+// global atomic and copies the batch out coalesced.  A single global counter hit
+// by every warp serialises at one L2 slice (measured ~1.5e9 atomics/s on B200:
+// 0.5 s on the 10^9-vertex instance before this).  Iteration i pushes into slot
+// i&1, so the copy-out of slot i&1 never races with the next iteration's pushes.
+// Overflow beyond QCAP falls back to a warp-aggregated global append, so
+// correctness never depends on QCAP.
+// ---------------------------------------------------------------------------
+template <typename T, int QCAP, int BLOCK>
+struct BlockQueueT {
+    T buf[2][QCAP];
+    uint32_t n[2];
+    uint32_t cnt;
+    ull base;
+};
+
+template <typename T, int QCAP, int BLOCK>
+__device__ __forceinline__ void bq_init(BlockQueueT<T, QCAP, BLOCK> &q) {
+    if (threadIdx.x == 0) { q.n[0] = 0; q.n[1] = 0; }
+}
+
+template <typename T, int QCAP, int BLOCK>
+__device__ __forceinline__ void bq_push(BlockQueueT<T, QCAP, BLOCK> &q, int slot, T v, T *gl, ull *gcnt) {
+    cg::coalesced_group g = cg::coalesced_threads();
+    uint32_t pos = 0;
+    if (g.thread_rank() == 0) pos = atomicAdd(&q.n[slot], (uint32_t)g.size());
+    pos = g.shfl(pos, 0) + g.thread_rank();
+    if (pos < QCAP) {
+        q.buf[slot][pos] = v;
+    } else {
+        cg::coalesced_group h = cg::coalesced_threads();
+        ull b = 0;
+        if (h.thread_rank() == 0) b = atomicAdd(gcnt, (ull)h.size());
+        gl[h.shfl(b, 0) + h.thread_rank()] = v;
+    }
+}
+
+// every thread of the block must call it.  Entries at positions >= cap of the
+// global list are counted but not stored (callers with bounded outputs).
+template <typename T, int QCAP, int BLOCK>
+__device__ __forceinline__ void bq_flush(BlockQueueT<T, QCAP, BLOCK> &q, int slot, T *gl, ull *gcnt,
+                                         ull cap = ~0ull) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = min(q.n[slot], (uint32_t)QCAP);
+        q.cnt = c;
+        q.base = c ? atomicAdd(gcnt, (ull)c) : 0ull;
+        q.n[slot] = 0;
+    }
+    __syncthreads();
+    const uint32_t c = q.cnt;
+    const ull b = q.base;
+    for (uint32_t i = threadIdx.x; i < c; i += BLOCK)
+        if (b + i < cap) gl[b + i] = q.buf[slot][i];
+}
+
 }  // namespace peel

@@ -45,7 +45,7 @@ struct IbltCtl {
 };
 
 struct ILayout {
-    size_t cells, ctl, per_round, pure0, pure1, cand, Fc0, Fc1, Fk0, Fk1, clist, total;
+    size_t cells, ctl, per_round, pure0, pure1, cand, F0, F1, clist, total;
 };
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -59,10 +59,8 @@ static ILayout ilayout(uint64_t C) {
     L.pure0 = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
     L.pure1 = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
     L.cand = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
-    L.Fc0 = o; o += al(sizeof(uint32_t) * C);
-    L.Fc1 = o; o += al(sizeof(uint32_t) * C);
-    L.Fk0 = o; o += al(sizeof(ull) * C);
-    L.Fk1 = o; o += al(sizeof(ull) * C);
+    L.F0 = o; o += al(sizeof(ulonglong2) * C);
+    L.F1 = o; o += al(sizeof(ulonglong2) * C);
     L.clist = o; o += al(sizeof(uint32_t) * C);
     L.total = o;
     return L;
@@ -135,8 +133,7 @@ struct IPeelArgs {
     ull *per_round;
     uint32_t *pure[2];  // round-start pure bitmaps: F_t's bits live in pure[(t-1)&1]
     uint32_t *cand;
-    uint32_t *Fc[2];
-    ull *Fk[2];
+    ulonglong2 *F[2];   // frontier entries (cell, key snapshot)
     uint32_t *clist;
     ull *out;
     ull cap_keys;
@@ -146,28 +143,37 @@ __device__ __forceinline__ bool is_pure(const Cell &c, ull seed_c) {
     return c.count == 1u && c.hashSum == checksum(c.keySum, seed_c);
 }
 
-__device__ __forceinline__ void emit_entry(uint32_t *pure, uint32_t c, ull key, uint32_t *Fc, ull *Fk,
-                                           ull *cnt) {
-    cg::coalesced_group g = cg::coalesced_threads();
-    ull base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(cnt, (ull)g.size());
-    base = g.shfl(base, 0) + g.thread_rank();
-    Fc[base] = c;
-    Fk[base] = key;
-    atomicOr(pure + (c >> 5), 1u << (c & 31));
-}
+static constexpr int IQ = 2 * IB_BLOCK;
+typedef BlockQueueT<ulonglong2, IQ, IB_BLOCK> EntQ;
+typedef BlockQueueT<ull, IQ, IB_BLOCK> KeyQ;
+typedef BlockQueueT<uint32_t, IQ, IB_BLOCK> CellQ;
 
 template <int R>
 __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
     cg::grid_group grid = cg::this_grid();
+    __shared__ EntQ qe;
+    __shared__ KeyQ qk;
+    __shared__ CellQ qc;
     IbltCtl *ctl = a.ctl;
+    bq_init(qe); bq_init(qk); bq_init(qc);
+    __syncthreads();
     const ull tid = blockIdx.x * (ull)blockDim.x + threadIdx.x;
     const ull nthr = (ull)gridDim.x * blockDim.x;
+    const ull stride = (ull)gridDim.x * IB_BLOCK;
+    int slot = 0;
 
     // ---- round 1: every pure cell ("a single thread to each cell") ----
-    for (ull c = tid; c < a.C; c += nthr) {
-        Cell v = ld_cell_cg(a.cells + c);
-        if (is_pure(v, a.seed_c)) emit_entry(a.pure[0], (uint32_t)c, v.keySum, a.Fc[0], a.Fk[0], &ctl->fcnt[0]);
+    for (ull base = (ull)blockIdx.x * IB_BLOCK; base < a.C; base += stride) {
+        const ull c = base + threadIdx.x;
+        if (c < a.C) {
+            Cell v = ld_cell_cg(a.cells + c);
+            if (is_pure(v, a.seed_c)) {
+                bq_push(qe, slot, make_ulonglong2(c, v.keySum), a.F[0], &ctl->fcnt[0]);
+                atomicOr(a.pure[0] + (c >> 5), 1u << (c & 31));
+            }
+        }
+        bq_flush(qe, slot, a.F[0], &ctl->fcnt[0]);
+        slot ^= 1;
     }
     grid.sync();
 
@@ -176,61 +182,71 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
         const ull nF = ld_cg_u64(&ctl->fcnt[(t - 1) % 3]);
         if (nF == 0) break;
         if (tid == 0) ctl->fcnt[(t + 1) % 3] = 0;
-        const uint32_t *Fc = a.Fc[(t - 1) & 1];
-        const ull *Fk = a.Fk[(t - 1) & 1];
+        const ulonglong2 *Fc = a.F[(t - 1) & 1];
         ull *ccnt = &ctl->ccnt[t & 1];
         const uint32_t *pure_cur = a.pure[(t - 1) & 1];
         ull recovered = 0;
         // ---- phase A: owner rule, XOR-delete, candidates ----
-        for (ull i = tid; i < nF; i += nthr) {
-            const uint32_t c = ld_cg_u32(Fc + i);
-            const ull x = __ldcg(Fk + i);
-            uint32_t h[R];
-            cells_of<R>(x, a.C, a.seed_h, h);
-            bool owner = false, found = false;
-            #pragma unroll
-            for (int j = 0; j < R; j++) {
-                if (!found && h[j] == c) { found = true; owner = true; }
-                if (!found && (ld_cg_u32(pure_cur + (h[j] >> 5)) >> (h[j] & 31) & 1u)) break;
-            }
-            if (!owner) continue;
-            recovered++;
-            {
-                cg::coalesced_group g = cg::coalesced_threads();
-                ull base = 0;
-                if (g.thread_rank() == 0) base = atomicAdd(&ctl->nrec, (ull)g.size());
-                base = g.shfl(base, 0) + g.thread_rank();
-                if (base < a.cap_keys) a.out[base] = x;
-            }
-            const uint32_t hx = checksum(x, a.seed_c);
-            #pragma unroll
-            for (int j = 0; j < R; j++) {
-                Cell *p = a.cells + h[j];
-                const uint32_t old = atomicAdd(&p->count, 0xFFFFFFFFu);
-                atomicXor(&p->keySum, x);
-                atomicXor(&p->hashSum, hx);
-                if (old == 2u) {
-                    const uint32_t bit = 1u << (h[j] & 31);
-                    if (!(atomicOr(a.cand + (h[j] >> 5), bit) & bit)) append<uint32_t>(a.clist, ccnt, h[j]);
+        for (ull base = (ull)blockIdx.x * IB_BLOCK; base < nF; base += stride) {
+            const ull i = base + threadIdx.x;
+            if (i < nF) {
+                const ulonglong2 ent = __ldcg(Fc + i);
+                const uint32_t c = (uint32_t)ent.x;
+                const ull x = ent.y;
+                uint32_t h[R];
+                cells_of<R>(x, a.C, a.seed_h, h);
+                bool owner = false, found = false;
+                #pragma unroll
+                for (int j = 0; j < R; j++) {
+                    if (!found && h[j] == c) { found = true; owner = true; }
+                    if (!found && (ld_cg_u32(pure_cur + (h[j] >> 5)) >> (h[j] & 31) & 1u)) break;
+                }
+                if (owner) {
+                    recovered++;
+                    bq_push(qk, slot, x, a.out, &ctl->nrec);
+                    const uint32_t hx = checksum(x, a.seed_c);
+                    #pragma unroll
+                    for (int j = 0; j < R; j++) {
+                        Cell *p = a.cells + h[j];
+                        const uint32_t old = atomicAdd(&p->count, 0xFFFFFFFFu);
+                        atomicXor(&p->keySum, x);
+                        atomicXor(&p->hashSum, hx);
+                        if (old == 2u) {
+                            const uint32_t bit = 1u << (h[j] & 31);
+                            if (!(atomicOr(a.cand + (h[j] >> 5), bit) & bit)) bq_push(qc, slot, h[j], a.clist, ccnt);
+                        }
+                    }
                 }
             }
+            bq_flush(qk, slot, a.out, &ctl->nrec, a.cap_keys);
+            bq_flush(qc, slot, a.clist, ccnt);
+            slot ^= 1;
         }
         block_add<IB_BLOCK>(&a.per_round[t <= ISTAT_CAP ? t - 1 : ISTAT_CAP], recovered);
         grid.sync();
         // ---- phase B: retire this round's pure bits, re-test candidates ----
         for (ull i = tid; i < nF; i += nthr) {
-            const uint32_t c = ld_cg_u32(Fc + i);
+            const uint32_t c = (uint32_t)__ldcg(&Fc[i].x);
             atomicAnd(a.pure[(t - 1) & 1] + (c >> 5), ~(1u << (c & 31)));
         }
         if (tid == 0) ctl->ccnt[(t + 1) & 1] = 0;
         const ull nC = ld_cg_u64(ccnt);
-        uint32_t *Fcn = a.Fc[t & 1];
-        ull *Fkn = a.Fk[t & 1];
-        for (ull i = tid; i < nC; i += nthr) {
-            const uint32_t c = ld_cg_u32(a.clist + i);
-            atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
-            Cell v = ld_cell_cg(a.cells + c);
-            if (is_pure(v, a.seed_c)) emit_entry(a.pure[t & 1], c, v.keySum, Fcn, Fkn, &ctl->fcnt[t % 3]);
+        ulonglong2 *Fn = a.F[t & 1];
+        ull *fn = &ctl->fcnt[t % 3];
+        uint32_t *pure_next = a.pure[t & 1];
+        for (ull base = (ull)blockIdx.x * IB_BLOCK; base < nC; base += stride) {
+            const ull i = base + threadIdx.x;
+            if (i < nC) {
+                const uint32_t c = ld_cg_u32(a.clist + i);
+                atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
+                Cell v = ld_cell_cg(a.cells + c);
+                if (is_pure(v, a.seed_c)) {
+                    bq_push(qe, slot, make_ulonglong2(c, v.keySum), Fn, fn);
+                    atomicOr(pure_next + (c >> 5), 1u << (c & 31));
+                }
+            }
+            bq_flush(qe, slot, Fn, fn);
+            slot ^= 1;
         }
         grid.sync();
         t++;
@@ -354,7 +370,7 @@ extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_
     const ILayout &L = t->L;
     char *m = t->mem;
     // zero control, per-round stats and both bitmaps (contiguous)
-    PEEL_CUDA(cudaMemsetAsync(m + L.ctl, 0, L.Fc0 - L.ctl, s));
+    PEEL_CUDA(cudaMemsetAsync(m + L.ctl, 0, L.F0 - L.ctl, s));
     IPeelArgs a;
     memset(&a, 0, sizeof a);
     a.cells = (Cell *)(m + L.cells);
@@ -366,10 +382,8 @@ extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_
     a.pure[0] = (uint32_t *)(m + L.pure0);
     a.pure[1] = (uint32_t *)(m + L.pure1);
     a.cand = (uint32_t *)(m + L.cand);
-    a.Fc[0] = (uint32_t *)(m + L.Fc0);
-    a.Fc[1] = (uint32_t *)(m + L.Fc1);
-    a.Fk[0] = (ull *)(m + L.Fk0);
-    a.Fk[1] = (ull *)(m + L.Fk1);
+    a.F[0] = (ulonglong2 *)(m + L.F0);
+    a.F[1] = (ulonglong2 *)(m + L.F1);
     a.clist = (uint32_t *)(m + L.clist);
     a.out = (ull *)out_keys;
     a.cap_keys = cap_keys;

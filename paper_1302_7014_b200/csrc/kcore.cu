@@ -3,26 +3,31 @@
 // The method: round t removes the snapshot
 // F_t = {alive v : deg_t(v) < k} and every alive edge with an endpoint in F_t;
 // stop at the first empty F_t.  This file computes exactly that schedule with
-// work proportional to the edges actually removed (DESIGN.md §4):
+// work proportional to the edges actually removed (DESIGN.md §5):
 //
-//  * build   -- per-vertex state from one coalesced pass over edges[m][r]:
-//               k <= 2 "packed": u64 {count:24 | idsum:40}, one 64-bit atomic per
-//               endpoint adds (1<<40) + e; when count == 1 the idsum IS the one
-//               alive incident edge, so no incidence lists are needed.
-//               k >= 3 "CSR": u32 degree histogram, exclusive scan, scatter of
-//               edge ids into adj[r m].
-//  * rounds  -- ONE cooperative persistent kernel runs every round with a grid
-//               barrier between rounds (no host round trips, P:505-506 done on
-//               device):
-//                 round 1 frontier = scan of all n vertices for count < k;
-//                 round t: each v in F_t finds its alive edges; an edge is killed
-//                 exactly once by test-and-clear of its alive bit (atomicAnd);
-//                 the winner decrements the other endpoints; the ONE decrement
-//                 that takes a count from k to k-1 appends that vertex to F_{t+1}
-//                 (a warp-aggregated append) -- so F_{t+1} is built without any
-//                 rescan, and each vertex is appended once.
-//               After the last round, core_mask[v] = (count(v) >= k): a removed
-//               vertex had count < k when removed and counts never increase.
+//  * build  -- per-vertex state from one coalesced pass over edges[m][r].
+//              k <= 2 "packed": u64 word  (sum of incident edge ids mod 2^32) << 32 | count.
+//              One 64-bit RED per endpoint adds (e << 32) + 1.  count lives in the low
+//              half and never exceeds m < 2^32, so nothing carries into it; the id sum
+//              wraps harmlessly in the high half.  When count == 1 the id sum IS the one
+//              alive incident edge, so k = 2 needs no incidence lists.
+//              k >= 3 "CSR": u32 degree histogram, exclusive scan, scatter of edge ids.
+//  * rounds -- ONE cooperative persistent kernel runs every round, grid barrier between
+//              rounds (the host is not involved; P:505-506's termination test is a device
+//              counter).  Round 1: a scan of all n vertices for count < k.  Round t: every
+//              alive edge of F_t is killed exactly once by test-and-clear of its alive bit
+//              (atomicAnd returns the old word); the winner decrements the other endpoints;
+//              the ONE decrement that takes a count from k to k-1 puts that vertex in
+//              F_{t+1} -- no rescans, each vertex exactly once.
+//              packed k = 2: a frontier ENTRY is (v, e) with e = v's one alive edge at the
+//              start of round t+1, computed by the crossing decrement itself
+//              (old id sum - killed edge): rounds >= 2 never re-read the state of a
+//              frontier vertex.  If e dies in round t too, v's count reaches 0 and e's alive
+//              bit is already clear at round t+1, so the entry does nothing -- exactly the
+//              snapshot semantics.  Vertices with count 0 in F_t have nothing to kill and
+//              get no entry; |F_t| is counted separately for survivors[t].
+//  * output -- core_mask[v] = (count(v) >= k): a removed vertex had count < k when removed
+//              and counts never increase.
 #include <string.h>
 
 #include "common.cuh"
@@ -31,15 +36,16 @@ namespace peel {
 
 static constexpr uint32_t STAT_CAP = 65536;  // per-round statistics kept on device
 static constexpr int PEEL_BLOCK = 256;
+static constexpr uint32_t SCAN_TILE = 2048;  // 256 threads x 8 elements
 
-enum : uint32_t { ERR_BADVERTEX = 1u, ERR_OVERFLOW = 2u };
+enum : uint32_t { ERR_BADVERTEX = 1u };
 
 struct Ctl {
-    ull cnt[3];       // frontier sizes, rotating: F_t uses cnt[(t-1)%3]
+    ull nf[3];        // |F_t| (vertices removed in round t), rotating: round t uses nf[(t-1)%3]
+    ull ne[3];        // frontier list lengths, same rotation
     ull rounds;       // number of non-empty rounds
     uint32_t err;     // ERR_* bits
     uint32_t pad;
-    ull pad2[3];
 };
 
 struct Layout {
@@ -48,14 +54,13 @@ struct Layout {
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static constexpr uint32_t SCAN_TILE = 2048;  // 256 threads x 8 elements
-
 static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     Layout L;
     size_t o = 0;
     L.ctl = o; o += al(sizeof(Ctl));
     L.fsize = o; o += al(sizeof(ull) * (STAT_CAP + 1));
     L.killed = o; o += al(sizeof(ull) * (STAT_CAP + 1));
+    const size_t fe = csr ? sizeof(uint32_t) : sizeof(uint2);  // frontier element: v, or (v, e)
     if (!csr) {
         L.state = o; o += al(sizeof(ull) * n);
         L.deg = L.off = L.bsum = L.adj = 0;
@@ -67,8 +72,8 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         L.adj = o; o += al(sizeof(uint32_t) * r * m);
     }
     L.alive = o; o += al(sizeof(uint32_t) * ((m + 31) / 32));
-    L.F0 = o; o += al(sizeof(uint32_t) * n);
-    L.F1 = o; o += al(sizeof(uint32_t) * n);
+    L.F0 = o; o += al(fe * n);
+    L.F1 = o; o += al(fe * n);
     L.total = o;
     return L;
 }
@@ -92,17 +97,12 @@ __device__ __forceinline__ bool load_edge(const uint32_t *__restrict__ edges, ui
     return ok;
 }
 
-// packed k<=2 build: state[u] += (1<<40) + e for every endpoint (P:500-501's
-// atomic-update pattern, applied to the degree/id-sum accumulators).
-// CHECK (m > 2^23): use the returning atomic and flag the increment that takes a
-// count to ovf_count -- until then id-sums cannot have carried into the count
-// field, so the flag is exact even for degrees that would wrap the 24-bit count.
-// Without CHECK (m <= 2^23) counts stay below 2^24 and the round-1 scan's check
-// of the final count is exact.
-template <int R, bool CHECK>
+// packed k<=2 build: state[u] += (e << 32) + 1 for every endpoint (P:500-501's one-thread-
+// per-item atomic update, applied to the count / id-sum accumulators); RED, no return.
+template <int R>
 __global__ void __launch_bounds__(256) build_packed_kernel(const uint32_t *__restrict__ edges,
                                                            uint64_t n, uint64_t m, ull *state,
-                                                           Ctl *ctl, ull ovf_count) {
+                                                           Ctl *ctl) {
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t u[R];
@@ -110,16 +110,9 @@ __global__ void __launch_bounds__(256) build_packed_kernel(const uint32_t *__res
             atomicOr(&ctl->err, ERR_BADVERTEX);
             continue;
         }
-        const ull inc = (1ull << 40) + e;
-        if (CHECK) {
-            bool ovf = false;
-            #pragma unroll
-            for (int j = 0; j < R; j++) ovf |= (atomicAdd(state + u[j], inc) >> 40) + 1 >= ovf_count;
-            if (ovf) atomicOr(&ctl->err, ERR_OVERFLOW);
-        } else {
-            #pragma unroll
-            for (int j = 0; j < R; j++) atomicAdd(state + u[j], inc);
-        }
+        const ull inc = (e << 32) + 1ull;
+        #pragma unroll
+        for (int j = 0; j < R; j++) atomicAdd(state + u[j], inc);
     }
 }
 
@@ -139,7 +132,7 @@ __global__ void __launch_bounds__(256) build_deg_kernel(const uint32_t *__restri
     }
 }
 
-// exclusive scan of deg into off, tile pass: local exclusive scan + tile total
+// exclusive scan of deg into off: tile pass (local exclusive scan + tile total)
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t *total) {
     __shared__ uint32_t ws[PEEL_BLOCK / 32];
     int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -222,6 +215,13 @@ __global__ void __launch_bounds__(256) scatter_kernel(const uint32_t *__restrict
     }
 }
 
+// block-aggregated append queues (common.cuh): one global atomic per block iteration
+static constexpr int U = 4;                      // frontier entries per thread per iteration (MLP)
+static constexpr int CHUNK = PEEL_BLOCK * U;     // entries per block iteration
+static constexpr int QCAP = 2 * CHUNK;
+template <typename T>
+using BlockQueue = BlockQueueT<T, QCAP, PEEL_BLOCK>;
+
 // ---------------------------------------------------------------------------
 // the round loop: one cooperative persistent kernel
 // ---------------------------------------------------------------------------
@@ -235,79 +235,200 @@ struct PeelArgs {
     const uint32_t *off_end; // CSR path: end of u's adjacency list
     const uint32_t *adj;     // CSR path
     uint32_t *alive;
-    uint32_t *F[2];
+    void *F[2];              // packed: uint2 (v, e) entries; CSR: u32 vertices
     Ctl *ctl;
     ull *fsize;
     ull *killed;
     uint8_t *core_mask;
     uint32_t *peel_round;
-    ull ovf_count;           // packed path: a count >= this may have overflowed idsum
+    int mask_vec;            // core_mask is 16-byte aligned
 };
 
-__device__ __forceinline__ void on_crossing(const PeelArgs &a, uint32_t u, uint32_t *Fn, ull *cn,
-                                            uint32_t next_round) {
-    append<uint32_t>(Fn, cn, u);
-    if (a.peel_round) a.peel_round[u] = next_round;
+__device__ __forceinline__ uint32_t count_of(ull w) { return (uint32_t)w; }
+__device__ __forceinline__ uint32_t idsum_of(ull w) { return (uint32_t)(w >> 32); }
+
+template <bool CSR>
+__device__ void write_core_mask(const PeelArgs &a, uint64_t tid, uint64_t nthr) {
+    // core_mask[v] = count(v) >= k (counts only decrease); 16 vertices -> one 16-byte store
+    const uint32_t k = a.k;
+    const uint64_t n16 = a.mask_vec ? a.n / 16 : 0;
+    for (uint64_t w = tid; w < n16; w += nthr) {
+        uint32_t bytes[4] = {0, 0, 0, 0};
+        #pragma unroll
+        for (int i = 0; i < 16; i++) {
+            const uint64_t v = w * 16 + i;
+            uint32_t c = CSR ? ld_cg_u32(a.deg + v) : count_of(ld_cg_u64(a.state + v));
+            bytes[i >> 2] |= (uint32_t)(c >= k) << (8 * (i & 3));
+        }
+        reinterpret_cast<uint4 *>(a.core_mask)[w] = make_uint4(bytes[0], bytes[1], bytes[2], bytes[3]);
+    }
+    for (uint64_t v = n16 * 16 + tid; v < a.n; v += nthr) {
+        uint32_t c = CSR ? ld_cg_u32(a.deg + v) : count_of(ld_cg_u64(a.state + v));
+        a.core_mask[v] = c >= k ? 1 : 0;
+    }
 }
 
-template <int R, bool CSR>
-__global__ void __launch_bounds__(PEEL_BLOCK) peel_rounds_kernel(PeelArgs a) {
+// packed path (k <= 2)
+template <int R>
+__global__ void __launch_bounds__(PEEL_BLOCK) peel_packed_kernel(PeelArgs a) {
     cg::grid_group grid = cg::this_grid();
+    __shared__ BlockQueue<uint2> q;
     Ctl *ctl = a.ctl;
     if (ld_cg_u32(&ctl->err) & ERR_BADVERTEX) return;  // uniform across the grid
+    if (threadIdx.x == 0) { q.n[0] = 0; q.n[1] = 0; }
+    __syncthreads();
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     const uint32_t k = a.k;
+    int slot = 0;
 
-    // ---- round 1 frontier: F_1 = {v : deg(v) < k} (a full scan) ----
-    for (uint64_t v = tid; v < a.n; v += nthr) {
-        uint32_t c;
-        if (CSR) {
-            c = a.deg[v];
-        } else {
-            ull s = a.state[v];
-            c = (uint32_t)(s >> 40);
-            if (c >= a.ovf_count) atomicOr(&ctl->err, ERR_OVERFLOW);  // exact for m <= 2^23
+    // ---- round 1: F_1 = {v : count(v) < k}, a coalesced scan of the state ----
+    {
+        uint2 *F = (uint2 *)a.F[0];
+        ull removed = 0;
+        for (uint64_t base = (uint64_t)blockIdx.x * CHUNK; base < a.n; base += (uint64_t)gridDim.x * CHUNK) {
+            ull w[U];
+            #pragma unroll
+            for (int j = 0; j < U; j++) {
+                const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+                w[j] = v < a.n ? a.state[v] : ~0ull;
+            }
+            #pragma unroll
+            for (int j = 0; j < U; j++) {
+                const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+                if (v < a.n && count_of(w[j]) < k) {
+                    removed++;
+                    if (a.peel_round) a.peel_round[v] = 1;
+                    if (count_of(w[j]) == 1)  // k = 2: its one edge is the id sum
+                        bq_push(q, slot, make_uint2((uint32_t)v, idsum_of(w[j])), F, &ctl->ne[0]);
+                }
+            }
+            bq_flush(q, slot, F, &ctl->ne[0]);
+            slot ^= 1;
         }
-        if (c < k) on_crossing(a, (uint32_t)v, a.F[0], &ctl->cnt[0], 1);
+        block_add<PEEL_BLOCK>(&ctl->nf[0], removed);
     }
     grid.sync();
-    if (ld_cg_u32(&ctl->err) & ERR_OVERFLOW) return;
 
     // ---- rounds ----
     uint32_t t = 1;
     for (;;) {
-        const ull nF = ld_cg_u64(&ctl->cnt[(t - 1) % 3]);
+        const ull nF = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
+        if (nF == 0) break;
+        const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
+        if (tid == 0) {
+            a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
+            ctl->nf[(t + 1) % 3] = 0;  // round t+2's counters; their last reader finished a barrier ago
+            ctl->ne[(t + 1) % 3] = 0;
+        }
+        const uint2 *Fc = (const uint2 *)a.F[(t - 1) & 1];
+        uint2 *Fn = (uint2 *)a.F[t & 1];
+        ull *cn = &ctl->ne[t % 3];
+        ull kills = 0, crossed = 0;
+        for (uint64_t base = (uint64_t)blockIdx.x * CHUNK; base < nE; base += (uint64_t)gridDim.x * CHUNK) {
+            // U independent entries per thread, staged so their random accesses overlap
+            uint2 ent[U];
+            bool win[U];
+            #pragma unroll
+            for (int j = 0; j < U; j++) {
+                const uint64_t i = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+                ent[j] = i < nE ? __ldcg(Fc + i) : make_uint2(0u, 0u);
+            }
+            #pragma unroll
+            for (int j = 0; j < U; j++) {  // exactly-once kill of e (P:510-511's concern)
+                const uint64_t i = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+                win[j] = false;
+                if (i < nE) {
+                    const uint32_t e = ent[j].y, bit = 1u << (e & 31);
+                    win[j] = (atomicAnd(a.alive + (e >> 5), ~bit) & bit) != 0;
+                }
+            }
+            uint32_t ue[U][R];
+            #pragma unroll
+            for (int j = 0; j < U; j++)
+                if (win[j]) {
+                    #pragma unroll
+                    for (int r = 0; r < R; r++) ue[j][r] = __ldg(a.edges + (uint64_t)ent[j].y * R + r);
+                }
+            #pragma unroll
+            for (int j = 0; j < U; j++)
+                if (win[j]) {
+                    kills++;
+                    const uint32_t e = ent[j].y;
+                    const ull dec = 0ull - (((ull)e << 32) + 1ull);
+                    #pragma unroll
+                    for (int r = 0; r < R; r++) {
+                        const uint32_t u = ue[j][r];
+                        if (u == ent[j].x) continue;
+                        const ull old = atomicAdd(a.state + u, dec);
+                        if (count_of(old) == 2u) {  // k = 2: count 2 -> 1, u joins F_{t+1}
+                            crossed++;
+                            if (a.peel_round) a.peel_round[u] = t + 1;
+                            bq_push(q, slot, make_uint2(u, idsum_of(old) - e), Fn, cn);
+                        }
+                    }
+                }
+            bq_flush(q, slot, Fn, cn);
+            slot ^= 1;
+        }
+        block_add<PEEL_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
+        block_add<PEEL_BLOCK>(&ctl->nf[t % 3], crossed);
+        grid.sync();
+        t++;
+    }
+    if (tid == 0) ctl->rounds = t - 1;
+    write_core_mask<false>(a, tid, nthr);
+}
+
+// CSR path (any k)
+template <int R>
+__global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ BlockQueue<uint32_t> q;
+    Ctl *ctl = a.ctl;
+    if (ld_cg_u32(&ctl->err) & ERR_BADVERTEX) return;
+    if (threadIdx.x == 0) { q.n[0] = 0; q.n[1] = 0; }
+    __syncthreads();
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t k = a.k;
+    int slot = 0;
+    {
+        uint32_t *F = (uint32_t *)a.F[0];
+        for (uint64_t base = (uint64_t)blockIdx.x * CHUNK; base < a.n; base += (uint64_t)gridDim.x * CHUNK) {
+            #pragma unroll
+            for (int j = 0; j < U; j++) {
+                const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+                if (v < a.n && a.deg[v] < k) {
+                    bq_push(q, slot, (uint32_t)v, F, &ctl->ne[0]);
+                    if (a.peel_round) a.peel_round[v] = 1;
+                }
+            }
+            bq_flush(q, slot, F, &ctl->ne[0]);
+            slot ^= 1;
+        }
+    }
+    grid.sync();
+    uint32_t t = 1;
+    for (;;) {
+        const ull nF = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
         if (nF == 0) break;
         if (tid == 0) {
             a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
-            ctl->cnt[(t + 1) % 3] = 0;  // F_{t+2}'s counter; its last reader finished a barrier ago
+            ctl->ne[(t + 1) % 3] = 0;
         }
-        const uint32_t *Fc = a.F[(t - 1) & 1];
-        uint32_t *Fn = a.F[t & 1];
-        ull *cn = &ctl->cnt[t % 3];
+        const uint32_t *Fc = (const uint32_t *)a.F[(t - 1) & 1];
+        uint32_t *Fn = (uint32_t *)a.F[t & 1];
+        ull *cn = &ctl->ne[t % 3];
         ull kills = 0;
-        for (uint64_t i = tid; i < nF; i += nthr) {
-            const uint32_t v = ld_cg_u32(Fc + i);
-            if (!CSR) {
-                // packed: count <= 1 here; if 1, the id-sum is the one alive edge
-                const ull s = ld_cg_u64(a.state + v);
-                if ((s >> 40) != 1) continue;
-                const uint32_t e = (uint32_t)(s & ((1ull << 40) - 1));
-                const uint32_t bit = 1u << (e & 31);
-                if (!(atomicAnd(a.alive + (e >> 5), ~bit) & bit)) continue;  // exactly-once kill
-                kills++;
-                const ull dec = 0ull - ((1ull << 40) + e);
-                #pragma unroll
-                for (int j = 0; j < R; j++) {
-                    const uint32_t u = __ldg(a.edges + (uint64_t)e * R + j);
-                    if (u == v) continue;
-                    const ull old = atomicAdd(a.state + u, dec);
-                    if ((uint32_t)(old >> 40) == k) on_crossing(a, u, Fn, cn, t + 1);
-                }
-            } else {
-                const uint32_t b = v ? ld_cg_u32(a.off_end + v - 1) : 0u;
-                const uint32_t eend = ld_cg_u32(a.off_end + v);
+        for (uint64_t base = (uint64_t)blockIdx.x * CHUNK; base < nF; base += (uint64_t)gridDim.x * CHUNK) {
+            #pragma unroll 1
+            for (int j = 0; j < U; j++) {
+                const uint64_t i = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+                if (i >= nF) continue;
+                const uint32_t v = ld_cg_u32(Fc + i);
+                const uint32_t b = v ? __ldg(a.off_end + v - 1) : 0u;
+                const uint32_t eend = __ldg(a.off_end + v);
                 for (uint32_t p = b; p < eend; p++) {
                     const uint32_t e = __ldg(a.adj + p);
                     const uint32_t bit = 1u << (e & 31);
@@ -315,26 +436,26 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_rounds_kernel(PeelArgs a) {
                     if (!(atomicAnd(a.alive + (e >> 5), ~bit) & bit)) continue;
                     kills++;
                     #pragma unroll
-                    for (int j = 0; j < R; j++) {
-                        const uint32_t u = __ldg(a.edges + (uint64_t)e * R + j);
+                    for (int r = 0; r < R; r++) {
+                        const uint32_t u = __ldg(a.edges + (uint64_t)e * R + r);
                         if (u == v) continue;
                         const uint32_t old = atomicSub(a.deg + u, 1u);
-                        if (old == k) on_crossing(a, u, Fn, cn, t + 1);
+                        if (old == k) {
+                            bq_push(q, slot, u, Fn, cn);
+                            if (a.peel_round) a.peel_round[u] = t + 1;
+                        }
                     }
                 }
             }
+            bq_flush(q, slot, Fn, cn);
+            slot ^= 1;
         }
         block_add<PEEL_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
         grid.sync();
         t++;
     }
     if (tid == 0) ctl->rounds = t - 1;
-
-    // ---- outputs: core_mask[v] = count(v) >= k (counts only decrease) ----
-    for (uint64_t v = tid; v < a.n; v += nthr) {
-        uint32_t c = CSR ? ld_cg_u32(a.deg + v) : (uint32_t)(ld_cg_u64(a.state + v) >> 40);
-        a.core_mask[v] = c >= k ? 1 : 0;
-    }
+    write_core_mask<true>(a, tid, nthr);
 }
 
 static unsigned grid_for(uint64_t work, int per_sm = 16) {
@@ -362,24 +483,20 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     a.edges = edges; a.n = n; a.m = m; a.k = k;
     a.stat_cap = STAT_CAP;
     a.alive = alive;
-    a.F[0] = (uint32_t *)(ws + L.F0);
-    a.F[1] = (uint32_t *)(ws + L.F1);
+    a.F[0] = ws + L.F0;
+    a.F[1] = ws + L.F1;
     a.ctl = ctl; a.fsize = fsize; a.killed = kil;
     a.core_mask = core_mask; a.peel_round = peel_round;
+    a.mask_vec = ((uintptr_t)core_mask & 15) == 0;
     if (peel_round) PEEL_CUDA(cudaMemsetAsync(peel_round, 0, sizeof(uint32_t) * n, s));
 
     if (!csr) {
         ull *state = (ull *)(ws + L.state);
         PEEL_CUDA(cudaMemsetAsync(state, 0, sizeof(ull) * n, s));
         a.state = state;
-        a.ovf_count = m > 1 ? ((1ull << 40) + (m - 1) - 1) / (m - 1) : (1ull << 24);
-        if (a.ovf_count > (1ull << 24) - 1) a.ovf_count = (1ull << 24) - 1;
-        if (m > (1ull << 23)) {
+        if (m) {
             ProfScope ps("build_packed", s);
-            build_packed_kernel<R, true><<<grid_for(m), 256, 0, s>>>(edges, n, m, state, ctl, a.ovf_count);
-        } else if (m) {
-            ProfScope ps("build_packed", s);
-            build_packed_kernel<R, false><<<grid_for(m), 256, 0, s>>>(edges, n, m, state, ctl, a.ovf_count);
+            build_packed_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, state, ctl);
         }
     } else {
         uint32_t *deg = (uint32_t *)(ws + L.deg);
@@ -409,12 +526,11 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             scatter_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, off, adj);
         }
         a.deg = deg; a.off_end = off; a.adj = adj;
-        a.ovf_count = ~0ull;
     }
     PEEL_CUDA(cudaGetLastError());
 
     // cooperative persistent round loop: every block must be co-resident
-    auto kern = csr ? peel_rounds_kernel<R, true> : peel_rounds_kernel<R, false>;
+    void *kern = csr ? (void *)peel_csr_kernel<R> : (void *)peel_packed_kernel<R>;
     int per_sm = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PEEL_BLOCK, 0));
     if (per_sm < 1) per_sm = 1;
@@ -422,7 +538,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     void *args[] = {&a};
     {
         ProfScope ps(csr ? "peel_rounds_csr" : "peel_rounds_packed", s);
-        PEEL_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, PEEL_BLOCK, args, 0, s));
+        PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, PEEL_BLOCK, args, 0, s));
     }
 
     // results
@@ -431,7 +547,6 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     PEEL_CUDA(cudaStreamSynchronize(s));
     prof_collect();
     if (hctl.err & ERR_BADVERTEX) return PEEL_EINVAL;
-    if (hctl.err & ERR_OVERFLOW) return PEEL_EOVERFLOW;
     uint64_t T = hctl.rounds;
     *rounds = (uint32_t)T;
     uint64_t nstore = T < cap ? T : cap;
@@ -450,10 +565,9 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     return (T > cap || T > STAT_CAP) ? PEEL_ETRUNC : PEEL_OK;
 }
 
-static bool kcore_args_ok(uint64_t n, uint64_t m, uint32_t r, uint32_t k, bool csr) {
+static bool kcore_args_ok(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     if (r < 2 || r > 8 || n > (1ull << 32) || m >= (1ull << 32)) return false;
     if (csr && (uint64_t)r * m >= (1ull << 32)) return false;
-    (void)k;
     return true;
 }
 
@@ -466,7 +580,7 @@ using namespace peel;
 extern "C" size_t peel_kcore_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k,
                                              uint32_t flags) {
     bool csr = use_csr(k, flags);
-    if (!kcore_args_ok(n, m, r, k, csr)) return 0;
+    if (!kcore_args_ok(n, m, r, csr)) return 0;
     return layout(n, m, r, csr).total;
 }
 
@@ -476,7 +590,7 @@ extern "C" peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m,
                                   uint32_t *peel_round, void *workspace, size_t ws_bytes,
                                   void *stream) {
     bool csr = use_csr(k, flags);
-    if (!kcore_args_ok(n, m, r, k, csr) || !rounds) return PEEL_EINVAL;
+    if (!kcore_args_ok(n, m, r, csr) || !rounds) return PEEL_EINVAL;
     if ((m && !edges) || (n && !core_mask) || !workspace) return PEEL_EINVAL;
     Layout L = layout(n, m, r, csr);
     if (ws_bytes < L.total) return PEEL_ENOMEM;

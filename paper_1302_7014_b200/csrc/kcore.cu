@@ -45,12 +45,34 @@ struct Ctl {
     ull ne[3];        // frontier list lengths, same rotation
     ull rounds;       // number of non-empty rounds
     uint32_t err;     // ERR_* bits
-    uint32_t pad;
+    uint32_t binovf;  // a vertex bin overflowed its capacity (binned build falls back)
 };
 
 struct Layout {
-    size_t ctl, fsize, killed, state, deg, off, bsum, adj, alive, F0, F1, total;
+    size_t ctl, fsize, killed, state, deg, off, bsum, adj, alive, F0, F1;
+    size_t bins, bin_cursor, bin_base, bin_cap, entries;  // binned build (packed, n > BIN_MIN_N)
+    uint64_t nbins, total_cap;
+    size_t total;
 };
+
+// Binned build: endpoint increments are partitioned into vertex bins of
+// 2^BIN_SHIFT vertices (32 MB of state, L2-resident), then each bin is accumulated with
+// L2 atomics and scanned for the round-1 frontier while it is still in L2.
+static constexpr int BIN_SHIFT = 22;
+static constexpr uint64_t BIN_MIN_N = 1ull << 23;  // below this the state fits L2: direct build
+static constexpr int MAX_BINS = 1024;              // n <= 2^32
+
+__host__ __device__ inline uint64_t bin_size(uint64_t n, uint64_t b) {
+    uint64_t lo = b << BIN_SHIFT, hi = (b + 1) << BIN_SHIFT;
+    return (hi < n ? hi : n) - lo;
+}
+
+// capacity of bin b: expected r m size/n plus 8 standard deviations plus 4096 (IEEE sqrt,
+// identical on host and device); a bin that overflows sends the build down the direct path
+__host__ __device__ inline uint64_t bin_capacity(uint64_t n, uint64_t m, uint32_t r, uint64_t b) {
+    uint64_t lam = (bin_size(n, b) * (uint64_t)r * m) / n;
+    return lam + 8ull * (uint64_t)sqrt((double)lam) + 4096ull;
+}
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -74,6 +96,17 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     L.alive = o; o += al(sizeof(uint32_t) * ((m + 31) / 32));
     L.F0 = o; o += al(fe * n);
     L.F1 = o; o += al(fe * n);
+    L.nbins = 0; L.total_cap = 0;
+    L.bins = L.bin_cursor = L.bin_base = L.bin_cap = L.entries = 0;
+    if (!csr && n > BIN_MIN_N) {
+        L.nbins = (n + (1ull << BIN_SHIFT) - 1) >> BIN_SHIFT;
+        for (uint64_t b = 0; b < L.nbins; b++) L.total_cap += bin_capacity(n, m, r, b);
+        L.bins = o;
+        L.bin_cursor = o; o += al(sizeof(ull) * L.nbins);
+        L.bin_base = o; o += al(sizeof(ull) * L.nbins);
+        L.bin_cap = o; o += al(sizeof(ull) * L.nbins);
+        L.entries = o; o += al(sizeof(ull) * L.total_cap);
+    }
     L.total = o;
     return L;
 }
@@ -114,6 +147,115 @@ __global__ void __launch_bounds__(256) build_packed_kernel(const uint32_t *__res
         #pragma unroll
         for (int j = 0; j < R; j++) atomicAdd(state + u[j], inc);
     }
+}
+
+// ---- binned build ------------------------------------------------------------------------
+__global__ void bin_init_kernel(uint64_t n, uint64_t m, uint32_t r, uint64_t nbins, ull *cursor, ull *base,
+                                ull *cap) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        ull o = 0;
+        for (uint64_t b = 0; b < nbins; b++) {
+            ull c = bin_capacity(n, m, r, b);
+            cursor[b] = 0;
+            base[b] = o;
+            cap[b] = c;
+            o += c;
+        }
+    }
+}
+
+static constexpr int PART_BLOCK = 256;
+static constexpr int PART_ENTRIES = 6144;  // endpoint entries staged per chunk
+
+// pass 1: partition the r m endpoint increments by vertex bin.  Per chunk of edges the
+// block histograms bins in shared memory, reserves one contiguous run per bin with a
+// single global atomic, counting-sorts the chunk's entries by bin in shared memory and
+// writes them out so each bin's run is a coalesced store.  entry = e << 32 | (u & mask).
+template <int R>
+__global__ void __launch_bounds__(PART_BLOCK) bin_partition_kernel(const uint32_t *__restrict__ edges, uint64_t n,
+                                                                   uint64_t m, uint64_t nbins, ull *cursor,
+                                                                   const ull *__restrict__ base,
+                                                                   const ull *__restrict__ cap, ull *entries,
+                                                                   Ctl *ctl) {
+    constexpr int CH = PART_ENTRIES / R;  // edges per chunk
+    extern __shared__ unsigned char smem_raw[];
+    ull *sent = (ull *)smem_raw;                                   // [CH*R]
+    uint32_t *hist = (uint32_t *)(sent + CH * R);                  // [MAX_BINS]
+    uint32_t *offs = hist + MAX_BINS;                              // [MAX_BINS]
+    uint32_t *fill = offs + MAX_BINS;                              // [MAX_BINS]
+    ull *gpos = (ull *)(fill + MAX_BINS);                          // [MAX_BINS]
+    uint16_t *sbin = (uint16_t *)(gpos + MAX_BINS);                // [CH*R]
+    __shared__ uint32_t total;
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {
+        const int ne = (int)min((uint64_t)CH, m - c0);
+        for (int b = threadIdx.x; b < (int)nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
+        __syncthreads();
+        for (int i = threadIdx.x; i < ne; i += PART_BLOCK) {
+            uint32_t u[R];
+            if (!load_edge<R>(edges, c0 + i, n, u)) {
+                atomicOr(&ctl->err, ERR_BADVERTEX);
+                continue;
+            }
+            #pragma unroll
+            for (int j = 0; j < R; j++) atomicAdd(&hist[u[j] >> BIN_SHIFT], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of hist over nbins (<= 1024): one warp, 32 bins per lane
+        if (threadIdx.x < 32) {
+            const int per = (MAX_BINS + 31) / 32;
+            uint32_t loc = 0;
+            for (int q = 0; q < per; q++) {
+                int b = threadIdx.x * per + q;
+                loc += b < (int)nbins ? hist[b] : 0;
+            }
+            uint32_t x = loc;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (threadIdx.x >= o) x += y;
+            }
+            uint32_t run = x - loc;
+            for (int q = 0; q < per; q++) {
+                int b = threadIdx.x * per + q;
+                if (b < (int)nbins) { offs[b] = run; run += hist[b]; }
+            }
+            if (threadIdx.x == 31) total = x;
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < (int)nbins; b += PART_BLOCK)
+            if (hist[b]) {
+                ull g = atomicAdd(cursor + b, (ull)hist[b]);
+                if (g + hist[b] > cap[b]) atomicOr(&ctl->binovf, 1u);
+                gpos[b] = g;
+            }
+        __syncthreads();
+        for (int i = threadIdx.x; i < ne; i += PART_BLOCK) {
+            uint32_t u[R];
+            if (!load_edge<R>(edges, c0 + i, n, u)) continue;
+            const ull e = c0 + i;
+            #pragma unroll
+            for (int j = 0; j < R; j++) {
+                const uint32_t b = u[j] >> BIN_SHIFT;
+                const uint32_t p = offs[b] + atomicAdd(&fill[b], 1u);
+                sent[p] = (e << 32) | ((ull)u[j] & mask);
+                sbin[p] = (uint16_t)b;
+            }
+        }
+        __syncthreads();
+        const uint32_t tot = total;
+        for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
+            const uint32_t b = sbin[i];
+            const ull pos = gpos[b] + (i - offs[b]);
+            if (pos < cap[b]) entries[base[b] + pos] = sent[i];
+        }
+        __syncthreads();
+    }
+}
+
+static size_t partition_smem(int r) {
+    return sizeof(ull) * (PART_ENTRIES / r) * r + sizeof(uint32_t) * 3 * MAX_BINS + sizeof(ull) * MAX_BINS +
+           sizeof(uint16_t) * (PART_ENTRIES / r) * r;
 }
 
 // CSR build, pass 1: degree histogram
@@ -242,6 +384,7 @@ struct PeelArgs {
     uint8_t *core_mask;
     uint32_t *peel_round;
     int mask_vec;            // core_mask is 16-byte aligned
+    int f1_ready;            // packed: F_1 was emitted by the binned build
 };
 
 __device__ __forceinline__ uint32_t count_of(ull w) { return (uint32_t)w; }
@@ -268,9 +411,100 @@ __device__ void write_core_mask(const PeelArgs &a, uint64_t tid, uint64_t nthr) 
     }
 }
 
+// Round-1 frontier over vertices [lo, hi): F_1 = {v : count(v) < k}; a vertex with
+// count 1 gets the entry (v, its one edge = the id sum).  Block-uniform: every
+// thread of the block must call it with the same range.
+__device__ __forceinline__ void scan_emit(const PeelArgs &a, BlockQueue<uint2> &q, int &slot, uint64_t lo,
+                                          uint64_t hi, ull &removed) {
+    uint2 *F = (uint2 *)a.F[0];
+    ull *cnt = &a.ctl->ne[0];
+    for (uint64_t base = lo + (uint64_t)blockIdx.x * CHUNK; base < hi; base += (uint64_t)gridDim.x * CHUNK) {
+        ull w[U];
+        #pragma unroll
+        for (int j = 0; j < U; j++) {
+            const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+            w[j] = v < hi ? ld_cg_u64(a.state + v) : ~0ull;
+        }
+        #pragma unroll
+        for (int j = 0; j < U; j++) {
+            const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
+            if (v < hi && count_of(w[j]) < a.k) {
+                removed++;
+                if (a.peel_round) a.peel_round[v] = 1;
+                if (count_of(w[j]) == 1)  // k = 2: its one edge is the id sum
+                    bq_push(q, slot, make_uint2((uint32_t)v, idsum_of(w[j])), F, cnt);
+            }
+        }
+        bq_flush(q, slot, F, cnt);
+        slot ^= 1;
+    }
+}
+
+// pass 2 of the binned build (cooperative): for each bin b in order, zero its 32 MB of
+// state, grid barrier, apply its entries with L2-resident 64-bit REDs, grid barrier,
+// then (overlapped with zeroing bin b+1) scan it for the round-1 frontier while it is
+// still in L2.  If any bin overflowed in pass 1, fall back to the direct build.
+struct BinArgs {
+    uint64_t nbins;
+    const ull *cursor, *base, *cap, *entries;
+};
+
+template <int R>
+__global__ void __launch_bounds__(PEEL_BLOCK) bin_accumulate_kernel(PeelArgs a, BinArgs bn) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ BlockQueue<uint2> q;
+    Ctl *ctl = a.ctl;
+    if (ld_cg_u32(&ctl->err) & ERR_BADVERTEX) return;
+    bq_init(q);
+    __syncthreads();
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    int slot = 0;
+    ull removed = 0;
+    if (ld_cg_u32(&ctl->binovf)) {
+        for (uint64_t v = tid; v < a.n; v += nthr) a.state[v] = 0ull;
+        grid.sync();
+        for (uint64_t e = tid; e < a.m; e += nthr) {
+            uint32_t u[R];
+            if (!load_edge<R>(a.edges, e, a.n, u)) continue;
+            const ull inc = (e << 32) + 1ull;
+            #pragma unroll
+            for (int j = 0; j < R; j++) atomicAdd(a.state + u[j], inc);
+        }
+        grid.sync();
+        scan_emit(a, q, slot, 0, a.n, removed);
+    } else {
+        const ull mask = (1ull << BIN_SHIFT) - 1;
+        for (uint64_t b = 0; b <= bn.nbins; b++) {
+            if (b > 0) {
+                const uint64_t lo = (b - 1) << BIN_SHIFT;
+                scan_emit(a, q, slot, lo, lo + bin_size(a.n, b - 1), removed);
+            }
+            if (b < bn.nbins) {
+                const uint64_t lo = b << BIN_SHIFT, sz = bin_size(a.n, b);
+                ulonglong2 *z = reinterpret_cast<ulonglong2 *>(a.state + lo);  // lo is 2^22-aligned
+                for (uint64_t i = tid; i < sz / 2; i += nthr) z[i] = make_ulonglong2(0ull, 0ull);
+                if ((sz & 1) && tid == 0) a.state[lo + sz - 1] = 0ull;
+            }
+            grid.sync();
+            if (b < bn.nbins) {
+                ull *st = a.state + (b << BIN_SHIFT);
+                const ull *ent = bn.entries + bn.base[b];
+                const ull cnt = min(bn.cursor[b], bn.cap[b]);
+                for (ull i = tid; i < cnt; i += nthr) {
+                    const ull x = __ldcs(ent + i);
+                    atomicAdd(st + (x & mask), (x & ~0xFFFFFFFFull) + 1ull);
+                }
+            }
+            grid.sync();
+        }
+    }
+    block_add<PEEL_BLOCK>(&ctl->nf[0], removed);
+}
+
 // packed path (k <= 2)
 template <int R>
-__global__ void __launch_bounds__(PEEL_BLOCK) peel_packed_kernel(PeelArgs a) {
+__global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ BlockQueue<uint2> q;
     Ctl *ctl = a.ctl;
@@ -283,32 +517,13 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_packed_kernel(PeelArgs a) {
     int slot = 0;
 
     // ---- round 1: F_1 = {v : count(v) < k}, a coalesced scan of the state ----
-    {
-        uint2 *F = (uint2 *)a.F[0];
+    // (already emitted by bin_accumulate_kernel when the build was binned)
+    if (!a.f1_ready) {
         ull removed = 0;
-        for (uint64_t base = (uint64_t)blockIdx.x * CHUNK; base < a.n; base += (uint64_t)gridDim.x * CHUNK) {
-            ull w[U];
-            #pragma unroll
-            for (int j = 0; j < U; j++) {
-                const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
-                w[j] = v < a.n ? a.state[v] : ~0ull;
-            }
-            #pragma unroll
-            for (int j = 0; j < U; j++) {
-                const uint64_t v = base + (uint64_t)j * PEEL_BLOCK + threadIdx.x;
-                if (v < a.n && count_of(w[j]) < k) {
-                    removed++;
-                    if (a.peel_round) a.peel_round[v] = 1;
-                    if (count_of(w[j]) == 1)  // k = 2: its one edge is the id sum
-                        bq_push(q, slot, make_uint2((uint32_t)v, idsum_of(w[j])), F, &ctl->ne[0]);
-                }
-            }
-            bq_flush(q, slot, F, &ctl->ne[0]);
-            slot ^= 1;
-        }
+        scan_emit(a, q, slot, 0, a.n, removed);
         block_add<PEEL_BLOCK>(&ctl->nf[0], removed);
+        grid.sync();
     }
-    grid.sync();
 
     // ---- rounds ----
     uint32_t t = 1;
@@ -490,7 +705,40 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     a.mask_vec = ((uintptr_t)core_mask & 15) == 0;
     if (peel_round) PEEL_CUDA(cudaMemsetAsync(peel_round, 0, sizeof(uint32_t) * n, s));
 
-    if (!csr) {
+    if (!csr && L.nbins) {
+        // binned build: partition endpoint increments by vertex bin, accumulate each bin in L2
+        ull *state = (ull *)(ws + L.state);
+        a.state = state;
+        ull *cursor = (ull *)(ws + L.bin_cursor), *bbase = (ull *)(ws + L.bin_base), *bcap = (ull *)(ws + L.bin_cap);
+        ull *entries = (ull *)(ws + L.entries);
+        {
+            ProfScope ps("bin_init", s);
+            bin_init_kernel<<<1, 32, 0, s>>>(n, m, R, L.nbins, cursor, bbase, bcap);
+        }
+        const size_t smem = partition_smem(R);
+        PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int pblocks = 0;
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
+        if (pblocks < 1) pblocks = 1;
+        if (m) {
+            ProfScope ps("bin_partition", s);
+            bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, L.nbins, cursor, bbase,
+                                                                                   bcap, entries, ctl);
+        }
+        PEEL_CUDA(cudaGetLastError());
+        BinArgs bn;
+        bn.nbins = L.nbins; bn.cursor = cursor; bn.base = bbase; bn.cap = bcap; bn.entries = entries;
+        int per_sm = 0;
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bin_accumulate_kernel<R>, PEEL_BLOCK, 0));
+        if (per_sm < 1) per_sm = 1;
+        void *bargs[] = {&a, &bn};
+        {
+            ProfScope ps("bin_accumulate", s);
+            PEEL_CUDA(cudaLaunchCooperativeKernel((void *)bin_accumulate_kernel<R>, num_sms() * per_sm, PEEL_BLOCK,
+                                                  bargs, 0, s));
+        }
+        a.f1_ready = 1;
+    } else if (!csr) {
         ull *state = (ull *)(ws + L.state);
         PEEL_CUDA(cudaMemsetAsync(state, 0, sizeof(ull) * n, s));
         a.state = state;

@@ -122,6 +122,32 @@ def test_paper_shaped_vs_oracle(r, k, c):
         check_vs_oracle(e_np, n, k, flags=pk.PEEL_FLAG_CSR, twice=False)
 
 
+@pytest.mark.parametrize("n,c,r,seed", [((1 << 23) + 12345, 0.75, 3, 21), ((1 << 23) + 1, 0.85, 3, 22),
+                                        (3 * (1 << 22) - 7, 0.8, 4, 23)])
+def test_binned_build_vs_oracle(n, c, r, seed):
+    # n > 2^23: the build partitions increments into 2^22-vertex bins (several bins + ragged last)
+    m = int(c * n)
+    e = pk.gen_hypergraph(n, m, r, seed, device=DEV)
+    e_np = e.cpu().numpy().view(np.uint32)
+    ref = O.sync_peel(e_np, n, 2, want_peel_round=True)
+    res = pk.peel_kcore(e, n, 2, want_peel_round=True)
+    assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist()
+    assert res.killed.tolist() == ref.killed.tolist()
+    assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
+    assert np.array_equal(res.peel_round.cpu().numpy().view(np.uint32), ref.peel_round)
+
+
+def test_binned_build_overflow_fallback():
+    # every edge contains vertex 0: bin 0 overflows its capacity -> direct-build fallback
+    n, m = (1 << 23) + 999, 600000
+    rng = np.random.default_rng(5)
+    e_np = np.zeros((m, 3), dtype=np.uint32)
+    e_np[:, 1] = rng.integers(1, n // 2, m)
+    e_np[:, 2] = e_np[:, 1] + n // 2 - 1
+    e_np[m // 2:, 0] = 5  # a second hub
+    check_vs_oracle(e_np, n, 2, twice=False)
+
+
 def test_c1_golden_and_oracle(goldens):
     g = goldens["C1"]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)

@@ -272,6 +272,7 @@ def main():
     t_ev1.record(stream)
     barrier()
     clocks = clk.stop()
+    round_ms = [round(x, 3) for x in pk.profile_rounds()]
     pk.profile_enable(False)
     ms_total = t_ev0.elapsed_time(t_ev1)
     ms_step = ms_total / args.steps
@@ -359,7 +360,7 @@ def main():
             "rounds": res.rounds,
             "hbm_roofline_step": {"alg_bytes": step_alg, "frac_of_measured": round(step_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
                                   "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "kernels": kernels, "round_ms": round_ms, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

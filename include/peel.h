@@ -116,9 +116,9 @@ size_t peel_kcore_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k
  *      any contents; clobbered.
  * Blocking: synchronises `stream` before returning.
  * Status: PEEL_ETRUNC if rounds > cap (or > 65536): rounds is exact, the
- *      first cap entries are written.  PEEL_EOVERFLOW (k <= 2 packed path
- *      only, impossible for random inputs) if some vertex degree d has
- *      d * (m-1) >= 2^40; rerun with PEEL_FLAG_CSR.
+ *      first cap entries are written.  (PEEL_EOVERFLOW is reserved: the k <= 2
+ *      packed state -- count in the low 32 bits, edge-id sum mod 2^32 above it --
+ *      cannot overflow for m < 2^32.)
  */
 peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k,
                        uint32_t flags, uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
@@ -220,6 +220,9 @@ void peel_profile_enable(int on);
 int peel_profile_read(const char **names, double *ms, uint32_t *launches, int cap);
 /* Kernel launches made by the last peel_kcore / iblt_* call (always counted). */
 uint32_t peel_last_launches(void);
+/* With profiling enabled: per-round device time (ms, from %globaltimer at each
+ * round barrier) of the last peel_kcore call; returns the number of rounds. */
+int peel_profile_rounds(double *ms, uint32_t cap);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,8 @@ def _L() -> ctypes.CDLL:
         L.peel_profile_read.argtypes = [p, p, p, i32]
         L.peel_profile_read.restype = i32
         L.peel_last_launches.restype = u32
+        L.peel_profile_rounds.argtypes = [p, u32]
+        L.peel_profile_rounds.restype = i32
         for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "iblt_build",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
@@ -295,6 +297,13 @@ def profile_read() -> list[tuple[str, float, int]]:
     nl = (ctypes.c_uint32 * 64)()
     n = _L().peel_profile_read(ctypes.addressof(names), ctypes.addressof(ms), ctypes.addressof(nl), 64)
     return [(names[i].decode(), ms[i], nl[i]) for i in range(min(n, 64))]
+
+
+def profile_rounds() -> list[float]:
+    """Per-round device time (ms) of the last peel_kcore call (profiling enabled)."""
+    buf = (ctypes.c_double * 65536)()
+    n = _L().peel_profile_rounds(ctypes.addressof(buf), 65536)
+    return [buf[i] for i in range(min(n, 65536))]
 
 
 def last_launches() -> int:

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "peel.h"
 
 namespace cg = cooperative_groups;
@@ -33,6 +35,8 @@ void prof_begin_call();                                   // resets the per-call
 void prof_pre(const char *name, cudaStream_t s);          // before a kernel launch
 void prof_post(const char *name, cudaStream_t s);         // after it (counts the launch)
 int prof_collect();                                       // after stream sync: resolve events
+bool prof_enabled();
+void prof_set_rounds(const std::vector<double> &ms);      // per-round device time of the last peel
 
 struct ProfScope {
     const char *name;

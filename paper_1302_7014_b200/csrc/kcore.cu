@@ -30,6 +30,8 @@
 //              and counts never increase.
 #include <string.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace peel {
@@ -49,7 +51,7 @@ struct Ctl {
 };
 
 struct Layout {
-    size_t ctl, fsize, killed, state, deg, off, bsum, adj, alive, F0, F1;
+    size_t ctl, fsize, killed, rtime, state, deg, off, bsum, adj, alive, F0, F1;
     size_t bins, bin_cursor, bin_base, bin_cap, entries;  // binned build (packed, n > BIN_MIN_N)
     uint64_t nbins, total_cap;
     size_t total;
@@ -82,6 +84,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     L.ctl = o; o += al(sizeof(Ctl));
     L.fsize = o; o += al(sizeof(ull) * (STAT_CAP + 1));
     L.killed = o; o += al(sizeof(ull) * (STAT_CAP + 1));
+    L.rtime = o; o += al(sizeof(ull) * (STAT_CAP + 2));
     const size_t fe = csr ? sizeof(uint32_t) : sizeof(uint2);  // frontier element: v, or (v, e)
     if (!csr) {
         L.state = o; o += al(sizeof(ull) * n);
@@ -165,31 +168,32 @@ __global__ void bin_init_kernel(uint64_t n, uint64_t m, uint32_t r, uint64_t nbi
 }
 
 static constexpr int PART_BLOCK = 256;
-static constexpr int PART_ENTRIES = 6144;  // endpoint entries staged per chunk
+static constexpr int PART_ENTRIES = 4096;  // endpoint entries staged per chunk
 
 // pass 1: partition the r m endpoint increments by vertex bin.  Per chunk of edges the
 // block histograms bins in shared memory, reserves one contiguous run per bin with a
 // single global atomic, counting-sorts the chunk's entries by bin in shared memory and
-// writes them out so each bin's run is a coalesced store.  entry = e << 32 | (u & mask).
+// writes them out so each bin's run is a coalesced store.  Stored entry =
+// e << 32 | (u mod 2^BIN_SHIFT); in shared memory the full u is kept (its bin is u >> BIN_SHIFT).
+// Shared memory = 8 B x PART_ENTRIES + 20 B x nbins (sized per launch).
 template <int R>
-__global__ void __launch_bounds__(PART_BLOCK) bin_partition_kernel(const uint32_t *__restrict__ edges, uint64_t n,
-                                                                   uint64_t m, uint64_t nbins, ull *cursor,
-                                                                   const ull *__restrict__ base,
-                                                                   const ull *__restrict__ cap, ull *entries,
-                                                                   Ctl *ctl) {
+__global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint32_t *__restrict__ edges,
+                                                                      uint64_t n, uint64_t m, uint32_t nbins,
+                                                                      ull *cursor, const ull *__restrict__ base,
+                                                                      const ull *__restrict__ cap, ull *entries,
+                                                                      Ctl *ctl) {
     constexpr int CH = PART_ENTRIES / R;  // edges per chunk
     extern __shared__ unsigned char smem_raw[];
-    ull *sent = (ull *)smem_raw;                                   // [CH*R]
-    uint32_t *hist = (uint32_t *)(sent + CH * R);                  // [MAX_BINS]
-    uint32_t *offs = hist + MAX_BINS;                              // [MAX_BINS]
-    uint32_t *fill = offs + MAX_BINS;                              // [MAX_BINS]
-    ull *gpos = (ull *)(fill + MAX_BINS);                          // [MAX_BINS]
-    uint16_t *sbin = (uint16_t *)(gpos + MAX_BINS);                // [CH*R]
+    ull *sent = (ull *)smem_raw;                  // [CH*R]  (e << 32 | u)
+    ull *gpos = sent + CH * R;                    // [nbins]
+    uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
+    uint32_t *offs = hist + nbins;                // [nbins]
+    uint32_t *fill = offs + nbins;                // [nbins]
     __shared__ uint32_t total;
     const ull mask = (1ull << BIN_SHIFT) - 1;
     for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {
         const int ne = (int)min((uint64_t)CH, m - c0);
-        for (int b = threadIdx.x; b < (int)nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
         __syncthreads();
         for (int i = threadIdx.x; i < ne; i += PART_BLOCK) {
             uint32_t u[R];
@@ -201,29 +205,29 @@ __global__ void __launch_bounds__(PART_BLOCK) bin_partition_kernel(const uint32_
             for (int j = 0; j < R; j++) atomicAdd(&hist[u[j] >> BIN_SHIFT], 1u);
         }
         __syncthreads();
-        // exclusive scan of hist over nbins (<= 1024): one warp, 32 bins per lane
+        // exclusive scan of hist over nbins (<= 1024): one warp
         if (threadIdx.x < 32) {
-            const int per = (MAX_BINS + 31) / 32;
+            const uint32_t per = (nbins + 31) / 32;
             uint32_t loc = 0;
-            for (int q = 0; q < per; q++) {
-                int b = threadIdx.x * per + q;
-                loc += b < (int)nbins ? hist[b] : 0;
+            for (uint32_t q = 0; q < per; q++) {
+                uint32_t b = threadIdx.x * per + q;
+                loc += b < nbins ? hist[b] : 0;
             }
             uint32_t x = loc;
             #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (threadIdx.x >= o) x += y;
+                if ((int)threadIdx.x >= o) x += y;
             }
             uint32_t run = x - loc;
-            for (int q = 0; q < per; q++) {
-                int b = threadIdx.x * per + q;
-                if (b < (int)nbins) { offs[b] = run; run += hist[b]; }
+            for (uint32_t q = 0; q < per; q++) {
+                uint32_t b = threadIdx.x * per + q;
+                if (b < nbins) { offs[b] = run; run += hist[b]; }
             }
             if (threadIdx.x == 31) total = x;
         }
         __syncthreads();
-        for (int b = threadIdx.x; b < (int)nbins; b += PART_BLOCK)
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)
             if (hist[b]) {
                 ull g = atomicAdd(cursor + b, (ull)hist[b]);
                 if (g + hist[b] > cap[b]) atomicOr(&ctl->binovf, 1u);
@@ -237,25 +241,23 @@ __global__ void __launch_bounds__(PART_BLOCK) bin_partition_kernel(const uint32_
             #pragma unroll
             for (int j = 0; j < R; j++) {
                 const uint32_t b = u[j] >> BIN_SHIFT;
-                const uint32_t p = offs[b] + atomicAdd(&fill[b], 1u);
-                sent[p] = (e << 32) | ((ull)u[j] & mask);
-                sbin[p] = (uint16_t)b;
+                sent[offs[b] + atomicAdd(&fill[b], 1u)] = (e << 32) | u[j];
             }
         }
         __syncthreads();
         const uint32_t tot = total;
         for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
-            const uint32_t b = sbin[i];
+            const ull x = sent[i];
+            const uint32_t b = (uint32_t)x >> BIN_SHIFT;
             const ull pos = gpos[b] + (i - offs[b]);
-            if (pos < cap[b]) entries[base[b] + pos] = sent[i];
+            if (pos < cap[b]) entries[base[b] + pos] = x & ~(0xFFFFFFFFull ^ mask);
         }
         __syncthreads();
     }
 }
 
-static size_t partition_smem(int r) {
-    return sizeof(ull) * (PART_ENTRIES / r) * r + sizeof(uint32_t) * 3 * MAX_BINS + sizeof(ull) * MAX_BINS +
-           sizeof(uint16_t) * (PART_ENTRIES / r) * r;
+static size_t partition_smem(int r, uint64_t nbins) {
+    return sizeof(ull) * (PART_ENTRIES / r) * r + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
 }
 
 // CSR build, pass 1: degree histogram
@@ -385,7 +387,14 @@ struct PeelArgs {
     uint32_t *peel_round;
     int mask_vec;            // core_mask is 16-byte aligned
     int f1_ready;            // packed: F_1 was emitted by the binned build
+    ull *rtime;              // %globaltimer at the start of each round (profiling)
 };
+
+__device__ __forceinline__ ull globaltimer() {
+    ull t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ uint32_t count_of(ull w) { return (uint32_t)w; }
 __device__ __forceinline__ uint32_t idsum_of(ull w) { return (uint32_t)(w >> 32); }
@@ -532,6 +541,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
         if (nF == 0) break;
         const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
         if (tid == 0) {
+            if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
             a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
             ctl->nf[(t + 1) % 3] = 0;  // round t+2's counters; their last reader finished a barrier ago
             ctl->ne[(t + 1) % 3] = 0;
@@ -591,7 +601,10 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
         grid.sync();
         t++;
     }
-    if (tid == 0) ctl->rounds = t - 1;
+    if (tid == 0) {
+        ctl->rounds = t - 1;
+        if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
+    }
     write_core_mask<false>(a, tid, nthr);
 }
 
@@ -629,6 +642,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
         const ull nF = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
         if (nF == 0) break;
         if (tid == 0) {
+            if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
             a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
             ctl->ne[(t + 1) % 3] = 0;
         }
@@ -669,7 +683,10 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
         grid.sync();
         t++;
     }
-    if (tid == 0) ctl->rounds = t - 1;
+    if (tid == 0) {
+        ctl->rounds = t - 1;
+        if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
+    }
     write_core_mask<true>(a, tid, nthr);
 }
 
@@ -701,6 +718,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     a.F[0] = ws + L.F0;
     a.F[1] = ws + L.F1;
     a.ctl = ctl; a.fsize = fsize; a.killed = kil;
+    a.rtime = (ull *)(ws + L.rtime);
     a.core_mask = core_mask; a.peel_round = peel_round;
     a.mask_vec = ((uintptr_t)core_mask & 15) == 0;
     if (peel_round) PEEL_CUDA(cudaMemsetAsync(peel_round, 0, sizeof(uint32_t) * n, s));
@@ -715,14 +733,14 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             ProfScope ps("bin_init", s);
             bin_init_kernel<<<1, 32, 0, s>>>(n, m, R, L.nbins, cursor, bbase, bcap);
         }
-        const size_t smem = partition_smem(R);
+        const size_t smem = partition_smem(R, L.nbins);
         PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int pblocks = 0;
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
         if (pblocks < 1) pblocks = 1;
         if (m) {
             ProfScope ps("bin_partition", s);
-            bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, L.nbins, cursor, bbase,
+            bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)L.nbins, cursor, bbase,
                                                                                    bcap, entries, ctl);
         }
         PEEL_CUDA(cudaGetLastError());
@@ -796,6 +814,14 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     prof_collect();
     if (hctl.err & ERR_BADVERTEX) return PEEL_EINVAL;
     uint64_t T = hctl.rounds;
+    if (prof_enabled()) {
+        uint64_t nt = (T < STAT_CAP ? T : STAT_CAP - 1) + 1;
+        std::vector<ull> rt(nt);
+        PEEL_CUDA(cudaMemcpy(rt.data(), a.rtime, sizeof(ull) * nt, cudaMemcpyDeviceToHost));
+        std::vector<double> ms(nt > 1 ? nt - 1 : 0);
+        for (uint64_t i = 0; i + 1 < nt; i++) ms[i] = (rt[i + 1] - rt[i]) * 1e-6;
+        prof_set_rounds(ms);
+    }
     *rounds = (uint32_t)T;
     uint64_t nstore = T < cap ? T : cap;
     if (nstore > STAT_CAP) nstore = STAT_CAP;

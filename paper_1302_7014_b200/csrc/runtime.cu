@@ -26,6 +26,7 @@ static bool g_prof_on = false;
 static std::vector<ProfEntry> g_prof;          // events of the current call
 static std::vector<ProfEntry> g_pool;          // recycled events
 static uint32_t g_launches = 0;
+static std::vector<double> g_round_ms;                 // per-round device time of the last peel
 static std::vector<const char *> g_res_names;  // resolved results of the last call
 static std::vector<double> g_res_ms;
 static std::vector<uint32_t> g_res_n;
@@ -45,6 +46,7 @@ static ProfEntry take_pair(const char *name) {
 
 void prof_begin_call() {
     g_launches = 0;
+    g_round_ms.clear();
     for (auto &p : g_prof) g_pool.push_back(p);
     g_prof.clear();
 }
@@ -83,6 +85,9 @@ int prof_collect() {
     }
     return (int)g_res_names.size();
 }
+
+bool prof_enabled() { return g_prof_on; }
+void prof_set_rounds(const std::vector<double> &ms) { g_round_ms = ms; }
 
 int num_sms() {
     static int sms = 0;
@@ -129,5 +134,11 @@ int peel_profile_read(const char **names, double *ms, uint32_t *launches, int ca
 }
 
 uint32_t peel_last_launches(void) { return peel::g_launches; }
+
+int peel_profile_rounds(double *ms, uint32_t cap) {
+    int n = (int)peel::g_round_ms.size();
+    for (int i = 0; i < n && i < (int)cap; i++) ms[i] = peel::g_round_ms[i];
+    return n;
+}
 
 }  // extern "C"

@@ -139,6 +139,28 @@ peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, uint64_t m, 
                             size_t ws_bytes, void *stream);
 
 /* ======================================================================= */
+/* e1 -- independent-trial sweeps (the paper's simulation protocol)  */
+/* ======================================================================= */
+
+/*
+ * peel_sweep -- for each trial t in [0, ntrials): generate G^r_{n, m[t]} with
+ * seed seeds[t] (exactly peel_gen_hypergraph(n, m[t], r, seeds[t])) and peel it
+ * to its k-core (exactly peel_kcore); report out_rounds[t] (host u32) and
+ * out_core[t] (host u64: k-core vertices; "Failed" in Table 1 iff > 0).
+ * m[], seeds[] are host arrays.  Trials are processed `batch` at a time as one
+ * disjoint-union hypergraph (the synchronous peel of a disjoint union is the
+ * trials' synchronous peels in lockstep), so batch * n <= 2^32 and
+ * batch * max(m) < 2^32.  Multi-GPU sweeps shard the trial index range across
+ * ranks (no data-path collective); see paper_1302_7014_b200/trials.py.
+ * workspace: dev, peel_sweep_workspace_bytes(n, max(m), r, k, batch) bytes.
+ * Blocking (one stream sync per batch).
+ */
+size_t peel_sweep_workspace_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch);
+peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
+                       uint64_t ntrials, uint32_t batch, uint32_t *out_rounds, uint64_t *out_core,
+                       void *workspace, size_t ws_bytes, void *stream);
+
+/* ======================================================================= */
 /* IBLT -- cells {count, checksum, key} with XOR accumulators   */
 /* ======================================================================= */
 
@@ -210,15 +232,17 @@ void iblt_destroy(peel_iblt *t);
 /* ======================================================================= */
 
 /*
- * When enabled, every peel_kcore / iblt_peel / iblt_insert call records a
- * CUDA event pair on `stream` around each kernel it launches; after the call
- * peel_profile_read returns up to `cap` (name, milliseconds, launches)
- * triples of the LAST call, in launch order.  Names are static strings.
- * Returns the number of entries.  Disabled by default (no events recorded).
+ * When enabled, every library call records a CUDA event pair on `stream`
+ * around each kernel it launches.  Blocking calls (peel_kcore, iblt_peel)
+ * resolve them: afterwards peel_profile_read returns up to `cap` (name,
+ * milliseconds, launches) triples for every launch since the previous blocking
+ * call (e.g. iblt_insert + iblt_peel), in first-launch order.  Names are static
+ * strings.  Returns the number of entries.  Disabled by default.
  */
 void peel_profile_enable(int on);
 int peel_profile_read(const char **names, double *ms, uint32_t *launches, int cap);
-/* Kernel launches made by the last peel_kcore / iblt_* call (always counted). */
+/* Kernel launches since the previous blocking call, counted through the last
+ * blocking call (always counted, profiling or not). */
 uint32_t peel_last_launches(void);
 /* With profiling enabled: per-round device time (ms, from %globaltimer at each
  * round barrier) of the last peel_kcore call; returns the number of rounds. */

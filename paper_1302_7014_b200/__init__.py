@@ -54,6 +54,9 @@ def _L() -> ctypes.CDLL:
         L.peel_kcore_host_workspace_bytes.argtypes = [u64, u64, u32, u32, u32]
         L.peel_kcore_host_workspace_bytes.restype = sz
         L.peel_kcore_host.argtypes = [p, u64, u64, u32, u32, u32, p, p, p, p, u32, p, sz, p]
+        L.peel_sweep_workspace_bytes.argtypes = [u64, u64, u32, u32, u32]
+        L.peel_sweep_workspace_bytes.restype = sz
+        L.peel_sweep.argtypes = [u64, u32, u32, p, p, u64, u32, p, p, p, sz, p]
         L.iblt_mem_bytes.argtypes = [u64, u32]
         L.iblt_mem_bytes.restype = sz
         L.iblt_build.argtypes = [u64, u32, u64, p, sz, p, ctypes.POINTER(p)]
@@ -70,7 +73,7 @@ def _L() -> ctypes.CDLL:
         L.peel_last_launches.restype = u32
         L.peel_profile_rounds.argtypes = [p, u32]
         L.peel_profile_rounds.restype = i32
-        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "iblt_build",
+        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "peel_sweep", "iblt_build",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
         _lib = L
@@ -216,6 +219,31 @@ def peel_kcore_host(edges_host: np.ndarray, n: int, k: int, flags: int = 0, cap:
 
 
 # ---------------------------------------------------------------------------
+# trial sweeps (e1)
+# ---------------------------------------------------------------------------
+def sweep(n: int, r: int, k: int, m, seeds, batch: int = 32, device=None, ws: torch.Tensor | None = None,
+          stream=None):
+    """Per-trial (rounds, core vertices) for trials (m[t], seeds[t]) of G^r_{n,m[t]} (peel.h peel_sweep)."""
+    m = np.ascontiguousarray(m, dtype=np.uint64)
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    assert m.shape == seeds.shape
+    T = m.size
+    rounds = np.zeros(T, dtype=np.uint32)
+    core = np.zeros(T, dtype=np.uint64)
+    if T == 0:
+        return rounds, core
+    batch = max(1, min(batch, T))
+    need = int(_L().peel_sweep_workspace_bytes(n, int(m.max()), r, k, batch))
+    if need == 0:
+        raise PeelError(PEEL_EINVAL, "peel_sweep_workspace_bytes")
+    if ws is None:
+        ws = workspace(need, _dev(device))
+    _check(_L().peel_sweep(n, r, k, m.ctypes.data, seeds.ctypes.data, T, batch, rounds.ctypes.data,
+                           core.ctypes.data, _ptr(ws), ws.numel(), _stream(stream)), "peel_sweep")
+    return rounds, core
+
+
+# ---------------------------------------------------------------------------
 # IBLT
 # ---------------------------------------------------------------------------
 class IbltResult:
@@ -231,16 +259,23 @@ class IbltResult:
 class Iblt:
     """IBLT of `cells` 16-byte cells and r hashes in a torch-owned device buffer (peel.h iblt_*)."""
 
-    def __init__(self, cells: int, r: int, seed: int, device=None, stream=None):
+    def __init__(self, cells: int, r: int, seed: int, device=None, stream=None, mem: torch.Tensor | None = None):
         self.C, self.r, self.seed = cells, r, seed
-        self.device = _dev(device)
+        self.device = _dev(device) if mem is None else mem.device
         nb = int(_L().iblt_mem_bytes(cells, r))
         if nb == 0:
             raise PeelError(PEEL_EINVAL, "iblt_mem_bytes")
-        self.mem = torch.empty((nb,), dtype=torch.uint8, device=self.device)
+        self.mem = torch.empty((nb,), dtype=torch.uint8, device=self.device) if mem is None else mem
+        self._h = None
+        self.reset(stream)
+
+    def reset(self, stream=None):
+        """(Re)build: zero the cells in place (peel.h iblt_build)."""
+        if self._h is not None and self._h.value:
+            _L().iblt_destroy(self._h)
         h = ctypes.c_void_p(0)
-        _check(_L().iblt_build(cells, r, seed & (2**64 - 1), _ptr(self.mem), nb, _stream(stream),
-                               ctypes.byref(h)), "iblt_build")
+        _check(_L().iblt_build(self.C, self.r, self.seed & (2**64 - 1), _ptr(self.mem), self.mem.numel(),
+                               _stream(stream), ctypes.byref(h)), "iblt_build")
         self._h = h
 
     def __del__(self):

@@ -48,6 +48,10 @@ struct ProfScope {
 // number of SMs and cooperative occupancy helpers
 int num_sms();
 
+// generator launch shared by peel_gen_hypergraph and peel_sweep (gen.cu)
+peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, uint32_t *edges, uint32_t voff,
+                             cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // device helpers
 // ---------------------------------------------------------------------------

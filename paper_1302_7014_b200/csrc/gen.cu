@@ -23,7 +23,7 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
 
 template <int R>
 __global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, uint64_t seed,
-                                                        uint32_t *__restrict__ edges) {
+                                                        uint32_t *__restrict__ edges, uint32_t voff) {
     const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, 
             }
         }
         #pragma unroll
-        for (int i = 0; i < R; i++) edges[e * R + i] = acc[i];
+        for (int i = 0; i < R; i++) edges[e * R + i] = acc[i] + voff;
     }
 }
 
@@ -70,28 +70,35 @@ static unsigned grid_for(uint64_t work, int per_sm = 16) {
 
 using namespace peel;
 
+namespace peel {
+// edges[m][r] of G^r_{n,cn}(seed) with every vertex id shifted by voff (voff = 0: the ABI call;
+// voff = b n: trial b of a disjoint-union batch, peel_sweep)
+peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, uint32_t *edges, uint32_t voff,
+                             cudaStream_t s) {
+    unsigned g = grid_for(m);
+    ProfScope ps("gen_edges", s);
+    switch (r) {
+        case 2: gen_edges_kernel<2><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        case 3: gen_edges_kernel<3><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        case 4: gen_edges_kernel<4><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        case 5: gen_edges_kernel<5><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        case 6: gen_edges_kernel<6><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        case 7: gen_edges_kernel<7><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        case 8: gen_edges_kernel<8><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        default: return PEEL_EINVAL;
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+}  // namespace peel
+
 extern "C" peel_status peel_gen_hypergraph(uint64_t n, uint64_t m, uint32_t r, uint64_t seed,
                                            uint32_t *edges, void *stream) {
     if (r < 2 || r > 8 || n < r || n > (1ull << 32) || m >= (1ull << 32)) return PEEL_EINVAL;
     if (m == 0) return PEEL_OK;
     if (!edges) return PEEL_EINVAL;
-    cudaStream_t s = (cudaStream_t)stream;
     prof_begin_call();
-    unsigned g = grid_for(m);
-    {
-        ProfScope ps("gen_edges", s);
-        switch (r) {
-            case 2: gen_edges_kernel<2><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-            case 3: gen_edges_kernel<3><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-            case 4: gen_edges_kernel<4><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-            case 5: gen_edges_kernel<5><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-            case 6: gen_edges_kernel<6><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-            case 7: gen_edges_kernel<7><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-            case 8: gen_edges_kernel<8><<<g, 256, 0, s>>>(n, m, seed, edges); break;
-        }
-    }
-    PEEL_CUDA(cudaGetLastError());
-    return PEEL_OK;
+    return launch_gen_edges(n, m, r, seed, edges, 0u, (cudaStream_t)stream);
 }
 
 extern "C" peel_status peel_gen_keys(uint64_t nkeys, uint64_t seed, uint64_t *keys, void *stream) {

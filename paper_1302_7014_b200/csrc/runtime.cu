@@ -44,7 +44,14 @@ static ProfEntry take_pair(const char *name) {
     return p;
 }
 
+// Launch counts and events accumulate from the first call after the last blocking
+// (collecting) call, so an async iblt_insert followed by a blocking iblt_peel report
+// together.
+static bool g_collected = true;
+
 void prof_begin_call() {
+    if (!g_collected) return;
+    g_collected = false;
     g_launches = 0;
     g_round_ms.clear();
     for (auto &p : g_prof) g_pool.push_back(p);
@@ -65,6 +72,7 @@ void prof_post(const char *name, cudaStream_t s) {
 }
 
 int prof_collect() {
+    g_collected = true;
     g_res_names.clear();
     g_res_ms.clear();
     g_res_n.clear();

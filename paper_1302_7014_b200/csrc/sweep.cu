@@ -1,0 +1,114 @@
+// sweep.cu -- independent-trial sweeps (the paper's simulation protocol,
+// "we ran the program 1000 times ... and computed the average number of rounds").
+//
+// A batch of B trials is peeled as ONE disjoint-union hypergraph: trial b's vertices are
+// [b n, (b+1) n) and its edges are G^r_{n,m_b}(seed_b) shifted by b n.  Round-synchronous
+// peeling of a disjoint union is exactly the B independent synchronous peels run in
+// lockstep (F_t of the union = the union of the trials' F_t), so one peel_kcore call over
+// the union -- with its binned build, persistent round loop and all -- computes every
+// trial.  Per trial: rounds = max over its vertices of the removal round, core = number
+// of its vertices never removed (a segmented reduction over peel_round / core_mask).
+#include "common.cuh"
+
+namespace peel {
+
+static inline size_t al2(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__global__ void __launch_bounds__(256) sweep_reduce_kernel(const uint32_t *__restrict__ peel_round,
+                                                           const uint8_t *__restrict__ mask, uint64_t n,
+                                                           ull *out_rounds, ull *out_core) {
+    const uint64_t b = blockIdx.x;
+    const uint32_t *pr = peel_round + b * n;
+    const uint8_t *mk = mask + b * n;
+    uint32_t mx = 0;
+    ull core = 0;
+    for (uint64_t v = threadIdx.x; v < n; v += blockDim.x) {
+        mx = max(mx, pr[v]);
+        core += mk[v];
+    }
+    __shared__ uint32_t smx[8];
+    __shared__ ull score[8];
+    #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        core += __shfl_xor_sync(0xffffffffu, core, o);
+    }
+    if ((threadIdx.x & 31) == 0) { smx[threadIdx.x >> 5] = mx; score[threadIdx.x >> 5] = core; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; w++) { mx = max(mx, smx[w]); core += score[w]; }
+        out_rounds[b] = mx;
+        out_core[b] = core;
+    }
+}
+
+struct SweepLayout {
+    size_t edges, mask, pr, res, kws, total;
+    size_t kws_bytes;
+};
+
+static SweepLayout sweep_layout(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
+    SweepLayout L;
+    size_t o = 0;
+    L.edges = o; o += al2(sizeof(uint32_t) * r * max_m * batch);
+    L.mask = o; o += al2(n * batch);
+    L.pr = o; o += al2(sizeof(uint32_t) * n * batch);
+    L.res = o; o += al2(sizeof(ull) * 2 * batch);
+    L.kws_bytes = peel_kcore_workspace_bytes(n * batch, max_m * batch, r, k, 0);
+    L.kws = o; o += al2(L.kws_bytes);
+    L.total = L.kws_bytes ? o : 0;
+    return L;
+}
+
+}  // namespace peel
+
+using namespace peel;
+
+extern "C" size_t peel_sweep_workspace_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
+    if (batch == 0 || n < r || n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return 0;
+    return sweep_layout(n, max_m, r, k, batch).total;
+}
+
+extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
+                                  uint64_t ntrials, uint32_t batch, uint32_t *out_rounds, uint64_t *out_core,
+                                  void *workspace, size_t ws_bytes, void *stream) {
+    if (!m || !seeds || !out_rounds || !out_core || !workspace || batch == 0 || r < 2 || r > 8 || n < r)
+        return PEEL_EINVAL;
+    uint64_t max_m = 0;
+    for (uint64_t t = 0; t < ntrials; t++) max_m = m[t] > max_m ? m[t] : max_m;
+    if (n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return PEEL_EINVAL;
+    SweepLayout L = sweep_layout(n, max_m, r, k, batch);
+    if (!L.total) return PEEL_EINVAL;
+    if (ws_bytes < L.total) return PEEL_ENOMEM;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *ws = (char *)workspace;
+    uint32_t *edges = (uint32_t *)(ws + L.edges);
+    uint8_t *mask = (uint8_t *)(ws + L.mask);
+    uint32_t *pr = (uint32_t *)(ws + L.pr);
+    ull *res = (ull *)(ws + L.res);
+    std::vector<ull> hres(2 * batch);
+    for (uint64_t t0 = 0; t0 < ntrials; t0 += batch) {
+        const uint32_t B = (uint32_t)(ntrials - t0 < batch ? ntrials - t0 : batch);
+        uint64_t off = 0;
+        for (uint32_t b = 0; b < B; b++) {
+            if (m[t0 + b]) {
+                peel_status st = launch_gen_edges(n, m[t0 + b], r, seeds[t0 + b], edges + off * r, (uint32_t)(b * n), s);
+                if (st != PEEL_OK) return st;
+            }
+            off += m[t0 + b];
+        }
+        uint32_t rounds = 0;
+        peel_status st = peel_kcore(edges, n * B, off, r, k, 0, mask, &rounds, nullptr, nullptr, 0, pr,
+                                    ws + L.kws, L.kws_bytes, stream);
+        if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
+        sweep_reduce_kernel<<<B, 256, 0, s>>>(pr, mask, n, res, res + batch);
+        PEEL_CUDA(cudaGetLastError());
+        PEEL_CUDA(cudaMemcpyAsync(hres.data(), res, sizeof(ull) * 2 * batch, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        for (uint32_t b = 0; b < B; b++) {
+            out_rounds[t0 + b] = (uint32_t)hres[b];
+            out_core[t0 + b] = hres[batch + b];
+        }
+    }
+    return PEEL_OK;
+}

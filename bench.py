@@ -353,6 +353,66 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
     return 0
 
 
+def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barrier, stream):
+    """One instance partitioned by vertex range over the ranks: NCCL under
+    torchrun, or --virtual-shards P on one GPU.  Strong scaling: the instance is fixed."""
+    import torch
+    import torch.distributed as dist
+    if args.virtual_shards > 0:
+        comm = pk.Comm.virtual_shards(args.virtual_shards)
+        P = args.virtual_shards
+    else:
+        comm = pk.Comm.from_process_group(device=dev)
+        P = ws
+    edges = pk.gen_hypergraph(n, m, r, seed, device=dev)  # replicated (same seed on every rank)
+    need = int(pk.lib().peel_kcore_dist_workspace_bytes(comm._h, n, m, r, k))
+    wsp = torch.empty((need,), dtype=torch.uint8, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        res = pk.peel_kcore_dist(comm, edges, n, k, ws=wsp, cap=4096)
+    n_core_local = int(res.core_mask.sum().item())
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    pk.profile_enable(True)
+    per_kernel, launches = {}, 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = pk.peel_kcore_dist(comm, edges, n, k, ws=wsp, cap=4096)
+        launches += pk.last_launches()
+        for name, ms_, nl in pk.profile_read():
+            a = per_kernel.setdefault(name, [0.0, 0])
+            a[0] += ms_
+            a[1] += nl
+    e1.record(stream)
+    barrier()
+    pk.profile_enable(False)
+    clocks = clk.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    cores = torch.tensor([float(n_core_local)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cores)
+    peeled = int(sum(res.killed))
+    value = peeled * args.steps / (t.item() / 1e3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": round(t.item() / args.steps, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 integer",
+                "data": "synthetic G^r_{n,cn}, edge list replicated on every rank",
+                "config": {"workload": f"{args.config}: {text}", "n": n, "m": m, "r": r, "k": k, "seed": seed,
+                           "rounds": res.rounds, "core_vertices": int(cores.item()), "peeled_edges": peeled,
+                           "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"vertex-partitioned{P}")},
+                "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
+                "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
+        print(json.dumps(line), flush=True)
+    del comm
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -363,6 +423,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "dist"],
+                    help="N>1: 'dist' = one instance vertex-partitioned over the ranks (peel_kcore_dist, "
+                         "strong scaling; default for k<=2 configs), 'replicas' = one instance per rank (weak)")
+    ap.add_argument("--virtual-shards", type=int, default=0,
+                    help="N=1 only: run the partitioned path with P virtual shards on one GPU")
     ap.add_argument("--profile-steps", action="store_true",
                     help="record per-kernel CUDA events inside the timed steps (default on)")
     args = ap.parse_args()
@@ -393,6 +458,9 @@ def main():
         return run_iblt(args, pk, dev, ws, rank, local, n, m, r, seed, text, barrier, stream)
     if kind == "sweep":
         return run_sweep_bench(args, pk, dev, ws, rank, local, n, m, r, k, text, barrier, stream)
+    use_dist = args.virtual_shards > 0 or (ws > 1 and k <= 2 and args.mode in ("auto", "dist"))
+    if use_dist:
+        return run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed - rank, text, barrier, stream)
 
     edges = pk.gen_hypergraph(n, m, r, seed, device=dev)
     wsb = pk.kcore_workspace_bytes(n, m, r, k)

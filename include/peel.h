@@ -161,6 +161,40 @@ peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, co
                        void *workspace, size_t ws_bytes, void *stream);
 
 /* ======================================================================= */
+/* e2 -- one instance partitioned by vertex range over P GPUs               */
+/* ======================================================================= */
+
+/*
+ * Rank p of P owns vertices [p n / P, (p+1) n / P).  The edge list is
+ * replicated (read-only) on every rank.  Each round: local kills, ONE
+ * all-to-all of killed edge ids to the other owners of their endpoints (NCCL
+ * grouped send/recv), receiver-side exactly-once application, and a 3-word
+ * allreduce (|F_{t+1}|, edges killed, errors) that is the termination test.
+ * Results are bit-identical to peel_kcore (k <= 2; EINVAL for k >= 3).
+ *
+ * peel_comm_unique_id: fill 128 bytes with an NCCL unique id (rank 0), to be
+ *   broadcast to the other ranks by the caller (e.g. torch.distributed).
+ * peel_comm_init: NCCL communicator, one process per GPU (current device).
+ * peel_comm_init_virtual: P shards inside ONE process on ONE GPU, the
+ *   all-to-all done by device copies through the same send/receive buffers
+ *   and kernels -- the partitioning logic testable without P GPUs.
+ * peel_kcore_dist: edges dev u32 [m][r] (replicated); core_mask dev u8: the
+ *   rank's slice [v1 - v0] (NCCL) or all n (virtual); rounds/survivors/killed
+ *   host, global (identical on every rank); workspace dev,
+ *   peel_kcore_dist_workspace_bytes bytes (per rank; virtual: all shards).
+ *   Blocking (host-driven rounds: two stream syncs per round).
+ */
+typedef struct peel_comm peel_comm;
+peel_status peel_comm_unique_id(void *id128);
+peel_status peel_comm_init(const void *id128, int nranks, int rank, peel_comm **out);
+peel_status peel_comm_init_virtual(int nshards, peel_comm **out);
+void peel_comm_destroy(peel_comm *c);
+size_t peel_kcore_dist_workspace_bytes(const peel_comm *c, uint64_t n, uint64_t m, uint32_t r, uint32_t k);
+peel_status peel_kcore_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k,
+                            uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors, uint64_t *killed,
+                            uint32_t cap, void *workspace, size_t ws_bytes, void *stream);
+
+/* ======================================================================= */
 /* IBLT -- cells {count, checksum, key} with XOR accumulators   */
 /* ======================================================================= */
 

@@ -57,6 +57,13 @@ def _L() -> ctypes.CDLL:
         L.peel_sweep_workspace_bytes.argtypes = [u64, u64, u32, u32, u32]
         L.peel_sweep_workspace_bytes.restype = sz
         L.peel_sweep.argtypes = [u64, u32, u32, p, p, u64, u32, p, p, p, sz, p]
+        L.peel_comm_unique_id.argtypes = [p]
+        L.peel_comm_init.argtypes = [p, i32, i32, ctypes.POINTER(p)]
+        L.peel_comm_init_virtual.argtypes = [i32, ctypes.POINTER(p)]
+        L.peel_comm_destroy.argtypes = [p]
+        L.peel_kcore_dist_workspace_bytes.argtypes = [p, u64, u64, u32, u32]
+        L.peel_kcore_dist_workspace_bytes.restype = sz
+        L.peel_kcore_dist.argtypes = [p, p, u64, u64, u32, u32, p, p, p, p, u32, p, sz, p]
         L.iblt_mem_bytes.argtypes = [u64, u32]
         L.iblt_mem_bytes.restype = sz
         L.iblt_build.argtypes = [u64, u32, u64, p, sz, p, ctypes.POINTER(p)]
@@ -73,7 +80,8 @@ def _L() -> ctypes.CDLL:
         L.peel_last_launches.restype = u32
         L.peel_profile_rounds.argtypes = [p, u32]
         L.peel_profile_rounds.restype = i32
-        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "peel_sweep", "iblt_build",
+        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "peel_sweep",
+                  "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
         _lib = L
@@ -241,6 +249,72 @@ def sweep(n: int, r: int, k: int, m, seeds, batch: int = 32, device=None, ws: to
     _check(_L().peel_sweep(n, r, k, m.ctypes.data, seeds.ctypes.data, T, batch, rounds.ctypes.data,
                            core.ctypes.data, _ptr(ws), ws.numel(), _stream(stream)), "peel_sweep")
     return rounds, core
+
+
+# ---------------------------------------------------------------------------
+# vertex-partitioned single instance over P GPUs (e2)
+# ---------------------------------------------------------------------------
+class Comm:
+    """peel_comm: NCCL (one process per GPU) or P virtual shards on one GPU (peel.h e2)."""
+
+    def __init__(self, handle, nshards: int, rank: int, virtual: bool):
+        self._h, self.P, self.rank, self.virtual = handle, nshards, rank, virtual
+
+    @classmethod
+    def virtual_shards(cls, nshards: int):
+        h = ctypes.c_void_p(0)
+        _check(_L().peel_comm_init_virtual(nshards, ctypes.byref(h)), "peel_comm_init_virtual")
+        return cls(h, nshards, -1, True)
+
+    @classmethod
+    def from_process_group(cls, group=None, device=None):
+        """NCCL communicator over the ranks of a torch.distributed group (rank 0 makes the
+        unique id, broadcast as a byte tensor); call after torch.cuda.set_device."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        idb = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            _check(_L().peel_comm_unique_id(idb.ctypes.data), "peel_comm_unique_id")
+        t = torch.from_numpy(idb).to(_dev(device))
+        dist.broadcast(t, src=0, group=group)
+        idb = t.cpu().numpy()
+        h = ctypes.c_void_p(0)
+        _check(_L().peel_comm_init(idb.ctypes.data, world, rank, ctypes.byref(h)), "peel_comm_init")
+        return cls(h, world, rank, False)
+
+    def shard(self, n: int, q: int | None = None) -> tuple[int, int]:
+        q = self.rank if q is None else q
+        return q * n // self.P, (q + 1) * n // self.P
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.peel_comm_destroy(h)
+            self._h = None
+
+
+def peel_kcore_dist(comm: Comm, edges: torch.Tensor, n: int, k: int, cap: int = 65536,
+                    core_mask: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None):
+    """Vertex-partitioned peel (peel.h peel_kcore_dist).  core_mask: this rank's slice
+    (NCCL) or all n vertices (virtual shards).  rounds/survivors/killed are global."""
+    assert edges.dim() == 2 and edges.dtype == torch.int32 and edges.is_cuda and edges.is_contiguous()
+    m, r = edges.shape
+    need = int(_L().peel_kcore_dist_workspace_bytes(comm._h, n, m, r, k))
+    if need == 0:
+        raise PeelError(PEEL_EINVAL, "peel_kcore_dist_workspace_bytes")
+    if ws is None:
+        ws = workspace(need, edges.device)
+    if core_mask is None:
+        lo, hi = (0, n) if comm.virtual else comm.shard(n)
+        core_mask = torch.empty((hi - lo,), dtype=torch.uint8, device=edges.device)
+    rounds = ctypes.c_uint32(0)
+    surv = np.zeros(cap, dtype=np.uint64)
+    killed = np.zeros(cap, dtype=np.uint64)
+    st = _L().peel_kcore_dist(comm._h, _ptr(edges), n, m, r, k, _ptr(core_mask), ctypes.addressof(rounds),
+                              surv.ctypes.data, killed.ctypes.data, cap, _ptr(ws), ws.numel(), _stream(stream))
+    _check(st, "peel_kcore_dist")
+    t = rounds.value
+    return KcoreResult(core_mask, t, surv[:min(t, cap)].copy(), killed[:min(t, cap)].copy(), None, st)
 
 
 # ---------------------------------------------------------------------------

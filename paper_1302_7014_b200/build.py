@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libpeel.so")
-SOURCES = ["runtime.cu", "gen.cu", "kcore.cu", "iblt.cu", "sweep.cu"]
+SOURCES = ["runtime.cu", "gen.cu", "kcore.cu", "iblt.cu", "sweep.cu", "dist.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr"]
 
@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(out.decode())
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs]
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lnccl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

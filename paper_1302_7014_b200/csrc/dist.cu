@@ -1,0 +1,536 @@
+// dist.cu -- e2: one peeling instance partitioned by vertex range over P GPUs
+// (BASELINE.json configs[4] "vertex-partitioned single instance").
+//
+// Rank p owns vertices [p n / P, (p+1) n / P): their packed state (Σ edge ids << 32 | count),
+// frontier entries and core-mask slice.  The edge list is replicated read-only, and each
+// rank keeps its own m-bit alive bitmap, meaningful for edges touching its vertices.
+// A round (k = 2, the round-synchronous schedule of P:48-50):
+//   kill    for each local frontier entry (v, e): test-and-clear alive_p[e]; the winner
+//           decrements its own endpoints of e (crossing 2 -> 1 appends (u, Σ - e) to the
+//           local F_{t+1}) and queues e for every OTHER rank owning an endpoint of e;
+//   exchange  one all-to-all of the queued edge ids (NCCL grouped send/recv; or device
+//           copies between virtual shards of one GPU);
+//   receive each received e: test-and-clear alive_q[e]; the winner decrements its own
+//           endpoints of e.  Every (e, rank) pair is applied exactly once -- by that rank's
+//           test-and-clear -- even when several ranks kill e in the same round;
+//   stats   allreduce of (|F_{t+1}|, edges killed) -- an edge's kill is counted by the
+//           owner of its smallest endpoint -- the termination test.
+// Bit-exact with the single-GPU peel by construction: every vertex's count sees exactly
+// the decrements of its killed edges, and F_{t+1} is the set of k -> k-1 crossings.
+#include <nccl.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace peel {
+
+static constexpr int DB = 256;            // block size
+static constexpr int DQ = 2 * DB;         // block-queue capacity
+static constexpr uint32_t DSTAT_CAP = 65536;
+
+struct DCtl {
+    ull nf[2];      // |F_t| local, double-buffered by round parity
+    ull ne[2];      // frontier entry counts
+    ull kills;      // edges killed this round, counted at the owner of the smallest endpoint
+    ull nsend[8];   // per-destination queue lengths this round
+    uint32_t err;
+    uint32_t pad;
+};
+
+static inline size_t dal(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__host__ __device__ inline uint64_t shard_lo(uint64_t n, int P, int q) { return (uint64_t)q * n / (uint64_t)P; }
+
+__device__ __forceinline__ int owner_of(uint32_t u, uint64_t n, int P) {
+    int q = (int)(((uint64_t)u * (uint64_t)P) / n);
+    if (q >= P) q = P - 1;
+    while (q > 0 && (uint64_t)u < shard_lo(n, P, q)) q--;
+    while (q + 1 < P && (uint64_t)u >= shard_lo(n, P, q + 1)) q++;
+    return q;
+}
+
+struct DShard {
+    int q;                 // shard index (= rank for NCCL)
+    uint64_t v0, v1;       // owned vertices
+    ull *state;            // [v1 - v0]
+    uint32_t *alive;       // [m/32]
+    uint2 *F[2];           // frontier entries (global v, e), cap v1 - v0
+    uint32_t *send;        // P segments of cap (v1 - v0) each
+    uint32_t *recv;        // cap n
+    DCtl *ctl;
+};
+
+struct DLayout {
+    size_t ctl, scratch, state, alive, F0, F1, send, recv, total;
+};
+
+static DLayout dlayout(uint64_t n, uint64_t m, int P, uint64_t nloc) {
+    DLayout L;
+    size_t o = 0;
+    L.ctl = o; o += dal(sizeof(DCtl));
+    L.scratch = o; o += dal(sizeof(ull) * (4 + 64));  // NCCL staging: 3 sums + the P x P count matrix
+    L.state = o; o += dal(sizeof(ull) * nloc);
+    L.alive = o; o += dal(sizeof(uint32_t) * ((m + 31) / 32));
+    L.F0 = o; o += dal(sizeof(uint2) * nloc);
+    L.F1 = o; o += dal(sizeof(uint2) * nloc);
+    L.send = o; o += dal(sizeof(uint32_t) * nloc * P);
+    L.recv = o; o += dal(sizeof(uint32_t) * n);
+    L.total = o;
+    return L;
+}
+
+typedef BlockQueueT<uint2, DQ, DB> DEntQ;
+typedef BlockQueueT<uint32_t, DQ, DB> DIdQ;
+
+template <int R>
+__device__ __forceinline__ bool dload_edge(const uint32_t *__restrict__ edges, uint64_t e, uint64_t n,
+                                           uint32_t (&u)[R]) {
+    bool ok = true;
+    #pragma unroll
+    for (int j = 0; j < R; j++) {
+        u[j] = __ldg(edges + e * R + j);
+        ok &= (uint64_t)u[j] < n;
+    }
+    #pragma unroll
+    for (int i = 0; i < R; i++)
+        #pragma unroll
+        for (int j = i + 1; j < R; j++) ok &= u[i] != u[j];
+    return ok;
+}
+
+// build: every rank scans all edges, accumulates its own endpoints
+template <int R>
+__global__ void __launch_bounds__(DB) dist_build_kernel(const uint32_t *__restrict__ edges, uint64_t n, uint64_t m,
+                                                        uint64_t v0, uint64_t v1, ull *state, DCtl *ctl) {
+    for (uint64_t e = blockIdx.x * (uint64_t)DB + threadIdx.x; e < m; e += (uint64_t)gridDim.x * DB) {
+        uint32_t u[R];
+        if (!dload_edge<R>(edges, e, n, u)) {
+            atomicOr(&ctl->err, 1u);
+            continue;
+        }
+        const ull inc = (e << 32) + 1ull;
+        #pragma unroll
+        for (int j = 0; j < R; j++)
+            if (u[j] >= v0 && u[j] < v1) atomicAdd(state + (u[j] - v0), inc);
+    }
+}
+
+// round 1: F_1 over owned vertices
+__global__ void __launch_bounds__(DB) dist_scan_kernel(const ull *__restrict__ state, uint64_t v0, uint64_t nloc,
+                                                       uint32_t k, uint2 *F, DCtl *ctl) {
+    __shared__ DEntQ q;
+    bq_init(q);
+    __syncthreads();
+    ull removed = 0;
+    int slot = 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * DB; base < nloc; base += (uint64_t)gridDim.x * DB) {
+        const uint64_t i = base + threadIdx.x;
+        if (i < nloc) {
+            const ull w = state[i];
+            if ((uint32_t)w < k) {
+                removed++;
+                if ((uint32_t)w == 1u) bq_push(q, slot, make_uint2((uint32_t)(v0 + i), (uint32_t)(w >> 32)), F, &ctl->ne[1]);
+            }
+        }
+        bq_flush(q, slot, F, &ctl->ne[1]);
+        slot ^= 1;
+    }
+    block_add<DB>(&ctl->nf[1], removed);
+}
+
+// decrement owned endpoint u of killed edge e; crossing count 2 -> 1 joins F_{t+1}
+__device__ __forceinline__ void dist_decrement(ull *state, uint64_t v0, uint32_t u, uint32_t e, uint32_t k,
+                                               DEntQ &q, int slot, uint2 *Fn, ull *cn, ull &crossed) {
+    const ull old = atomicAdd(state + (u - v0), 0ull - (((ull)e << 32) + 1ull));
+    if ((uint32_t)old == k) {
+        crossed++;
+        bq_push(q, slot, make_uint2(u, (uint32_t)(old >> 32) - e), Fn, cn);
+    }
+}
+
+struct DKArgs {
+    const uint32_t *edges;
+    uint64_t n;
+    int P, p;
+    uint32_t k;
+    uint64_t v0, v1, nloc;
+    ull *state;
+    uint32_t *alive;
+    const uint2 *Fc;
+    ull nE;
+    uint2 *Fn;
+    uint32_t *send;
+    DCtl *ctl;
+    int par;  // parity of round t+1's counters
+};
+
+// kill: local frontier entries
+template <int R>
+__global__ void __launch_bounds__(DB) dist_kill_kernel(DKArgs a) {
+    __shared__ DEntQ q;
+    __shared__ DIdQ qs[8];
+    bq_init(q);
+    for (int d = 0; d < 8; d++) bq_init(qs[d]);
+    __syncthreads();
+    ull *cn = &a.ctl->ne[a.par];
+    ull crossed = 0, kills = 0;
+    int slot = 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * DB; base < a.nE; base += (uint64_t)gridDim.x * DB) {
+        const uint64_t i = base + threadIdx.x;
+        if (i < a.nE) {
+            const uint2 ent = __ldcg(a.Fc + i);
+            const uint32_t e = ent.y, bit = 1u << (e & 31);
+            if (atomicAnd(a.alive + (e >> 5), ~bit) & bit) {
+                uint32_t u[R];
+                uint32_t mn = 0xFFFFFFFFu;
+                #pragma unroll
+                for (int j = 0; j < R; j++) { u[j] = __ldg(a.edges + (uint64_t)e * R + j); mn = min(mn, u[j]); }
+                if (owner_of(mn, a.n, a.P) == a.p) kills++;
+                uint32_t sent_mask = 0;
+                #pragma unroll
+                for (int j = 0; j < R; j++) {
+                    const int o = owner_of(u[j], a.n, a.P);
+                    if (o == a.p) {
+                        if (u[j] != ent.x) dist_decrement(a.state, a.v0, u[j], e, a.k, q, slot, a.Fn, cn, crossed);
+                    } else if (!(sent_mask >> o & 1u)) {
+                        sent_mask |= 1u << o;
+                        bq_push(qs[o], slot, e, a.send + (uint64_t)o * a.nloc, &a.ctl->nsend[o]);
+                    }
+                }
+            }
+        }
+        bq_flush(q, slot, a.Fn, cn);
+        for (int d = 0; d < a.P; d++) bq_flush(qs[d], slot, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
+        slot ^= 1;
+    }
+    block_add<DB>(&a.ctl->nf[a.par], crossed);
+    block_add<DB>(&a.ctl->kills, kills);
+}
+
+// receive: edge ids killed by other ranks this round
+template <int R>
+__global__ void __launch_bounds__(DB) dist_recv_kernel(DKArgs a, const uint32_t *__restrict__ recv, ull nrecv) {
+    __shared__ DEntQ q;
+    bq_init(q);
+    __syncthreads();
+    ull *cn = &a.ctl->ne[a.par];
+    ull crossed = 0, kills = 0;
+    int slot = 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * DB; base < nrecv; base += (uint64_t)gridDim.x * DB) {
+        const uint64_t i = base + threadIdx.x;
+        if (i < nrecv) {
+            const uint32_t e = __ldcg(recv + i), bit = 1u << (e & 31);
+            if (atomicAnd(a.alive + (e >> 5), ~bit) & bit) {
+                uint32_t mn = 0xFFFFFFFFu;
+                uint32_t u[R];
+                #pragma unroll
+                for (int j = 0; j < R; j++) { u[j] = __ldg(a.edges + (uint64_t)e * R + j); mn = min(mn, u[j]); }
+                if (owner_of(mn, a.n, a.P) == a.p) kills++;
+                #pragma unroll
+                for (int j = 0; j < R; j++)
+                    if (u[j] >= a.v0 && u[j] < a.v1) dist_decrement(a.state, a.v0, u[j], e, a.k, q, slot, a.Fn, cn, crossed);
+            }
+        }
+        bq_flush(q, slot, a.Fn, cn);
+        slot ^= 1;
+    }
+    block_add<DB>(&a.ctl->nf[a.par], crossed);
+    block_add<DB>(&a.ctl->kills, kills);
+}
+
+__global__ void dist_mask_kernel(const ull *__restrict__ state, uint64_t nloc, uint32_t k, uint8_t *mask) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nloc; i += (uint64_t)gridDim.x * blockDim.x)
+        mask[i] = (uint32_t)state[i] >= k ? 1 : 0;
+}
+
+static unsigned dgrid(uint64_t work) {
+    uint64_t b = (work + DB - 1) / DB, cap = (uint64_t)num_sms() * 8;
+    return (unsigned)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace peel
+
+using namespace peel;
+
+struct peel_comm {
+    int P;          // number of shards (ranks)
+    int rank;       // this process's rank (NCCL), -1 for virtual shards
+    bool virt;
+    ncclComm_t nccl;
+};
+
+#define PEEL_NCCL(call)                                                 \
+    do {                                                                \
+        ncclResult_t _r = (call);                                       \
+        if (_r != ncclSuccess) {                                        \
+            snprintf_nccl_error(_r, #call);                             \
+            return PEEL_ENCCL;                                          \
+        }                                                               \
+    } while (0)
+
+static void snprintf_nccl_error(ncclResult_t r, const char *where) {
+    (void)where;
+    peel::set_cuda_error(cudaErrorUnknown, ncclGetErrorString(r));
+}
+
+extern "C" peel_status peel_comm_unique_id(void *id128) {
+    if (!id128) return PEEL_EINVAL;
+    ncclUniqueId id;
+    PEEL_NCCL(ncclGetUniqueId(&id));
+    memcpy(id128, &id, sizeof(id));
+    return PEEL_OK;
+}
+
+extern "C" peel_status peel_comm_init(const void *id128, int nranks, int rank, peel_comm **out) {
+    if (!id128 || !out || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return PEEL_EINVAL;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    peel_comm *c = new peel_comm;
+    c->P = nranks;
+    c->rank = rank;
+    c->virt = false;
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        snprintf_nccl_error(r, "ncclCommInitRank");
+        return PEEL_ENCCL;
+    }
+    *out = c;
+    return PEEL_OK;
+}
+
+extern "C" peel_status peel_comm_init_virtual(int nshards, peel_comm **out) {
+    if (!out || nshards < 1 || nshards > 8) return PEEL_EINVAL;
+    peel_comm *c = new peel_comm;
+    c->P = nshards;
+    c->rank = -1;
+    c->virt = true;
+    c->nccl = nullptr;
+    *out = c;
+    return PEEL_OK;
+}
+
+extern "C" void peel_comm_destroy(peel_comm *c) {
+    if (!c) return;
+    if (!c->virt && c->nccl) ncclCommDestroy(c->nccl);
+    delete c;
+}
+
+static uint64_t max_shard(uint64_t n, int P) {
+    uint64_t mx = 0;
+    for (int q = 0; q < P; q++) mx = std::max(mx, shard_lo(n, P, q + 1) - shard_lo(n, P, q));
+    return mx;
+}
+
+extern "C" size_t peel_kcore_dist_workspace_bytes(const peel_comm *c, uint64_t n, uint64_t m, uint32_t r, uint32_t k) {
+    if (!c || r < 2 || r > 8 || k > 2 || n > (1ull << 32) || m >= (1ull << 32) || n < (uint64_t)c->P) return 0;
+    DLayout L = dlayout(n, m, c->P, max_shard(n, c->P));
+    return c->virt ? L.total * c->P : L.total;
+}
+
+template <int R>
+static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k,
+                            uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors, uint64_t *killed,
+                            uint32_t cap, char *ws, cudaStream_t s) {
+    const int P = c->P;
+    const uint64_t nl_max = max_shard(n, P);
+    const DLayout L = dlayout(n, m, P, nl_max);
+    // local shards: all P (virtual) or just this rank's
+    std::vector<DShard> sh;
+    for (int q = 0; q < P; q++) {
+        if (!c->virt && q != c->rank) continue;
+        char *b = ws + (c->virt ? (size_t)q * L.total : 0);
+        DShard d;
+        d.q = q;
+        d.v0 = shard_lo(n, P, q);
+        d.v1 = shard_lo(n, P, q + 1);
+        d.ctl = (DCtl *)(b + L.ctl);
+        d.state = (ull *)(b + L.state);
+        d.alive = (uint32_t *)(b + L.alive);
+        d.F[0] = (uint2 *)(b + L.F0);
+        d.F[1] = (uint2 *)(b + L.F1);
+        d.send = (uint32_t *)(b + L.send);
+        d.recv = (uint32_t *)(b + L.recv);
+        sh.push_back(d);
+    }
+    for (auto &d : sh) {
+        PEEL_CUDA(cudaMemsetAsync(d.ctl, 0, sizeof(DCtl), s));
+        PEEL_CUDA(cudaMemsetAsync(d.state, 0, sizeof(ull) * (d.v1 - d.v0), s));
+        PEEL_CUDA(cudaMemsetAsync(d.alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s));
+        if (m) {
+            ProfScope ps("dist_build", s);
+            dist_build_kernel<R><<<dgrid(m), DB, 0, s>>>(edges, n, m, d.v0, d.v1, d.state, d.ctl);
+        }
+        ProfScope ps("dist_scan", s);
+        dist_scan_kernel<<<dgrid(d.v1 - d.v0), DB, 0, s>>>(d.state, d.v0, d.v1 - d.v0, k, d.F[1], d.ctl);
+    }
+    PEEL_CUDA(cudaGetLastError());
+
+    // host-side views of the per-shard control blocks
+    std::vector<DCtl> hc(sh.size());
+    auto fetch_ctl = [&]() -> peel_status {
+        for (size_t i = 0; i < sh.size(); i++)
+            PEEL_CUDA(cudaMemcpyAsync(&hc[i], sh[i].ctl, sizeof(DCtl), cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        return PEEL_OK;
+    };
+    // global sums of (|F|, kills, err) over all shards/ranks
+    ull *dsum = (ull *)(ws + L.scratch);  // device staging for the NCCL collectives (3 words)
+    auto global_sums = [&](int par, ull out[3]) -> peel_status {
+        peel_status st = fetch_ctl();
+        if (st != PEEL_OK) return st;
+        ull loc[3] = {0, 0, 0};
+        for (auto &h : hc) { loc[0] += h.nf[par]; loc[1] += h.kills; loc[2] |= h.err; }
+        if (c->virt) {
+            memcpy(out, loc, sizeof loc);
+            return PEEL_OK;
+        }
+        PEEL_CUDA(cudaMemcpyAsync(dsum, loc, sizeof loc, cudaMemcpyHostToDevice, s));
+        PEEL_NCCL(ncclAllReduce(dsum, dsum, 3, ncclUint64, ncclSum, c->nccl, s));
+        PEEL_CUDA(cudaMemcpyAsync(out, dsum, sizeof loc, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        return PEEL_OK;
+    };
+
+    ull g[3];
+    peel_status st = global_sums(1, g);
+    if (st != PEEL_OK) return st;
+    if (g[2]) return PEEL_EINVAL;
+    uint64_t alive_v = n;
+    uint32_t t = 0;
+    std::vector<ull> cnt_mat((size_t)P * P);
+    std::vector<ull> loc_cnt(P);
+    ull *dcnt = dsum + 4;  // P x P count matrix
+    while (g[0] > 0) {
+        t++;
+        alive_v -= g[0];
+        if (t <= cap) {
+            if (survivors) survivors[t - 1] = alive_v;
+        }
+        const int cur = t & 1, nxt = cur ^ 1;  // round t's entries live at parity (t&1): round 1 uses F[1]
+        // reset next-round counters and per-destination queues
+        for (auto &d : sh) {
+            PEEL_CUDA(cudaMemsetAsync(&d.ctl->nf[nxt], 0, sizeof(ull), s));
+            PEEL_CUDA(cudaMemsetAsync(&d.ctl->ne[nxt], 0, sizeof(ull), s));
+            PEEL_CUDA(cudaMemsetAsync(&d.ctl->kills, 0, sizeof(ull) * 9, s));  // kills + nsend[8]
+        }
+        st = fetch_ctl();
+        if (st != PEEL_OK) return st;
+        // kill
+        for (size_t i = 0; i < sh.size(); i++) {
+            DShard &d = sh[i];
+            DKArgs a;
+            a.edges = edges; a.n = n; a.P = P; a.p = d.q; a.k = k;
+            a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
+            a.state = d.state; a.alive = d.alive;
+            a.Fc = d.F[cur]; a.nE = hc[i].ne[cur]; a.Fn = d.F[nxt];
+            a.send = d.send; a.ctl = d.ctl; a.par = nxt;
+            ProfScope ps("dist_kill", s);
+            dist_kill_kernel<R><<<dgrid(a.nE), DB, 0, s>>>(a);
+        }
+        PEEL_CUDA(cudaGetLastError());
+        st = fetch_ctl();
+        if (st != PEEL_OK) return st;
+        // exchange: counts matrix cnt_mat[src * P + dst]
+        if (c->virt) {
+            for (int q = 0; q < P; q++)
+                for (int d = 0; d < P; d++) cnt_mat[(size_t)q * P + d] = hc[q].nsend[d];
+        } else {
+            for (int d = 0; d < P; d++) loc_cnt[d] = hc[0].nsend[d];
+            PEEL_CUDA(cudaMemcpyAsync(dcnt + (size_t)c->rank * P, loc_cnt.data(), sizeof(ull) * P,
+                                      cudaMemcpyHostToDevice, s));
+            PEEL_NCCL(ncclAllGather(dcnt + (size_t)c->rank * P, dcnt, P, ncclUint64, c->nccl, s));
+            PEEL_CUDA(cudaMemcpyAsync(cnt_mat.data(), dcnt, sizeof(ull) * P * P, cudaMemcpyDeviceToHost, s));
+            PEEL_CUDA(cudaStreamSynchronize(s));
+        }
+        // payload: shard dst receives, from each src != dst, cnt[src][dst] ids into recv at running offsets
+        std::vector<ull> nrecv(sh.size(), 0);
+        if (c->virt) {
+            for (int dst = 0; dst < P; dst++) {
+                ull off = 0;
+                for (int src = 0; src < P; src++) {
+                    if (src == dst) continue;
+                    ull cntv = cnt_mat[(size_t)src * P + dst];
+                    if (off + cntv > n) return PEEL_ENOMEM;
+                    if (cntv)
+                        PEEL_CUDA(cudaMemcpyAsync(sh[dst].recv + off, sh[src].send + (uint64_t)dst * nl_max,
+                                                  sizeof(uint32_t) * cntv, cudaMemcpyDeviceToDevice, s));
+                    off += cntv;
+                }
+                nrecv[dst] = off;
+            }
+        } else {
+            const int me = c->rank;
+            PEEL_NCCL(ncclGroupStart());
+            ull off = 0;
+            for (int src = 0; src < P; src++) {
+                if (src == me) continue;
+                ull cin = cnt_mat[(size_t)src * P + me];
+                if (off + cin > n) { ncclGroupEnd(); return PEEL_ENOMEM; }
+                if (cin) PEEL_NCCL(ncclRecv(sh[0].recv + off, cin * sizeof(uint32_t), ncclUint8, src, c->nccl, s));
+                off += cin;
+            }
+            for (int dst = 0; dst < P; dst++) {
+                if (dst == me) continue;
+                ull cout = cnt_mat[(size_t)me * P + dst];
+                if (cout)
+                    PEEL_NCCL(ncclSend(sh[0].send + (uint64_t)dst * nl_max, cout * sizeof(uint32_t), ncclUint8, dst,
+                                       c->nccl, s));
+            }
+            PEEL_NCCL(ncclGroupEnd());
+            nrecv[0] = off;
+        }
+        // receive
+        for (size_t i = 0; i < sh.size(); i++) {
+            DShard &d = sh[i];
+            if (!nrecv[i]) continue;
+            DKArgs a;
+            a.edges = edges; a.n = n; a.P = P; a.p = d.q; a.k = k;
+            a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
+            a.state = d.state; a.alive = d.alive;
+            a.Fc = nullptr; a.nE = 0; a.Fn = d.F[nxt];
+            a.send = d.send; a.ctl = d.ctl; a.par = nxt;
+            ProfScope ps("dist_recv", s);
+            dist_recv_kernel<R><<<dgrid(nrecv[i]), DB, 0, s>>>(a, d.recv, nrecv[i]);
+        }
+        PEEL_CUDA(cudaGetLastError());
+        st = global_sums(nxt, g);
+        if (st != PEEL_OK) return st;
+        if (t <= cap && killed) killed[t - 1] = g[1];
+    }
+    *rounds = t;
+    for (auto &d : sh) {
+        uint8_t *mk = core_mask + (c->virt ? d.v0 : 0);
+        ProfScope ps("dist_mask", s);
+        dist_mask_kernel<<<dgrid(d.v1 - d.v0), DB, 0, s>>>(d.state, d.v1 - d.v0, k, mk);
+    }
+    PEEL_CUDA(cudaGetLastError());
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    prof_collect();
+    return t > cap ? PEEL_ETRUNC : PEEL_OK;
+}
+
+extern "C" peel_status peel_kcore_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r,
+                                       uint32_t k, uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
+                                       uint64_t *killed, uint32_t cap, void *workspace, size_t ws_bytes,
+                                       void *stream) {
+    size_t need = peel_kcore_dist_workspace_bytes(c, n, m, r, k);
+    if (!need || !rounds || !workspace || (m && !edges) || !core_mask) return PEEL_EINVAL;
+    if (ws_bytes < need) return PEEL_ENOMEM;
+    prof_begin_call();
+    cudaStream_t s = (cudaStream_t)stream;
+    char *ws = (char *)workspace;
+    switch (r) {
+        case 2: return run_dist<2>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+        case 3: return run_dist<3>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+        case 4: return run_dist<4>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+        case 5: return run_dist<5>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+        case 6: return run_dist<6>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+        case 7: return run_dist<7>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+        case 8: return run_dist<8>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);
+    }
+    return PEEL_EINVAL;
+}

@@ -119,6 +119,8 @@ __device__ __forceinline__ void bq_init(BlockQueueT<T, QCAP, BLOCK> &q) {
     if (threadIdx.x == 0) { q.n[0] = 0; q.n[1] = 0; }
 }
 
+// NOTE: warp-aggregated -- every thread of the coalesced group at the call site must
+// push to the SAME queue q (call it under a warp-uniform selection of q).
 template <typename T, int QCAP, int BLOCK>
 __device__ __forceinline__ void bq_push(BlockQueueT<T, QCAP, BLOCK> &q, int slot, T v, T *gl, ull *gcnt) {
     cg::coalesced_group g = cg::coalesced_threads();

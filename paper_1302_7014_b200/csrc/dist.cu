@@ -195,11 +195,14 @@ __global__ void __launch_bounds__(DB) dist_kill_kernel(DKArgs a) {
                     const int o = owner_of(u[j], a.n, a.P);
                     if (o == a.p) {
                         if (u[j] != ent.x) dist_decrement(a.state, a.v0, u[j], e, a.k, q, slot, a.Fn, cn, crossed);
-                    } else if (!(sent_mask >> o & 1u)) {
+                    } else {
                         sent_mask |= 1u << o;
-                        bq_push(qs[o], slot, e, a.send + (uint64_t)o * a.nloc, &a.ctl->nsend[o]);
                     }
                 }
+                // one push per destination rank; d is warp-uniform, so each coalesced
+                // group inside bq_push targets a single queue
+                for (int d = 0; d < a.P; d++)
+                    if (sent_mask >> d & 1u) bq_push(qs[d], slot, e, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
             }
         }
         bq_flush(q, slot, a.Fn, cn);

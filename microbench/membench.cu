@@ -122,6 +122,23 @@ int main() {
     float ms = timeit([](void *) { k_copy<<<C.grid, C.block>>>(C.a, C.b, 1ull << 30); }, 0);
     printf("{\"test\": \"seq_copy_8GiB\", \"ms\": %.3f, \"GBps\": %.1f}\n", ms, 2.0 * 8 * (1ull << 30) / ms / 1e6);
 
+    {
+        size_t g0 = 0;
+        cudaDeviceGetLimit(&g0, cudaLimitMaxL2FetchGranularity);
+        printf("{\"l2_fetch_granularity_default\": %zu}\n", g0);
+        for (size_t gran : {32, 64, 128}) {
+            cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+            size_t got = 0;
+            cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+            C.span = 1ull << 30; C.nops = NOPS;
+            float g = timeit([](void *) { k_gather<<<C.grid, C.block>>>(C.a, C.span, C.nops, C.out); }, 0);
+            float r = timeit([](void *) { k_red<<<C.grid, C.block>>>(C.a, C.span, C.nops); }, 0);
+            float t = timeit([](void *) { k_atom<<<C.grid, C.block>>>(C.a, C.span, C.nops, C.out); }, 0);
+            printf("{\"test\": \"random_u64_8GiB_fetch_gran\", \"set\": %zu, \"got\": %zu, \"err\": %d, \"gather_Gops\": %.2f, \"red_Gops\": %.2f, \"atom_Gops\": %.2f}\n",
+                   gran, got, (int)e, NOPS / g / 1e6, NOPS / r / 1e6, NOPS / t / 1e6);
+        }
+        cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, g0);
+    }
     ull spans[] = {1ull << 30, 1ull << 27, 1ull << 25, 1ull << 23, 1ull << 21, 1ull << 18};
     for (ull sp : spans) {
         C.span = sp; C.nops = NOPS;

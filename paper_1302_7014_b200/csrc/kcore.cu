@@ -28,6 +28,7 @@
 //              get no entry; |F_t| is counted separately for survivors[t].
 //  * output -- core_mask[v] = (count(v) >= k): a removed vertex had count < k when removed
 //              and counts never increase.
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -46,6 +47,7 @@ struct Ctl {
     ull nf[3];        // |F_t| (vertices removed in round t), rotating: round t uses nf[(t-1)%3]
     ull ne[3];        // frontier list lengths, same rotation
     ull rounds;       // number of non-empty rounds
+    ull work;         // binned-round work-item counter
     uint32_t err;     // ERR_* bits
     uint32_t binovf;  // a vertex bin overflowed its capacity (binned build falls back)
 };
@@ -387,6 +389,7 @@ struct PeelArgs {
     uint32_t *peel_round;
     int mask_vec;            // core_mask is 16-byte aligned
     int f1_ready;            // packed: F_1 was emitted by the binned build
+    uint32_t t0;             // first round run by the persistent kernel (earlier rounds were binned)
     ull *rtime;              // %globaltimer at the start of each round (profiling)
 };
 
@@ -511,6 +514,228 @@ __global__ void __launch_bounds__(PEEL_BLOCK) bin_accumulate_kernel(PeelArgs a, 
     block_add<PEEL_BLOCK>(&ctl->nf[0], removed);
 }
 
+// ---- binned rounds (large frontiers) --------------------------------------------------------
+// A round whose frontier is a large fraction of n touches most 64 B granules of the state,
+// so applying its decrements as random DRAM read-modify-writes (~20 G/s on B200) loses to
+// streaming: phase K kills edges and partitions the decrements (e << 32 | u) by vertex bin,
+// reusing the build's entry buffer (a round's decrements of bin b are a subset of the build's
+// entries of bin b, so capacities always suffice); phase D applies them bin-major with
+// L2-resident returning atomics while the next bin's state is prefetched into L2.  The
+// crossing rule (old count == k) and the (v, e) frontier entries are those of the persistent
+// kernel, so the schedule is unchanged.
+static constexpr int KU = 4;                      // frontier entries per thread per K iteration
+static constexpr int KCH = PART_BLOCK * KU;       // entries per block iteration
+static constexpr int DCH = 512;                   // decrement entries per D work item (in-flight window ~ one bin)
+
+struct BinRound {
+    uint32_t nbins;
+    ull *cursor;
+    const ull *base;
+    ull *entries;
+    ull *work;          // D work-item counter
+    uint32_t t;         // the round
+};
+
+template <int R>
+__global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelArgs a, BinRound br) {
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t nbins = br.nbins;
+    ull *sent = (ull *)smem_raw;                         // [(R-1) KCH] unsorted (e << 32 | u)
+    ull *sorted = sent + (R - 1) * KCH;                  // [(R-1) KCH]
+    ull *gpos = sorted + (R - 1) * KCH;                  // [nbins]
+    uint32_t *hist = (uint32_t *)(gpos + nbins);         // [nbins]
+    uint32_t *offs = hist + nbins;                       // [nbins]
+    uint32_t *fill = offs + nbins;                       // [nbins]
+    __shared__ uint32_t wsum[PART_BLOCK / 32], total;
+    Ctl *ctl = a.ctl;
+    const uint32_t t = br.t;
+    const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
+    const uint2 *Fc = (const uint2 *)a.F[(t - 1) & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
+        a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
+        ctl->nf[(t + 1) % 3] = 0;
+        ctl->ne[(t + 1) % 3] = 0;
+    }
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    ull kills = 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * KCH; base < nE; base += (uint64_t)gridDim.x * KCH) {
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
+        uint2 ent[KU];
+        bool win[KU];
+        #pragma unroll
+        for (int j = 0; j < KU; j++) {
+            const uint64_t i = base + (uint64_t)j * PART_BLOCK + threadIdx.x;
+            ent[j] = i < nE ? __ldcg(Fc + i) : make_uint2(0u, 0u);
+        }
+        #pragma unroll
+        for (int j = 0; j < KU; j++) {
+            const uint64_t i = base + (uint64_t)j * PART_BLOCK + threadIdx.x;
+            win[j] = false;
+            if (i < nE) {
+                const uint32_t e = ent[j].y, bit = 1u << (e & 31);
+                win[j] = (atomicAnd(a.alive + (e >> 5), ~bit) & bit) != 0;
+            }
+        }
+        uint32_t ue[KU][R];
+        uint32_t mine = 0;
+        #pragma unroll
+        for (int j = 0; j < KU; j++)
+            if (win[j]) {
+                kills++;
+                mine += R - 1;
+                #pragma unroll
+                for (int r = 0; r < R; r++) ue[j][r] = __ldg(a.edges + (uint64_t)ent[j].y * R + r);
+            }
+        // block exclusive scan of per-thread decrement counts -> staging positions
+        uint32_t x = mine;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= (unsigned)o) x += y;
+        }
+        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint32_t w = threadIdx.x < PART_BLOCK / 32 ? wsum[threadIdx.x] : 0, z = w;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (threadIdx.x >= (unsigned)o) z += y;
+            }
+            if (threadIdx.x < PART_BLOCK / 32) wsum[threadIdx.x] = z - w;
+            if (threadIdx.x == PART_BLOCK / 32 - 1) total = z;
+        }
+        __syncthreads();
+        uint32_t pos = wsum[threadIdx.x >> 5] + x - mine;
+        #pragma unroll
+        for (int j = 0; j < KU; j++)
+            if (win[j]) {
+                #pragma unroll
+                for (int r = 0; r < R; r++)
+                    if (ue[j][r] != ent[j].x) {
+                        sent[pos++] = ((ull)ent[j].y << 32) | ue[j][r];
+                        atomicAdd(&hist[ue[j][r] >> BIN_SHIFT], 1u);
+                    }
+            }
+        __syncthreads();
+        const uint32_t tot = total;
+        if (threadIdx.x < 32) {
+            const uint32_t per = (nbins + 31) / 32;
+            uint32_t loc = 0;
+            for (uint32_t q2 = 0; q2 < per; q2++) {
+                uint32_t b = threadIdx.x * per + q2;
+                loc += b < nbins ? hist[b] : 0;
+            }
+            uint32_t z = loc;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (threadIdx.x >= (unsigned)o) z += y;
+            }
+            uint32_t run = z - loc;
+            for (uint32_t q2 = 0; q2 < per; q2++) {
+                uint32_t b = threadIdx.x * per + q2;
+                if (b < nbins) { offs[b] = run; run += hist[b]; }
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)
+            if (hist[b]) gpos[b] = atomicAdd(br.cursor + b, (ull)hist[b]);
+        for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
+            const ull v = sent[i];
+            const uint32_t b = (uint32_t)v >> BIN_SHIFT;
+            sorted[offs[b] + atomicAdd(&fill[b], 1u)] = v;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
+            const ull v = sorted[i];
+            const uint32_t b = (uint32_t)v >> BIN_SHIFT;
+            br.entries[br.base[b] + gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ mask);
+        }
+        __syncthreads();
+    }
+    block_add<PART_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
+}
+
+static size_t kill_partition_smem(int r, uint32_t nbins) {
+    return 2 * sizeof(ull) * (size_t)(r - 1) * KCH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// phase D: apply the round's decrements bin-major; work items of DCH entries are taken in
+// bin order from a global counter, so the blocks in flight share one or two bins (L2-resident).
+__global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, BinRound br) {
+    extern __shared__ unsigned char smem_raw[];
+    uint32_t *pre = (uint32_t *)smem_raw;  // [nbins + 1] prefix of work items per bin
+    __shared__ BlockQueue<uint2> q;
+    __shared__ ull item;
+    Ctl *ctl = a.ctl;
+    const uint32_t t = br.t, nbins = br.nbins, k = a.k;
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (uint32_t b = 0; b < nbins; b++) {
+            pre[b] = acc;
+            acc += (uint32_t)((ld_cg_u64(br.cursor + b) + DCH - 1) / DCH);
+        }
+        pre[nbins] = acc;
+    }
+    bq_init(q);
+    __syncthreads();
+    const uint32_t nitems = pre[nbins];
+    uint2 *Fn = (uint2 *)a.F[t & 1];
+    ull *cn = &ctl->ne[t % 3];
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    ull crossed = 0;
+    int slot = 0;
+    for (;;) {
+        if (threadIdx.x == 0) item = atomicAdd(br.work, 1ull);
+        __syncthreads();
+        const ull c = item;
+        if (c >= nitems) break;
+        uint32_t lo = 0, hi = nbins;  // bin b with pre[b] <= c < pre[b+1]
+        while (hi - lo > 1) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= c) lo = mid; else hi = mid;
+        }
+        const uint32_t b = lo, j = (uint32_t)c - pre[b];
+        if (threadIdx.x == 0 && b + 1 < nbins) {
+            // prefetch slice j of the next bin's state (its items follow this bin's)
+            const uint32_t nj = pre[b + 1] - pre[b];
+            const uint64_t bytes = bin_size(a.n, b + 1) * sizeof(ull);
+            const uint64_t sl = ((bytes + nj - 1) / nj + 15) & ~15ull;
+            const uint64_t off = (uint64_t)j * sl;
+            if (off < bytes) {
+                const uint32_t len = (uint32_t)min((ull)sl, (ull)((bytes - off + 15) & ~15ull));
+                prefetch_l2((const char *)(a.state + ((uint64_t)(b + 1) << BIN_SHIFT)) + off, len);
+            }
+        }
+        const ull cnt = ld_cg_u64(br.cursor + b);
+        const ull *ent = br.entries + br.base[b] + (ull)j * DCH;
+        const uint32_t nin = (uint32_t)min((ull)DCH, cnt - (ull)j * DCH);
+        ull *st = a.state + ((uint64_t)b << BIN_SHIFT);
+        for (uint32_t i = threadIdx.x; i < nin; i += PEEL_BLOCK) {
+            const ull x = __ldcs(ent + i);
+            const uint32_t e = (uint32_t)(x >> 32);
+            const uint32_t ul = (uint32_t)(x & mask);
+            const ull old = atomicAdd(st + ul, 0ull - (((ull)e << 32) + 1ull));
+            if (count_of(old) == k) {
+                crossed++;
+                const uint32_t u = (b << BIN_SHIFT) + ul;
+                if (a.peel_round) a.peel_round[u] = t + 1;
+                bq_push(q, slot, make_uint2(u, idsum_of(old) - e), Fn, cn);
+            }
+        }
+        bq_flush(q, slot, Fn, cn);
+        slot ^= 1;
+        __syncthreads();  // item is rewritten next iteration
+    }
+    block_add<PEEL_BLOCK>(&ctl->nf[t % 3], crossed);
+}
+
 // packed path (k <= 2)
 template <int R>
 __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) {
@@ -535,7 +760,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
     }
 
     // ---- rounds ----
-    uint32_t t = 1;
+    uint32_t t = a.t0;
     for (;;) {
         const ull nF = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
         if (nF == 0) break;
@@ -690,6 +915,17 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
     write_core_mask<true>(a, tid, nthr);
 }
 
+// frontier-size threshold (fraction of n) above which a round runs binned; PEEL_BIN_ROUND_FRAC
+// overrides (0 disables) for A/B measurement
+static double bin_round_frac() {
+    static double f = -1.0;
+    if (f < 0.0) {
+        const char *e = getenv("PEEL_BIN_ROUND_FRAC");
+        f = e ? atof(e) : 0.05;
+    }
+    return f;
+}
+
 static unsigned grid_for(uint64_t work, int per_sm = 16) {
     uint64_t blocks = (work + 255) / 256;
     uint64_t cap = (uint64_t)num_sms() * per_sm;
@@ -794,6 +1030,50 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         a.deg = deg; a.off_end = off; a.adj = adj;
     }
     PEEL_CUDA(cudaGetLastError());
+
+    // binned rounds while the frontier is a large fraction of n (see round_apply_kernel)
+    a.t0 = 1;
+    if (!csr && L.nbins && bin_round_frac() > 0.0) {
+        ull *cursor = (ull *)(ws + L.bin_cursor);
+        BinRound br;
+        br.nbins = (uint32_t)L.nbins;
+        br.cursor = cursor;
+        br.base = (const ull *)(ws + L.bin_base);
+        br.entries = (ull *)(ws + L.entries);
+        br.work = &ctl->work;
+        const size_t ksmem = kill_partition_smem(R, br.nbins);
+        PEEL_CUDA(cudaFuncSetAttribute(round_kill_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ksmem));
+        int kb = 0, db = 0;
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, round_kill_partition_kernel<R>, PART_BLOCK, ksmem));
+        const size_t dsmem = sizeof(uint32_t) * (br.nbins + 1);
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
+        kb = kb < 1 ? 1 : kb;
+        db = db < 1 ? 1 : db;
+        uint32_t t = 1;
+        for (;;) {
+            Ctl h;
+            PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+            PEEL_CUDA(cudaStreamSynchronize(s));
+            if (h.err) break;  // the persistent kernel reports it
+            const ull nF = h.nf[(t - 1) % 3], nE = h.ne[(t - 1) % 3];
+            if (nF == 0 || (double)nE < bin_round_frac() * (double)n) break;
+            PEEL_CUDA(cudaMemsetAsync(cursor, 0, sizeof(ull) * L.nbins, s));
+            PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
+            br.t = t;
+            {
+                ProfScope ps("round_kill_partition", s);
+                round_kill_partition_kernel<R><<<num_sms() * kb, PART_BLOCK, ksmem, s>>>(a, br);
+            }
+            {
+                ProfScope ps("round_apply", s);
+                round_apply_kernel<<<num_sms() * db, PEEL_BLOCK, dsmem, s>>>(a, br);
+            }
+            PEEL_CUDA(cudaGetLastError());
+            t++;
+        }
+        a.t0 = t;
+    }
 
     // cooperative persistent round loop: every block must be co-resident
     void *kern = csr ? (void *)peel_csr_kernel<R> : (void *)peel_packed_kernel<R>;

@@ -1,6 +1,7 @@
 // runtime.cu -- status strings, CUDA error capture, launch accounting and the
 // optional per-kernel CUDA-event profiler of libpeel (peel.h "Measurement support").
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>

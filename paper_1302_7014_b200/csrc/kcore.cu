@@ -31,6 +31,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -103,7 +104,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     L.F1 = o; o += al(fe * n);
     L.nbins = 0; L.total_cap = 0;
     L.bins = L.bin_cursor = L.bin_base = L.bin_cap = L.entries = 0;
-    if (!csr && n > BIN_MIN_N) {
+    if (n > BIN_MIN_N) {  // packed: binned build + rounds; CSR: binned degree count + scatter
         L.nbins = (n + (1ull << BIN_SHIFT) - 1) >> BIN_SHIFT;
         for (uint64_t b = 0; b < L.nbins; b++) L.total_cap += bin_capacity(n, m, r, b);
         L.bins = o;
@@ -260,6 +261,46 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
 
 static size_t partition_smem(int r, uint64_t nbins) {
     return sizeof(ull) * (PART_ENTRIES / r) * r + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
+}
+
+// CSR build from the binned entries: blockIdx.y = bin, blocks scheduled bin-major, so the
+// degree / offset range of the bin being processed (16 MB) stays L2-resident.
+static constexpr int CSRB_PER = 16;  // entries per thread per block
+
+__global__ void __launch_bounds__(256) csr_bin_deg_kernel(const ull *__restrict__ entries, const ull *__restrict__ base,
+                                                          const ull *__restrict__ cursor, uint32_t *deg) {
+    const uint32_t b = blockIdx.y;
+    const ull cnt = cursor[b];
+    const ull lo = (ull)blockIdx.x * 256 * CSRB_PER;
+    if (lo >= cnt) return;
+    const ull *ent = entries + base[b];
+    uint32_t *d = deg + ((uint64_t)b << BIN_SHIFT);
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    #pragma unroll 4
+    for (int i = 0; i < CSRB_PER; i++) {
+        const ull p = lo + (ull)i * 256 + threadIdx.x;
+        if (p < cnt) atomicAdd(d + (__ldcs(ent + p) & mask), 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) csr_bin_scatter_kernel(const ull *__restrict__ entries, const ull *__restrict__ base,
+                                                              const ull *__restrict__ cursor, uint32_t *off,
+                                                              uint32_t *adj) {
+    const uint32_t b = blockIdx.y;
+    const ull cnt = cursor[b];
+    const ull lo = (ull)blockIdx.x * 256 * CSRB_PER;
+    if (lo >= cnt) return;
+    const ull *ent = entries + base[b];
+    uint32_t *o = off + ((uint64_t)b << BIN_SHIFT);
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    #pragma unroll 4
+    for (int i = 0; i < CSRB_PER; i++) {
+        const ull p = lo + (ull)i * 256 + threadIdx.x;
+        if (p < cnt) {
+            const ull x = __ldcs(ent + p);
+            adj[atomicAdd(o + (x & mask), 1u)] = (uint32_t)(x >> 32);
+        }
+    }
 }
 
 // CSR build, pass 1: degree histogram
@@ -1006,7 +1047,43 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         uint32_t *bsum = (uint32_t *)(ws + L.bsum);
         uint32_t *adj = (uint32_t *)(ws + L.adj);
         PEEL_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * n, s));
-        if (m) {
+        const bool binned = L.nbins > 0 && m > 0;
+        ull *cursor = (ull *)(ws + L.bin_cursor), *bbase = (ull *)(ws + L.bin_base), *bcap = (ull *)(ws + L.bin_cap);
+        ull *entries = (ull *)(ws + L.entries);
+        uint64_t maxcap = 0;
+        for (uint64_t b = 0; b < L.nbins; b++) maxcap = std::max<uint64_t>(maxcap, bin_capacity(n, m, R, b));
+        const dim3 bgrid((unsigned)((maxcap + 256 * CSRB_PER - 1) / (256 * CSRB_PER)), (unsigned)L.nbins);
+        if (binned) {
+            {
+                ProfScope ps("bin_init", s);
+                bin_init_kernel<<<1, 32, 0, s>>>(n, m, R, L.nbins, cursor, bbase, bcap);
+            }
+            const size_t smem = partition_smem(R, L.nbins);
+            PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int pblocks = 0;
+            PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
+            pblocks = pblocks < 1 ? 1 : pblocks;
+            {
+                ProfScope ps("bin_partition", s);
+                bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)L.nbins,
+                                                                                       cursor, bbase, bcap, entries, ctl);
+            }
+            // a bin overflow (adversarial degree skew) only loses entries of the binned copy:
+            // fall back to the direct histogram below if it happened (checked on the host)
+            Ctl h;
+            PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+            PEEL_CUDA(cudaStreamSynchronize(s));
+            if (h.err) return PEEL_EINVAL;
+            if (!h.binovf) {
+                ProfScope ps("csr_bin_deg", s);
+                csr_bin_deg_kernel<<<bgrid, 256, 0, s>>>(entries, bbase, cursor, deg);
+            }
+            if (h.binovf) {
+                ProfScope ps("build_deg", s);
+                build_deg_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, deg, ctl);
+            }
+            a.f1_ready = h.binovf ? 0 : 1;  // reused below as "scatter from bins"
+        } else if (m) {
             ProfScope ps("build_deg", s);
             build_deg_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, deg, ctl);
         }
@@ -1023,10 +1100,14 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             ProfScope ps("scan_add", s);
             scan_add_kernel<<<grid_for(n), PEEL_BLOCK, 0, s>>>(off, n, bsum);
         }
-        if (m) {
+        if (binned && a.f1_ready) {
+            ProfScope ps("csr_bin_scatter", s);
+            csr_bin_scatter_kernel<<<bgrid, 256, 0, s>>>(entries, bbase, cursor, off, adj);
+        } else if (m) {
             ProfScope ps("scatter", s);
             scatter_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, off, adj);
         }
+        a.f1_ready = 0;
         a.deg = deg; a.off_end = off; a.adj = adj;
     }
     PEEL_CUDA(cudaGetLastError());

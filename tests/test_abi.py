@@ -46,8 +46,9 @@ def test_workspace_queries():
     assert 24 * n + 8 * 3 * m < ws < 24 * n + 8 * 3 * m * 1.004 + m // 8 + (16 << 20)
     small = L.peel_kcore_workspace_bytes(10**6, 750000, 3, 2, 0)   # no binning below 2^23
     assert 24 * 10**6 < small < 24 * 10**6 + (8 << 20)
-    csr = L.peel_kcore_workspace_bytes(n, m, 3, 3, 0)  # CSR: deg + end offsets + 2 frontiers (4n each) + adj 4rm
-    assert 16 * n + 4 * 3 * m < csr < 16 * n + 4 * 3 * m + m // 8 + (16 << 20)
+    # CSR: deg + end offsets + 2 frontiers (4n each) + adj 4rm, plus the binned entries (n > 2^23)
+    csr = L.peel_kcore_workspace_bytes(n, m, 3, 3, 0)
+    assert 16 * n + 12 * 3 * m < csr < 16 * n + 12 * 3 * m * 1.004 + m // 8 + (16 << 20)
     assert L.peel_kcore_workspace_bytes(10, 10, 1, 2, 0) == 0  # r < 2
     assert L.peel_kcore_workspace_bytes(10, 10, 9, 2, 0) == 0  # r > 8
     assert L.peel_kcore_workspace_bytes(2**32 + 1, 10, 3, 2, 0) == 0

@@ -59,6 +59,10 @@ def lib() -> ctypes.CDLL:
             L.ora_sync_peel.argtypes = [p, u64, u64, u32, u32, p, p, p, p, u32, p]
             L.ora_sync_peel.restype = i32
             L.ora_queue_peel.argtypes = [p, u64, u64, u32, u32, p]
+            L.ora_gen_partitioned.argtypes = [u64, u64, u64, u32, p]
+            L.ora_gen_partitioned.restype = i32
+            L.ora_subround_peel.argtypes = [p, u64, u64, u32, u32, p, p, p, p, u32]
+            L.ora_subround_peel.restype = i32
             L.ora_queue_peel.restype = i32
             L.ora_iblt_new.argtypes = [u64, u32, u64]
             L.ora_iblt_new.restype = p
@@ -108,6 +112,14 @@ def gen_hypergraph(n: int, m: int, r: int, seed: int) -> np.ndarray:
     edges = np.zeros((m, r), dtype=np.uint32)
     if lib().ora_gen_hypergraph(seed, n, m, r, _ptr(edges)):
         raise ValueError("bad generator arguments (need r>=2, n>=r)")
+    return edges
+
+
+def gen_partitioned(n: int, m: int, r: int, seed: int) -> np.ndarray:
+    """edges[m][r]: the subtable model, one uniform vertex per class j in [j n/r, (j+1) n/r)."""
+    edges = np.zeros((m, r), dtype=np.uint32)
+    if lib().ora_gen_partitioned(seed, n, m, r, _ptr(edges)):
+        raise ValueError("bad arguments (need r>=2, n>=r, r | n)")
     return edges
 
 
@@ -177,6 +189,28 @@ def sync_peel(edges: np.ndarray, n: int, k: int, cap: int = 1 << 16,
     t = rounds.value
     return PeelResult(core[:n].copy(), t, surv[:t].copy(), killed[:t].copy(),
                       pr[:n].copy() if pr is not None else None)
+
+
+class SubroundResult:
+    def __init__(self, core_mask, rounds, subrounds, survivors):
+        self.core_mask, self.rounds, self.subrounds, self.survivors = core_mask, rounds, subrounds, survivors
+
+
+def subround_peel(edges: np.ndarray, n: int, k: int, cap: int = 1 << 16) -> SubroundResult:
+    """Subround peel, classes [j n/r, (j+1) n/r).  survivors[s-1] after flattened subround s."""
+    edges = np.ascontiguousarray(edges, dtype=np.uint32)
+    m, r = edges.shape
+    core = np.zeros(max(n, 1), dtype=np.uint8)
+    rounds = ctypes.c_uint32(0)
+    sub = ctypes.c_uint32(0)
+    surv = np.zeros(cap, dtype=np.uint64)
+    st = lib().ora_subround_peel(_ptr(edges) if m else None, n, m, r, k, _ptr(core), ctypes.addressof(rounds),
+                                 ctypes.addressof(sub), _ptr(surv), cap)
+    if st < 0:
+        raise ValueError("oracle subround_peel: bad input (r | n required)")
+    if st == 1:
+        raise OverflowError("more subrounds than cap")
+    return SubroundResult(core[:n].copy(), rounds.value, sub.value, surv[:sub.value].copy())
 
 
 def queue_peel(edges: np.ndarray, n: int, k: int) -> np.ndarray:

@@ -16,6 +16,8 @@
  *   - ora_gen_edge ............. G^r_{n,cn}: edge e = r distinct vertices
  *   - ora_sync_peel ............ round-synchronous peel, literal
  *   - ora_queue_peel ........... serial greedy peel
+ *   - ora_gen_partitioned ...... the subtable hypergraph model
+ *   - ora_subround_peel ........ the subround (subtable) peel
  *   - ora_iblt_* ............... IBLT insert / round-synchronous recovery
  *   - ora_iblt_serial_recover .. one-pure-cell-at-a-time recovery
  * Nothing here is blocked, fused or reordered beyond what the definitions state.
@@ -89,6 +91,32 @@ int ora_gen_hypergraph(uint64_t seed, uint64_t n, uint64_t m, uint32_t r, uint32
     if (r < 2 || n < r) return -1;
     for (uint64_t e = 0; e < m; e++)
         if (ora_gen_edge(seed, n, r, e, edges + e * r)) return -1;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* The subtable (r-partite) model: vertices are split into r      */
+/* classes of size n/r, class j = [j n/r, (j+1) n/r), and every edge has     */
+/* exactly one vertex in each class, chosen independently and uniformly.     */
+/* The vertex of class j is draw j (half j%2 of Philox block j/2, tag 'SUBT') */
+/* mapped by umulhi64 onto the class; no rejection is needed.                */
+/* ------------------------------------------------------------------------- */
+#define ORA_SUBT_TAG 0x53554254u /* 'SUBT' */
+
+int ora_gen_partitioned(uint64_t seed, uint64_t n, uint64_t m, uint32_t r, uint32_t *edges) {
+    if (r < 2 || n < r || n % r) return -1;
+    uint64_t s = n / r;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t w[4];
+    for (uint64_t e = 0; e < m; e++)
+        for (uint32_t j = 0; j < r; j++) {
+            if (j % 2 == 0) {
+                uint32_t ctr[4] = {(uint32_t)e, (uint32_t)(e >> 32), j / 2, ORA_SUBT_TAG};
+                ora_philox4x32_10(ctr, key, w);
+            }
+            uint64_t d = (j % 2 == 0) ? (((uint64_t)w[1] << 32) | w[0]) : (((uint64_t)w[3] << 32) | w[2]);
+            edges[e * r + j] = (uint32_t)(j * s + umulhi64(d, s));
+        }
     return 0;
 }
 
@@ -203,6 +231,78 @@ int ora_sync_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uin
         }
     }
     *rounds = t;
+    for (uint64_t v = 0; v < n; v++) core_mask[v] = alive_v[v];
+    free(deg); free(alive_v); free(alive_e); free(inF); free(F);
+    return status;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Subround peel: vertices in r classes [j n/r, (j+1) n/r);       */
+/* round i = r subrounds, and subround j removes every alive vertex of class */
+/* j whose degree is < k at the START of the subround (a snapshot), together */
+/* with its alive edges, after subrounds 1..j-1 of the same round applied.   */
+/* Stops after the first full round that removes nothing.  Written           */
+/* literally: each subround scans the class and then every alive edge.      */
+/* outputs: core_mask, *subrounds = flattened index (i-1) r + j of the last  */
+/* subround that removed a vertex, *rounds = rounds with a removal,          */
+/* survivors[s-1] = alive vertices after flattened subround s (s =           */
+/* 1..subrounds).  returns 0, 1 if subrounds > cap, -1 on bad input/alloc.   */
+/* ------------------------------------------------------------------------- */
+int ora_subround_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k,
+                      uint8_t *core_mask, uint32_t *rounds, uint32_t *subrounds,
+                      uint64_t *survivors, uint32_t cap) {
+    if (r < 2 || n % r) return -1;
+    uint64_t cs = n / r;
+    int64_t *deg = (int64_t *)calloc(n ? n : 1, sizeof(int64_t));
+    uint8_t *alive_v = (uint8_t *)malloc(n ? n : 1);
+    uint8_t *alive_e = (uint8_t *)malloc(m ? m : 1);
+    uint8_t *inF = (uint8_t *)calloc(n ? n : 1, 1);
+    uint64_t *F = (uint64_t *)malloc((cs ? cs : 1) * sizeof(uint64_t));
+    if (!deg || !alive_v || !alive_e || !inF || !F) {
+        free(deg); free(alive_v); free(alive_e); free(inF); free(F);
+        return -1;
+    }
+    for (uint64_t e = 0; e < m * r; e++) {
+        if (edges[e] >= n) { free(deg); free(alive_v); free(alive_e); free(inF); free(F); return -1; }
+        deg[edges[e]] += 1;
+    }
+    memset(alive_v, 1, n);
+    memset(alive_e, 1, m);
+    uint64_t surv = n, flat = 0, last = 0;
+    uint32_t nrounds = 0;
+    int status = 0;
+    for (uint32_t i = 1;; i++) {
+        int any = 0;
+        for (uint32_t j = 0; j < r; j++) {
+            flat++;
+            uint64_t nF = 0;
+            for (uint64_t v = j * cs; v < (j + 1) * cs; v++)
+                if (alive_v[v] && deg[v] < (int64_t)k) F[nF++] = v;
+            if (nF) {
+                for (uint64_t q = 0; q < nF; q++) { alive_v[F[q]] = 0; inF[F[q]] = 1; }
+                for (uint64_t e = 0; e < m; e++) {
+                    if (!alive_e[e]) continue;
+                    int hit = 0;
+                    for (uint32_t t = 0; t < r; t++)
+                        if (inF[edges[e * r + t]]) hit = 1;
+                    if (hit) {
+                        alive_e[e] = 0;
+                        for (uint32_t t = 0; t < r; t++) deg[edges[e * r + t]] -= 1;
+                    }
+                }
+                for (uint64_t q = 0; q < nF; q++) inF[F[q]] = 0;
+                surv -= nF;
+                any = 1;
+                last = flat;
+            }
+            if (flat <= cap) survivors[flat - 1] = surv;
+            else if (nF) status = 1;
+        }
+        if (!any) break;
+        nrounds = i;
+    }
+    *rounds = nrounds;
+    *subrounds = (uint32_t)last;
     for (uint64_t v = 0; v < n; v++) core_mask[v] = alive_v[v];
     free(deg); free(alive_v); free(alive_e); free(inF); free(F);
     return status;

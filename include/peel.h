@@ -69,6 +69,15 @@ peel_status peel_gen_hypergraph(uint64_t n, uint64_t m, uint32_t r, uint64_t see
                                 uint32_t *edges, void *stream);
 
 /*
+ * peel_gen_partitioned -- the subtable model: r | n, vertex class
+ * c = [c n/r, (c+1) n/r), and edge e has exactly one vertex per class: the
+ * class-c vertex is c n/r + umulhi64(draw c, n/r), draw c = half c%2 of
+ * Philox4x32-10(ctr = {e_lo, e_hi, c/2, 'SUBT'}, key = {seed_lo, seed_hi}).
+ * EINVAL: r < 2, r > 8, n % r != 0, n > 2^32, m >= 2^32.
+ */
+peel_status peel_gen_partitioned(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, uint32_t *edges, void *stream);
+
+/*
  * peel_gen_keys -- keys[i] (dev, u64) = i-th output of a SplitMix64 stream
  * with state `seed`: mix64(seed + (i+1) * 0x9E3779B97F4A7C15).  A bijection of
  * i, so the nkeys keys are distinct (the IBLT stores a set).
@@ -81,6 +90,13 @@ peel_status peel_gen_keys(uint64_t nkeys, uint64_t seed, uint64_t *keys, void *s
 
 /* flags */
 #define PEEL_FLAG_CSR 1u /* force the general-k incidence (CSR) path even for k <= 2 */
+/* The subround (subtable) variant of P:565-579: vertices in r classes
+ * [c n/r, (c+1) n/r) (r must divide n; k <= 2); round i = r subrounds, subround j
+ * removing the class-j vertices of degree < k at ITS start, after subrounds
+ * 1..j-1 applied.  With this flag `rounds` is the flattened index (i-1) r + j of
+ * the last subround that removed a vertex (Table 4's "subrounds"), and
+ * survivors / killed / peel_round are per flattened subround (Table 5). */
+#define PEEL_FLAG_SUBROUNDS 2u
 
 /*
  * Bytes of device workspace peel_kcore needs for (n, m, r, k, flags).
@@ -104,7 +120,7 @@ size_t peel_kcore_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k
  *                r ids of an edge distinct, else PEEL_EINVAL (checked on device).
  *                Edges are a multiset (duplicates allowed).
  *      n, m, r, k  sizes; k = 0 peels nothing (rounds = 0).
- *      flags     0 or PEEL_FLAG_CSR.
+ *      flags     0, PEEL_FLAG_CSR or PEEL_FLAG_SUBROUNDS.
  * out: core_mask dev u8 [n]: 1 iff v is in the k-core.
  *      rounds    host u32: number of rounds with F_t non-empty.
  *      survivors host u64 [cap] (nullable): survivors[t-1] = |alive vertices|

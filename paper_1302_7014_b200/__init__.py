@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libpeel.so")
 
 PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOVERFLOW = range(7)
 PEEL_FLAG_CSR = 1
+PEEL_FLAG_SUBROUNDS = 2
 
 _lib = None
 
@@ -48,6 +49,7 @@ def _L() -> ctypes.CDLL:
         L.peel_abi_version.restype = i32
         L.peel_gen_hypergraph.argtypes = [u64, u64, u32, u64, p, p]
         L.peel_gen_keys.argtypes = [u64, u64, p, p]
+        L.peel_gen_partitioned.argtypes = [u64, u64, u32, u64, p, p]
         L.peel_kcore_workspace_bytes.argtypes = [u64, u64, u32, u32, u32]
         L.peel_kcore_workspace_bytes.restype = sz
         L.peel_kcore.argtypes = [p, u64, u64, u32, u32, u32, p, p, p, p, u32, p, p, sz, p]
@@ -80,7 +82,7 @@ def _L() -> ctypes.CDLL:
         L.peel_last_launches.restype = u32
         L.peel_profile_rounds.argtypes = [p, u32]
         L.peel_profile_rounds.restype = i32
-        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_kcore", "peel_kcore_host", "peel_sweep",
+        for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_gen_partitioned", "peel_kcore", "peel_kcore_host", "peel_sweep",
                   "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
@@ -124,6 +126,16 @@ def gen_hypergraph(n: int, m: int, r: int, seed: int, out: torch.Tensor | None =
         out = torch.empty((m, r), dtype=torch.int32, device=_dev(device))
     _check(_L().peel_gen_hypergraph(n, m, r, seed & (2**64 - 1), _ptr(out), _stream(stream)),
            "peel_gen_hypergraph")
+    return out
+
+
+def gen_partitioned(n: int, m: int, r: int, seed: int, out: torch.Tensor | None = None,
+                    device=None, stream=None) -> torch.Tensor:
+    """edges [m, r] of the subtable model: one vertex per class [c n/r, (c+1) n/r) (peel.h)."""
+    if out is None:
+        out = torch.empty((m, r), dtype=torch.int32, device=_dev(device))
+    _check(_L().peel_gen_partitioned(n, m, r, seed & (2**64 - 1), _ptr(out), _stream(stream)),
+           "peel_gen_partitioned")
     return out
 
 

@@ -51,6 +51,26 @@ __global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, 
     }
 }
 
+// the subtable model: one uniform vertex per class, draw c for class c
+template <int R>
+__global__ void __launch_bounds__(256) gen_partitioned_kernel(uint64_t m, uint64_t cs, uint64_t seed,
+                                                              uint32_t *__restrict__ edges) {
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t w[4];
+        #pragma unroll
+        for (int c = 0; c < R; c++) {
+            if ((c & 1) == 0) {
+                w[0] = (uint32_t)e; w[1] = (uint32_t)(e >> 32); w[2] = (uint32_t)c >> 1; w[3] = 0x53554254u;
+                philox4x32_10(w, k0, k1);
+            }
+            const uint64_t d = (c & 1) ? (((uint64_t)w[3] << 32) | w[2]) : (((uint64_t)w[1] << 32) | w[0]);
+            edges[e * R + c] = (uint32_t)(c * cs + __umul64hi(d, cs));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) gen_keys_kernel(uint64_t nkeys, uint64_t seed,
                                                        uint64_t *__restrict__ keys) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nkeys;
@@ -99,6 +119,31 @@ extern "C" peel_status peel_gen_hypergraph(uint64_t n, uint64_t m, uint32_t r, u
     if (!edges) return PEEL_EINVAL;
     prof_begin_call();
     return launch_gen_edges(n, m, r, seed, edges, 0u, (cudaStream_t)stream);
+}
+
+extern "C" peel_status peel_gen_partitioned(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, uint32_t *edges,
+                                            void *stream) {
+    if (r < 2 || r > 8 || n < r || n % r || n > (1ull << 32) || m >= (1ull << 32)) return PEEL_EINVAL;
+    if (m == 0) return PEEL_OK;
+    if (!edges) return PEEL_EINVAL;
+    prof_begin_call();
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t cs = n / r;
+    unsigned g = grid_for(m);
+    {
+        ProfScope ps("gen_partitioned", s);
+        switch (r) {
+            case 2: gen_partitioned_kernel<2><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+            case 3: gen_partitioned_kernel<3><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+            case 4: gen_partitioned_kernel<4><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+            case 5: gen_partitioned_kernel<5><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+            case 6: gen_partitioned_kernel<6><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+            case 7: gen_partitioned_kernel<7><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+            case 8: gen_partitioned_kernel<8><<<g, 256, 0, s>>>(m, cs, seed, edges); break;
+        }
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
 }
 
 extern "C" peel_status peel_gen_keys(uint64_t nkeys, uint64_t seed, uint64_t *keys, void *stream) {

@@ -54,7 +54,7 @@ struct Ctl {
 };
 
 struct Layout {
-    size_t ctl, fsize, killed, rtime, state, deg, off, bsum, adj, alive, F0, F1;
+    size_t ctl, sub, fsize, killed, rtime, state, deg, off, bsum, adj, alive, F0, F1;
     size_t bins, bin_cursor, bin_base, bin_cap, entries;  // binned build (packed, n > BIN_MIN_N)
     uint64_t nbins, total_cap;
     size_t total;
@@ -65,7 +65,6 @@ struct Layout {
 // L2 atomics and scanned for the round-1 frontier while it is still in L2.
 static constexpr int BIN_SHIFT = 22;
 static constexpr uint64_t BIN_MIN_N = 1ull << 23;  // below this the state fits L2: direct build
-static constexpr int MAX_BINS = 1024;              // n <= 2^32
 
 __host__ __device__ inline uint64_t bin_size(uint64_t n, uint64_t b) {
     uint64_t lo = b << BIN_SHIFT, hi = (b + 1) << BIN_SHIFT;
@@ -85,6 +84,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     Layout L;
     size_t o = 0;
     L.ctl = o; o += al(sizeof(Ctl));
+    L.sub = o; o += al(sizeof(ull) * 64);  // subround mode: per-class list counters
     L.fsize = o; o += al(sizeof(ull) * (STAT_CAP + 1));
     L.killed = o; o += al(sizeof(ull) * (STAT_CAP + 1));
     L.rtime = o; o += al(sizeof(ull) * (STAT_CAP + 2));
@@ -431,6 +431,9 @@ struct PeelArgs {
     int mask_vec;            // core_mask is 16-byte aligned
     int f1_ready;            // packed: F_1 was emitted by the binned build
     uint32_t t0;             // first round run by the persistent kernel (earlier rounds were binned)
+    uint32_t r;              // subround mode: number of vertex classes (= r)
+    uint64_t cs;             // subround mode: class size n / r
+    ull *sub;                // subround mode: counters [class][buffer][kind: 0 |F|, 1 entries]
     ull *rtime;              // %globaltimer at the start of each round (profiling)
 };
 
@@ -852,7 +855,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
                         const uint32_t u = ue[j][r];
                         if (u == ent[j].x) continue;
                         const ull old = atomicAdd(a.state + u, dec);
-                        if (count_of(old) == 2u) {  // k = 2: count 2 -> 1, u joins F_{t+1}
+                        if (count_of(old) == k) {  // count k -> k-1: u joins F_{t+1}
                             crossed++;
                             if (a.peel_round) a.peel_round[u] = t + 1;
                             bq_push(q, slot, make_uint2(u, idsum_of(old) - e), Fn, cn);
@@ -870,6 +873,155 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
     if (tid == 0) {
         ctl->rounds = t - 1;
         if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
+    }
+    write_core_mask<false>(a, tid, nthr);
+}
+
+// ---- subround (subtable) variant, P:565-579 -------------------------------------------------
+// Vertex classes [c n/r, (c+1) n/r).  Round i = r subrounds; subround j removes the class-j
+// vertices whose count is < k at the START of the subround, with their alive edges, after
+// subrounds 1..j-1 applied.  Per class c two entry lists (F[b] + c cs, b = 0, 1): the
+// "current" list cb[c] gathers class-c crossings until subround c processes it; a class-c
+// crossing DURING subround c (possible only when an edge has two class-c vertices) goes to
+// the other list, which becomes current afterwards.  cb[] is tracked identically by every
+// thread.  Stats are per flattened subround s = (i-1) r + j; the loop stops after a round that
+// removes nothing, and `rounds` reports the flattened index of the last non-empty subround.
+static constexpr int SUB_QCAP = PEEL_BLOCK;  // one crossing per class per entry in the subtable model
+typedef BlockQueueT<uint2, SUB_QCAP, PEEL_BLOCK> SubQ;
+
+template <int R>
+__global__ void __launch_bounds__(PEEL_BLOCK) peel_subround_kernel(PeelArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ SubQ q[R];
+    Ctl *ctl = a.ctl;
+    if (ld_cg_u32(&ctl->err) & ERR_BADVERTEX) return;
+    #pragma unroll
+    for (int c = 0; c < R; c++) bq_init(q[c]);
+    __syncthreads();
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t k = a.k;
+    const uint64_t cs = a.cs;
+    ull *sub = a.sub;  // sub[(c * 2 + b) * 2 + kind]
+    uint2 *F0 = (uint2 *)a.F[0], *F1 = (uint2 *)a.F[1];
+    auto list = [&](uint32_t c, uint32_t b) { return (b ? F1 : F0) + (uint64_t)c * cs; };
+    int slot = 0;
+    // initial scan: every vertex with count < k goes to its class's list 0
+    {
+        ull removed[R];
+        #pragma unroll
+        for (int c = 0; c < R; c++) removed[c] = 0;
+        for (uint64_t base = (uint64_t)blockIdx.x * PEEL_BLOCK; base < a.n; base += (uint64_t)gridDim.x * PEEL_BLOCK) {
+            const uint64_t v = base + threadIdx.x;
+            const ull w = v < a.n ? ld_cg_u64(a.state + v) : ~0ull;
+            const bool in = v < a.n && count_of(w) < k;
+            const uint32_t cv = in ? (uint32_t)(v / cs) : 0u;
+            #pragma unroll
+            for (int c = 0; c < R; c++)
+                if (in && cv == (uint32_t)c) {
+                    removed[c]++;
+                    if (a.peel_round) a.peel_round[v] = (uint32_t)c + 1;  // flattened subround (1, c)
+                    if (count_of(w) == 1)
+                        bq_push(q[c], slot, make_uint2((uint32_t)v, idsum_of(w)), list(c, 0), &sub[(c * 2 + 0) * 2 + 1]);
+                }
+            #pragma unroll
+            for (int c = 0; c < R; c++) bq_flush(q[c], slot, list(c, 0), &sub[(c * 2 + 0) * 2 + 1]);
+            slot ^= 1;
+        }
+        #pragma unroll
+        for (int c = 0; c < R; c++) block_add<PEEL_BLOCK>(&sub[(c * 2 + 0) * 2 + 0], removed[c]);
+    }
+    grid.sync();
+    uint32_t cb[R];
+    #pragma unroll
+    for (int c = 0; c < R; c++) cb[c] = 0;
+    uint32_t flat = 0, last = 0;
+    for (;;) {
+        bool any = false;
+        #pragma unroll 1
+        for (uint32_t j = 0; j < (uint32_t)R; j++) {
+            flat++;
+            const uint32_t cur = cb[j];
+            const ull nF = ld_cg_u64(&sub[(j * 2 + cur) * 2 + 0]);
+            const ull nE = ld_cg_u64(&sub[(j * 2 + cur) * 2 + 1]);
+            if (tid == 0) {
+                if (flat <= a.stat_cap) a.rtime[flat - 1] = globaltimer();
+                a.fsize[flat <= a.stat_cap ? flat - 1 : a.stat_cap] = nF;
+            }
+            ull kills = 0;
+            ull xc[R];  // crossings per class this subround
+            #pragma unroll
+            for (int c = 0; c < R; c++) xc[c] = 0;
+            if (nF) {
+                any = true;
+                last = flat;
+                const uint2 *Fc = list(j, cur);
+                for (uint64_t base = (uint64_t)blockIdx.x * PEEL_BLOCK; base < nE; base += (uint64_t)gridDim.x * PEEL_BLOCK) {
+                    const uint64_t i = base + threadIdx.x;
+                    uint32_t cu[R], ce[R], cc[R];
+                    bool cv[R];
+                    #pragma unroll
+                    for (int q2 = 0; q2 < R; q2++) cv[q2] = false;
+                    if (i < nE) {
+                        const uint2 ent = __ldcg(Fc + i);
+                        const uint32_t e = ent.y, bit = 1u << (e & 31);
+                        if (atomicAnd(a.alive + (e >> 5), ~bit) & bit) {
+                            kills++;
+                            const ull dec = 0ull - (((ull)e << 32) + 1ull);
+                            #pragma unroll
+                            for (int q2 = 0; q2 < R; q2++) {
+                                const uint32_t u = __ldg(a.edges + (uint64_t)e * R + q2);
+                                if (u == ent.x) continue;
+                                const ull old = atomicAdd(a.state + u, dec);
+                                if (count_of(old) == k) {
+                                    cv[q2] = true;
+                                    cu[q2] = u;
+                                    ce[q2] = idsum_of(old) - e;
+                                    cc[q2] = (uint32_t)(u / cs);
+                                }
+                            }
+                        }
+                    }
+                    // push crossings, one class at a time (warp-uniform queue selection)
+                    #pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const uint32_t b = (uint32_t)c == j ? (cb[c] ^ 1u) : cb[c];
+                        #pragma unroll
+                        for (int q2 = 0; q2 < R; q2++)
+                            if (cv[q2] && cc[q2] == (uint32_t)c) {
+                                xc[c]++;
+                                bq_push(q[c], slot, make_uint2(cu[q2], ce[q2]), list(c, b), &sub[(c * 2 + b) * 2 + 1]);
+                            }
+                    }
+                    #pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const uint32_t b = (uint32_t)c == j ? (cb[c] ^ 1u) : cb[c];
+                        bq_flush(q[c], slot, list(c, b), &sub[(c * 2 + b) * 2 + 1]);
+                    }
+                    slot ^= 1;
+                }
+                if (a.peel_round) {  // removal subround of this list's vertices
+                    for (uint64_t i = tid; i < nE; i += nthr) a.peel_round[__ldcg(&Fc[i].x)] = flat;
+                }
+            }
+            block_add<PEEL_BLOCK>(&a.killed[flat <= a.stat_cap ? flat - 1 : a.stat_cap], kills);
+            #pragma unroll
+            for (int c = 0; c < R; c++) {
+                const uint32_t b = (uint32_t)c == j ? (cb[c] ^ 1u) : cb[c];
+                block_add<PEEL_BLOCK>(&sub[(c * 2 + b) * 2 + 0], xc[c]);
+            }
+            grid.sync();
+            if (tid == 0) {  // this list is consumed; its counters restart (its next append is >= 1 barrier away)
+                sub[(j * 2 + cur) * 2 + 0] = 0;
+                sub[(j * 2 + cur) * 2 + 1] = 0;
+            }
+            cb[j] ^= 1u;
+        }
+        if (!any) break;
+    }
+    if (tid == 0) {
+        ctl->rounds = last;
+        if (flat <= a.stat_cap) a.rtime[flat - 1] = globaltimer();
     }
     write_core_mask<false>(a, tid, nthr);
 }
@@ -976,10 +1128,11 @@ static unsigned grid_for(uint64_t work, int per_sm = 16) {
 }
 
 template <int R>
-static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr,
+static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr, uint32_t flags,
                              uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
                              uint64_t *killed, uint32_t cap, uint32_t *peel_round, char *ws,
                              const Layout &L, cudaStream_t s) {
+    const bool subr = (flags & PEEL_FLAG_SUBROUNDS) != 0;
     Ctl *ctl = (Ctl *)(ws + L.ctl);
     ull *fsize = (ull *)(ws + L.fsize);
     ull *kil = (ull *)(ws + L.killed);
@@ -1114,7 +1267,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
 
     // binned rounds while the frontier is a large fraction of n (see round_apply_kernel)
     a.t0 = 1;
-    if (!csr && L.nbins && bin_round_frac() > 0.0) {
+    if (!csr && !subr && L.nbins && bin_round_frac() > 0.0) {
         ull *cursor = (ull *)(ws + L.bin_cursor);
         BinRound br;
         br.nbins = (uint32_t)L.nbins;
@@ -1157,14 +1310,19 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     }
 
     // cooperative persistent round loop: every block must be co-resident
-    void *kern = csr ? (void *)peel_csr_kernel<R> : (void *)peel_packed_kernel<R>;
+    void *kern = csr ? (void *)peel_csr_kernel<R> : (subr ? (void *)peel_subround_kernel<R> : (void *)peel_packed_kernel<R>);
+    if (subr) {
+        a.r = R;
+        a.cs = n / R;
+        a.sub = (ull *)(ws + L.sub);
+    }
     int per_sm = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PEEL_BLOCK, 0));
     if (per_sm < 1) per_sm = 1;
     unsigned grid = (unsigned)(num_sms() * per_sm);
     void *args[] = {&a};
     {
-        ProfScope ps(csr ? "peel_rounds_csr" : "peel_rounds_packed", s);
+        ProfScope ps(csr ? "peel_rounds_csr" : (subr ? "peel_subrounds" : "peel_rounds_packed"), s);
         PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, PEEL_BLOCK, args, 0, s));
     }
 
@@ -1227,6 +1385,7 @@ extern "C" peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m,
     bool csr = use_csr(k, flags);
     if (!kcore_args_ok(n, m, r, csr) || !rounds) return PEEL_EINVAL;
     if ((m && !edges) || (n && !core_mask) || !workspace) return PEEL_EINVAL;
+    if ((flags & PEEL_FLAG_SUBROUNDS) && (csr || k > 2 || n % r != 0)) return PEEL_EINVAL;
     Layout L = layout(n, m, r, csr);
     if (ws_bytes < L.total) return PEEL_ENOMEM;
     prof_begin_call();
@@ -1237,13 +1396,13 @@ extern "C" peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m,
     }
     char *ws = (char *)workspace;
     switch (r) {
-        case 2: return run_kcore<2>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 3: return run_kcore<3>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 4: return run_kcore<4>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 5: return run_kcore<5>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 6: return run_kcore<6>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 7: return run_kcore<7>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 8: return run_kcore<8>(edges, n, m, k, csr, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 2: return run_kcore<2>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 3: return run_kcore<3>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 4: return run_kcore<4>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 5: return run_kcore<5>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 6: return run_kcore<6>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 7: return run_kcore<7>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 8: return run_kcore<8>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
     }
     return PEEL_EINVAL;
 }

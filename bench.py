@@ -518,7 +518,11 @@ def main():
     t_max_s = t_max.item() / 1e3
     value = total_peeled * args.steps / t_max_s
 
-    # roofline for the dominant kernel (algorithmic bytes per launch / avg launch time)
+    # roofline for the dominant kernel: algorithmic bytes apportioned to the
+    # kernels that did the work.  Per round t: 8 |F_t| (state of removed vertices) +
+    # killed_t (4r re-read of the edge + 16(r-1) RMW of its other endpoints); the first
+    # `nb` rounds run as round_kill_partition (8|F_t| + 4r killed_t) + round_apply
+    # (16(r-1) killed_t), the rest in the persistent kernel (+ n for the mask).
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -527,13 +531,27 @@ def main():
     hbm = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback (B200_PROFILING.md 6.65 TB/s)"
     hbm = hbm or 6650.0
-    kb = {"build_packed": b_build, "build_deg": b_build, "peel_rounds_packed": b_rounds, "peel_rounds_csr": b_rounds}
+    surv = [n] + [int(x) for x in res.survivors]
+    F = [surv[i] - surv[i + 1] for i in range(len(surv) - 1)]
+    kl = [int(x) for x in res.killed]
+    nb = int(round(per_kernel.get("round_kill_partition", [0.0, 0])[1] / args.steps))
+    kb = {}
+    if k <= 2:
+        kb["bin_partition"] = 4 * r * m
+        kb["bin_accumulate"] = 8 * n
+        kb["build_packed"] = 4 * r * m + 8 * n
+        kb["round_kill_partition"] = sum(8 * F[t] + 4 * r * kl[t] for t in range(min(nb, len(F))))
+        kb["round_apply"] = sum(16 * (r - 1) * kl[t] for t in range(min(nb, len(F))))
+        kb["peel_rounds_packed"] = sum(8 * F[t] + (4 * r + 16 * (r - 1)) * kl[t] for t in range(nb, len(F))) + n
     dom = max(per_kernel.items(), key=lambda kv: kv[1][0]) if per_kernel else None
     roof = None
     if dom:
         name, (ms_sum, nl) = dom
         avg_ms = ms_sum / max(nl, 1)
-        alg = kb.get(name, b_build + b_rounds)
+        alg = kb.get(name)
+        if alg is None:  # CSR path: whole-step formula over the whole-step time of its kernels
+            alg = b_build + b_rounds
+            avg_ms = sum(v[0] for v in per_kernel.values()) / args.steps
         ach = alg / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
@@ -591,7 +609,8 @@ def main():
             "rounds": res.rounds,
             "hbm_roofline_step": {"alg_bytes": step_alg, "frac_of_measured": round(step_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
                                   "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},
-            "roofline": roof, "kernels": kernels, "round_ms": round_ms, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "kernels": kernels, "round_ms": round_ms,
+            "kernel_alg_bytes": kb, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -61,11 +61,16 @@ def lib() -> ctypes.CDLL:
             L.ora_queue_peel.argtypes = [p, u64, u64, u32, u32, p]
             L.ora_gen_partitioned.argtypes = [u64, u64, u64, u32, p]
             L.ora_gen_partitioned.restype = i32
-            L.ora_subround_peel.argtypes = [p, u64, u64, u32, u32, p, p, p, p, u32]
+            L.ora_subround_peel.argtypes = [p, u64, u64, u32, u32, p, p, p, p, p, u32]
             L.ora_subround_peel.restype = i32
             L.ora_queue_peel.restype = i32
             L.ora_iblt_new.argtypes = [u64, u32, u64]
             L.ora_iblt_new.restype = p
+            L.ora_iblt_new_ex.argtypes = [u64, u32, u64, i32]
+            L.ora_iblt_new_ex.restype = p
+            L.ora_iblt_peel_subtables.argtypes = [p, p, u64, p, p, p, u32, p]
+            L.ora_iblt_peel_subtables.restype = i32
+            L.ora_cells_of_subtable.argtypes = [u64, u64, u32, u64, p]
             L.ora_iblt_free.argtypes = [p]
             L.ora_iblt_seed_h.argtypes = [p]
             L.ora_iblt_seed_h.restype = u64
@@ -145,6 +150,12 @@ def checksum(x: int, seed: int) -> int:
     return int(lib().ora_checksum(x, seed_c(seed)))
 
 
+def cells_of_subtable(x: int, C: int, r: int, seed: int) -> np.ndarray:
+    out = np.zeros(r, dtype=np.uint64)
+    lib().ora_cells_of_subtable(x, C, r, seed_h(seed), _ptr(out))
+    return out
+
+
 def cells_of(x: int, C: int, r: int, seed: int) -> np.ndarray:
     out = np.zeros(r, dtype=np.uint64)
     if lib().ora_cells_of(x, C, r, seed_h(seed), _ptr(out)):
@@ -192,8 +203,9 @@ def sync_peel(edges: np.ndarray, n: int, k: int, cap: int = 1 << 16,
 
 
 class SubroundResult:
-    def __init__(self, core_mask, rounds, subrounds, survivors):
-        self.core_mask, self.rounds, self.subrounds, self.survivors = core_mask, rounds, subrounds, survivors
+    def __init__(self, core_mask, rounds, subrounds, survivors, killed):
+        self.core_mask, self.rounds, self.subrounds = core_mask, rounds, subrounds
+        self.survivors, self.killed = survivors, killed
 
 
 def subround_peel(edges: np.ndarray, n: int, k: int, cap: int = 1 << 16) -> SubroundResult:
@@ -204,13 +216,15 @@ def subround_peel(edges: np.ndarray, n: int, k: int, cap: int = 1 << 16) -> Subr
     rounds = ctypes.c_uint32(0)
     sub = ctypes.c_uint32(0)
     surv = np.zeros(cap, dtype=np.uint64)
+    kil = np.zeros(cap, dtype=np.uint64)
     st = lib().ora_subround_peel(_ptr(edges) if m else None, n, m, r, k, _ptr(core), ctypes.addressof(rounds),
-                                 ctypes.addressof(sub), _ptr(surv), cap)
+                                 ctypes.addressof(sub), _ptr(surv), _ptr(kil), cap)
     if st < 0:
         raise ValueError("oracle subround_peel: bad input (r | n required)")
     if st == 1:
         raise OverflowError("more subrounds than cap")
-    return SubroundResult(core[:n].copy(), rounds.value, sub.value, surv[:sub.value].copy())
+    return SubroundResult(core[:n].copy(), rounds.value, sub.value, surv[:sub.value].copy(),
+                          kil[:sub.value].copy())
 
 
 def queue_peel(edges: np.ndarray, n: int, k: int) -> np.ndarray:
@@ -238,11 +252,11 @@ class IbltResult:
 class Iblt:
     """IBLT with C cells and r hashes."""
 
-    def __init__(self, C: int, r: int, seed: int):
-        self.C, self.r, self.seed = C, r, seed
-        self._t = lib().ora_iblt_new(C, r, seed)
+    def __init__(self, C: int, r: int, seed: int, subtables: bool = False):
+        self.C, self.r, self.seed, self.subtables = C, r, seed, subtables
+        self._t = lib().ora_iblt_new_ex(C, r, seed, 1 if subtables else 0)
         if not self._t:
-            raise ValueError("bad IBLT arguments (need r>=2, C>=r)")
+            raise ValueError("bad IBLT arguments (need r>=2, C>=r, and r | C for subtables)")
 
     def __del__(self):
         t = getattr(self, "_t", None)
@@ -282,6 +296,23 @@ class Iblt:
             raise OverflowError("cap exceeded")
         t = rounds.value
         return IbltResult(out[:nrec.value].copy(), t, per_round[:t].copy(), bool(complete.value))
+
+    def peel_subtables(self, cap_keys: int | None = None, cap: int = 1 << 16) -> IbltResult:
+        """Subtable recovery, destructive; rounds = flattened index of the last
+        subtable step that recovered a key, per_round = keys per flattened step."""
+        cap_keys = self.C * 2 if cap_keys is None else cap_keys
+        out = np.zeros(max(cap_keys, 1), dtype=np.uint64)
+        nrec = ctypes.c_uint64(0)
+        sub = ctypes.c_uint32(0)
+        per = np.zeros(cap, dtype=np.uint64)
+        complete = ctypes.c_int(0)
+        st = lib().ora_iblt_peel_subtables(self._t, _ptr(out), cap_keys, ctypes.addressof(nrec),
+                                           ctypes.addressof(sub), _ptr(per), cap, ctypes.addressof(complete))
+        if st < 0:
+            raise ValueError("not a subtable IBLT")
+        if st == 1:
+            raise OverflowError("cap exceeded")
+        return IbltResult(out[:nrec.value].copy(), sub.value, per[:sub.value].copy(), bool(complete.value))
 
     def serial_recover(self):
         """One-pure-cell-at-a-time recovery, destructive."""

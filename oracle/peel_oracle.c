@@ -246,11 +246,12 @@ int ora_sync_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uin
 /* outputs: core_mask, *subrounds = flattened index (i-1) r + j of the last  */
 /* subround that removed a vertex, *rounds = rounds with a removal,          */
 /* survivors[s-1] = alive vertices after flattened subround s (s =           */
-/* 1..subrounds).  returns 0, 1 if subrounds > cap, -1 on bad input/alloc.   */
+/* 1..subrounds), killed[s-1] = edges killed there (nullable).  returns 0, 1 */
+/* if subrounds > cap, -1 on bad input/alloc.                                */
 /* ------------------------------------------------------------------------- */
 int ora_subround_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k,
                       uint8_t *core_mask, uint32_t *rounds, uint32_t *subrounds,
-                      uint64_t *survivors, uint32_t cap) {
+                      uint64_t *survivors, uint64_t *killed, uint32_t cap) {
     if (r < 2 || n % r) return -1;
     uint64_t cs = n / r;
     int64_t *deg = (int64_t *)calloc(n ? n : 1, sizeof(int64_t));
@@ -275,7 +276,7 @@ int ora_subround_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r,
         int any = 0;
         for (uint32_t j = 0; j < r; j++) {
             flat++;
-            uint64_t nF = 0;
+            uint64_t nF = 0, nkill = 0;
             for (uint64_t v = j * cs; v < (j + 1) * cs; v++)
                 if (alive_v[v] && deg[v] < (int64_t)k) F[nF++] = v;
             if (nF) {
@@ -287,6 +288,7 @@ int ora_subround_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r,
                         if (inF[edges[e * r + t]]) hit = 1;
                     if (hit) {
                         alive_e[e] = 0;
+                        nkill++;
                         for (uint32_t t = 0; t < r; t++) deg[edges[e * r + t]] -= 1;
                     }
                 }
@@ -295,8 +297,10 @@ int ora_subround_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r,
                 any = 1;
                 last = flat;
             }
-            if (flat <= cap) survivors[flat - 1] = surv;
-            else if (nF) status = 1;
+            if (flat <= cap) {
+                survivors[flat - 1] = surv;
+                if (killed) killed[flat - 1] = nkill;
+            } else if (nF) status = 1;
         }
         if (!any) break;
         nrounds = i;
@@ -368,17 +372,18 @@ int ora_queue_peel(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, ui
 typedef struct {
     uint64_t C;
     uint32_t r;
+    int subtables; /* 1: r subtables of C/r cells, one cell per subtable per key */
     uint64_t seed_h, seed_c;
     int64_t *count;
     uint64_t *keySum;
     uint32_t *hashSum;
 } ora_iblt;
 
-ora_iblt *ora_iblt_new(uint64_t C, uint32_t r, uint64_t seed) {
-    if (r < 2 || C < r) return NULL;
+ora_iblt *ora_iblt_new_ex(uint64_t C, uint32_t r, uint64_t seed, int subtables) {
+    if (r < 2 || C < r || (subtables && C % r)) return NULL;
     ora_iblt *t = (ora_iblt *)calloc(1, sizeof(ora_iblt));
     if (!t) return NULL;
-    t->C = C; t->r = r;
+    t->C = C; t->r = r; t->subtables = subtables;
     t->seed_h = ora_seed_h(seed);
     t->seed_c = ora_seed_c(seed);
     t->count = (int64_t *)calloc(C, sizeof(int64_t));
@@ -389,6 +394,21 @@ ora_iblt *ora_iblt_new(uint64_t C, uint32_t r, uint64_t seed) {
         return NULL;
     }
     return t;
+}
+
+ora_iblt *ora_iblt_new(uint64_t C, uint32_t r, uint64_t seed) { return ora_iblt_new_ex(C, r, seed, 0); }
+
+/* subtable hashing ("hash each item into one cell in each subtable"):  */
+/* h_j(x) = j C/r + umulhi64(mix64(x ^ seed_h ^ (j+1) 0xD1B54A32D192ED03), C/r) */
+void ora_cells_of_subtable(uint64_t x, uint64_t C, uint32_t r, uint64_t seed_h, uint64_t *out) {
+    uint64_t s = C / r;
+    for (uint32_t j = 0; j < r; j++)
+        out[j] = j * s + umulhi64(ora_mix64(x ^ seed_h ^ ((j + 1) * 0xD1B54A32D192ED03ull)), s);
+}
+
+static void key_cells(const ora_iblt *t, uint64_t x, uint64_t *cells) {
+    if (t->subtables) ora_cells_of_subtable(x, t->C, t->r, t->seed_h, cells);
+    else ora_cells_of(x, t->C, t->r, t->seed_h, cells);
 }
 
 void ora_iblt_free(ora_iblt *t) {
@@ -402,7 +422,7 @@ uint64_t ora_iblt_seed_c(const ora_iblt *t) { return t->seed_c; }
 /* sign = +1 insert, -1 delete ("the insertion and deletion procedures are identical") */
 static void iblt_apply(ora_iblt *t, uint64_t x, int sign) {
     uint64_t cells[16];
-    ora_cells_of(x, t->C, t->r, t->seed_h, cells);
+    key_cells(t, x, cells);
     uint32_t h = ora_checksum(x, t->seed_c);
     for (uint32_t j = 0; j < t->r; j++) {
         t->count[cells[j]] += sign;
@@ -482,6 +502,53 @@ int ora_iblt_peel(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *
     return status;
 }
 
+/* Subtable recovery: each round iterates the r subtables        */
+/* serially; subtable j's step snapshots its pure cells, recovers the set of  */
+/* their keys and deletes each from all r cells, so later subtables of the    */
+/* same round see those deletions.  Stops after a full round recovering       */
+/* nothing.  *subrounds = flattened index (i-1) r + j of the last step that   */
+/* recovered a key; per_sub[s-1] = keys recovered in flattened step s.        */
+int ora_iblt_peel_subtables(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
+                            uint32_t *subrounds, uint64_t *per_sub, uint32_t cap, int *complete) {
+    if (!t->subtables) return -1;
+    uint64_t C = t->C, cs = C / t->r;
+    uint64_t *X = (uint64_t *)malloc(cs * sizeof(uint64_t));
+    if (!X) return -1;
+    uint64_t nrec = 0, flat = 0, last = 0;
+    int status = 0;
+    for (;;) {
+        int any = 0;
+        for (uint32_t j = 0; j < t->r; j++) {
+            flat++;
+            uint64_t nX = 0;
+            for (uint64_t c = j * cs; c < (j + 1) * cs; c++)
+                if (iblt_pure(t, c)) X[nX++] = t->keySum[c];
+            qsort(X, nX, sizeof(uint64_t), cmp_u64);
+            uint64_t u = 0;
+            for (uint64_t i = 0; i < nX; i++)
+                if (i == 0 || X[i] != X[i - 1]) X[u++] = X[i];
+            nX = u;
+            for (uint64_t i = 0; i < nX; i++) {
+                iblt_apply(t, X[i], -1);
+                if (nrec < cap_keys) out_keys[nrec] = X[i]; else status = 1;
+                nrec++;
+            }
+            if (nX) { any = 1; last = flat; }
+            if (flat <= cap) per_sub[flat - 1] = nX;
+            else if (nX) status = 1;
+        }
+        if (!any) break;
+    }
+    free(X);
+    *nrecovered = nrec;
+    *subrounds = (uint32_t)last;
+    int z = 1;
+    for (uint64_t c = 0; c < C; c++)
+        if (t->count[c] != 0 || t->keySum[c] != 0 || t->hashSum[c] != 0) { z = 0; break; }
+    *complete = z;
+    return status;
+}
+
 /* Serial recovery: repeatedly take ONE pure cell, recover its key,   */
 /* delete it, until no pure cell remains.  A stack of candidate cells stands   */
 /* in for "iteratively look for pure cells"; every cell is re-tested when     */
@@ -500,7 +567,7 @@ int ora_iblt_serial_recover(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys,
         if (!iblt_pure(t, c)) continue;
         uint64_t x = t->keySum[c];
         uint64_t cells[16];
-        ora_cells_of(x, t->C, t->r, t->seed_h, cells);
+        key_cells(t, x, cells);
         iblt_apply(t, x, -1);
         if (nrec < cap_keys) out_keys[nrec] = x; else status = 1;
         nrec++;
@@ -520,7 +587,7 @@ int ora_iblt_serial_recover(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys,
 void ora_iblt_to_hypergraph(const ora_iblt *t, const uint64_t *keys, uint64_t nkeys, uint32_t *edges) {
     uint64_t cells[16];
     for (uint64_t i = 0; i < nkeys; i++) {
-        ora_cells_of(keys[i], t->C, t->r, t->seed_h, cells);
+        key_cells(t, keys[i], cells);
         for (uint32_t j = 0; j < t->r; j++) edges[i * t->r + j] = (uint32_t)cells[j];
     }
 }

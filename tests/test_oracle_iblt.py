@@ -126,3 +126,49 @@ def test_c2_golden(goldens):
     assert res.complete == g["complete"]
     assert hashlib.sha256(np.sort(res.keys).tobytes()).hexdigest() == g["sorted_keys_sha256"]
     assert hashlib.sha256(np.sort(keys).tobytes()).hexdigest() == g["sorted_keys_sha256"]
+
+
+# ---- subtable IBLT ------------------------------------------------
+def test_subtable_hashing_one_cell_per_subtable():
+    C, r = 3000, 3
+    for x in O.gen_keys(200, 4):
+        cells = O.cells_of_subtable(int(x), C, r, 4)
+        assert np.array_equal(cells // (C // r), np.arange(r))
+
+
+@pytest.mark.parametrize("r", [3, 4])
+@pytest.mark.parametrize("load", [0.5, 0.75, 0.83])
+def test_subtable_recovery_equals_plain_and_subround_peel(r, load):
+    C = r * 5000
+    N = int(load * C)
+    keys = O.gen_keys(N, 40 + r)
+    a = O.Iblt(C, r, 3, subtables=True)
+    b = O.Iblt(C, r, 3, subtables=True)
+    a.insert(keys)
+    b.insert(keys)
+    sub = a.peel_subtables()
+    pl = b.peel()
+    # the recovered set is the complement of the 2-core whatever the schedule
+    assert np.array_equal(np.sort(sub.keys), np.sort(pl.keys)) and sub.complete == pl.complete
+    # and the subtable steps are exactly the subround peel of the IBLT's (partitioned)
+    # hypergraph: keys recovered at flattened step s = edges killed at subround s
+    edges = O.Iblt(C, r, 3, subtables=True).to_hypergraph(keys)
+    assert np.all(edges // (C // r) == np.arange(r))
+    sp = O.subround_peel(edges, C, 2)
+    kk = sp.killed[: sub.rounds]
+    assert sub.per_round.tolist() == kk.tolist()
+    assert np.all(sp.killed[sub.rounds:] == 0)
+    assert np.array_equal(np.sort(sub.keys), np.sort(keys[~sp.core_mask[edges].all(axis=1)]))
+
+
+def test_subtable_steps_fewer_than_r_times_rounds():
+    # subrounds < r x rounds; about 2x at this load
+    C, r = 4 * 20000, 4
+    keys = O.gen_keys(int(0.7 * C), 8)
+    a = O.Iblt(C, r, 5, subtables=True)
+    a.insert(keys)
+    sub = a.peel_subtables()
+    b = O.Iblt(C, r, 5, subtables=True)
+    b.insert(keys)
+    pl = b.peel()
+    assert sub.complete and pl.complete and sub.rounds < r * pl.rounds

@@ -238,6 +238,17 @@ size_t iblt_mem_bytes(uint64_t cells, uint32_t r);
 peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, void *mem, size_t mem_bytes,
                        void *stream, peel_iblt **out);
 
+/* IBLT_FLAG_SUBTABLES -- the paper's GPU layout: the table is split into r
+ * subtables of cells / r cells (r must divide cells) and key x goes to ONE cell per
+ * subtable, h_j(x) = j cells/r + umulhi64(mix64(x ^ seed_h ^ (j+1) 0xD1B54A32D192ED03), cells/r).
+ * iblt_peel on such a table runs the paper's schedule: each round iterates the r subtables
+ * serially, recovering all pure cells of subtable j in parallel; `rounds` is then the
+ * flattened index of the last subtable step that recovered a key and per_round[s-1] the
+ * keys recovered at step s. */
+#define IBLT_FLAG_SUBTABLES 1u
+peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags, void *mem,
+                          size_t mem_bytes, void *stream, peel_iblt **out);
+
 /* Insert nkeys keys (dev u64): XOR x into keySum and checkSum(x) into
  * hashSum of each of x's r cells, count += 1 (one thread per key
  * with atomic XOR).  Keys must be distinct and not already in the

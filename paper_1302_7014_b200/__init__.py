@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_PKG, "libpeel.so")
 PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOVERFLOW = range(7)
 PEEL_FLAG_CSR = 1
 PEEL_FLAG_SUBROUNDS = 2
+IBLT_FLAG_SUBTABLES = 1
 
 _lib = None
 
@@ -69,6 +70,7 @@ def _L() -> ctypes.CDLL:
         L.iblt_mem_bytes.argtypes = [u64, u32]
         L.iblt_mem_bytes.restype = sz
         L.iblt_build.argtypes = [u64, u32, u64, p, sz, p, ctypes.POINTER(p)]
+        L.iblt_build_ex.argtypes = [u64, u32, u64, u32, p, sz, p, ctypes.POINTER(p)]
         L.iblt_insert.argtypes = [p, p, u64, p]
         L.iblt_delete.argtypes = [p, p, u64, p]
         L.iblt_peel.argtypes = [p, p, u64, p, p, p, u32, p, p]
@@ -83,7 +85,7 @@ def _L() -> ctypes.CDLL:
         L.peel_profile_rounds.argtypes = [p, u32]
         L.peel_profile_rounds.restype = i32
         for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_gen_partitioned", "peel_kcore", "peel_kcore_host", "peel_sweep",
-                  "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build",
+                  "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build", "iblt_build_ex",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
         _lib = L
@@ -345,8 +347,9 @@ class IbltResult:
 class Iblt:
     """IBLT of `cells` 16-byte cells and r hashes in a torch-owned device buffer (peel.h iblt_*)."""
 
-    def __init__(self, cells: int, r: int, seed: int, device=None, stream=None, mem: torch.Tensor | None = None):
-        self.C, self.r, self.seed = cells, r, seed
+    def __init__(self, cells: int, r: int, seed: int, device=None, stream=None, mem: torch.Tensor | None = None,
+                 subtables: bool = False):
+        self.C, self.r, self.seed, self.subtables = cells, r, seed, subtables
         self.device = _dev(device) if mem is None else mem.device
         nb = int(_L().iblt_mem_bytes(cells, r))
         if nb == 0:
@@ -360,8 +363,8 @@ class Iblt:
         if self._h is not None and self._h.value:
             _L().iblt_destroy(self._h)
         h = ctypes.c_void_p(0)
-        _check(_L().iblt_build(self.C, self.r, self.seed & (2**64 - 1), _ptr(self.mem), self.mem.numel(),
-                               _stream(stream), ctypes.byref(h)), "iblt_build")
+        _check(_L().iblt_build_ex(self.C, self.r, self.seed & (2**64 - 1), IBLT_FLAG_SUBTABLES if self.subtables else 0,
+                                  _ptr(self.mem), self.mem.numel(), _stream(stream), ctypes.byref(h)), "iblt_build_ex")
         self._h = h
 
     def __del__(self):

@@ -40,6 +40,7 @@ struct IbltCtl {
     ull ccnt[2];   // candidate-list sizes, round t appends ccnt[t%2]
     ull nrec;      // keys recovered so far
     ull rounds;
+    ull scnt[16];  // subtable mode: list lengths [subtable j][round parity b] at j * 2 + b
     uint32_t nonzero;
     uint32_t pad;
 };
@@ -84,6 +85,20 @@ __device__ __forceinline__ void cells_of(ull x, ull C, ull seed_h, uint32_t (&c)
     }
 }
 
+// subtable hashing ("hash each item into one cell in each subtable"):
+// h_j(x) = j C/r + umulhi64(mix64(x ^ seed_h ^ (j+1) 0xD1B54A32D192ED03), C/r)
+template <int R>
+__device__ __forceinline__ void key_cells(ull x, ull C, ull seed_h, bool subt, uint32_t (&c)[R]) {
+    if (subt) {
+        const ull cs = C / R;
+        #pragma unroll
+        for (int j = 0; j < R; j++)
+            c[j] = (uint32_t)(j * cs + __umul64hi(mix64(x ^ seed_h ^ ((ull)(j + 1) * 0xD1B54A32D192ED03ull)), cs));
+    } else {
+        cells_of<R>(x, C, seed_h, c);
+    }
+}
+
 // checkSum(x)
 __device__ __forceinline__ uint32_t checksum(ull x, ull seed_c) { return (uint32_t)(mix64(x ^ seed_c) >> 32); }
 
@@ -99,11 +114,11 @@ __device__ __forceinline__ Cell ld_cell_cg(const Cell *p) {
 template <int R>
 __global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ull seed_h, ull seed_c,
                                                           const ull *__restrict__ keys, ull nkeys,
-                                                          uint32_t delta) {
+                                                          uint32_t delta, bool subt) {
     for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
         const ull x = __ldg(keys + i);
         uint32_t c[R];
-        cells_of<R>(x, C, seed_h, c);
+        key_cells<R>(x, C, seed_h, subt, c);
         const uint32_t h = checksum(x, seed_c);
         #pragma unroll
         for (int j = 0; j < R; j++) {
@@ -117,10 +132,10 @@ __global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ul
 
 template <int R>
 __global__ void __launch_bounds__(256) iblt_edges_kernel(ull C, ull seed_h, const ull *__restrict__ keys,
-                                                         ull nkeys, uint32_t *edges) {
+                                                         ull nkeys, uint32_t *edges, bool subt) {
     for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
         uint32_t c[R];
-        cells_of<R>(__ldg(keys + i), C, seed_h, c);
+        key_cells<R>(__ldg(keys + i), C, seed_h, subt, c);
         #pragma unroll
         for (int j = 0; j < R; j++) edges[i * R + j] = c[j];
     }
@@ -261,6 +276,121 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
     if (__any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nonzero, 1u);
 }
 
+// ---- subtable recovery: each round iterates the r subtables serially --------
+// Subtable j's step processes the list of subtable-j cells that may be pure: each is
+// re-tested and, if pure, its key recovered and deleted from its r cells (one per
+// subtable, so a key is found in at most one pure cell of subtable j: exactly once without
+// any owner rule).  A cell of subtable j' whose count drops 2 -> 1 joins subtable j''s list
+// for this round (j' > j) or the next (j' < j); subtable j's own cells only drop 1 -> 0.
+// Lists: (uint32 *)F0 + b C + j C/r, b = round parity.
+static constexpr int SQ = 2 * IB_BLOCK;
+typedef BlockQueueT<uint32_t, SQ, IB_BLOCK> SCellQ;
+
+template <int R>
+__global__ void __launch_bounds__(IB_BLOCK) iblt_subtable_peel_kernel(IPeelArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ SCellQ qs[R];
+    __shared__ KeyQ qk;
+    IbltCtl *ctl = a.ctl;
+    #pragma unroll
+    for (int j = 0; j < R; j++) bq_init(qs[j]);
+    bq_init(qk);
+    __syncthreads();
+    const ull tid = blockIdx.x * (ull)blockDim.x + threadIdx.x;
+    const ull nthr = (ull)gridDim.x * blockDim.x;
+    const ull stride = (ull)gridDim.x * IB_BLOCK;
+    const ull cs = a.C / R;
+    uint32_t *L0 = reinterpret_cast<uint32_t *>(a.F[0]);
+    auto list = [&](uint32_t j, uint32_t b) { return L0 + (ull)b * a.C + (ull)j * cs; };
+    int slot = 0;
+    // round 1's lists: every pure cell, in its subtable's list (parity 0)
+    for (ull base = (ull)blockIdx.x * IB_BLOCK; base < a.C; base += stride) {
+        const ull c = base + threadIdx.x;
+        bool p = false;
+        if (c < a.C) {
+            Cell v = ld_cell_cg(a.cells + c);
+            p = is_pure(v, a.seed_c);
+            if (p) atomicOr(a.cand + (c >> 5), 1u << (c & 31));
+        }
+        const uint32_t jc = (uint32_t)(c / cs);
+        #pragma unroll
+        for (int j = 0; j < R; j++)
+            if (p && jc == (uint32_t)j) bq_push(qs[j], slot, (uint32_t)c, list(j, 0), &ctl->scnt[j * 2 + 0]);
+        #pragma unroll
+        for (int j = 0; j < R; j++) bq_flush(qs[j], slot, list(j, 0), &ctl->scnt[j * 2 + 0]);
+        slot ^= 1;
+    }
+    grid.sync();
+    uint32_t flat = 0, last = 0;
+    for (uint32_t i = 0;; i++) {
+        bool any = false;
+        const uint32_t b = i & 1u;
+        #pragma unroll 1
+        for (uint32_t j = 0; j < (uint32_t)R; j++) {
+            flat++;
+            const ull nL = ld_cg_u64(&ctl->scnt[j * 2 + b]);
+            const uint32_t *Lc = list(j, b);
+            ull recovered = 0;
+            for (ull base = (ull)blockIdx.x * IB_BLOCK; base < nL; base += stride) {
+                const ull q = base + threadIdx.x;
+                uint32_t h[R];
+                bool cand[R];
+                ull x = 0;
+                #pragma unroll
+                for (int jj = 0; jj < R; jj++) cand[jj] = false;
+                if (q < nL) {
+                    const uint32_t c = ld_cg_u32(Lc + q);
+                    atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
+                    Cell v = ld_cell_cg(a.cells + c);
+                    if (is_pure(v, a.seed_c)) {
+                        x = v.keySum;
+                        recovered++;
+                        bq_push(qk, slot, x, a.out, &ctl->nrec);
+                        key_cells<R>(x, a.C, a.seed_h, true, h);
+                        const uint32_t hx = checksum(x, a.seed_c);
+                        #pragma unroll
+                        for (int jj = 0; jj < R; jj++) {
+                            Cell *p = a.cells + h[jj];
+                            const uint32_t old = atomicAdd(&p->count, 0xFFFFFFFFu);
+                            atomicXor(&p->keySum, x);
+                            atomicXor(&p->hashSum, hx);
+                            if (old == 2u && (uint32_t)jj != j) {
+                                const uint32_t bit = 1u << (h[jj] & 31);
+                                cand[jj] = !(atomicOr(a.cand + (h[jj] >> 5), bit) & bit);
+                            }
+                        }
+                    }
+                }
+                #pragma unroll
+                for (int jj = 0; jj < R; jj++) {
+                    const uint32_t bb = (uint32_t)jj > j ? b : (b ^ 1u);
+                    if (cand[jj]) bq_push(qs[jj], slot, h[jj], list(jj, bb), &ctl->scnt[jj * 2 + bb]);
+                }
+                #pragma unroll
+                for (int jj = 0; jj < R; jj++) {
+                    const uint32_t bb = (uint32_t)jj > j ? b : (b ^ 1u);
+                    bq_flush(qs[jj], slot, list(jj, bb), &ctl->scnt[jj * 2 + bb]);
+                }
+                bq_flush(qk, slot, a.out, &ctl->nrec, a.cap_keys);
+                slot ^= 1;
+            }
+            block_add<IB_BLOCK>(&a.per_round[flat <= ISTAT_CAP ? flat - 1 : ISTAT_CAP], recovered);
+            grid.sync();
+            const ull got = ld_cg_u64(&a.per_round[flat <= ISTAT_CAP ? flat - 1 : ISTAT_CAP]);
+            if (tid == 0) ctl->scnt[j * 2 + b] = 0;  // consumed; next appended a round later
+            if (got) { any = true; last = flat; }
+        }
+        if (!any) break;
+    }
+    if (tid == 0) ctl->rounds = last;
+    uint32_t nz = 0;
+    for (ull c = tid; c < a.C; c += nthr) {
+        Cell v = ld_cell_cg(a.cells + c);
+        nz |= (v.count | v.hashSum) != 0u || v.keySum != 0ull;
+    }
+    if (__any_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0) atomicOr(&ctl->nonzero, 1u);
+}
+
 static unsigned grid_for(ull work, int per_sm = 16) {
     ull blocks = (work + 255) / 256;
     ull cap = (ull)num_sms() * per_sm;
@@ -276,6 +406,7 @@ using namespace peel;
 struct peel_iblt {
     ull C;
     uint32_t r;
+    bool subt;  // IBLT_FLAG_SUBTABLES
     ull seed, seed_h, seed_c;
     char *mem;
     ILayout L;
@@ -292,9 +423,10 @@ extern "C" size_t iblt_mem_bytes(uint64_t cells, uint32_t r) {
     return ilayout(cells).total;
 }
 
-extern "C" peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, void *mem, size_t mem_bytes,
-                                  void *stream, peel_iblt **out) {
+extern "C" peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags, void *mem,
+                                     size_t mem_bytes, void *stream, peel_iblt **out) {
     if (!out || !mem || r < 2 || r > 8 || cells < r || cells >= (1ull << 32)) return PEEL_EINVAL;
+    if ((flags & IBLT_FLAG_SUBTABLES) && cells % r) return PEEL_EINVAL;
     if (((uintptr_t)mem & 15) != 0) return PEEL_EINVAL;
     ILayout L = ilayout(cells);
     if (mem_bytes < L.total) return PEEL_ENOMEM;
@@ -304,6 +436,7 @@ extern "C" peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, voi
     peel_iblt *t = new peel_iblt;
     t->C = cells;
     t->r = r;
+    t->subt = (flags & IBLT_FLAG_SUBTABLES) != 0;
     t->seed = seed;
     const ull G = 0x9E3779B97F4A7C15ull;
     t->seed_h = host_mix64((seed ^ 0x6A09E667F3BCC909ull) + G);
@@ -312,6 +445,11 @@ extern "C" peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, voi
     t->L = L;
     *out = t;
     return PEEL_OK;
+}
+
+extern "C" peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, void *mem, size_t mem_bytes,
+                                  void *stream, peel_iblt **out) {
+    return iblt_build_ex(cells, r, seed, 0u, mem, mem_bytes, stream, out);
 }
 
 static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, uint32_t delta,
@@ -326,13 +464,13 @@ static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkey
     {
         ProfScope ps(delta == 1u ? "iblt_insert" : "iblt_delete", s);
         switch (t->r) {
-            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
-            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
-            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
-            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
-            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
-            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
-            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta); break;
+            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
         }
     }
     PEEL_CUDA(cudaGetLastError());
@@ -349,15 +487,14 @@ extern "C" peel_status iblt_delete(peel_iblt *t, const uint64_t *keys, uint64_t 
 
 template <int R>
 static peel_status run_iblt_peel(peel_iblt *t, IPeelArgs &a, cudaStream_t s) {
-    auto kern = iblt_peel_kernel<R>;
+    void *kern = t->subt ? (void *)iblt_subtable_peel_kernel<R> : (void *)iblt_peel_kernel<R>;
     int per_sm = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, IB_BLOCK, 0));
     if (per_sm < 1) per_sm = 1;
     unsigned grid = (unsigned)(num_sms() * per_sm);
     void *args[] = {&a};
-    ProfScope ps("iblt_peel_rounds", s);
-    PEEL_CUDA(cudaLaunchCooperativeKernel((void *)kern, grid, IB_BLOCK, args, 0, s));
-    (void)t;
+    ProfScope ps(t->subt ? "iblt_subtable_peel" : "iblt_peel_rounds", s);
+    PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, IB_BLOCK, args, 0, s));
     return PEEL_OK;
 }
 
@@ -426,13 +563,13 @@ extern "C" peel_status iblt_to_hypergraph(const peel_iblt *t, const uint64_t *ke
     {
         ProfScope ps("iblt_edges", s);
         switch (t->r) {
-            case 2: iblt_edges_kernel<2><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
-            case 3: iblt_edges_kernel<3><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
-            case 4: iblt_edges_kernel<4><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
-            case 5: iblt_edges_kernel<5><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
-            case 6: iblt_edges_kernel<6><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
-            case 7: iblt_edges_kernel<7><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
-            case 8: iblt_edges_kernel<8><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges); break;
+            case 2: iblt_edges_kernel<2><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 3: iblt_edges_kernel<3><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 4: iblt_edges_kernel<4><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 5: iblt_edges_kernel<5><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 6: iblt_edges_kernel<6><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 7: iblt_edges_kernel<7><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 8: iblt_edges_kernel<8><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
         }
     }
     PEEL_CUDA(cudaGetLastError());

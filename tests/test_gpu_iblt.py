@@ -119,3 +119,39 @@ def test_c2_full_config(goldens):
     assert res.complete
     got = np.sort(res.keys.cpu().numpy().view(np.uint64))
     assert hashlib.sha256(got.tobytes()).hexdigest() == g["sorted_keys_sha256"]
+
+
+# ---- subtable IBLT: the paper's GPU schedule ------------------------------------
+@pytest.mark.parametrize("r", [2, 3, 4, 5])
+@pytest.mark.parametrize("load", [0.5, 0.75, 0.83, 1.1])
+def test_subtable_recovery_vs_oracle(r, load):
+    C = r * 30011
+    N = int(load * C)
+    keys = O.gen_keys(N, 60 + r)
+    t = pk.Iblt(C, r, 9, device=DEV, subtables=True)
+    o = O.Iblt(C, r, 9, subtables=True)
+    t.insert(keys_dev(keys))
+    o.insert(keys)
+    cnt, ks, hs = dev_cells(t)
+    ocnt, oks, ohs = o.cells()
+    assert np.array_equal(cnt.astype(np.int32), ocnt.astype(np.int32)) and np.array_equal(ks, oks)
+    res = t.peel()
+    ref = o.peel_subtables()
+    assert res.rounds == ref.rounds and res.per_round.tolist() == ref.per_round.tolist()
+    assert np.array_equal(np.sort(res.keys.cpu().numpy().view(np.uint64)), np.sort(ref.keys))
+    assert res.complete == ref.complete
+
+
+def test_subtable_table3_shape():
+    # Tables 3a/3b workload shape (2^24 cells in the paper; 2^21 here), r=3, load 0.75 and 0.83
+    for load in (0.75, 0.83):
+        C = 3 * (1 << 21)
+        N = int(load * C)
+        keys = pk.gen_keys(N, 3, device=DEV)
+        t = pk.Iblt(C, 3, 3, device=DEV, subtables=True)
+        t.insert(keys)
+        res = t.peel(cap_keys=N)
+        o = O.Iblt(C, 3, 3, subtables=True)
+        o.insert(O.gen_keys(N, 3))
+        ref = o.peel_subtables(cap_keys=N + 1)
+        assert res.rounds == ref.rounds and res.nrecovered == ref.keys.size and res.complete == ref.complete

@@ -174,11 +174,12 @@ static constexpr int PART_BLOCK = 256;
 static constexpr int PART_ENTRIES = 4096;  // endpoint entries staged per chunk
 
 // pass 1: partition the r m endpoint increments by vertex bin.  Per chunk of edges the
-// block histograms bins in shared memory, reserves one contiguous run per bin with a
-// single global atomic, counting-sorts the chunk's entries by bin in shared memory and
-// writes them out so each bin's run is a coalesced store.  Stored entry =
-// e << 32 | (u mod 2^BIN_SHIFT); in shared memory the full u is kept (its bin is u >> BIN_SHIFT).
-// Shared memory = 8 B x PART_ENTRIES + 20 B x nbins (sized per launch).
+// block stages the chunk's edge words in shared memory with 16-byte coalesced loads,
+// histograms bins in shared memory, reserves one contiguous run per bin with a single
+// global atomic, counting-sorts the chunk's entries by bin in shared memory and writes
+// them out so each bin's run is a coalesced store.  Stored entry =
+// e << 32 | (u mod 2^BIN_SHIFT); in shared memory the full u is kept (bin = u >> BIN_SHIFT).
+// Shared memory = 4 B + 8 B per entry + 20 B per bin + 1 B per edge (sized per launch).
 template <int R>
 __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint32_t *__restrict__ edges,
                                                                       uint64_t n, uint64_t m, uint32_t nbins,
@@ -186,27 +187,47 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
                                                                       const ull *__restrict__ cap, ull *entries,
                                                                       Ctl *ctl) {
     constexpr int CH = PART_ENTRIES / R;  // edges per chunk
+    constexpr int CW = CH * R;            // edge words per chunk
+    constexpr int CWP = (CW + 3) & ~3;    // padded: keeps every array below 16-byte aligned
     extern __shared__ unsigned char smem_raw[];
-    ull *sent = (ull *)smem_raw;                  // [CH*R]  (e << 32 | u)
-    ull *gpos = sent + CH * R;                    // [nbins]
+    ull *sent = (ull *)smem_raw;                  // [CWP]  (e << 32 | u), bin-sorted
+    uint32_t *words = (uint32_t *)(sent + CWP);   // [CWP]  the chunk's edge words
+    ull *gpos = (ull *)(words + CWP);             // [nbins]
     uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
     uint32_t *offs = hist + nbins;                // [nbins]
     uint32_t *fill = offs + nbins;                // [nbins]
+    uint8_t *okb = (uint8_t *)(fill + nbins);     // [CH]  edge valid
     __shared__ uint32_t total;
     const ull mask = (1ull << BIN_SHIFT) - 1;
     for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {
         const int ne = (int)min((uint64_t)CH, m - c0);
+        const int nw = ne * R;
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
+        // stage the chunk's words (the chunk starts at word c0 R; 16-byte loads where aligned)
+        const uint32_t *src = edges + c0 * R;
+        if ((((uintptr_t)src) & 15) == 0) {
+            const int nv = nw / 4;
+            for (int i = threadIdx.x; i < nv; i += PART_BLOCK)
+                reinterpret_cast<uint4 *>(words)[i] = __ldcs(reinterpret_cast<const uint4 *>(src) + i);
+            for (int i = nv * 4 + threadIdx.x; i < nw; i += PART_BLOCK) words[i] = __ldcs(src + i);
+        } else {
+            for (int i = threadIdx.x; i < nw; i += PART_BLOCK) words[i] = __ldcs(src + i);
+        }
         __syncthreads();
         for (int i = threadIdx.x; i < ne; i += PART_BLOCK) {
-            uint32_t u[R];
-            if (!load_edge<R>(edges, c0 + i, n, u)) {
-                atomicOr(&ctl->err, ERR_BADVERTEX);
-                continue;
-            }
+            bool ok = true;
             #pragma unroll
-            for (int j = 0; j < R; j++) atomicAdd(&hist[u[j] >> BIN_SHIFT], 1u);
+            for (int j = 0; j < R; j++) ok &= (uint64_t)words[i * R + j] < n;
+            #pragma unroll
+            for (int j = 0; j < R; j++)
+                #pragma unroll
+                for (int q = j + 1; q < R; q++) ok &= words[i * R + j] != words[i * R + q];
+            okb[i] = ok;
+            if (!ok) atomicOr(&ctl->err, ERR_BADVERTEX);
         }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nw; i += PART_BLOCK)
+            if (okb[i / R]) atomicAdd(&hist[words[i] >> BIN_SHIFT], 1u);
         __syncthreads();
         // exclusive scan of hist over nbins (<= 1024): one warp
         if (threadIdx.x < 32) {
@@ -236,16 +257,12 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
                 if (g + hist[b] > cap[b]) atomicOr(&ctl->binovf, 1u);
                 gpos[b] = g;
             }
-        __syncthreads();
-        for (int i = threadIdx.x; i < ne; i += PART_BLOCK) {
-            uint32_t u[R];
-            if (!load_edge<R>(edges, c0 + i, n, u)) continue;
-            const ull e = c0 + i;
-            #pragma unroll
-            for (int j = 0; j < R; j++) {
-                const uint32_t b = u[j] >> BIN_SHIFT;
-                sent[offs[b] + atomicAdd(&fill[b], 1u)] = (e << 32) | u[j];
-            }
+        for (int i = threadIdx.x; i < nw; i += PART_BLOCK) {
+            const int ed = i / R;
+            if (!okb[ed]) continue;
+            const uint32_t u = words[i];
+            const uint32_t b = u >> BIN_SHIFT;
+            sent[offs[b] + atomicAdd(&fill[b], 1u)] = ((c0 + ed) << 32) | u;
         }
         __syncthreads();
         const uint32_t tot = total;
@@ -260,7 +277,8 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
 }
 
 static size_t partition_smem(int r, uint64_t nbins) {
-    return sizeof(ull) * (PART_ENTRIES / r) * r + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
+    const size_t cw = (((size_t)(PART_ENTRIES / r) * r) + 3) & ~(size_t)3;
+    return (sizeof(ull) + sizeof(uint32_t)) * cw + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins + PART_ENTRIES / r + 16;
 }
 
 // CSR build from the binned entries: blockIdx.y = bin, blocks scheduled bin-major, so the

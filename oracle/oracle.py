@@ -71,6 +71,10 @@ def lib() -> ctypes.CDLL:
             L.ora_iblt_peel_subtables.argtypes = [p, p, u64, p, p, p, u32, p]
             L.ora_iblt_peel_subtables.restype = i32
             L.ora_cells_of_subtable.argtypes = [u64, u64, u32, u64, p]
+            L.ora_iblt_subtract.argtypes = [p, p]
+            L.ora_iblt_subtract.restype = i32
+            L.ora_iblt_peel_signed.argtypes = [p, p, p, u64, p, p, p, u32, p]
+            L.ora_iblt_peel_signed.restype = i32
             L.ora_iblt_free.argtypes = [p]
             L.ora_iblt_seed_h.argtypes = [p]
             L.ora_iblt_seed_h.restype = u64
@@ -313,6 +317,28 @@ class Iblt:
         if st == 1:
             raise OverflowError("cap exceeded")
         return IbltResult(out[:nrec.value].copy(), sub.value, per[:sub.value].copy(), bool(complete.value))
+
+    def subtract(self, other: "Iblt"):
+        """self <- self - other cell-wise: the IBLT of the signed multiset difference."""
+        if lib().ora_iblt_subtract(self._t, other._t):
+            raise ValueError("tables differ in C, r, seed or layout")
+
+    def peel_signed(self, cap_keys: int | None = None, cap: int = 1 << 16):
+        """Recovery of a signed table: pure = count +-1 with a matching checksum.
+        Returns (IbltResult, signs) with signs[i] = +1 (key of A only) or -1 (key of B only)."""
+        cap_keys = self.C * 2 if cap_keys is None else cap_keys
+        out = np.zeros(max(cap_keys, 1), dtype=np.uint64)
+        sg = np.zeros(max(cap_keys, 1), dtype=np.int8)
+        nrec = ctypes.c_uint64(0)
+        rounds = ctypes.c_uint32(0)
+        per = np.zeros(cap, dtype=np.uint64)
+        complete = ctypes.c_int(0)
+        st = lib().ora_iblt_peel_signed(self._t, _ptr(out), _ptr(sg), cap_keys, ctypes.addressof(nrec),
+                                        ctypes.addressof(rounds), _ptr(per), cap, ctypes.addressof(complete))
+        if st != 0:
+            raise OverflowError("cap exceeded")
+        t = rounds.value
+        return IbltResult(out[:nrec.value].copy(), t, per[:t].copy(), bool(complete.value)), sg[:nrec.value].copy()
 
     def serial_recover(self):
         """One-pure-cell-at-a-time recovery, destructive."""

@@ -549,6 +549,80 @@ int ora_iblt_peel_subtables(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys, 
     return status;
 }
 
+/* Set difference: a <- a - b cell-wise (count      */
+/* subtracts, key and checksum fields XOR), the IBLT of the signed multiset   */
+/* A - B.  Both tables must share C, r and seed.                              */
+int ora_iblt_subtract(ora_iblt *a, const ora_iblt *b) {
+    if (a->C != b->C || a->r != b->r || a->seed_h != b->seed_h || a->subtables != b->subtables) return -1;
+    for (uint64_t c = 0; c < a->C; c++) {
+        a->count[c] -= b->count[c];
+        a->keySum[c] ^= b->keySum[c];
+        a->hashSum[c] ^= b->hashSum[c];
+    }
+    return 0;
+}
+
+/* Round-synchronous recovery of a signed table: a cell is pure when its     */
+/* count is +1 or -1 and its checksum field equals checkSum(key field); each */
+/* round recovers the SET of (key, sign) of the round-start pure cells and   */
+/* removes each (deleting a +1 key, re-inserting a -1 key).  out_sign[i] is  */
+/* +1 for keys of A \ B, -1 for keys of B \ A.                              */
+static int iblt_pure_signed(const ora_iblt *t, uint64_t c, int *sign) {
+    if ((t->count[c] == 1 || t->count[c] == -1) && t->hashSum[c] == ora_checksum(t->keySum[c], t->seed_c)) {
+        *sign = (int)t->count[c];
+        return 1;
+    }
+    return 0;
+}
+
+static int cmp_key_sign(const void *a, const void *b) {
+    const uint64_t *x = (const uint64_t *)a, *y = (const uint64_t *)b;
+    if (x[0] != y[0]) return (x[0] > y[0]) - (x[0] < y[0]);
+    return (x[1] > y[1]) - (x[1] < y[1]);
+}
+
+int ora_iblt_peel_signed(ora_iblt *t, uint64_t *out_keys, int8_t *out_sign, uint64_t cap_keys,
+                         uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
+                         int *complete) {
+    uint64_t C = t->C;
+    uint64_t *X = (uint64_t *)malloc(2 * C * sizeof(uint64_t));  /* (key, sign + 1) pairs */
+    if (!X) return -1;
+    uint64_t nrec = 0;
+    uint32_t rt = 0;
+    int status = 0;
+    for (;;) {
+        uint64_t nX = 0;
+        for (uint64_t c = 0; c < C; c++) {
+            int sg;
+            if (iblt_pure_signed(t, c, &sg)) { X[2 * nX] = t->keySum[c]; X[2 * nX + 1] = (uint64_t)(sg + 1); nX++; }
+        }
+        if (nX == 0) break;
+        qsort(X, nX, 2 * sizeof(uint64_t), cmp_key_sign);
+        uint64_t u = 0;
+        for (uint64_t i = 0; i < nX; i++)
+            if (i == 0 || X[2 * i] != X[2 * (i - 1)] || X[2 * i + 1] != X[2 * (i - 1) + 1]) {
+                X[2 * u] = X[2 * i]; X[2 * u + 1] = X[2 * i + 1]; u++;
+            }
+        nX = u;
+        rt += 1;
+        for (uint64_t i = 0; i < nX; i++) {
+            int sg = (int)X[2 * i + 1] - 1;
+            iblt_apply(t, X[2 * i], -sg);
+            if (nrec < cap_keys) { out_keys[nrec] = X[2 * i]; out_sign[nrec] = (int8_t)sg; } else status = 1;
+            nrec++;
+        }
+        if (rt <= cap) per_round[rt - 1] = nX; else status = 1;
+    }
+    free(X);
+    *nrecovered = nrec;
+    *rounds = rt;
+    int z = 1;
+    for (uint64_t c = 0; c < C; c++)
+        if (t->count[c] != 0 || t->keySum[c] != 0 || t->hashSum[c] != 0) { z = 0; break; }
+    *complete = z;
+    return status;
+}
+
 /* Serial recovery: repeatedly take ONE pure cell, recover its key,   */
 /* delete it, until no pure cell remains.  A stack of candidate cells stands   */
 /* in for "iteratively look for pure cells"; every cell is re-tested when     */

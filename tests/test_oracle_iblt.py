@@ -172,3 +172,47 @@ def test_subtable_steps_fewer_than_r_times_rounds():
     b.insert(keys)
     pl = b.peel()
     assert sub.complete and pl.complete and sub.rounds < r * pl.rounds
+
+
+# ---- set difference / sparse recovery with signed counts -----------
+@pytest.mark.parametrize("r", [3, 4])
+def test_set_difference_recovers_both_sides(r):
+    C = 30000
+    common = synth.random_keys(200000, 11)
+    only_a = synth.random_keys(9000, 12)
+    only_b = synth.random_keys(9000, 13)
+    a = O.Iblt(C, r, 6)
+    b = O.Iblt(C, r, 6)
+    a.insert(np.concatenate([common, only_a]))
+    b.insert(np.concatenate([only_b, common]))
+    a.subtract(b)
+    res, sg = a.peel_signed()
+    assert res.complete
+    assert np.array_equal(np.sort(res.keys[sg == 1]), np.sort(only_a))
+    assert np.array_equal(np.sort(res.keys[sg == -1]), np.sort(only_b))
+
+
+def test_signed_peel_equals_plain_on_insert_only_tables():
+    C, r = 20000, 3
+    keys = O.gen_keys(15000, 3)
+    a = O.Iblt(C, r, 2)
+    b = O.Iblt(C, r, 2)
+    a.insert(keys)
+    b.insert(keys)
+    pa = a.peel()
+    pb, sg = b.peel_signed()
+    assert np.all(sg == 1) and pa.rounds == pb.rounds and pa.per_round.tolist() == pb.per_round.tolist()
+    assert np.array_equal(np.sort(pa.keys), np.sort(pb.keys))
+
+
+def test_subtract_is_cellwise_difference_and_inverse_of_insert():
+    C, r = 5000, 3
+    ka, kb = synth.random_keys(3000, 1), synth.random_keys(3000, 2)
+    a, b, d = O.Iblt(C, r, 4), O.Iblt(C, r, 4), O.Iblt(C, r, 4)
+    a.insert(ka)
+    b.insert(kb)
+    d.insert(ka)
+    d.delete(kb)  # delete == subtracting an insert
+    a.subtract(b)
+    for x, y in zip(a.cells(), d.cells()):
+        assert np.array_equal(x, y)

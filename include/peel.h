@@ -277,6 +277,19 @@ peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint6
                       uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete,
                       void *stream);
 
+/* Set difference (the sparse-recovery use of P:476-480): a <- a - b cell-wise
+ * (count subtracts, key and checksum fields XOR) -- the IBLT of the signed multiset A - B.
+ * Both tables must have equal cells, r, seed and layout (else EINVAL).  Stream-ordered. */
+peel_status iblt_subtract(peel_iblt *a, const peel_iblt *b, void *stream);
+
+/* iblt_peel for signed tables: a cell is pure when count is +1 or -1 and hashSum ==
+ * checkSum(keySum); a recovered key is removed with the opposite sign.  out_sign dev
+ * int8 [cap_keys]: +1 for keys only in A, -1 for keys only in B.  Other arguments and
+ * the result as iblt_peel.  EINVAL on a subtable table. */
+peel_status iblt_peel_signed(peel_iblt *t, uint64_t *out_keys, int8_t *out_sign, uint64_t cap_keys,
+                             uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
+                             int *complete, void *stream);
+
 /* Device pointer to the 16-byte cell array (for tests and serialisation). */
 void *iblt_cells(const peel_iblt *t);
 

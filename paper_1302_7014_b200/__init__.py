@@ -74,6 +74,8 @@ def _L() -> ctypes.CDLL:
         L.iblt_insert.argtypes = [p, p, u64, p]
         L.iblt_delete.argtypes = [p, p, u64, p]
         L.iblt_peel.argtypes = [p, p, u64, p, p, p, u32, p, p]
+        L.iblt_subtract.argtypes = [p, p, p]
+        L.iblt_peel_signed.argtypes = [p, p, p, u64, p, p, p, u32, p, p]
         L.iblt_cells.argtypes = [p]
         L.iblt_cells.restype = p
         L.iblt_to_hypergraph.argtypes = [p, p, u64, p, p]
@@ -86,7 +88,7 @@ def _L() -> ctypes.CDLL:
         L.peel_profile_rounds.restype = i32
         for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_gen_partitioned", "peel_kcore", "peel_kcore_host", "peel_sweep",
                   "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build", "iblt_build_ex",
-                  "iblt_insert", "iblt_delete", "iblt_peel", "iblt_to_hypergraph"):
+                  "iblt_insert", "iblt_delete", "iblt_peel", "iblt_subtract", "iblt_peel_signed", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -400,6 +402,27 @@ class Iblt:
         t = rounds.value
         return IbltResult(out[: min(nrec.value, cap_keys)], nrec.value, t, per_round[:min(t, cap)].copy(),
                           bool(complete.value), st)
+
+    def subtract(self, other: "Iblt", stream=None):
+        """self <- self - other cell-wise: the IBLT of the signed difference (peel.h iblt_subtract)."""
+        _check(_L().iblt_subtract(self._h, other._h, _stream(stream)), "iblt_subtract")
+
+    def peel_signed(self, cap_keys: int | None = None, cap: int = 65536, stream=None):
+        """Recovery of a signed table (peel.h iblt_peel_signed): returns (IbltResult, signs)."""
+        cap_keys = self.C if cap_keys is None else cap_keys
+        out = torch.empty((max(cap_keys, 1),), dtype=torch.int64, device=self.device)
+        sg = torch.empty((max(cap_keys, 1),), dtype=torch.int8, device=self.device)
+        nrec = ctypes.c_uint64(0)
+        rounds = ctypes.c_uint32(0)
+        per_round = np.zeros(cap, dtype=np.uint64)
+        complete = ctypes.c_int(0)
+        st = _L().iblt_peel_signed(self._h, _ptr(out), _ptr(sg), cap_keys, ctypes.addressof(nrec),
+                                   ctypes.addressof(rounds), per_round.ctypes.data, cap, ctypes.addressof(complete),
+                                   _stream(stream))
+        _check(st, "iblt_peel_signed")
+        t = rounds.value
+        k = min(nrec.value, cap_keys)
+        return IbltResult(out[:k], nrec.value, t, per_round[:min(t, cap)].copy(), bool(complete.value), st), sg[:k]
 
     def to_hypergraph(self, keys: torch.Tensor, stream=None) -> torch.Tensor:
         edges = torch.empty((keys.numel(), self.r), dtype=torch.int32, device=self.device)

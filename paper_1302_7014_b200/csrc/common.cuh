@@ -156,4 +156,22 @@ __device__ __forceinline__ void bq_flush(BlockQueueT<T, QCAP, BLOCK> &q, int slo
         if (b + i < cap) gl[b + i] = q.buf[slot][i];
 }
 
+// bq_flush with a custom writer: writer(global_index, value) for each queued value
+// (e.g. to split a queued pair into two output arrays).  Same contract as bq_flush.
+template <typename T, int QCAP, int BLOCK, typename W>
+__device__ __forceinline__ void bq_flush_with(BlockQueueT<T, QCAP, BLOCK> &q, int slot, ull *gcnt, ull cap, W writer) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = min(q.n[slot], (uint32_t)QCAP);
+        q.cnt = c;
+        q.base = c ? atomicAdd(gcnt, (ull)c) : 0ull;
+        q.n[slot] = 0;
+    }
+    __syncthreads();
+    const uint32_t c = q.cnt;
+    const ull b = q.base;
+    for (uint32_t i = threadIdx.x; i < c; i += BLOCK)
+        if (b + i < cap) writer(b + i, q.buf[slot][i]);
+}
+
 }  // namespace peel

@@ -151,11 +151,22 @@ struct IPeelArgs {
     ulonglong2 *F[2];   // frontier entries (cell, key snapshot)
     uint32_t *clist;
     ull *out;
+    int8_t *out_sign;   // signed recovery: +1 / -1 per recovered key
     ull cap_keys;
+    bool subt;          // subtable hashing
 };
 
 __device__ __forceinline__ bool is_pure(const Cell &c, ull seed_c) {
     return c.count == 1u && c.hashSum == checksum(c.keySum, seed_c);
+}
+
+// signed tables (set difference): pure = count +1 or -1 with a matching checksum; returns
+// +1 / -1, or 0 if not pure.  Unsigned recovery accepts only count == +1.
+template <bool SIGNED>
+__device__ __forceinline__ int pure_sign(const Cell &c, ull seed_c) {
+    const bool cnt = SIGNED ? (c.count == 1u || c.count == 0xFFFFFFFFu) : (c.count == 1u);
+    if (!cnt || c.hashSum != checksum(c.keySum, seed_c)) return 0;
+    return c.count == 1u ? 1 : -1;
 }
 
 static constexpr int IQ = 2 * IB_BLOCK;
@@ -163,11 +174,12 @@ typedef BlockQueueT<ulonglong2, IQ, IB_BLOCK> EntQ;
 typedef BlockQueueT<ull, IQ, IB_BLOCK> KeyQ;
 typedef BlockQueueT<uint32_t, IQ, IB_BLOCK> CellQ;
 
-template <int R>
+// entry.x = cell | (negative sign) << 32, entry.y = key snapshot
+template <int R, bool SIGNED>
 __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ EntQ qe;
-    __shared__ KeyQ qk;
+    __shared__ EntQ qk;  // recovered (key, sign)
     __shared__ CellQ qc;
     IbltCtl *ctl = a.ctl;
     bq_init(qe); bq_init(qk); bq_init(qc);
@@ -176,14 +188,19 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
     const ull nthr = (ull)gridDim.x * blockDim.x;
     const ull stride = (ull)gridDim.x * IB_BLOCK;
     int slot = 0;
+    auto write_key = [&](ull i, ulonglong2 v) {
+        a.out[i] = v.x;
+        if (SIGNED) a.out_sign[i] = (int8_t)(v.y ? -1 : 1);
+    };
 
     // ---- round 1: every pure cell ("a single thread to each cell") ----
     for (ull base = (ull)blockIdx.x * IB_BLOCK; base < a.C; base += stride) {
         const ull c = base + threadIdx.x;
         if (c < a.C) {
             Cell v = ld_cell_cg(a.cells + c);
-            if (is_pure(v, a.seed_c)) {
-                bq_push(qe, slot, make_ulonglong2(c, v.keySum), a.F[0], &ctl->fcnt[0]);
+            const int sg = pure_sign<SIGNED>(v, a.seed_c);
+            if (sg) {
+                bq_push(qe, slot, make_ulonglong2(c | ((ull)(sg < 0) << 32), v.keySum), a.F[0], &ctl->fcnt[0]);
                 atomicOr(a.pure[0] + (c >> 5), 1u << (c & 31));
             }
         }
@@ -207,9 +224,10 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
             if (i < nF) {
                 const ulonglong2 ent = __ldcg(Fc + i);
                 const uint32_t c = (uint32_t)ent.x;
+                const bool neg = (ent.x >> 32) != 0;
                 const ull x = ent.y;
                 uint32_t h[R];
-                cells_of<R>(x, a.C, a.seed_h, h);
+                key_cells<R>(x, a.C, a.seed_h, a.subt, h);
                 bool owner = false, found = false;
                 #pragma unroll
                 for (int j = 0; j < R; j++) {
@@ -218,22 +236,24 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                 }
                 if (owner) {
                     recovered++;
-                    bq_push(qk, slot, x, a.out, &ctl->nrec);
+                    // <= one push per thread per iteration < IQ: the queue never takes its overflow path
+                    bq_push(qk, slot, make_ulonglong2(x, neg ? 1ull : 0ull), (ulonglong2 *)nullptr, &ctl->nrec);
                     const uint32_t hx = checksum(x, a.seed_c);
+                    const uint32_t delta = neg ? 1u : 0xFFFFFFFFu;  // remove: count -= sign
                     #pragma unroll
                     for (int j = 0; j < R; j++) {
                         Cell *p = a.cells + h[j];
-                        const uint32_t old = atomicAdd(&p->count, 0xFFFFFFFFu);
+                        const uint32_t now = atomicAdd(&p->count, delta) + delta;
                         atomicXor(&p->keySum, x);
                         atomicXor(&p->hashSum, hx);
-                        if (old == 2u) {
+                        if (now == 1u || (SIGNED && now == 0xFFFFFFFFu)) {
                             const uint32_t bit = 1u << (h[j] & 31);
                             if (!(atomicOr(a.cand + (h[j] >> 5), bit) & bit)) bq_push(qc, slot, h[j], a.clist, ccnt);
                         }
                     }
                 }
             }
-            bq_flush(qk, slot, a.out, &ctl->nrec, a.cap_keys);
+            bq_flush_with(qk, slot, &ctl->nrec, a.cap_keys, write_key);
             bq_flush(qc, slot, a.clist, ccnt);
             slot ^= 1;
         }
@@ -255,8 +275,9 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                 const uint32_t c = ld_cg_u32(a.clist + i);
                 atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
                 Cell v = ld_cell_cg(a.cells + c);
-                if (is_pure(v, a.seed_c)) {
-                    bq_push(qe, slot, make_ulonglong2(c, v.keySum), Fn, fn);
+                const int sg = pure_sign<SIGNED>(v, a.seed_c);
+                if (sg) {
+                    bq_push(qe, slot, make_ulonglong2(c | ((ull)(sg < 0) << 32), v.keySum), Fn, fn);
                     atomicOr(pure_next + (c >> 5), 1u << (c & 31));
                 }
             }
@@ -486,22 +507,25 @@ extern "C" peel_status iblt_delete(peel_iblt *t, const uint64_t *keys, uint64_t 
 }
 
 template <int R>
-static peel_status run_iblt_peel(peel_iblt *t, IPeelArgs &a, cudaStream_t s) {
-    void *kern = t->subt ? (void *)iblt_subtable_peel_kernel<R> : (void *)iblt_peel_kernel<R>;
+static peel_status run_iblt_peel(peel_iblt *t, IPeelArgs &a, bool sgn, cudaStream_t s) {
+    void *kern = t->subt ? (void *)iblt_subtable_peel_kernel<R>
+                         : (sgn ? (void *)iblt_peel_kernel<R, true> : (void *)iblt_peel_kernel<R, false>);
     int per_sm = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, IB_BLOCK, 0));
     if (per_sm < 1) per_sm = 1;
     unsigned grid = (unsigned)(num_sms() * per_sm);
     void *args[] = {&a};
-    ProfScope ps(t->subt ? "iblt_subtable_peel" : "iblt_peel_rounds", s);
+    ProfScope ps(t->subt ? "iblt_subtable_peel" : (sgn ? "iblt_peel_signed_rounds" : "iblt_peel_rounds"), s);
     PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, IB_BLOCK, args, 0, s));
     return PEEL_OK;
 }
 
-extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
-                                 uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete,
-                                 void *stream) {
+static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_sign, uint64_t cap_keys,
+                                  uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
+                                  int *complete, void *stream) {
+    const bool sgn = out_sign != nullptr;
     if (!t || !nrecovered || !rounds || (cap_keys && !out_keys)) return PEEL_EINVAL;
+    if (sgn && t->subt) return PEEL_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     prof_begin_call();
     const ILayout &L = t->L;
@@ -523,16 +547,18 @@ extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_
     a.F[1] = (ulonglong2 *)(m + L.F1);
     a.clist = (uint32_t *)(m + L.clist);
     a.out = (ull *)out_keys;
+    a.out_sign = out_sign;
     a.cap_keys = cap_keys;
+    a.subt = t->subt;
     peel_status st = PEEL_EINVAL;
     switch (t->r) {
-        case 2: st = run_iblt_peel<2>(t, a, s); break;
-        case 3: st = run_iblt_peel<3>(t, a, s); break;
-        case 4: st = run_iblt_peel<4>(t, a, s); break;
-        case 5: st = run_iblt_peel<5>(t, a, s); break;
-        case 6: st = run_iblt_peel<6>(t, a, s); break;
-        case 7: st = run_iblt_peel<7>(t, a, s); break;
-        case 8: st = run_iblt_peel<8>(t, a, s); break;
+        case 2: st = run_iblt_peel<2>(t, a, sgn, s); break;
+        case 3: st = run_iblt_peel<3>(t, a, sgn, s); break;
+        case 4: st = run_iblt_peel<4>(t, a, sgn, s); break;
+        case 5: st = run_iblt_peel<5>(t, a, sgn, s); break;
+        case 6: st = run_iblt_peel<6>(t, a, sgn, s); break;
+        case 7: st = run_iblt_peel<7>(t, a, sgn, s); break;
+        case 8: st = run_iblt_peel<8>(t, a, sgn, s); break;
     }
     if (st != PEEL_OK) return st;
     IbltCtl h;
@@ -547,6 +573,47 @@ extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_
     if (per_round && nstore)
         PEEL_CUDA(cudaMemcpy(per_round, a.per_round, sizeof(ull) * nstore, cudaMemcpyDeviceToHost));
     if (h.nrec > cap_keys || h.rounds > cap || h.rounds > ISTAT_CAP) return PEEL_ETRUNC;
+    return PEEL_OK;
+}
+
+extern "C" peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
+                                 uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete,
+                                 void *stream) {
+    return iblt_peel_impl(t, out_keys, nullptr, cap_keys, nrecovered, rounds, per_round, cap, complete, stream);
+}
+
+extern "C" peel_status iblt_peel_signed(peel_iblt *t, uint64_t *out_keys, int8_t *out_sign, uint64_t cap_keys,
+                                        uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
+                                        int *complete, void *stream) {
+    if (!out_sign && cap_keys) return PEEL_EINVAL;
+    static int8_t dummy;
+    return iblt_peel_impl(t, out_keys, out_sign ? out_sign : &dummy, cap_keys, nrecovered, rounds, per_round, cap,
+                          complete, stream);
+}
+
+// a <- a - b cell-wise: count subtracts, key and checksum fields XOR
+__global__ void __launch_bounds__(256) iblt_subtract_kernel(Cell *a, const Cell *__restrict__ b, ull C) {
+    for (ull c = blockIdx.x * (ull)blockDim.x + threadIdx.x; c < C; c += (ull)gridDim.x * blockDim.x) {
+        uint4 x = reinterpret_cast<uint4 *>(a)[c];
+        const uint4 y = __ldg(reinterpret_cast<const uint4 *>(b) + c);
+        x.x -= y.x;
+        x.y ^= y.y;
+        x.z ^= y.z;
+        x.w ^= y.w;
+        reinterpret_cast<uint4 *>(a)[c] = x;
+    }
+}
+
+extern "C" peel_status iblt_subtract(peel_iblt *a, const peel_iblt *b, void *stream) {
+    if (!a || !b || a->C != b->C || a->r != b->r || a->seed != b->seed || a->subt != b->subt) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    prof_begin_call();
+    {
+        ProfScope ps("iblt_subtract", s);
+        iblt_subtract_kernel<<<grid_for(a->C), 256, 0, s>>>((Cell *)(a->mem + a->L.cells),
+                                                           (const Cell *)(b->mem + b->L.cells), a->C);
+    }
+    PEEL_CUDA(cudaGetLastError());
     return PEEL_OK;
 }
 

@@ -155,3 +155,47 @@ def test_subtable_table3_shape():
         o.insert(O.gen_keys(N, 3))
         ref = o.peel_subtables(cap_keys=N + 1)
         assert res.rounds == ref.rounds and res.nrecovered == ref.keys.size and res.complete == ref.complete
+
+
+# ---- set difference -------------------------------------------------
+@pytest.mark.parametrize("r", [3, 4])
+@pytest.mark.parametrize("diff", [100, 9000, 16000])
+def test_set_difference_vs_oracle(r, diff):
+    C = 30011
+    common = synth.random_keys(150000, 21)
+    only_a = synth.random_keys(diff, 22)
+    only_b = synth.random_keys(diff, 23)
+    ka, kb = np.concatenate([common, only_a]), np.concatenate([only_b, common])
+    ga, gb = pk.Iblt(C, r, 6, device=DEV), pk.Iblt(C, r, 6, device=DEV)
+    oa, ob = O.Iblt(C, r, 6), O.Iblt(C, r, 6)
+    ga.insert(keys_dev(ka)); gb.insert(keys_dev(kb))
+    oa.insert(ka); ob.insert(kb)
+    ga.subtract(gb)
+    oa.subtract(ob)
+    cnt, ks, hs = dev_cells(ga)
+    ocnt, oks, ohs = oa.cells()
+    assert np.array_equal(cnt.astype(np.int32), ocnt.astype(np.int32)) and np.array_equal(ks, oks)
+    assert np.array_equal(hs, ohs)
+    res, sg = ga.peel_signed()
+    ref, osg = oa.peel_signed()
+    assert res.rounds == ref.rounds and res.per_round.tolist() == ref.per_round.tolist()
+    assert res.complete == ref.complete
+    got = sorted(zip(res.keys.cpu().numpy().view(np.uint64).tolist(), sg.cpu().numpy().tolist()))
+    exp = sorted(zip(ref.keys.tolist(), osg.tolist()))
+    assert got == exp
+    if res.complete:
+        kk = res.keys.cpu().numpy().view(np.uint64)
+        s_ = sg.cpu().numpy()
+        assert np.array_equal(np.sort(kk[s_ == 1]), np.sort(only_a))
+        assert np.array_equal(np.sort(kk[s_ == -1]), np.sort(only_b))
+
+
+def test_signed_peel_on_insert_only_equals_plain():
+    C, r = 100003, 3
+    keys = O.gen_keys(75000, 7)
+    a, b = pk.Iblt(C, r, 1, device=DEV), pk.Iblt(C, r, 1, device=DEV)
+    a.insert(keys_dev(keys)); b.insert(keys_dev(keys))
+    pa = a.peel()
+    pb, sg = b.peel_signed()
+    assert pa.rounds == pb.rounds and pa.per_round.tolist() == pb.per_round.tolist()
+    assert bool((sg == 1).all())

@@ -730,10 +730,14 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
 
 // phase D: apply the round's decrements bin-major; work items of DCH entries are taken in
 // bin order from a global counter, so the blocks in flight share one or two bins (L2-resident).
+// a small crossing queue (<= DCH / PEEL_BLOCK pushes per thread per work item; overflow
+// falls back to global appends): less shared memory, more resident blocks, more atomics in flight
+typedef BlockQueueT<uint2, 2 * PEEL_BLOCK, PEEL_BLOCK> ApplyQ;
+
 __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, BinRound br) {
     extern __shared__ unsigned char smem_raw[];
     uint32_t *pre = (uint32_t *)smem_raw;  // [nbins + 1] prefix of work items per bin
-    __shared__ BlockQueue<uint2> q;
+    __shared__ ApplyQ q;
     __shared__ ull item;
     Ctl *ctl = a.ctl;
     const uint32_t t = br.t, nbins = br.nbins, k = a.k;

@@ -514,6 +514,8 @@ static peel_status run_iblt_peel(peel_iblt *t, IPeelArgs &a, bool sgn, cudaStrea
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, IB_BLOCK, 0));
     if (per_sm < 1) per_sm = 1;
     unsigned grid = (unsigned)(num_sms() * per_sm);
+    const ull want = (t->C + IB_BLOCK - 1) / IB_BLOCK;  // small tables: cheaper grid barriers
+    if (want < grid) grid = (unsigned)(want < (ull)num_sms() ? num_sms() : want);
     void *args[] = {&a};
     ProfScope ps(t->subt ? "iblt_subtable_peel" : (sgn ? "iblt_peel_signed_rounds" : "iblt_peel_rounds"), s);
     PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, IB_BLOCK, args, 0, s));

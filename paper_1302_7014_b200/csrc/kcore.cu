@@ -1342,6 +1342,9 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PEEL_BLOCK, 0));
     if (per_sm < 1) per_sm = 1;
     unsigned grid = (unsigned)(num_sms() * per_sm);
+    // small instances: no more blocks than one CHUNK of vertices each (cheaper grid barriers)
+    const uint64_t want = (n + CHUNK - 1) / CHUNK;
+    if (want < grid) grid = (unsigned)(want < (uint64_t)num_sms() ? num_sms() : want);
     void *args[] = {&a};
     {
         ProfScope ps(csr ? "peel_rounds_csr" : (subr ? "peel_subrounds" : "peel_rounds_packed"), s);

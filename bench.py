@@ -556,6 +556,22 @@ def main():
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
                 "alg_bytes_per_launch": alg, "avg_launch_ms": round(avg_ms, 4)}
+    # Supplementary roof for the persistent round kernel: the time its random DRAM operations
+    # need at the rates measured on this pool (microbench/membench.cu, profiles/r01_membench.jsonl:
+    # 8 B random read-modify-write 20.1 G/s, 8 B random gather 37.1 G/s, 4 B test-and-clear on a
+    # ~100 MB bitmap 55.3 G/s).  Per round t >= nb+1: |F_t| entries (one test-and-clear each; for
+    # t >= 2 every frontier vertex has an entry), killed_t edge gathers, (r-1) killed_t RMWs.
+    rand = None
+    if k <= 2 and "peel_rounds_packed" in per_kernel:
+        first = max(nb, 1)
+        E = sum(F[first:])
+        Kt = sum(kl[nb:])
+        floor_ms = 1e3 * (Kt * (r - 1) / 20.1e9 + Kt / 37.1e9 + E / 55.3e9)
+        ms_k = per_kernel["peel_rounds_packed"][0] / per_kernel["peel_rounds_packed"][1]
+        rand = {"kernel": "peel_rounds_packed", "random_rmw": Kt * (r - 1), "random_gathers": Kt,
+                "bitmap_test_and_clear": E, "floor_ms_at_measured_random_rates": round(floor_ms, 3),
+                "kernel_ms": round(ms_k, 3), "frac": round(floor_ms / ms_k, 4),
+                "rates_source": "profiles/r01_membench.jsonl (B200, this pool)"}
     step_alg = b_build + b_rounds
     kernels = {nm: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
                for nm, v in per_kernel.items()}
@@ -610,7 +626,7 @@ def main():
             "hbm_roofline_step": {"alg_bytes": step_alg, "frac_of_measured": round(step_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
                                   "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},
             "roofline": roof, "kernels": kernels, "round_ms": round_ms,
-            "kernel_alg_bytes": kb, "cpu_baseline": cpu, "e2e": e2e,
+            "kernel_alg_bytes": kb, "random_access_roofline": rand, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -29,7 +29,6 @@ namespace peel {
 
 static constexpr int DB = 256;            // block size
 static constexpr int DQ = 2 * DB;         // block-queue capacity
-static constexpr uint32_t DSTAT_CAP = 65536;
 
 struct DCtl {
     ull nf[2];      // |F_t| local, double-buffered by round parity

@@ -1223,6 +1223,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         uint32_t *adj = (uint32_t *)(ws + L.adj);
         PEEL_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * n, s));
         const bool binned = L.nbins > 0 && m > 0;
+        bool scatter_from_bins = false;
         ull *cursor = (ull *)(ws + L.bin_cursor), *bbase = (ull *)(ws + L.bin_base), *bcap = (ull *)(ws + L.bin_cap);
         ull *entries = (ull *)(ws + L.entries);
         uint64_t maxcap = 0;
@@ -1257,7 +1258,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                 ProfScope ps("build_deg", s);
                 build_deg_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, deg, ctl);
             }
-            a.f1_ready = h.binovf ? 0 : 1;  // reused below as "scatter from bins"
+            scatter_from_bins = !h.binovf;
         } else if (m) {
             ProfScope ps("build_deg", s);
             build_deg_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, deg, ctl);
@@ -1275,14 +1276,13 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             ProfScope ps("scan_add", s);
             scan_add_kernel<<<grid_for(n), PEEL_BLOCK, 0, s>>>(off, n, bsum);
         }
-        if (binned && a.f1_ready) {
+        if (scatter_from_bins) {
             ProfScope ps("csr_bin_scatter", s);
             csr_bin_scatter_kernel<<<bgrid, 256, 0, s>>>(entries, bbase, cursor, off, adj);
         } else if (m) {
             ProfScope ps("scatter", s);
             scatter_kernel<R><<<grid_for(m), 256, 0, s>>>(edges, n, m, off, adj);
         }
-        a.f1_ready = 0;
         a.deg = deg; a.off_end = off; a.adj = adj;
     }
     PEEL_CUDA(cudaGetLastError());

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpeel.so")
+LIB_PATH = os.environ.get("PEEL_LIB") or os.path.join(_PKG, "libpeel.so")  # PEEL_LIB: A/B builds
 
 PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOVERFLOW = range(7)
 PEEL_FLAG_CSR = 1

@@ -1130,15 +1130,19 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
     write_core_mask<true>(a, tid, nthr);
 }
 
-// frontier-size threshold (fraction of n) above which a round runs binned; PEEL_BIN_ROUND_FRAC
-// overrides (0 disables) for A/B measurement
-static double bin_round_frac() {
-    static double f = -1.0;
-    if (f < 0.0) {
+// frontier-size threshold (fraction of n) above which a round runs binned.  A binned round
+// streams the whole 8n-byte state through L2 once; a persistent round pays one random DRAM
+// read-modify-write per decrement, whose L2 hit rate falls as 8n outgrows the L2.  Measured
+// on B200: n = 10^9 is fastest at 0.02 (0.03..0.006 within noise, 0.05 is
+// +6.8 ms), n = 10^8 at 0.05 (0.02 is +0.3 ms).  PEEL_BIN_ROUND_FRAC overrides (0 disables).
+static double bin_round_frac(uint64_t n) {
+    static double f = -2.0;
+    if (f == -2.0) {
         const char *e = getenv("PEEL_BIN_ROUND_FRAC");
-        f = e ? atof(e) : 0.05;
+        f = e ? atof(e) : -1.0;
     }
-    return f;
+    if (f >= 0.0) return f;
+    return 8.0 * (double)n >= 2e9 ? 0.02 : 0.05;
 }
 
 static unsigned grid_for(uint64_t work, int per_sm = 16) {
@@ -1289,7 +1293,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
 
     // binned rounds while the frontier is a large fraction of n (see round_apply_kernel)
     a.t0 = 1;
-    if (!csr && !subr && L.nbins && bin_round_frac() > 0.0) {
+    if (!csr && !subr && L.nbins && bin_round_frac(n) > 0.0) {
         ull *cursor = (ull *)(ws + L.bin_cursor);
         BinRound br;
         br.nbins = (uint32_t)L.nbins;
@@ -1313,7 +1317,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             PEEL_CUDA(cudaStreamSynchronize(s));
             if (h.err) break;  // the persistent kernel reports it
             const ull nF = h.nf[(t - 1) % 3], nE = h.ne[(t - 1) % 3];
-            if (nF == 0 || (double)nE < bin_round_frac() * (double)n) break;
+            if (nF == 0 || (double)nE < bin_round_frac(n) * (double)n) break;
             PEEL_CUDA(cudaMemsetAsync(cursor, 0, sizeof(ull) * L.nbins, s));
             PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
             br.t = t;

@@ -1316,6 +1316,9 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
             PEEL_CUDA(cudaStreamSynchronize(s));
             if (h.err) break;  // the persistent kernel reports it
+            // an overflowed build bin bounds nothing: a round's decrements of bin b are a
+            // subset of the build's entries of bin b, which did not fit its capacity
+            if (h.binovf) break;
             const ull nF = h.nf[(t - 1) % 3], nE = h.ne[(t - 1) % 3];
             if (nF == 0 || (double)nE < bin_round_frac(n) * (double)n) break;
             PEEL_CUDA(cudaMemsetAsync(cursor, 0, sizeof(ull) * L.nbins, s));

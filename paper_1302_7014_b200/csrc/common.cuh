@@ -56,6 +56,65 @@ peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, 
 // device helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ ull ld_cg_u64(const ull *p) { return __ldcg(p); }
+
+// The R vertex ids of edge e, read with the 16-byte vector loads that cover the row
+// (R = 3: two 8-byte loads; R = 2, 4: one load) instead of R scalar loads: measured with
+// ncu, the scalar loads of one random row reach L2 as separate requests and miss separately
+// (DRAM reads 2x the rows' granules).  vec: edges is 16-byte aligned; m R words in total.
+template <int R>
+__device__ __forceinline__ void load_row(const uint32_t *__restrict__ edges, uint64_t e, uint64_t m, bool vec,
+                                         uint32_t (&u)[R]) {
+    const uint64_t w0 = e * R;
+    const uint64_t end = m * R;  // words in the array
+    if (R == 3 && vec && (w0 | 1) + 3 <= end) {  // two 8-byte loads, branch-free
+        const uint2 *p2 = reinterpret_cast<const uint2 *>(edges) + (w0 >> 1);
+        const uint2 x = __ldg(p2), y = __ldg(p2 + 1);
+        const bool odd = (w0 & 1) != 0;
+        u[0] = odd ? x.y : x.x;
+        u[1 % R] = odd ? y.x : x.y;
+        u[2 % R] = odd ? y.y : y.x;
+        return;
+    }
+    if (R == 2 && vec) {  // rows are 8-byte aligned
+        const uint2 x = __ldg(reinterpret_cast<const uint2 *>(edges) + (w0 >> 1));
+        u[0] = x.x;
+        u[1 % R] = x.y;
+        return;
+    }
+    const uint64_t q0 = w0 >> 2, q1 = (w0 + R - 1) >> 2;  // first / last 16-byte window
+    if (R <= 3 || !vec || (q1 + 1) * 4 > end) {             // unaligned array, or a window past its end
+        #pragma unroll
+        for (int j = 0; j < R; j++) u[j] = __ldg(edges + w0 + j);
+        return;
+    }
+    constexpr int NQ = (R + 6) / 4;  // windows a row can span
+    uint32_t w[4 * NQ];
+    const uint4 *p = reinterpret_cast<const uint4 *>(edges);
+    #pragma unroll
+    for (int i = 0; i < NQ; i++) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (i == 0 || q0 + i <= q1) v = __ldg(p + q0 + i);
+        w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+    }
+    switch ((uint32_t)(w0 & 3)) {  // constant register indices in every case
+        case 0:
+            #pragma unroll
+            for (int j = 0; j < R; j++) u[j] = w[j];
+            break;
+        case 1:
+            #pragma unroll
+            for (int j = 0; j < R; j++) u[j] = w[j + 1];
+            break;
+        case 2:
+            #pragma unroll
+            for (int j = 0; j < R; j++) u[j] = w[j + 2];
+            break;
+        default:
+            #pragma unroll
+            for (int j = 0; j < R; j++) u[j] = w[j + 3];
+            break;
+    }
+}
 __device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t *p) { return __ldcg(p); }
 
 // SplitMix64 finalizer (Steele-Lea-Flood); the IBLT hash/checksum mixer.

@@ -152,7 +152,8 @@ __device__ __forceinline__ void dist_decrement(ull *state, uint64_t v0, uint32_t
 
 struct DKArgs {
     const uint32_t *edges;
-    uint64_t n;
+    uint64_t n, m;
+    int edges_vec;  // edges is 16-byte aligned (vector row loads)
     int P, p;
     uint32_t k;
     uint64_t v0, v1, nloc;
@@ -185,8 +186,9 @@ __global__ void __launch_bounds__(DB) dist_kill_kernel(DKArgs a) {
             if (atomicAnd(a.alive + (e >> 5), ~bit) & bit) {
                 uint32_t u[R];
                 uint32_t mn = 0xFFFFFFFFu;
+                load_row<R>(a.edges, e, a.m, a.edges_vec, u);
                 #pragma unroll
-                for (int j = 0; j < R; j++) { u[j] = __ldg(a.edges + (uint64_t)e * R + j); mn = min(mn, u[j]); }
+                for (int j = 0; j < R; j++) mn = min(mn, u[j]);
                 if (owner_of(mn, a.n, a.P) == a.p) kills++;
                 uint32_t sent_mask = 0;
                 #pragma unroll
@@ -228,8 +230,9 @@ __global__ void __launch_bounds__(DB) dist_recv_kernel(DKArgs a, const uint32_t 
             if (atomicAnd(a.alive + (e >> 5), ~bit) & bit) {
                 uint32_t mn = 0xFFFFFFFFu;
                 uint32_t u[R];
+                load_row<R>(a.edges, e, a.m, a.edges_vec, u);
                 #pragma unroll
-                for (int j = 0; j < R; j++) { u[j] = __ldg(a.edges + (uint64_t)e * R + j); mn = min(mn, u[j]); }
+                for (int j = 0; j < R; j++) mn = min(mn, u[j]);
                 if (owner_of(mn, a.n, a.P) == a.p) kills++;
                 #pragma unroll
                 for (int j = 0; j < R; j++)
@@ -425,7 +428,8 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         for (size_t i = 0; i < sh.size(); i++) {
             DShard &d = sh[i];
             DKArgs a;
-            a.edges = edges; a.n = n; a.P = P; a.p = d.q; a.k = k;
+            a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
+            a.edges_vec = ((uintptr_t)edges & 15) == 0;
             a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
             a.state = d.state; a.alive = d.alive;
             a.Fc = d.F[cur]; a.nE = hc[i].ne[cur]; a.Fn = d.F[nxt];
@@ -490,7 +494,8 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             DShard &d = sh[i];
             if (!nrecv[i]) continue;
             DKArgs a;
-            a.edges = edges; a.n = n; a.P = P; a.p = d.q; a.k = k;
+            a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
+            a.edges_vec = ((uintptr_t)edges & 15) == 0;
             a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
             a.state = d.state; a.alive = d.alive;
             a.Fc = nullptr; a.nE = 0; a.Fn = d.F[nxt];

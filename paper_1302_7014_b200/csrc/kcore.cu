@@ -447,6 +447,7 @@ struct PeelArgs {
     uint8_t *core_mask;
     uint32_t *peel_round;
     int mask_vec;            // core_mask is 16-byte aligned
+    int edges_vec;           // edges is 16-byte aligned (vector row loads)
     int f1_ready;            // packed: F_1 was emitted by the binned build
     uint32_t t0;             // first round run by the persistent kernel (earlier rounds were binned)
     uint32_t r;              // subround mode: number of vertex classes (= r)
@@ -646,8 +647,7 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
             if (win[j]) {
                 kills++;
                 mine += R - 1;
-                #pragma unroll
-                for (int r = 0; r < R; r++) ue[j][r] = __ldg(a.edges + (uint64_t)ent[j].y * R + r);
+                load_row<R>(a.edges, ent[j].y, a.m, a.edges_vec, ue[j]);
             }
         // block exclusive scan of per-thread decrement counts -> staging positions
         uint32_t x = mine;
@@ -863,8 +863,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
             #pragma unroll
             for (int j = 0; j < U; j++)
                 if (win[j]) {
-                    #pragma unroll
-                    for (int r = 0; r < R; r++) ue[j][r] = __ldg(a.edges + (uint64_t)ent[j].y * R + r);
+                    load_row<R>(a.edges, ent[j].y, a.m, a.edges_vec, ue[j]);
                 }
             #pragma unroll
             for (int j = 0; j < U; j++)
@@ -990,9 +989,11 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_subround_kernel(PeelArgs a) {
                         if (atomicAnd(a.alive + (e >> 5), ~bit) & bit) {
                             kills++;
                             const ull dec = 0ull - (((ull)e << 32) + 1ull);
+                            uint32_t row[R];
+                            load_row<R>(a.edges, e, a.m, a.edges_vec, row);
                             #pragma unroll
                             for (int q2 = 0; q2 < R; q2++) {
-                                const uint32_t u = __ldg(a.edges + (uint64_t)e * R + q2);
+                                const uint32_t u = row[q2];
                                 if (u == ent.x) continue;
                                 const ull old = atomicAdd(a.state + u, dec);
                                 if (count_of(old) == k) {
@@ -1104,9 +1105,11 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
                     if (!(ld_cg_u32(a.alive + (e >> 5)) & bit)) continue;
                     if (!(atomicAnd(a.alive + (e >> 5), ~bit) & bit)) continue;
                     kills++;
+                    uint32_t row[R];
+                    load_row<R>(a.edges, e, a.m, a.edges_vec, row);
                     #pragma unroll
                     for (int r = 0; r < R; r++) {
-                        const uint32_t u = __ldg(a.edges + (uint64_t)e * R + r);
+                        const uint32_t u = row[r];
                         if (u == v) continue;
                         const uint32_t old = atomicSub(a.deg + u, 1u);
                         if (old == k) {
@@ -1177,6 +1180,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     a.rtime = (ull *)(ws + L.rtime);
     a.core_mask = core_mask; a.peel_round = peel_round;
     a.mask_vec = ((uintptr_t)core_mask & 15) == 0;
+    a.edges_vec = ((uintptr_t)edges & 15) == 0;
     if (peel_round) PEEL_CUDA(cudaMemsetAsync(peel_round, 0, sizeof(uint32_t) * n, s));
 
     if (!csr && L.nbins) {

@@ -588,7 +588,10 @@ __global__ void __launch_bounds__(PEEL_BLOCK) bin_accumulate_kernel(PeelArgs a, 
 // kernel, so the schedule is unchanged.
 static constexpr int KU = 4;                      // frontier entries per thread per K iteration
 static constexpr int KCH = PART_BLOCK * KU;       // entries per block iteration
-static constexpr int DCH = 512;                   // decrement entries per D work item (in-flight window ~ one bin)
+#ifndef PEEL_DCH
+#define PEEL_DCH 512
+#endif
+static constexpr int DCH = PEEL_DCH;                  // decrement entries per D work item (in-flight window ~ one bin)
 
 struct BinRound {
     uint32_t nbins;
@@ -783,16 +786,29 @@ __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, Bin
         const ull *ent = br.entries + br.base[b] + (ull)j * DCH;
         const uint32_t nin = (uint32_t)min((ull)DCH, cnt - (ull)j * DCH);
         ull *st = a.state + ((uint64_t)b << BIN_SHIFT);
-        for (uint32_t i = threadIdx.x; i < nin; i += PEEL_BLOCK) {
-            const ull x = __ldcs(ent + i);
-            const uint32_t e = (uint32_t)(x >> 32);
-            const uint32_t ul = (uint32_t)(x & mask);
-            const ull old = atomicAdd(st + ul, 0ull - (((ull)e << 32) + 1ull));
-            if (count_of(old) == k) {
+        // all DU entries of a thread are loaded and their returning atomics issued before any
+        // result is used: DU atomics in flight per thread
+        constexpr int DU = DCH / PEEL_BLOCK;
+        ull x[DU], old[DU];
+        #pragma unroll
+        for (int r = 0; r < DU; r++) {
+            const uint32_t i = threadIdx.x + r * PEEL_BLOCK;
+            x[r] = i < nin ? __ldcs(ent + i) : 0ull;
+        }
+        #pragma unroll
+        for (int r = 0; r < DU; r++) {
+            const uint32_t i = threadIdx.x + r * PEEL_BLOCK;
+            old[r] = 0;
+            if (i < nin) old[r] = atomicAdd(st + (x[r] & mask), 0ull - ((x[r] & ~0xFFFFFFFFull) + 1ull));
+        }
+        #pragma unroll
+        for (int r = 0; r < DU; r++) {
+            const uint32_t i = threadIdx.x + r * PEEL_BLOCK;
+            if (i < nin && count_of(old[r]) == k) {
                 crossed++;
-                const uint32_t u = (b << BIN_SHIFT) + ul;
+                const uint32_t u = (b << BIN_SHIFT) + (uint32_t)(x[r] & mask);
                 if (a.peel_round) a.peel_round[u] = t + 1;
-                bq_push(q, slot, make_uint2(u, idsum_of(old) - e), Fn, cn);
+                bq_push(q, slot, make_uint2(u, idsum_of(old[r]) - (uint32_t)(x[r] >> 32)), Fn, cn);
             }
         }
         bq_flush(q, slot, Fn, cn);
@@ -1314,6 +1330,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
         kb = kb < 1 ? 1 : kb;
         db = db < 1 ? 1 : db;
+        if (const char *ev = getenv("PEEL_D_BPS")) db = std::min(db, std::max(1, atoi(ev)));
         uint32_t t = 1;
         for (;;) {
             Ctl h;

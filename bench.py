@@ -109,6 +109,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(config, kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture of
+    this config (profiles/r01_traffic_<config>.json, tools/ncu_traffic.py), else None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))
+    except Exception:
+        return None, None
+    kname = kernel.replace("peel_rounds_packed", "peel_packed")
+    k = d.get("kernels", {}).get(kname)
+    if not k:
+        return None, None
+    return int(k["traffic_per_launch"]), f"profiles/r01_traffic_{config}.json (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -433,7 +447,7 @@ def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barri
                 "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
         print(json.dumps(line), flush=True)
     del comm
-    if ws > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
@@ -468,7 +482,12 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    if ws > 1 or (args.mode == "dist" and not args.virtual_shards):
+        # --mode dist at N=1 runs the NCCL transport with world size 1 (plain or torchrun)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(ws))
         dist.init_process_group("nccl", device_id=dev)
     kind, n, m, r, k, seed, text = CONFIGS[args.config]
     seed = seed + rank  # independent instance per rank (weak scaling)
@@ -483,7 +502,7 @@ def main():
         return run_iblt(args, pk, dev, ws, rank, local, n, m, r, seed, text, barrier, stream)
     if kind == "sweep":
         return run_sweep_bench(args, pk, dev, ws, rank, local, n, m, r, k, text, barrier, stream)
-    use_dist = args.virtual_shards > 0 or (ws > 1 and k <= 2 and args.mode in ("auto", "dist"))
+    use_dist = args.virtual_shards > 0 or (k <= 2 and (args.mode == "dist" or (ws > 1 and args.mode == "auto")))
     if use_dist:
         return run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed - rank, text, barrier, stream)
 
@@ -578,8 +597,9 @@ def main():
             alg = b_build + b_rounds
             avg_ms = sum(v[0] for v in per_kernel.values()) / args.steps
         ach = alg / (avg_ms / 1e3) / 1e9
+        traffic, tsrc = ncu_traffic(args.config, name)
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
+                "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
                 "alg_bytes_per_launch": alg, "avg_launch_ms": round(avg_ms, 4)}
     # Supplementary roof for the persistent round kernel: the time its random DRAM operations
     # need at the rates measured on this pool (microbench/membench.cu, profiles/r01_membench.jsonl:

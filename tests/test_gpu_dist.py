@@ -55,3 +55,42 @@ def test_full_c3_shape_matches_single_gpu(goldens):
     assert res.survivors[:4].tolist() == g["survivors_head"] and res.killed[-4:].tolist() == g["killed_tail"]
     pk._ws_cache.clear()
     torch.cuda.empty_cache()
+
+
+NCCL_WORLD1 = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["REPO"]); sys.path.insert(0, os.path.join(os.environ["REPO"], "tests"))
+import paper_1302_7014_b200 as pk
+from oracle import oracle as O
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%s" % os.environ["PORT"], rank=0, world_size=1,
+                        device_id=torch.device("cuda:0"))
+comm = pk.Comm.from_process_group()
+for (n, c, r, seed) in [(100003, 0.75, 3, 5), (50021, 0.85, 3, 6), (40009, 0.8, 4, 7)]:
+    e = O.gen_hypergraph(n, int(c * n), r, seed)
+    ref = O.sync_peel(e, n, 2)
+    res = pk.peel_kcore_dist(comm, torch.from_numpy(e.view(np.int32)).cuda(), n, 2)
+    assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist()
+    assert res.killed.tolist() == ref.killed.tolist()
+    assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
+del comm
+dist.destroy_process_group()
+print("NCCL_OK")
+"""
+
+
+def test_nccl_transport_world1():
+    """The real NCCL transport (unique id broadcast over a torch.distributed NCCL group,
+    ncclCommInitRank, the per-round allgather / allreduce / grouped send-recv) at world
+    size 1: the only size one GPU allows.  Same results as the oracle."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, REPO=repo, PORT=str(port))
+    out = subprocess.run([sys.executable, "-c", NCCL_WORLD1], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "NCCL_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]

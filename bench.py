@@ -273,6 +273,7 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
     e1.record(stream)
     barrier()
     clocks = clk.stop()
+    round_ms = [round(x, 4) for x in pk.profile_rounds()]
     pk.profile_enable(False)
     ms_total = e0.elapsed_time(e1)
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
@@ -294,6 +295,37 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
             "frac": round(ach / hbm, 4), "traffic": None, "alg_bytes_per_launch": alg,
             "avg_launch_ms": round(ms_sum / nl, 4),
             "note": "160 MB table ~ L2-sized: L2-atomic/latency bound, HBM roofline is a loose bound"}
+    # e2e through the public API: pinned host keys -> device, insert, recover, recovered keys -> host
+    e2e = None
+    if not args.no_e2e:
+        k_host = torch.empty((N,), dtype=torch.int64, pin_memory=True)
+        k_host.copy_(keys)
+        o_host = torch.empty((N,), dtype=torch.int64, pin_memory=True)
+        k_dev = torch.empty_like(keys)
+
+        def e2e_step():
+            k_dev.copy_(k_host, non_blocking=True)
+            tb.reset()
+            tb.insert(k_dev)
+            rr = tb.peel(cap_keys=N, out=out)
+            o_host[:rr.nrecovered].copy_(out[:rr.nrecovered], non_blocking=True)
+            return rr
+        e2e_step()
+        barrier()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(args.e2e_steps):
+            rr = e2e_step()
+        h1.record(stream)
+        barrier()
+        te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        assert rr.complete and rr.nrecovered == N
+        e2e = {"value": float(rr.nrecovered) * ws * args.e2e_steps / (te.item() / 1e3), "unit": "keys/s",
+               "h2d_bytes_per_step": 8 * N, "d2h_bytes_per_step": 8 * int(rr.nrecovered), "steps": args.e2e_steps,
+               "api": "Iblt.reset/insert/peel (C-ABI iblt_insert / iblt_peel), pinned host keys in, recovered keys out"}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
@@ -320,7 +352,7 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
             "paper_context": "Tesla C2070, 2^24 cells, r=3, load 0.75: recovery 0.33 s + insert 0.31 s (P:539)",
             "roofline": roof,
             "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 4)} for k, v in per_kernel.items()},
-            "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches, "clocks": clocks,
+            "round_ms": round_ms, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -57,6 +57,13 @@ peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ ull ld_cg_u64(const ull *p) { return __ldcg(p); }
 
+// %globaltimer (ns): per-round device timestamps for profiling
+__device__ __forceinline__ ull globaltimer() {
+    ull t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // The R vertex ids of edge e, read with the 16-byte vector loads that cover the row
 // (R = 3: two 8-byte loads; R = 2, 4: one load) instead of R scalar loads: measured with
 // ncu, the scalar loads of one random row reach L2 as separate requests and miss separately

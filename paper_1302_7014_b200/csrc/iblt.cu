@@ -21,6 +21,8 @@
 //   stop      at the first round with an empty frontier.
 #include <string.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace peel {
@@ -46,7 +48,7 @@ struct IbltCtl {
 };
 
 struct ILayout {
-    size_t cells, ctl, per_round, pure0, pure1, cand, F0, F1, clist, total;
+    size_t cells, ctl, per_round, rtime, pure0, pure1, cand, F0, F1, clist, total;
 };
 
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -57,6 +59,7 @@ static ILayout ilayout(uint64_t C) {
     L.cells = o; o += al(sizeof(Cell) * C);
     L.ctl = o; o += al(sizeof(IbltCtl));
     L.per_round = o; o += al(sizeof(ull) * (ISTAT_CAP + 1));
+    L.rtime = o; o += al(sizeof(ull) * (ISTAT_CAP + 2));  // %globaltimer at each round start (profiling)
     L.pure0 = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
     L.pure1 = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
     L.cand = o; o += al(sizeof(uint32_t) * ((C + 31) / 32));
@@ -111,10 +114,13 @@ __device__ __forceinline__ Cell ld_cell_cg(const Cell *p) {
     return c;
 }
 
+// one pass of an insert/delete: the r cells of every key, restricted to cells in [lo, hi)
+// (a table larger than ~half the L2 is updated in several passes over the keys, each
+// pass's cell range L2-resident)
 template <int R>
 __global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ull seed_h, ull seed_c,
                                                           const ull *__restrict__ keys, ull nkeys,
-                                                          uint32_t delta, bool subt) {
+                                                          uint32_t delta, bool subt, uint32_t lo, uint32_t hi) {
     for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
         const ull x = __ldg(keys + i);
         uint32_t c[R];
@@ -122,6 +128,7 @@ __global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ul
         const uint32_t h = checksum(x, seed_c);
         #pragma unroll
         for (int j = 0; j < R; j++) {
+            if (c[j] < lo || c[j] >= hi) continue;
             Cell *p = cells + c[j];
             atomicAdd(&p->count, delta);
             atomicXor(&p->keySum, x);
@@ -146,6 +153,7 @@ struct IPeelArgs {
     ull C, seed_h, seed_c;
     IbltCtl *ctl;
     ull *per_round;
+    ull *rtime;
     uint32_t *pure[2];  // round-start pure bitmaps: F_t's bits live in pure[(t-1)&1]
     uint32_t *cand;
     ulonglong2 *F[2];   // frontier entries (cell, key snapshot)
@@ -213,7 +221,10 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
     for (;;) {
         const ull nF = ld_cg_u64(&ctl->fcnt[(t - 1) % 3]);
         if (nF == 0) break;
-        if (tid == 0) ctl->fcnt[(t + 1) % 3] = 0;
+        if (tid == 0) {
+            ctl->fcnt[(t + 1) % 3] = 0;
+            if (t <= ISTAT_CAP) a.rtime[t - 1] = globaltimer();
+        }
         const ulonglong2 *Fc = a.F[(t - 1) & 1];
         ull *ccnt = &ctl->ccnt[t & 1];
         const uint32_t *pure_cur = a.pure[(t - 1) & 1];
@@ -287,7 +298,10 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
         grid.sync();
         t++;
     }
-    if (tid == 0) ctl->rounds = t - 1;
+    if (tid == 0) {
+        ctl->rounds = t - 1;
+        if (t <= ISTAT_CAP) a.rtime[t - 1] = globaltimer();
+    }
     // ---- complete iff every cell is zero ----
     uint32_t nz = 0;
     for (ull c = tid; c < a.C; c += nthr) {
@@ -482,16 +496,21 @@ static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkey
     prof_begin_call();
     Cell *cells = (Cell *)(t->mem + t->L.cells);
     unsigned g = grid_for(nkeys);
-    {
-        ProfScope ps(delta == 1u ? "iblt_insert" : "iblt_delete", s);
+#ifndef PEEL_IBLT_PASS_BYTES
+#define PEEL_IBLT_PASS_BYTES (64ull << 20)
+#endif
+    const uint64_t npass = (t->C * sizeof(Cell) + PEEL_IBLT_PASS_BYTES - 1) / PEEL_IBLT_PASS_BYTES;
+    ProfScope ps(delta == 1u ? "iblt_insert" : "iblt_delete", s);
+    for (uint64_t q = 0; q < npass; q++) {
+        const uint32_t lo = (uint32_t)(q * t->C / npass), hi = (uint32_t)((q + 1) * t->C / npass);
         switch (t->r) {
-            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
-            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
-            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
-            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
-            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
-            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
-            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt); break;
+            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
         }
     }
     PEEL_CUDA(cudaGetLastError());
@@ -542,6 +561,7 @@ static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_
     a.seed_c = t->seed_c;
     a.ctl = (IbltCtl *)(m + L.ctl);
     a.per_round = (ull *)(m + L.per_round);
+    a.rtime = (ull *)(m + L.rtime);
     a.pure[0] = (uint32_t *)(m + L.pure0);
     a.pure[1] = (uint32_t *)(m + L.pure1);
     a.cand = (uint32_t *)(m + L.cand);
@@ -567,6 +587,14 @@ static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_
     PEEL_CUDA(cudaMemcpyAsync(&h, a.ctl, sizeof h, cudaMemcpyDeviceToHost, s));
     PEEL_CUDA(cudaStreamSynchronize(s));
     prof_collect();
+    if (prof_enabled() && !t->subt && h.rounds) {
+        const uint64_t nt = (h.rounds < ISTAT_CAP ? h.rounds : ISTAT_CAP - 1) + 1;
+        std::vector<ull> rt(nt);
+        PEEL_CUDA(cudaMemcpy(rt.data(), a.rtime, sizeof(ull) * nt, cudaMemcpyDeviceToHost));
+        std::vector<double> ms(nt - 1);
+        for (uint64_t i = 0; i + 1 < nt; i++) ms[i] = (rt[i + 1] - rt[i]) * 1e-6;
+        prof_set_rounds(ms);
+    }
     *nrecovered = h.nrec;
     *rounds = (uint32_t)h.rounds;
     if (complete) *complete = h.nonzero ? 0 : 1;

@@ -466,12 +466,6 @@ struct PeelArgs {
     ull *rtime;              // %globaltimer at the start of each round (profiling)
 };
 
-__device__ __forceinline__ ull globaltimer() {
-    ull t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
 __device__ __forceinline__ uint32_t count_of(ull w) { return (uint32_t)w; }
 __device__ __forceinline__ uint32_t idsum_of(ull w) { return (uint32_t)(w >> 32); }
 

@@ -54,7 +54,7 @@ struct Ctl {
 };
 
 struct Layout {
-    size_t ctl, sub, fsize, killed, rtime, state, deg, off, bsum, adj, alive, F0, F1;
+    size_t ctl, stats, sub, rtime, state, deg, off, bsum, adj, alive, F0, F1;
     size_t bins, bin_cursor, bin_base, bin_cap, entries;  // binned build (packed, n > BIN_MIN_N)
     uint64_t nbins, total_cap;
     size_t total;
@@ -84,9 +84,10 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     Layout L;
     size_t o = 0;
     L.ctl = o; o += al(sizeof(Ctl));
+    // per-round (|F_t|, killed_t) pairs right after the control block: one small copy brings
+    // back the control block and the first STAT_HEAD rounds' statistics
+    L.stats = o; o += al(2 * sizeof(ull) * (STAT_CAP + 1));
     L.sub = o; o += al(sizeof(ull) * 64);  // subround mode: per-class list counters
-    L.fsize = o; o += al(sizeof(ull) * (STAT_CAP + 1));
-    L.killed = o; o += al(sizeof(ull) * (STAT_CAP + 1));
     L.rtime = o; o += al(sizeof(ull) * (STAT_CAP + 2));
     const size_t fe = csr ? sizeof(uint32_t) : sizeof(uint2);  // frontier element: v, or (v, e)
     if (!csr) {
@@ -452,8 +453,7 @@ struct PeelArgs {
     uint32_t *alive;
     void *F[2];              // packed: uint2 (v, e) entries; CSR: u32 vertices
     Ctl *ctl;
-    ull *fsize;
-    ull *killed;
+    ull *stats;              // [2 t] = |F_{t+1}|, [2 t + 1] = edges killed in round t+1
     uint8_t *core_mask;
     uint32_t *peel_round;
     int mask_vec;            // core_mask is 16-byte aligned
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
     const uint2 *Fc = (const uint2 *)a.F[(t - 1) & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
-        a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
+        a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap)] = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
         ctl->nf[(t + 1) % 3] = 0;
         ctl->ne[(t + 1) % 3] = 0;
     }
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
         }
         __syncthreads();
     }
-    block_add<PART_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
+    block_add<PART_BLOCK>(&a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap) + 1], kills);
 }
 
 static size_t kill_partition_smem(int r, uint32_t nbins) {
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
         const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
         if (tid == 0) {
             if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
-            a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
+            a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap)] = nF;
             ctl->nf[(t + 1) % 3] = 0;  // round t+2's counters; their last reader finished a barrier ago
             ctl->ne[(t + 1) % 3] = 0;
         }
@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
             bq_flush(q, slot, Fn, cn);
             slot ^= 1;
         }
-        block_add<PEEL_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
+        block_add<PEEL_BLOCK>(&a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap) + 1], kills);
         block_add<PEEL_BLOCK>(&ctl->nf[t % 3], crossed);
         grid.sync();
         t++;
@@ -987,7 +987,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_subround_kernel(PeelArgs a) {
             const ull nE = ld_cg_u64(&sub[(j * 2 + cur) * 2 + 1]);
             if (tid == 0) {
                 if (flat <= a.stat_cap) a.rtime[flat - 1] = globaltimer();
-                a.fsize[flat <= a.stat_cap ? flat - 1 : a.stat_cap] = nF;
+                a.stats[2 * (flat <= a.stat_cap ? flat - 1 : a.stat_cap)] = nF;
             }
             ull kills = 0;
             ull xc[R];  // crossings per class this subround
@@ -1047,7 +1047,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_subround_kernel(PeelArgs a) {
                     for (uint64_t i = tid; i < nE; i += nthr) a.peel_round[__ldcg(&Fc[i].x)] = flat;
                 }
             }
-            block_add<PEEL_BLOCK>(&a.killed[flat <= a.stat_cap ? flat - 1 : a.stat_cap], kills);
+            block_add<PEEL_BLOCK>(&a.stats[2 * (flat <= a.stat_cap ? flat - 1 : a.stat_cap) + 1], kills);
             #pragma unroll
             for (int c = 0; c < R; c++) {
                 const uint32_t b = (uint32_t)c == j ? (cb[c] ^ 1u) : cb[c];
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
         if (nF == 0) break;
         if (tid == 0) {
             if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
-            a.fsize[t <= a.stat_cap ? t - 1 : a.stat_cap] = nF;
+            a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap)] = nF;
             ctl->ne[(t + 1) % 3] = 0;
         }
         const uint32_t *Fc = (const uint32_t *)a.F[(t - 1) & 1];
@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
             bq_flush(q, slot, Fn, cn);
             slot ^= 1;
         }
-        block_add<PEEL_BLOCK>(&a.killed[t <= a.stat_cap ? t - 1 : a.stat_cap], kills);
+        block_add<PEEL_BLOCK>(&a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap) + 1], kills);
         grid.sync();
         t++;
     }
@@ -1183,8 +1183,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                              const Layout &L, cudaStream_t s) {
     const bool subr = (flags & PEEL_FLAG_SUBROUNDS) != 0;
     Ctl *ctl = (Ctl *)(ws + L.ctl);
-    ull *fsize = (ull *)(ws + L.fsize);
-    ull *kil = (ull *)(ws + L.killed);
+    ull *stats = (ull *)(ws + L.stats);
     uint32_t *alive = (uint32_t *)(ws + L.alive);
     PEEL_CUDA(cudaMemsetAsync(ws + L.ctl, 0, L.state ? L.state - L.ctl : L.deg - L.ctl, s));
     PEEL_CUDA(cudaMemsetAsync(alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s));
@@ -1196,7 +1195,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     a.alive = alive;
     a.F[0] = ws + L.F0;
     a.F[1] = ws + L.F1;
-    a.ctl = ctl; a.fsize = fsize; a.killed = kil;
+    a.ctl = ctl; a.stats = stats;
     a.rtime = (ull *)(ws + L.rtime);
     a.core_mask = core_mask; a.peel_round = peel_round;
     a.mask_vec = ((uintptr_t)core_mask & 15) == 0;
@@ -1383,11 +1382,15 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, PEEL_BLOCK, args, 0, s));
     }
 
-    // results
-    Ctl hctl;
-    PEEL_CUDA(cudaMemcpyAsync(&hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    // results: the control block and the first STAT_HEAD rounds' statistics in one copy
+    static_assert(sizeof(Ctl) <= 256, "Ctl fits the first 256-byte slot (L.stats follows it)");
+    constexpr uint64_t STAT_HEAD = 64;
+    std::vector<ull> head((L.stats - L.ctl) / sizeof(ull) + 2 * STAT_HEAD);
+    PEEL_CUDA(cudaMemcpyAsync(head.data(), ws + L.ctl, head.size() * sizeof(ull), cudaMemcpyDeviceToHost, s));
     PEEL_CUDA(cudaStreamSynchronize(s));
     prof_collect();
+    Ctl hctl;
+    memcpy(&hctl, head.data(), sizeof(Ctl));
     if (hctl.err & ERR_BADVERTEX) return PEEL_EINVAL;
     uint64_t T = hctl.rounds;
     if (prof_enabled()) {
@@ -1402,15 +1405,19 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     uint64_t nstore = T < cap ? T : cap;
     if (nstore > STAT_CAP) nstore = STAT_CAP;
     if (nstore && (survivors || killed)) {
-        ull *hf = new ull[nstore];
-        cudaError_t e1 = cudaMemcpy(hf, fsize, sizeof(ull) * nstore, cudaMemcpyDeviceToHost);
-        if (e1 != cudaSuccess) { delete[] hf; set_cuda_error(e1, "copy fsize"); return PEEL_ECUDA; }
-        if (survivors) {
-            uint64_t alive_v = n;
-            for (uint64_t t = 0; t < nstore; t++) { alive_v -= hf[t]; survivors[t] = alive_v; }
+        const ull *hs = head.data() + (L.stats - L.ctl) / sizeof(ull);
+        std::vector<ull> more;
+        if (nstore > STAT_HEAD) {
+            more.resize(2 * nstore);
+            PEEL_CUDA(cudaMemcpy(more.data(), stats, sizeof(ull) * 2 * nstore, cudaMemcpyDeviceToHost));
+            hs = more.data();
         }
-        delete[] hf;
-        if (killed) PEEL_CUDA(cudaMemcpy(killed, kil, sizeof(ull) * nstore, cudaMemcpyDeviceToHost));
+        uint64_t alive_v = n;
+        for (uint64_t t = 0; t < nstore; t++) {
+            alive_v -= hs[2 * t];
+            if (survivors) survivors[t] = alive_v;
+            if (killed) killed[t] = hs[2 * t + 1];
+        }
     }
     return (T > cap || T > STAT_CAP) ? PEEL_ETRUNC : PEEL_OK;
 }

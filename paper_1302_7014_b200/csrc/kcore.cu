@@ -32,6 +32,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -822,6 +825,171 @@ __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, Bin
     block_add<PEEL_BLOCK>(&ctl->nf[t % 3], crossed);
 }
 
+// ---- small instances: the whole peel in ONE thread-block cluster's distributed shared memory
+// A round of the cooperative kernel is a chain of ~8 dependent global-memory operations plus
+// a grid barrier: ~11 us at n = 10^5 whatever the grid size (measured with per-phase clock64
+// traces).  For n up to ~1.4e5 every per-vertex and per-edge word fits the
+// shared memory of a 16-CTA cluster, so the chain runs on DSMEM (cross-CTA ~215 cycles,
+// local ~38) and the rounds are separated by the hardware cluster barrier:
+//   CTA c owns vertices [c nl, (c+1) nl)  -> its packed states (count | id sum << 32) and the
+//        frontier lists of those vertices (each vertex joins a frontier once: capacity nl);
+//   CTA c owns edges [c ml, (c+1) ml)     -> their alive bits;
+//   round t: each CTA walks its own list L_t; an entry (u, e) test-and-clears e's bit in the
+//        owner CTA (exactly-once kill), reads e's row from global memory (L2-resident), and
+//        decrements every other endpoint w in w's owner CTA; a k -> k-1 crossing appends
+//        (w, id sum - e) to the owner's L_{t+1}.  Per-round totals meet in CTA 0.
+// Same schedule, statistics and outputs as peel_packed_kernel (the state is built by
+// build_packed_kernel in global memory first and copied in).
+static constexpr int CL_THREADS = 1024;
+static constexpr int CL_MAX = 16;
+
+struct ClusterShape {
+    uint32_t cs;      // CTAs in the cluster
+    uint32_t nl;      // vertices per CTA (the last may have fewer)
+    uint32_t ml;      // edges per CTA, a multiple of 32
+    size_t smem;      // dynamic shared memory per CTA
+};
+
+static ClusterShape cluster_shape(uint64_t n, uint64_t m, uint32_t cs) {
+    ClusterShape c;
+    c.cs = cs;
+    c.nl = (uint32_t)((n + cs - 1) / cs);
+    c.ml = (uint32_t)((((m + cs - 1) / cs) + 31) & ~31ull);
+    c.smem = (size_t)c.nl * (sizeof(ull) + 2 * sizeof(uint2)) + c.ml / 8;
+    return c;
+}
+
+template <int R>
+__global__ void __launch_bounds__(CL_THREADS, 1) peel_cluster_kernel(PeelArgs a, ClusterShape cs) {
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t c = cluster.block_rank();
+    const uint32_t nl = cs.nl, ml = cs.ml, P = cs.cs;
+    ull *st = (ull *)smem_raw;                            // [nl] packed states of owned vertices
+    uint2 *L0 = (uint2 *)(st + nl);                       // [nl] frontier list, round parity 0
+    uint2 *L1 = L0 + nl;                                  // [nl] parity 1
+    uint32_t *alive = (uint32_t *)(L1 + nl);              // [ml / 32] alive bits of owned edges
+    __shared__ uint32_t fcnt[3];                          // list lengths, round t appends fcnt[t % 3]
+    __shared__ ull red[3][2];                             // CTA 0: (crossings, kills) of round t at [t % 3]
+    __shared__ ull wred[CL_THREADS / 32][2];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t k = a.k;
+    const uint64_t v0 = (uint64_t)c * nl;
+    const uint32_t nown = v0 >= a.n ? 0u : (uint32_t)min((uint64_t)nl, a.n - v0);
+    const uint64_t e0 = (uint64_t)c * ml;
+    const uint32_t eown = e0 >= a.m ? 0u : (uint32_t)min((uint64_t)ml, a.m - e0);
+    if (ld_cg_u32(&a.ctl->err) & ERR_BADVERTEX) return;  // uniform over the cluster
+
+    // block reduction of two counters, then one DSMEM atomic pair into CTA 0's red[slot]
+    auto reduce_to_cta0 = [&](ull x, ull y, uint32_t slot) {
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            x += __shfl_down_sync(0xffffffffu, x, o);
+            y += __shfl_down_sync(0xffffffffu, y, o);
+        }
+        if ((tid & 31) == 0) { wred[tid >> 5][0] = x; wred[tid >> 5][1] = y; }
+        __syncthreads();
+        if (tid < 32) {
+            x = wred[tid][0];
+            y = wred[tid][1];
+            #pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                x += __shfl_down_sync(0xffffffffu, x, o);
+                y += __shfl_down_sync(0xffffffffu, y, o);
+            }
+            if (tid == 0) {
+                ull *r0 = cluster.map_shared_rank(&red[slot][0], 0);
+                if (x) atomicAdd(r0, x);
+                if (y) atomicAdd(r0 + 1, y);
+            }
+        }
+    };
+
+    // ---- load: owned states, all alive bits set, counters zero; round-1 frontier ----
+    for (uint32_t i = tid; i < nown; i += CL_THREADS) st[i] = ld_cg_u64(a.state + v0 + i);
+    for (uint32_t i = tid; i < ml / 32; i += CL_THREADS) {
+        const uint32_t lo = i * 32;
+        alive[i] = lo >= eown ? 0u : (eown - lo >= 32 ? 0xFFFFFFFFu : ((1u << (eown - lo)) - 1u));
+    }
+    if (tid < 3) {
+        fcnt[tid] = 0;
+        red[tid][0] = red[tid][1] = 0;
+    }
+    cluster.sync();  // every CTA initialised before any DSMEM access
+    ull removed = 0;
+    for (uint32_t i = tid; i < nown; i += CL_THREADS) {
+        const ull w = st[i];
+        if (count_of(w) < k) {
+            removed++;
+            if (a.peel_round) a.peel_round[v0 + i] = 1;
+            if (count_of(w) == 1) L0[atomicAdd(&fcnt[0], 1u)] = make_uint2((uint32_t)(v0 + i), idsum_of(w));
+        }
+    }
+    reduce_to_cta0(removed, 0, 0);
+    cluster.sync();
+    ull nF = *cluster.map_shared_rank(&red[0][0], 0);  // |F_1|; red[0] is zeroed after B_1
+
+    uint32_t t = 1;
+    while (nF != 0) {
+        if (c == 0 && tid == 0) {
+            if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
+            a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap)] = nF;
+        }
+        const uint2 *Lc = (t & 1) ? L0 : L1;              // L_t lives in L[(t-1) & 1]
+        const uint32_t nE = fcnt[(t - 1) % 3];
+        const uint32_t nslot = t % 3;                     // L_{t+1}'s counter
+        const uint32_t nlist = t & 1;                     // L_{t+1}'s array
+        ull kills = 0, crossed = 0;
+        for (uint32_t i = tid; i < nE; i += CL_THREADS) {
+            const uint2 ent = Lc[i];
+            const uint32_t e = ent.y;
+            const uint32_t oe = e / ml, bit = 1u << (e & 31);
+            uint32_t *aw = cluster.map_shared_rank(alive + ((e - oe * ml) >> 5), oe);
+            if (!(atomicAnd(aw, ~bit) & bit)) continue;    // exactly-once kill
+            kills++;
+            uint32_t row[R];
+            load_row<R>(a.edges, e, a.m, a.edges_vec, row);
+            const ull dec = 0ull - (((ull)e << 32) + 1ull);
+            ull old[R];
+            #pragma unroll
+            for (int r = 0; r < R; r++) {
+                old[r] = ~0ull;
+                if (row[r] != ent.x) {
+                    const uint32_t ow = row[r] / nl;
+                    old[r] = atomicAdd(cluster.map_shared_rank(st + (row[r] - ow * nl), ow), dec);
+                }
+            }
+            #pragma unroll
+            for (int r = 0; r < R; r++)
+                if (count_of(old[r]) == k) {                // k -> k-1: row[r] joins F_{t+1}
+                    crossed++;
+                    const uint32_t w = row[r], ow = w / nl;
+                    if (a.peel_round) a.peel_round[w] = t + 1;
+                    const uint32_t pos = atomicAdd(cluster.map_shared_rank(&fcnt[nslot], ow), 1u);
+                    uint2 *dst = cluster.map_shared_rank((nlist ? L1 : L0) + pos, ow);
+                    *dst = make_uint2(w, idsum_of(old[r]) - e);
+                }
+        }
+        reduce_to_cta0(crossed, kills, t % 3);
+        cluster.sync();                                   // B_t: round t complete everywhere
+        const ull *r0 = cluster.map_shared_rank(&red[t % 3][0], 0);
+        nF = r0[0];
+        if (c == 0 && tid == 0) {
+            a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap) + 1] = r0[1];
+            red[(t + 2) % 3][0] = red[(t + 2) % 3][1] = 0;  // last read after B_{t-1}, next used in round t+2
+        }
+        if (tid == 0) fcnt[(t + 2) % 3] = 0;              // L_t's length: consumed; refilled in round t+2
+        __syncthreads();
+        t++;
+    }
+    if (c == 0 && tid == 0) {
+        a.ctl->rounds = t - 1;
+        if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
+    }
+    for (uint32_t i = tid; i < nown; i += CL_THREADS) a.core_mask[v0 + i] = count_of(st[i]) >= k ? 1 : 0;
+    cluster.sync();  // no CTA exits while others may still read its shared memory
+}
+
 // packed path (k <= 2)
 template <int R>
 __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) {
@@ -1176,6 +1344,112 @@ static unsigned grid_for(uint64_t work, int per_sm = 16) {
     return (unsigned)blocks;
 }
 
+// cluster size (16, else 8) for peel_cluster_kernel, or 0: the instance's words must fit
+// the cluster's shared memory.  PEEL_CLUSTER=0 disables the path (A/B measurement).
+static int cluster_eligible(uint64_t n, uint64_t m, const void *kern) {
+    const char *ev = getenv("PEEL_CLUSTER");  // read per call: tests toggle it in-process
+    if ((ev && atoi(ev) == 0) || n == 0) return 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+    // the launchability answer per (device, kernel, cluster size, shared-memory bytes rounded
+    // up to 4 KB) is cached: the occupancy query costs more than a small peel
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, int, size_t>, bool> ok;
+    static std::map<int, int> optin;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!optin.count(dev)) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+            cudaGetLastError();
+            v = 0;
+        }
+        optin[dev] = v;
+    }
+    for (int cs : {CL_MAX, 8}) {
+        const ClusterShape shp = cluster_shape(n, m, (uint32_t)cs);
+        if (shp.smem + 4096 > (size_t)optin[dev]) continue;  // + static shared memory
+        const size_t smem4k = (shp.smem + 4095) & ~(size_t)4095;
+        const auto key = std::make_tuple(dev, kern, cs, smem4k);
+        // the dynamic-smem attribute is per function and only ever raised here
+        static std::map<const void *, size_t> attr;
+        if (attr[kern] < smem4k) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4k) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            attr[kern] = smem4k;
+        }
+        auto it = ok.find(key);
+        if (it == ok.end()) {
+            bool good = cs <= 8 || cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+            if (good) {
+                cudaLaunchConfig_t cfg;
+                memset(&cfg, 0, sizeof cfg);
+                cfg.gridDim = dim3((unsigned)cs);
+                cfg.blockDim = dim3(CL_THREADS);
+                cfg.dynamicSmemBytes = smem4k;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = (unsigned)cs;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int nc = 0;
+                good = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) == cudaSuccess && nc >= 1;
+            }
+            if (!good) cudaGetLastError();
+            it = ok.emplace(key, good).first;
+        }
+        if (it->second) return cs;
+    }
+    return 0;
+}
+
+// read back rounds and per-round statistics after the round loop (one small copy)
+static peel_status finish_kcore(uint64_t n, uint32_t cap, uint32_t *rounds, uint64_t *survivors, uint64_t *killed,
+                                char *ws, const Layout &L, const PeelArgs &a, cudaStream_t s) {
+    ull *stats = (ull *)(ws + L.stats);
+    // results: the control block and the first STAT_HEAD rounds' statistics in one copy
+    static_assert(sizeof(Ctl) <= 256, "Ctl fits the first 256-byte slot (L.stats follows it)");
+    constexpr uint64_t STAT_HEAD = 64;
+    std::vector<ull> head((L.stats - L.ctl) / sizeof(ull) + 2 * STAT_HEAD);
+    PEEL_CUDA(cudaMemcpyAsync(head.data(), ws + L.ctl, head.size() * sizeof(ull), cudaMemcpyDeviceToHost, s));
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    prof_collect();
+    Ctl hctl;
+    memcpy(&hctl, head.data(), sizeof(Ctl));
+    if (hctl.err & ERR_BADVERTEX) return PEEL_EINVAL;
+    uint64_t T = hctl.rounds;
+    if (prof_enabled()) {
+        uint64_t nt = (T < STAT_CAP ? T : STAT_CAP - 1) + 1;
+        std::vector<ull> rt(nt);
+        PEEL_CUDA(cudaMemcpy(rt.data(), a.rtime, sizeof(ull) * nt, cudaMemcpyDeviceToHost));
+        std::vector<double> ms(nt > 1 ? nt - 1 : 0);
+        for (uint64_t i = 0; i + 1 < nt; i++) ms[i] = (rt[i + 1] - rt[i]) * 1e-6;
+        prof_set_rounds(ms);
+    }
+    *rounds = (uint32_t)T;
+    uint64_t nstore = T < cap ? T : cap;
+    if (nstore > STAT_CAP) nstore = STAT_CAP;
+    if (nstore && (survivors || killed)) {
+        const ull *hs = head.data() + (L.stats - L.ctl) / sizeof(ull);
+        std::vector<ull> more;
+        if (nstore > STAT_HEAD) {
+            more.resize(2 * nstore);
+            PEEL_CUDA(cudaMemcpy(more.data(), stats, sizeof(ull) * 2 * nstore, cudaMemcpyDeviceToHost));
+            hs = more.data();
+        }
+        uint64_t alive_v = n;
+        for (uint64_t t = 0; t < nstore; t++) {
+            alive_v -= hs[2 * t];
+            if (survivors) survivors[t] = alive_v;
+            if (killed) killed[t] = hs[2 * t + 1];
+        }
+    }
+    return (T > cap || T > STAT_CAP) ? PEEL_ETRUNC : PEEL_OK;
+}
+
 template <int R>
 static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr, uint32_t flags,
                              uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
@@ -1362,6 +1636,32 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         a.t0 = t;
     }
 
+    // small packed instances: the whole round loop in one cluster's shared memory
+    if (!csr && !subr && a.t0 == 1 && !L.nbins) {
+        const int cl = cluster_eligible(n, m, (const void *)peel_cluster_kernel<R>);
+        if (cl) {
+            const ClusterShape shp = cluster_shape(n, m, (uint32_t)cl);
+            cudaLaunchConfig_t cfg;
+            memset(&cfg, 0, sizeof cfg);
+            cfg.gridDim = dim3((unsigned)cl);
+            cfg.blockDim = dim3(CL_THREADS);
+            cfg.dynamicSmemBytes = shp.smem;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)cl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            {
+                ProfScope ps("peel_rounds_cluster", s);
+                PEEL_CUDA(cudaLaunchKernelEx(&cfg, peel_cluster_kernel<R>, a, shp));
+            }
+            return finish_kcore(n, cap, rounds, survivors, killed, ws, L, a, s);
+        }
+    }
+
     // cooperative persistent round loop: every block must be co-resident
     void *kern = csr ? (void *)peel_csr_kernel<R> : (subr ? (void *)peel_subround_kernel<R> : (void *)peel_packed_kernel<R>);
     if (subr) {
@@ -1382,44 +1682,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         PEEL_CUDA(cudaLaunchCooperativeKernel(kern, grid, PEEL_BLOCK, args, 0, s));
     }
 
-    // results: the control block and the first STAT_HEAD rounds' statistics in one copy
-    static_assert(sizeof(Ctl) <= 256, "Ctl fits the first 256-byte slot (L.stats follows it)");
-    constexpr uint64_t STAT_HEAD = 64;
-    std::vector<ull> head((L.stats - L.ctl) / sizeof(ull) + 2 * STAT_HEAD);
-    PEEL_CUDA(cudaMemcpyAsync(head.data(), ws + L.ctl, head.size() * sizeof(ull), cudaMemcpyDeviceToHost, s));
-    PEEL_CUDA(cudaStreamSynchronize(s));
-    prof_collect();
-    Ctl hctl;
-    memcpy(&hctl, head.data(), sizeof(Ctl));
-    if (hctl.err & ERR_BADVERTEX) return PEEL_EINVAL;
-    uint64_t T = hctl.rounds;
-    if (prof_enabled()) {
-        uint64_t nt = (T < STAT_CAP ? T : STAT_CAP - 1) + 1;
-        std::vector<ull> rt(nt);
-        PEEL_CUDA(cudaMemcpy(rt.data(), a.rtime, sizeof(ull) * nt, cudaMemcpyDeviceToHost));
-        std::vector<double> ms(nt > 1 ? nt - 1 : 0);
-        for (uint64_t i = 0; i + 1 < nt; i++) ms[i] = (rt[i + 1] - rt[i]) * 1e-6;
-        prof_set_rounds(ms);
-    }
-    *rounds = (uint32_t)T;
-    uint64_t nstore = T < cap ? T : cap;
-    if (nstore > STAT_CAP) nstore = STAT_CAP;
-    if (nstore && (survivors || killed)) {
-        const ull *hs = head.data() + (L.stats - L.ctl) / sizeof(ull);
-        std::vector<ull> more;
-        if (nstore > STAT_HEAD) {
-            more.resize(2 * nstore);
-            PEEL_CUDA(cudaMemcpy(more.data(), stats, sizeof(ull) * 2 * nstore, cudaMemcpyDeviceToHost));
-            hs = more.data();
-        }
-        uint64_t alive_v = n;
-        for (uint64_t t = 0; t < nstore; t++) {
-            alive_v -= hs[2 * t];
-            if (survivors) survivors[t] = alive_v;
-            if (killed) killed[t] = hs[2 * t + 1];
-        }
-    }
-    return (T > cap || T > STAT_CAP) ? PEEL_ETRUNC : PEEL_OK;
+    return finish_kcore(n, cap, rounds, survivors, killed, ws, L, a, s);
 }
 
 static bool kcore_args_ok(uint64_t n, uint64_t m, uint32_t r, bool csr) {

@@ -262,3 +262,27 @@ def test_full_scale_c5_north_star(goldens):
     del e, res
     pk._ws_cache.clear()
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("path", ["cluster", "cooperative"])
+def test_small_instances_both_round_loops(path, monkeypatch):
+    """Small packed instances run in one thread-block cluster's shared memory
+    (peel_cluster_kernel) unless PEEL_CLUSTER=0 selects the cooperative grid kernel:
+    both bit-exact against the oracle, including C1 and ragged / degenerate shapes."""
+    if path == "cooperative":
+        monkeypatch.setenv("PEEL_CLUSTER", "0")
+    else:
+        monkeypatch.delenv("PEEL_CLUSTER", raising=False)
+    rng = np.random.default_rng(77)
+    for trial in range(12):
+        r = int(rng.integers(2, 6))
+        n = int(rng.integers(r, 140000)) if trial % 3 == 0 else int(rng.integers(r, 5000))
+        m = int(rng.integers(0, int(0.95 * n)))
+        e = synth.random_hypergraph(n, m, r, seed=500 + trial)
+        check_vs_oracle(e, n, 2, twice=False)
+    check_vs_oracle(synth.star(4001, 3), 4001, 2, twice=False)
+    check_vs_oracle(synth.star(4001, 3), 4001, 1, twice=False)
+    e, n = synth.chain(3001, 2)
+    check_vs_oracle(e, n, 2, twice=False)
+    e = pk.gen_hypergraph(100000, 70000, 3, 1, device=DEV)
+    check_vs_oracle(e.cpu().numpy().view(np.uint32), 100000, 2, twice=False)

@@ -833,9 +833,8 @@ __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, Bin
 // local ~38) and the rounds are separated by the hardware cluster barrier:
 //   CTA c owns vertices [c nl, (c+1) nl)  -> its packed states (count | id sum << 32) and the
 //        frontier lists of those vertices (each vertex joins a frontier once: capacity nl);
-//   CTA c owns edges [c ml, (c+1) ml)     -> their alive bits;
-//   round t: each CTA walks its own list L_t; an entry (u, e) test-and-clears e's bit in the
-//        owner CTA (exactly-once kill), reads e's row from global memory (L2-resident), and
+//   round t: each CTA walks its own list L_t; an entry (u, e) test-and-clears e's alive bit
+//        (global bitmap, L2-resident; exactly-once kill), reads e's row (L2-resident), and
 //        decrements every other endpoint w in w's owner CTA; a k -> k-1 crossing appends
 //        (w, id sum - e) to the owner's L_{t+1}.  Per-round totals meet in CTA 0.
 // Same schedule, statistics and outputs as peel_packed_kernel (the state is built by
@@ -846,7 +845,6 @@ static constexpr int CL_MAX = 16;
 struct ClusterShape {
     uint32_t cs;      // CTAs in the cluster
     uint32_t nl;      // vertices per CTA (the last may have fewer)
-    uint32_t ml;      // edges per CTA, a multiple of 32
     size_t smem;      // dynamic shared memory per CTA
 };
 
@@ -854,8 +852,8 @@ static ClusterShape cluster_shape(uint64_t n, uint64_t m, uint32_t cs) {
     ClusterShape c;
     c.cs = cs;
     c.nl = (uint32_t)((n + cs - 1) / cs);
-    c.ml = (uint32_t)((((m + cs - 1) / cs) + 31) & ~31ull);
-    c.smem = (size_t)c.nl * (sizeof(ull) + 2 * sizeof(uint2)) + c.ml / 8;
+    (void)m;
+    c.smem = (size_t)c.nl * (sizeof(ull) + 2 * sizeof(uint2));
     return c;
 }
 
@@ -864,11 +862,10 @@ __global__ void __launch_bounds__(CL_THREADS, 1) peel_cluster_kernel(PeelArgs a,
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t c = cluster.block_rank();
-    const uint32_t nl = cs.nl, ml = cs.ml, P = cs.cs;
+    const uint32_t nl = cs.nl;
     ull *st = (ull *)smem_raw;                            // [nl] packed states of owned vertices
     uint2 *L0 = (uint2 *)(st + nl);                       // [nl] frontier list, round parity 0
     uint2 *L1 = L0 + nl;                                  // [nl] parity 1
-    uint32_t *alive = (uint32_t *)(L1 + nl);              // [ml / 32] alive bits of owned edges
     __shared__ uint32_t fcnt[3];                          // list lengths, round t appends fcnt[t % 3]
     __shared__ ull red[3][2];                             // CTA 0: (crossings, kills) of round t at [t % 3]
     __shared__ ull wred[CL_THREADS / 32][2];
@@ -876,8 +873,6 @@ __global__ void __launch_bounds__(CL_THREADS, 1) peel_cluster_kernel(PeelArgs a,
     const uint32_t k = a.k;
     const uint64_t v0 = (uint64_t)c * nl;
     const uint32_t nown = v0 >= a.n ? 0u : (uint32_t)min((uint64_t)nl, a.n - v0);
-    const uint64_t e0 = (uint64_t)c * ml;
-    const uint32_t eown = e0 >= a.m ? 0u : (uint32_t)min((uint64_t)ml, a.m - e0);
     if (ld_cg_u32(&a.ctl->err) & ERR_BADVERTEX) return;  // uniform over the cluster
 
     // block reduction of two counters, then one DSMEM atomic pair into CTA 0's red[slot]
@@ -907,15 +902,11 @@ __global__ void __launch_bounds__(CL_THREADS, 1) peel_cluster_kernel(PeelArgs a,
 
     // ---- load: owned states, all alive bits set, counters zero; round-1 frontier ----
     for (uint32_t i = tid; i < nown; i += CL_THREADS) st[i] = ld_cg_u64(a.state + v0 + i);
-    for (uint32_t i = tid; i < ml / 32; i += CL_THREADS) {
-        const uint32_t lo = i * 32;
-        alive[i] = lo >= eown ? 0u : (eown - lo >= 32 ? 0xFFFFFFFFu : ((1u << (eown - lo)) - 1u));
-    }
     if (tid < 3) {
         fcnt[tid] = 0;
         red[tid][0] = red[tid][1] = 0;
     }
-    cluster.sync();  // every CTA initialised before any DSMEM access
+    cluster.sync();  // every CTA initialised before any DSMEM access (the alive bits were set by the host)
     ull removed = 0;
     for (uint32_t i = tid; i < nown; i += CL_THREADS) {
         const ull w = st[i];
@@ -943,9 +934,10 @@ __global__ void __launch_bounds__(CL_THREADS, 1) peel_cluster_kernel(PeelArgs a,
         for (uint32_t i = tid; i < nE; i += CL_THREADS) {
             const uint2 ent = Lc[i];
             const uint32_t e = ent.y;
-            const uint32_t oe = e / ml, bit = 1u << (e & 31);
-            uint32_t *aw = cluster.map_shared_rank(alive + ((e - oe * ml) >> 5), oe);
-            if (!(atomicAnd(aw, ~bit) & bit)) continue;    // exactly-once kill
+            // exactly-once kill on the global alive bitmap: L2 atomics beat DSMEM atomics here
+            // (C1 round loop 87 -> 78 us with the bits in the owner CTAs' shared memory)
+            const uint32_t bit = 1u << (e & 31);
+            if (!(atomicAnd(a.alive + (e >> 5), ~bit) & bit)) continue;
             kills++;
             uint32_t row[R];
             load_row<R>(a.edges, e, a.m, a.edges_vec, row);

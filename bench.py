@@ -619,20 +619,26 @@ def main():
         kb["round_kill_partition"] = sum(8 * F[t] + 4 * r * kl[t] for t in range(min(nb, len(F))))
         kb["round_apply"] = sum(16 * (r - 1) * kl[t] for t in range(min(nb, len(F))))
         kb["peel_rounds_packed"] = sum(8 * F[t] + (4 * r + 16 * (r - 1)) * kl[t] for t in range(nb, len(F))) + n
+        kb["peel_rounds_cluster"] = kb["peel_rounds_packed"]
     dom = max(per_kernel.items(), key=lambda kv: kv[1][0]) if per_kernel else None
     roof = None
     if dom:
         name, (ms_sum, nl) = dom
         avg_ms = ms_sum / max(nl, 1)
-        alg = kb.get(name)
+        alg = kb.get(name)  # bytes per STEP of this kernel (all its launches)
         if alg is None:  # CSR path: whole-step formula over the whole-step time of its kernels
             alg = b_build + b_rounds
             avg_ms = sum(v[0] for v in per_kernel.values()) / args.steps
+        else:
+            alg = alg / max(nl / args.steps, 1.0)  # per launch, like avg_ms
         ach = alg / (avg_ms / 1e3) / 1e9
         traffic, tsrc = ncu_traffic(args.config, name)
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
-                "alg_bytes_per_launch": alg, "avg_launch_ms": round(avg_ms, 4)}
+                # the same kernel's real DRAM bytes (ncu) over its time here: random 8-12 B accesses move
+                # 64 B DRAM granules, so traffic >> algorithmic bytes by construction
+                "dram_frac_of_peak": (round(traffic / (avg_ms / 1e3) / 1e9 / hbm, 4) if traffic else None),
+                "alg_bytes_per_launch": int(alg), "avg_launch_ms": round(avg_ms, 4)}
     # Supplementary roof for the persistent round kernel: the time its random DRAM operations
     # need at the rates measured on this pool (microbench/membench.cu, profiles/r01_membench.jsonl:
     # 8 B random read-modify-write 20.1 G/s, 8 B random gather 37.1 G/s, 4 B test-and-clear on a

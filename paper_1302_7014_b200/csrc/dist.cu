@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "shard.h"
 
 namespace peel {
 
@@ -63,10 +64,10 @@ struct DShard {
 };
 
 struct DLayout {
-    size_t ctl, scratch, state, alive, F0, F1, send, recv, total;
+    size_t ctl, scratch, state, alive, F0, F1, send, recv, bins, bins_bytes, total;
 };
 
-static DLayout dlayout(uint64_t n, uint64_t m, int P, uint64_t nloc) {
+static DLayout dlayout(uint64_t n, uint64_t m, uint32_t r, int P, uint64_t nloc) {
     DLayout L;
     size_t o = 0;
     L.ctl = o; o += dal(sizeof(DCtl));
@@ -77,6 +78,8 @@ static DLayout dlayout(uint64_t n, uint64_t m, int P, uint64_t nloc) {
     L.F1 = o; o += dal(sizeof(uint2) * nloc);
     L.send = o; o += dal(sizeof(uint32_t) * nloc * P);
     L.recv = o; o += dal(sizeof(uint32_t) * n);
+    L.bins_bytes = shard_build_bytes(n, m, r, nloc);  // 0: the shard builds directly
+    L.bins = o; o += dal(L.bins_bytes);
     L.total = o;
     return L;
 }
@@ -332,7 +335,7 @@ static uint64_t max_shard(uint64_t n, int P) {
 
 extern "C" size_t peel_kcore_dist_workspace_bytes(const peel_comm *c, uint64_t n, uint64_t m, uint32_t r, uint32_t k) {
     if (!c || r < 2 || r > 8 || k > 2 || n > (1ull << 32) || m >= (1ull << 32) || n < (uint64_t)c->P) return 0;
-    DLayout L = dlayout(n, m, c->P, max_shard(n, c->P));
+    DLayout L = dlayout(n, m, r, c->P, max_shard(n, c->P));
     return c->virt ? L.total * c->P : L.total;
 }
 
@@ -342,7 +345,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                             uint32_t cap, char *ws, cudaStream_t s) {
     const int P = c->P;
     const uint64_t nl_max = max_shard(n, P);
-    const DLayout L = dlayout(n, m, P, nl_max);
+    const DLayout L = dlayout(n, m, R, P, nl_max);
     // local shards: all P (virtual) or just this rank's
     std::vector<DShard> sh;
     for (int q = 0; q < P; q++) {
@@ -363,11 +366,20 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     }
     for (auto &d : sh) {
         PEEL_CUDA(cudaMemsetAsync(d.ctl, 0, sizeof(DCtl), s));
-        PEEL_CUDA(cudaMemsetAsync(d.state, 0, sizeof(ull) * (d.v1 - d.v0), s));
         PEEL_CUDA(cudaMemsetAsync(d.alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s));
-        if (m) {
-            ProfScope ps("dist_build", s);
-            dist_build_kernel<R><<<dgrid(m), DB, 0, s>>>(edges, n, m, d.v0, d.v1, d.state, d.ctl);
+        // large shards: the binned build of kcore.cu restricted to the shard's endpoints
+        bool direct = true;
+        if (L.bins_bytes && d.v1 - d.v0 > 0) {
+            char *b = ws + (c->virt ? (size_t)d.q * L.total : 0);
+            peel_status st = shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct);
+            if (st != PEEL_OK) return st;
+        }
+        if (direct) {  // small shard, or a bin overflowed
+            PEEL_CUDA(cudaMemsetAsync(d.state, 0, sizeof(ull) * (d.v1 - d.v0), s));
+            if (m) {
+                ProfScope ps("dist_build", s);
+                dist_build_kernel<R><<<dgrid(m), DB, 0, s>>>(edges, n, m, d.v0, d.v1, d.state, d.ctl);
+            }
         }
         ProfScope ps("dist_scan", s);
         dist_scan_kernel<<<dgrid(d.v1 - d.v0), DB, 0, s>>>(d.state, d.v0, d.v1 - d.v0, k, d.F[1], d.ctl);

@@ -38,6 +38,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "shard.h"
 
 namespace peel {
 
@@ -76,8 +77,9 @@ __host__ __device__ inline uint64_t bin_size(uint64_t n, uint64_t b) {
 
 // capacity of bin b: expected r m size/n plus 8 standard deviations plus 4096 (IEEE sqrt,
 // identical on host and device); a bin that overflows sends the build down the direct path
-__host__ __device__ inline uint64_t bin_capacity(uint64_t n, uint64_t m, uint32_t r, uint64_t b) {
-    uint64_t lam = (bin_size(n, b) * (uint64_t)r * m) / n;
+// (a shard of nloc vertices of an n-vertex instance: its bins over [0, nloc), density r m / n)
+__host__ __device__ inline uint64_t bin_capacity(uint64_t n, uint64_t nloc, uint64_t m, uint32_t r, uint64_t b) {
+    uint64_t lam = (bin_size(nloc, b) * (uint64_t)r * m) / n;
     return lam + 8ull * (uint64_t)sqrt((double)lam) + 4096ull;
 }
 
@@ -110,7 +112,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     L.bins = L.bin_cursor = L.bin_base = L.bin_cap = L.entries = 0;
     if (n > BIN_MIN_N) {  // packed: binned build + rounds; CSR: binned degree count + scatter
         L.nbins = (n + (1ull << BIN_SHIFT) - 1) >> BIN_SHIFT;
-        for (uint64_t b = 0; b < L.nbins; b++) L.total_cap += bin_capacity(n, m, r, b);
+        for (uint64_t b = 0; b < L.nbins; b++) L.total_cap += bin_capacity(n, n, m, r, b);
         L.bins = o;
         L.bin_cursor = o; o += al(sizeof(ull) * L.nbins);
         L.bin_base = o; o += al(sizeof(ull) * L.nbins);
@@ -160,12 +162,12 @@ __global__ void __launch_bounds__(256) build_packed_kernel(const uint32_t *__res
 }
 
 // ---- binned build ------------------------------------------------------------------------
-__global__ void bin_init_kernel(uint64_t n, uint64_t m, uint32_t r, uint64_t nbins, ull *cursor, ull *base,
-                                ull *cap) {
+__global__ void bin_init_kernel(uint64_t n, uint64_t nloc, uint64_t m, uint32_t r, uint64_t nbins, ull *cursor,
+                                ull *base, ull *cap) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         ull o = 0;
         for (uint64_t b = 0; b < nbins; b++) {
-            ull c = bin_capacity(n, m, r, b);
+            ull c = bin_capacity(n, nloc, m, r, b);
             cursor[b] = 0;
             base[b] = o;
             cap[b] = c;
@@ -189,7 +191,8 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
                                                                       uint64_t n, uint64_t m, uint32_t nbins,
                                                                       ull *cursor, const ull *__restrict__ base,
                                                                       const ull *__restrict__ cap, ull *entries,
-                                                                      Ctl *ctl) {
+                                                                      uint32_t *err, uint32_t *binovf,
+                                                                      uint64_t v0, uint64_t v1) {
     constexpr int CH = PART_ENTRIES / R;  // edges per chunk
     constexpr int CW = CH * R;            // edge words per chunk
     constexpr int CWP = (CW + 3) & ~3;    // padded: keeps every array below 16-byte aligned
@@ -227,11 +230,16 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
                 #pragma unroll
                 for (int q = j + 1; q < R; q++) ok &= words[i * R + j] != words[i * R + q];
             okb[i] = ok;
-            if (!ok) atomicOr(&ctl->err, ERR_BADVERTEX);
+            if (!ok) atomicOr(err, ERR_BADVERTEX);
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < nw; i += PART_BLOCK)
-            if (okb[i / R]) atomicAdd(&hist[words[i] >> BIN_SHIFT], 1u);
+        // a shard keeps only its endpoints [v0, v1), binned by the local id u - v0
+        for (int i = threadIdx.x; i < nw; i += PART_BLOCK) {
+            const uint64_t w = words[i];
+            const bool mine = okb[i / R] && w >= v0 && w < v1;
+            words[i] = mine ? (uint32_t)(w - v0) : 0xFFFFFFFFu;  // local id, or "not kept"
+            if (mine) atomicAdd(&hist[(uint32_t)(w - v0) >> BIN_SHIFT], 1u);
+        }
         __syncthreads();
         // exclusive scan of hist over nbins (<= 1024): one warp
         if (threadIdx.x < 32) {
@@ -258,13 +266,13 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)
             if (hist[b]) {
                 ull g = atomicAdd(cursor + b, (ull)hist[b]);
-                if (g + hist[b] > cap[b]) atomicOr(&ctl->binovf, 1u);
+                if (g + hist[b] > cap[b]) atomicOr(binovf, 1u);
                 gpos[b] = g;
             }
         for (int i = threadIdx.x; i < nw; i += PART_BLOCK) {
             const int ed = i / R;
-            if (!okb[ed]) continue;
             const uint32_t u = words[i];
+            if (!okb[ed] || (u == 0xFFFFFFFFu && v1 - v0 <= 0xFFFFFFFFull)) continue;
             const uint32_t b = u >> BIN_SHIFT;
             sent[offs[b] + atomicAdd(&fill[b], 1u)] = ((c0 + ed) << 32) | u;
         }
@@ -331,6 +339,27 @@ __global__ void __launch_bounds__(256) csr_bin_scatter_kernel(const ull *__restr
             const ull x = CSR_SUB_LOG ? __ldcg(ent + p) : __ldcs(ent + p);
             if ((uint32_t)((x & mask) >> (BIN_SHIFT - CSR_SUB_LOG)) == sub)
                 adj[atomicAdd(o + (x & mask), 1u)] = (uint32_t)(x >> 32);
+        }
+    }
+}
+
+// binned build of a vertex shard (dist.cu): apply the bin-partitioned increments with 64-bit
+// REDs, bin-major (blockIdx.y = bin), so each bin's 32 MB of state is L2-resident while applied
+__global__ void __launch_bounds__(256) bin_red_kernel(const ull *__restrict__ entries, const ull *__restrict__ base,
+                                                      const ull *__restrict__ cursor, ull *state) {
+    const uint32_t b = blockIdx.y;
+    const ull cnt = cursor[b];
+    const ull lo = (ull)blockIdx.x * 256 * CSRB_PER;
+    if (lo >= cnt) return;
+    const ull *ent = entries + base[b];
+    ull *st = state + ((uint64_t)b << BIN_SHIFT);
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    #pragma unroll 4
+    for (int i = 0; i < CSRB_PER; i++) {
+        const ull p = lo + (ull)i * 256 + threadIdx.x;
+        if (p < cnt) {
+            const ull x = __ldcs(ent + p);
+            atomicAdd(st + (x & mask), (x & ~0xFFFFFFFFull) + 1ull);
         }
     }
 }
@@ -1375,8 +1404,7 @@ static int cluster_eligible(uint64_t n, uint64_t m, const void *kern) {
         if (it == ok.end()) {
             bool good = cs <= 8 || cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
             if (good) {
-                cudaLaunchConfig_t cfg;
-                memset(&cfg, 0, sizeof cfg);
+                cudaLaunchConfig_t cfg = {};
                 cfg.gridDim = dim3((unsigned)cs);
                 cfg.blockDim = dim3(CL_THREADS);
                 cfg.dynamicSmemBytes = smem4k;
@@ -1476,7 +1504,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         ull *entries = (ull *)(ws + L.entries);
         {
             ProfScope ps("bin_init", s);
-            bin_init_kernel<<<1, 32, 0, s>>>(n, m, R, L.nbins, cursor, bbase, bcap);
+            bin_init_kernel<<<1, 32, 0, s>>>(n, n, m, R, L.nbins, cursor, bbase, bcap);
         }
         const size_t smem = partition_smem(R, L.nbins);
         PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1486,7 +1514,8 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         if (m) {
             ProfScope ps("bin_partition", s);
             bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)L.nbins, cursor, bbase,
-                                                                                   bcap, entries, ctl);
+                                                                                   bcap, entries, &ctl->err, &ctl->binovf,
+                                                                                   0ull, n);
         }
         PEEL_CUDA(cudaGetLastError());
         BinArgs bn;
@@ -1520,12 +1549,12 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         ull *cursor = (ull *)(ws + L.bin_cursor), *bbase = (ull *)(ws + L.bin_base), *bcap = (ull *)(ws + L.bin_cap);
         ull *entries = (ull *)(ws + L.entries);
         uint64_t maxcap = 0;
-        for (uint64_t b = 0; b < L.nbins; b++) maxcap = std::max<uint64_t>(maxcap, bin_capacity(n, m, R, b));
+        for (uint64_t b = 0; b < L.nbins; b++) maxcap = std::max<uint64_t>(maxcap, bin_capacity(n, n, m, R, b));
         const dim3 bgrid((unsigned)((maxcap + 256 * CSRB_PER - 1) / (256 * CSRB_PER)), (unsigned)L.nbins);
         if (binned) {
             {
                 ProfScope ps("bin_init", s);
-                bin_init_kernel<<<1, 32, 0, s>>>(n, m, R, L.nbins, cursor, bbase, bcap);
+                bin_init_kernel<<<1, 32, 0, s>>>(n, n, m, R, L.nbins, cursor, bbase, bcap);
             }
             const size_t smem = partition_smem(R, L.nbins);
             PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1535,7 +1564,8 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             {
                 ProfScope ps("bin_partition", s);
                 bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)L.nbins,
-                                                                                       cursor, bbase, bcap, entries, ctl);
+                                                                                       cursor, bbase, bcap, entries, &ctl->err,
+                                                                                       &ctl->binovf, 0ull, n);
             }
             // a bin overflow (adversarial degree skew) only loses entries of the binned copy:
             // fall back to the direct histogram below if it happened (checked on the host)
@@ -1633,8 +1663,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         const int cl = cluster_eligible(n, m, (const void *)peel_cluster_kernel<R>);
         if (cl) {
             const ClusterShape shp = cluster_shape(n, m, (uint32_t)cl);
-            cudaLaunchConfig_t cfg;
-            memset(&cfg, 0, sizeof cfg);
+            cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3((unsigned)cl);
             cfg.blockDim = dim3(CL_THREADS);
             cfg.dynamicSmemBytes = shp.smem;
@@ -1684,6 +1713,90 @@ static bool kcore_args_ok(uint64_t n, uint64_t m, uint32_t r, bool csr) {
 }
 
 static bool use_csr(uint32_t k, uint32_t flags) { return (flags & PEEL_FLAG_CSR) || k >= 3; }
+
+// ---- the binned build for one vertex shard (shard.h; used by dist.cu) --------------------
+struct ShardBins {
+    uint64_t nbins, total_cap;
+    size_t cursor, base, cap, flag, entries, total;
+};
+
+static ShardBins shard_bins(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
+    ShardBins B;
+    B.nbins = (nloc + (1ull << BIN_SHIFT) - 1) >> BIN_SHIFT;
+    B.total_cap = 0;
+    for (uint64_t b = 0; b < B.nbins; b++) B.total_cap += bin_capacity(n, nloc, m, r, b);
+    size_t o = 0;
+    B.cursor = o; o += al(sizeof(ull) * B.nbins);
+    B.base = o; o += al(sizeof(ull) * B.nbins);
+    B.cap = o; o += al(sizeof(ull) * B.nbins);
+    B.flag = o; o += al(sizeof(uint32_t));
+    B.entries = o; o += al(sizeof(ull) * B.total_cap);
+    B.total = o;
+    return B;
+}
+
+size_t shard_build_bytes(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
+    if (nloc <= BIN_MIN_N || r < 2 || r > 8) return 0;
+    return shard_bins(n, m, r, nloc).total;
+}
+
+template <int R>
+static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1, ull *state,
+                                 uint32_t *err, char *scratch, cudaStream_t s, bool *overflow) {
+    const uint64_t nloc = v1 - v0;
+    const ShardBins B = shard_bins(n, m, R, nloc);
+    ull *cursor = (ull *)(scratch + B.cursor), *base = (ull *)(scratch + B.base), *cap = (ull *)(scratch + B.cap);
+    uint32_t *flag = (uint32_t *)(scratch + B.flag);
+    ull *entries = (ull *)(scratch + B.entries);
+    *overflow = false;
+    PEEL_CUDA(cudaMemsetAsync(state, 0, sizeof(ull) * nloc, s));
+    PEEL_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), s));
+    {
+        ProfScope ps("bin_init", s);
+        bin_init_kernel<<<1, 32, 0, s>>>(n, nloc, m, R, B.nbins, cursor, base, cap);
+    }
+    const size_t smem = partition_smem(R, B.nbins);
+    PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int pb = 0;
+    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, bin_partition_kernel<R>, PART_BLOCK, smem));
+    if (pb < 1) pb = 1;
+    if (m) {
+        ProfScope ps("bin_partition", s);
+        bin_partition_kernel<R><<<num_sms() * pb, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)B.nbins, cursor, base, cap,
+                                                                          entries, err, flag, v0, v1);
+    }
+    PEEL_CUDA(cudaGetLastError());
+    uint32_t hflag = 0;
+    PEEL_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof hflag, cudaMemcpyDeviceToHost, s));
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    if (hflag) {
+        *overflow = true;
+        return PEEL_OK;
+    }
+    uint64_t maxcap = 0;
+    for (uint64_t b = 0; b < B.nbins; b++) maxcap = std::max<uint64_t>(maxcap, bin_capacity(n, nloc, m, R, b));
+    const dim3 grid((unsigned)((maxcap + 256 * CSRB_PER - 1) / (256 * CSRB_PER)), (unsigned)B.nbins);
+    if (m) {
+        ProfScope ps("bin_red", s);
+        bin_red_kernel<<<grid, 256, 0, s>>>(entries, base, cursor, state);
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+
+peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
+                        unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow) {
+    switch (r) {
+        case 2: return shard_build_r<2>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 3: return shard_build_r<3>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 4: return shard_build_r<4>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 5: return shard_build_r<5>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 6: return shard_build_r<6>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 7: return shard_build_r<7>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 8: return shard_build_r<8>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+    }
+    return PEEL_EINVAL;
+}
 
 }  // namespace peel
 

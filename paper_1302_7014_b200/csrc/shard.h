@@ -1,0 +1,22 @@
+// shard.h -- internal (not part of the C-ABI): the binned build of kcore.cu applied to one
+// vertex shard [v0, v1) of an n-vertex instance, for the partitioned peel of dist.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "peel.h"
+
+namespace peel {
+
+// scratch bytes for shard_build (bin cursors, bases, capacities, flag, entries), or 0 if a
+// shard of nloc vertices is small enough for the direct build (state <= 64 MB, L2-resident)
+size_t shard_build_bytes(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc);
+
+// state[0 .. v1-v0) <- the packed (count | id sum << 32) states of the shard's vertices, from
+// every edge of `edges` (validated: bad edges set ERR bit 1 in *err).  *overflow = true if a
+// bin exceeded its capacity (adversarial degree skew): the caller then builds directly.
+// Stream-ordered except for one small device-to-host read of the overflow flag.
+peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
+                        unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow);
+
+}  // namespace peel

@@ -94,3 +94,20 @@ def test_nccl_transport_world1():
     env = dict(os.environ, REPO=repo, PORT=str(port))
     out = subprocess.run([sys.executable, "-c", NCCL_WORLD1], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "NCCL_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_binned_shard_build_vs_oracle(P):
+    """Shards larger than 2^23 vertices use the binned build restricted to their endpoints
+    (shard.h): bit-exact against the oracle, with a ragged n; then the same graph with a hub
+    that overflows a bin (direct-build fallback)."""
+    n = (1 << 24) + 12345
+    m = int(0.75 * n)
+    e = O.gen_hypergraph(n, m, 3, seed=31 + P)
+    check(e, n, 2, P)
+    hub = e[: 400000].copy()
+    hub[:, 0] = 7                      # vertex 7 is in 400k edges: its bin overflows
+    hub[:, 1] = np.where(hub[:, 1] == 7, 8, hub[:, 1])
+    hub[:, 2] = np.where(hub[:, 2] == 7, 9, hub[:, 2])
+    ok = (hub[:, 1] != hub[:, 2]) & (hub[:, 1] != 7) & (hub[:, 2] != 7)
+    check(np.concatenate([hub[ok], e[400000:]]), n, 2, P)

@@ -18,6 +18,7 @@
 // Bit-exact with the single-GPU peel by construction: every vertex's count sees exactly
 // the decrements of its killed edges, and F_{t+1} is the set of k -> k-1 crossings.
 #include <nccl.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -61,6 +62,8 @@ struct DShard {
     uint32_t *send;        // P segments of cap (v1 - v0) each
     uint32_t *recv;        // cap n
     DCtl *ctl;
+    bool binned;           // the shard was built binned: its bins serve the binned rounds
+    char *bins;            // shard_build scratch
 };
 
 struct DLayout {
@@ -249,9 +252,171 @@ __global__ void __launch_bounds__(DB) dist_recv_kernel(DKArgs a, const uint32_t 
     block_add<DB>(&a.ctl->kills, kills);
 }
 
+// ---- binned rounds on a shard (large local frontiers) -------------------------------------
+// Same split as the single-GPU binned rounds (kcore.cu): the kill kernel stages the round's
+// decrements of OWNED endpoints in the shard's vertex bins (shared-memory counting sort, one
+// global atomic per bin per chunk, coalesced runs) instead of applying them as random
+// read-modify-writes; shard_apply then applies them bin by bin with L2-resident atomics.
+// RECV = false: entries are the local frontier (v, e), remote owners are sent e;
+// RECV = true: entries are edge ids received from other shards.
+static constexpr int DKU = 4;                  // entries per thread per chunk
+static constexpr int DKCH = DB * DKU;          // entries per chunk
+
+static size_t dist_stage_smem(int r, uint32_t nbins) {
+    return 2 * sizeof(ull) * (size_t)r * DKCH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
+}
+
+template <int R, bool RECV>
+__global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint32_t *__restrict__ recv, ull nrecv,
+                                                            ShardBinsView bv) {
+    extern __shared__ unsigned char smem_raw[];
+    constexpr int SE = R * DKCH;
+    const uint32_t nbins = bv.nbins;
+    ull *sent = (ull *)smem_raw;                  // [SE] unsorted (e << 32 | local u)
+    ull *sorted = sent + SE;                      // [SE]
+    ull *gpos = sorted + SE;                      // [nbins]
+    uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
+    uint32_t *offs = hist + nbins;                // [nbins]
+    uint32_t *fill = offs + nbins;                // [nbins]
+    __shared__ DIdQ qs[8];
+    __shared__ uint32_t wsum[DB / 32], total;
+    if (!RECV)
+        for (int d = 0; d < 8; d++) bq_init(qs[d]);
+    const ull nE = RECV ? nrecv : a.nE;
+    const ull lmask = (1ull << SHARD_BIN_SHIFT) - 1;
+    ull kills = 0;
+    int slot = 0;
+    for (uint64_t base = (uint64_t)blockIdx.x * DKCH; base < nE; base += (uint64_t)gridDim.x * DKCH) {
+        for (uint32_t b = threadIdx.x; b < nbins; b += DB) { hist[b] = 0; fill[b] = 0; }
+        uint2 ent[DKU];
+        bool win[DKU];
+        #pragma unroll
+        for (int j = 0; j < DKU; j++) {
+            const uint64_t i = base + (uint64_t)j * DB + threadIdx.x;
+            if (RECV) ent[j] = make_uint2(0xFFFFFFFFu, i < nE ? __ldcg(recv + i) : 0u);
+            else ent[j] = i < nE ? __ldcg(a.Fc + i) : make_uint2(0u, 0u);
+        }
+        #pragma unroll
+        for (int j = 0; j < DKU; j++) {
+            const uint64_t i = base + (uint64_t)j * DB + threadIdx.x;
+            win[j] = false;
+            if (i < nE) {
+                const uint32_t e = ent[j].y, bit = 1u << (e & 31);
+                win[j] = (atomicAnd(a.alive + (e >> 5), ~bit) & bit) != 0;
+            }
+        }
+        uint32_t u[DKU][R];
+        uint32_t mine = 0, sendm[DKU];
+        #pragma unroll
+        for (int j = 0; j < DKU; j++) {
+            sendm[j] = 0;
+            if (!win[j]) continue;
+            load_row<R>(a.edges, ent[j].y, a.m, a.edges_vec, u[j]);
+            uint32_t mn = 0xFFFFFFFFu;
+            #pragma unroll
+            for (int r = 0; r < R; r++) {
+                mn = min(mn, u[j][r]);
+                const bool own = u[j][r] >= a.v0 && u[j][r] < a.v1;
+                if (own && (RECV || u[j][r] != ent[j].x)) mine++;
+                if (!own) sendm[j] |= 1u << owner_of(u[j][r], a.n, a.P);
+            }
+            if (owner_of(mn, a.n, a.P) == a.p) kills++;
+        }
+        if (!RECV) {
+            // one push per destination; d is warp-uniform (each coalesced group targets one queue)
+            #pragma unroll
+            for (int j = 0; j < DKU; j++)
+                for (int d = 0; d < a.P; d++)
+                    if (sendm[j] >> d & 1u) bq_push(qs[d], slot, ent[j].y, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
+        }
+        // block exclusive scan of per-thread staged counts -> staging positions
+        uint32_t x = mine;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) >= (unsigned)o) x += y;
+        }
+        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint32_t w = threadIdx.x < DB / 32 ? wsum[threadIdx.x] : 0, z = w;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (threadIdx.x >= (unsigned)o) z += y;
+            }
+            if (threadIdx.x < DB / 32) wsum[threadIdx.x] = z - w;
+            if (threadIdx.x == DB / 32 - 1) total = z;
+        }
+        __syncthreads();
+        uint32_t pos = wsum[threadIdx.x >> 5] + x - mine;
+        #pragma unroll
+        for (int j = 0; j < DKU; j++)
+            if (win[j]) {
+                #pragma unroll
+                for (int r = 0; r < R; r++)
+                    if (u[j][r] >= a.v0 && u[j][r] < a.v1 && (RECV || u[j][r] != ent[j].x)) {
+                        const uint32_t lu = (uint32_t)(u[j][r] - a.v0);
+                        sent[pos++] = ((ull)ent[j].y << 32) | lu;
+                        atomicAdd(&hist[lu >> SHARD_BIN_SHIFT], 1u);
+                    }
+            }
+        __syncthreads();
+        const uint32_t tot = total;
+        if (threadIdx.x < 32) {
+            const uint32_t per = (nbins + 31) / 32;
+            uint32_t loc = 0;
+            for (uint32_t q2 = 0; q2 < per; q2++) {
+                uint32_t b = threadIdx.x * per + q2;
+                loc += b < nbins ? hist[b] : 0;
+            }
+            uint32_t z = loc;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+                if (threadIdx.x >= (unsigned)o) z += y;
+            }
+            uint32_t run = z - loc;
+            for (uint32_t q2 = 0; q2 < per; q2++) {
+                uint32_t b = threadIdx.x * per + q2;
+                if (b < nbins) { offs[b] = run; run += hist[b]; }
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nbins; b += DB)
+            if (hist[b]) gpos[b] = atomicAdd(bv.cursor + b, (ull)hist[b]);
+        for (uint32_t i = threadIdx.x; i < tot; i += DB) {
+            const ull v = sent[i];
+            const uint32_t b = (uint32_t)v >> SHARD_BIN_SHIFT;
+            sorted[offs[b] + atomicAdd(&fill[b], 1u)] = v;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < tot; i += DB) {
+            const ull v = sorted[i];
+            const uint32_t b = (uint32_t)v >> SHARD_BIN_SHIFT;
+            bv.entries[bv.base[b] + gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ lmask);
+        }
+        if (!RECV)
+            for (int d = 0; d < a.P; d++) bq_flush(qs[d], slot, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
+        slot ^= 1;
+        __syncthreads();
+    }
+    block_add<DB>(&a.ctl->kills, kills);
+}
+
 __global__ void dist_mask_kernel(const ull *__restrict__ state, uint64_t nloc, uint32_t k, uint8_t *mask) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nloc; i += (uint64_t)gridDim.x * blockDim.x)
         mask[i] = (uint32_t)state[i] >= k ? 1 : 0;
+}
+
+// binned-round threshold for a shard of nloc vertices: as kcore.cu's bin_round_frac
+static double dist_bin_frac(uint64_t nloc) {
+    const char *e = getenv("PEEL_BIN_ROUND_FRAC");
+    if (e) {
+        const double f = atof(e);
+        return f > 0.0 ? f : 2.0;  // 0 disables (no frontier reaches 2 nloc)
+    }
+    return 8.0 * (double)nloc >= 2e9 ? 0.02 : 0.05;
 }
 
 static unsigned dgrid(uint64_t work) {
@@ -362,6 +527,8 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         d.F[1] = (uint2 *)(b + L.F1);
         d.send = (uint32_t *)(b + L.send);
         d.recv = (uint32_t *)(b + L.recv);
+        d.bins = b + L.bins;
+        d.binned = false;
         sh.push_back(d);
     }
     for (auto &d : sh) {
@@ -369,11 +536,13 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         PEEL_CUDA(cudaMemsetAsync(d.alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s));
         // large shards: the binned build of kcore.cu restricted to the shard's endpoints
         bool direct = true;
+        d.binned = false;
         if (L.bins_bytes && d.v1 - d.v0 > 0) {
             char *b = ws + (c->virt ? (size_t)d.q * L.total : 0);
             peel_status st = shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct);
             if (st != PEEL_OK) return st;
         }
+        d.binned = !direct;  // bins usable by the binned rounds (no overflow)
         if (direct) {  // small shard, or a bin overflowed
             PEEL_CUDA(cudaMemsetAsync(d.state, 0, sizeof(ull) * (d.v1 - d.v0), s));
             if (m) {
@@ -436,7 +605,8 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         }
         st = fetch_ctl();
         if (st != PEEL_OK) return st;
-        // kill
+        // kill: binned (decrements staged in the shard's bins) while the local frontier is large
+        std::vector<char> binr(sh.size(), 0);
         for (size_t i = 0; i < sh.size(); i++) {
             DShard &d = sh[i];
             DKArgs a;
@@ -446,8 +616,20 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             a.state = d.state; a.alive = d.alive;
             a.Fc = d.F[cur]; a.nE = hc[i].ne[cur]; a.Fn = d.F[nxt];
             a.send = d.send; a.ctl = d.ctl; a.par = nxt;
-            ProfScope ps("dist_kill", s);
-            dist_kill_kernel<R><<<dgrid(a.nE), DB, 0, s>>>(a);
+            binr[i] = d.binned && (double)a.nE >= dist_bin_frac(d.v1 - d.v0) * (double)(d.v1 - d.v0);
+            if (binr[i]) {
+                const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
+                PEEL_CUDA(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s));
+                const size_t sm = dist_stage_smem(R, bv.nbins);
+                PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                int kb = 0;
+                PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, false>, DB, sm));
+                ProfScope ps("dist_kill_binned", s);
+                dist_kill_bin_kernel<R, false><<<num_sms() * (kb < 1 ? 1 : kb), DB, sm, s>>>(a, nullptr, 0, bv);
+            } else {
+                ProfScope ps("dist_kill", s);
+                dist_kill_kernel<R><<<dgrid(a.nE), DB, 0, s>>>(a);
+            }
         }
         PEEL_CUDA(cudaGetLastError());
         st = fetch_ctl();
@@ -501,10 +683,9 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             PEEL_NCCL(ncclGroupEnd());
             nrecv[0] = off;
         }
-        // receive
+        // receive (binned shards stage the received kills, then apply the round's bins)
         for (size_t i = 0; i < sh.size(); i++) {
             DShard &d = sh[i];
-            if (!nrecv[i]) continue;
             DKArgs a;
             a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
             a.edges_vec = ((uintptr_t)edges & 15) == 0;
@@ -512,6 +693,21 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             a.state = d.state; a.alive = d.alive;
             a.Fc = nullptr; a.nE = 0; a.Fn = d.F[nxt];
             a.send = d.send; a.ctl = d.ctl; a.par = nxt;
+            if (binr[i]) {
+                const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
+                if (nrecv[i]) {
+                    const size_t sm = dist_stage_smem(R, bv.nbins);
+                    PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    int kb = 0;
+                    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, true>, DB, sm));
+                    ProfScope ps("dist_recv_binned", s);
+                    dist_kill_bin_kernel<R, true><<<num_sms() * (kb < 1 ? 1 : kb), DB, sm, s>>>(a, d.recv, nrecv[i], bv);
+                }
+                peel_status st2 = shard_apply(d.v1 - d.v0, d.v0, k, d.state, d.F[nxt], bv, t, &d.ctl->nf[nxt], &d.ctl->ne[nxt], s);
+                if (st2 != PEEL_OK) return st2;
+                continue;
+            }
+            if (!nrecv[i]) continue;
             ProfScope ps("dist_recv", s);
             dist_recv_kernel<R><<<dgrid(nrecv[i]), DB, 0, s>>>(a, d.recv, nrecv[i]);
         }

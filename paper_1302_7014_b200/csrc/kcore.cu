@@ -68,6 +68,7 @@ struct Layout {
 // 2^BIN_SHIFT vertices (32 MB of state, L2-resident), then each bin is accumulated with
 // L2 atomics and scanned for the round-1 frontier while it is still in L2.
 static constexpr int BIN_SHIFT = 22;
+static_assert(BIN_SHIFT == SHARD_BIN_SHIFT, "dist.cu stages decrements in kcore.cu's bins");
 static constexpr uint64_t BIN_MIN_N = 1ull << 23;  // below this the state fits L2: direct build
 
 __host__ __device__ inline uint64_t bin_size(uint64_t n, uint64_t b) {
@@ -496,6 +497,7 @@ struct PeelArgs {
     uint64_t cs;             // subround mode: class size n / r
     ull *sub;                // subround mode: counters [class][buffer][kind: 0 |F|, 1 entries]
     ull *rtime;              // %globaltimer at the start of each round (profiling)
+    uint64_t v0;             // vertex id of state[0] (a shard of dist.cu; 0 otherwise)
 };
 
 __device__ __forceinline__ uint32_t count_of(ull w) { return (uint32_t)w; }
@@ -842,7 +844,7 @@ __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, Bin
             const uint32_t i = threadIdx.x + r * PEEL_BLOCK;
             if (i < nin && count_of(old[r]) == k) {
                 crossed++;
-                const uint32_t u = (b << BIN_SHIFT) + (uint32_t)(x[r] & mask);
+                const uint32_t u = (uint32_t)(a.v0 + (b << BIN_SHIFT)) + (uint32_t)(x[r] & mask);
                 if (a.peel_round) a.peel_round[u] = t + 1;
                 bq_push(q, slot, make_uint2(u, idsum_of(old[r]) - (uint32_t)(x[r] >> 32)), Fn, cn);
             }
@@ -1717,7 +1719,7 @@ static bool use_csr(uint32_t k, uint32_t flags) { return (flags & PEEL_FLAG_CSR)
 // ---- the binned build for one vertex shard (shard.h; used by dist.cu) --------------------
 struct ShardBins {
     uint64_t nbins, total_cap;
-    size_t cursor, base, cap, flag, entries, total;
+    size_t cursor, base, cap, flag, ctl, entries, total;
 };
 
 static ShardBins shard_bins(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
@@ -1729,7 +1731,8 @@ static ShardBins shard_bins(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
     B.cursor = o; o += al(sizeof(ull) * B.nbins);
     B.base = o; o += al(sizeof(ull) * B.nbins);
     B.cap = o; o += al(sizeof(ull) * B.nbins);
-    B.flag = o; o += al(sizeof(uint32_t));
+    B.flag = o; o += al(sizeof(uint32_t) + 8 + sizeof(ull));  // overflow flag, then the D work counter
+    B.ctl = o; o += al(sizeof(Ctl));                           // binned rounds: round_apply's counters
     B.entries = o; o += al(sizeof(ull) * B.total_cap);
     B.total = o;
     return B;
@@ -1781,6 +1784,58 @@ static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, 
         bin_red_kernel<<<grid, 256, 0, s>>>(entries, base, cursor, state);
     }
     PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+
+ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc, char *scratch) {
+    const ShardBins B = shard_bins(n, m, r, nloc);
+    ShardBinsView v;
+    v.nbins = (uint32_t)B.nbins;
+    v.cursor = (ull *)(scratch + B.cursor);
+    v.base = (const ull *)(scratch + B.base);
+    v.entries = (ull *)(scratch + B.entries);
+    v.work = (ull *)(scratch + B.flag + 8);  // after the overflow flag, in the same 256-byte slot
+    v.ctl = scratch + B.ctl;
+    return v;
+}
+
+// phase D of a binned round on a shard: the decrements staged in the shard's bins (by
+// dist.cu's kill/receive kernels) are applied by round_apply_kernel; crossings append
+// (v0 + local id, remaining edge) to Fn.  |F_{t+1}| and Fn's length are copied to out_nf /
+// out_ne (device words).
+peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long long *state, void *Fn,
+                        const ShardBinsView &v, uint32_t t, unsigned long long *out_nf, unsigned long long *out_ne,
+                        cudaStream_t s) {
+    Ctl *ctl = (Ctl *)v.ctl;
+    PEEL_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), s));
+    PEEL_CUDA(cudaMemsetAsync(v.work, 0, sizeof(ull), s));
+    PeelArgs a;
+    memset(&a, 0, sizeof a);
+    a.n = nloc;
+    a.k = k;
+    a.state = state;
+    a.F[0] = a.F[1] = Fn;
+    a.ctl = ctl;
+    a.v0 = v0;
+    BinRound br;
+    memset(&br, 0, sizeof br);
+    br.nbins = v.nbins;
+    br.cursor = v.cursor;
+    br.base = v.base;
+    br.entries = v.entries;
+    br.work = v.work;
+    br.t = t;
+    const size_t dsmem = sizeof(uint32_t) * (v.nbins + 1);
+    int db = 0;
+    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
+    db = db < 1 ? 1 : db;
+    {
+        ProfScope ps("round_apply", s);
+        round_apply_kernel<<<num_sms() * db, PEEL_BLOCK, dsmem, s>>>(a, br);
+    }
+    PEEL_CUDA(cudaGetLastError());
+    PEEL_CUDA(cudaMemcpyAsync(out_nf, &ctl->nf[t % 3], sizeof(ull), cudaMemcpyDeviceToDevice, s));
+    PEEL_CUDA(cudaMemcpyAsync(out_ne, &ctl->ne[t % 3], sizeof(ull), cudaMemcpyDeviceToDevice, s));
     return PEEL_OK;
 }
 

@@ -19,4 +19,25 @@ size_t shard_build_bytes(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc);
 peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
                         unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow);
 
+// the shard's bins as the binned rounds use them: per-bin cursors and bases into `entries`
+// (capacities from the build: a round's decrements of a bin are a subset of the build's),
+// the apply phase's work counter, and an opaque control block for its counters
+struct ShardBinsView {
+    uint32_t nbins;
+    unsigned long long *cursor;
+    const unsigned long long *base;
+    unsigned long long *entries;
+    unsigned long long *work;
+    char *ctl;
+};
+ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc, char *scratch);
+
+// phase D of a binned round t on the shard starting at vertex v0 (see kcore.cu)
+peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long long *state, void *Fn,
+                        const ShardBinsView &v, uint32_t t, unsigned long long *out_nf, unsigned long long *out_ne,
+                        cudaStream_t s);
+
+// BIN_SHIFT of kcore.cu (vertex bins of 2^22 local ids)
+constexpr int SHARD_BIN_SHIFT = 22;
+
 }  // namespace peel

@@ -66,7 +66,8 @@ torch.cuda.set_device(0)
 dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%s" % os.environ["PORT"], rank=0, world_size=1,
                         device_id=torch.device("cuda:0"))
 comm = pk.Comm.from_process_group()
-for (n, c, r, seed) in [(100003, 0.75, 3, 5), (50021, 0.85, 3, 6), (40009, 0.8, 4, 7)]:
+for (n, c, r, seed) in [(100003, 0.75, 3, 5), (50021, 0.85, 3, 6), (40009, 0.8, 4, 7),
+                        ((1 << 24) + 12345, 0.75, 3, 8)]:  # the last one: binned build and rounds
     e = O.gen_hypergraph(n, int(c * n), r, seed)
     ref = O.sync_peel(e, n, 2)
     res = pk.peel_kcore_dist(comm, torch.from_numpy(e.view(np.int32)).cuda(), n, 2)

@@ -60,6 +60,7 @@ struct Ctl {
 struct Layout {
     size_t ctl, stats, sub, rtime, state, deg, off, bsum, adj, alive, F0, F1;
     size_t bins, bin_cursor, bin_base, bin_cap, entries;  // binned build (packed, n > BIN_MIN_N)
+    size_t esort;                                          // binned rounds: edge-bin counters of the frontier sort
     uint64_t nbins, total_cap;
     size_t total;
 };
@@ -69,7 +70,10 @@ struct Layout {
 // L2 atomics and scanned for the round-1 frontier while it is still in L2.
 static constexpr int BIN_SHIFT = 22;
 static_assert(BIN_SHIFT == SHARD_BIN_SHIFT, "dist.cu stages decrements in kcore.cu's bins");
-static constexpr uint64_t BIN_MIN_N = 1ull << 23;  // below this the state fits L2: direct build
+static constexpr uint64_t BIN_MIN_N = 1ull << 23;
+// binned rounds sort the frontier by edge bin (2^EB_SHIFT edges: 512 KB of alive bits, 48 MB
+// of r=3 rows) before the kill phase, so the blocks in flight test alive bits of one bin
+static constexpr int EB_SHIFT = 22;  // below this the state fits L2: direct build
 
 __host__ __device__ inline uint64_t bin_size(uint64_t n, uint64_t b) {
     uint64_t lo = b << BIN_SHIFT, hi = (b + 1) << BIN_SHIFT;
@@ -111,6 +115,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
     L.F1 = o; o += al(fe * n);
     L.nbins = 0; L.total_cap = 0;
     L.bins = L.bin_cursor = L.bin_base = L.bin_cap = L.entries = 0;
+    L.esort = 0;
     if (n > BIN_MIN_N) {  // packed: binned build + rounds; CSR: binned degree count + scatter
         L.nbins = (n + (1ull << BIN_SHIFT) - 1) >> BIN_SHIFT;
         for (uint64_t b = 0; b < L.nbins; b++) L.total_cap += bin_capacity(n, n, m, r, b);
@@ -119,6 +124,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         L.bin_base = o; o += al(sizeof(ull) * L.nbins);
         L.bin_cap = o; o += al(sizeof(ull) * L.nbins);
         L.entries = o; o += al(sizeof(ull) * L.total_cap);
+        L.esort = o; o += al(sizeof(ull) * 2 * (((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT) + 1));
     }
     L.total = o;
     return L;
@@ -638,6 +644,7 @@ struct BinRound {
     ull *entries;
     ull *work;          // D work-item counter
     uint32_t t;         // the round
+    const uint2 *Fsrc;  // K: the round's frontier entries (edge-sorted copy), or null: F[(t-1)&1]
 };
 
 template <int R>
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
     Ctl *ctl = a.ctl;
     const uint32_t t = br.t;
     const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
-    const uint2 *Fc = (const uint2 *)a.F[(t - 1) & 1];
+    const uint2 *Fc = br.Fsrc ? br.Fsrc : (const uint2 *)a.F[(t - 1) & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
         a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap)] = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
@@ -759,6 +766,104 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
         __syncthreads();
     }
     block_add<PART_BLOCK>(&a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap) + 1], kills);
+}
+
+// ---- frontier sort by edge bin (binned rounds) ---------------------------------------------
+// Two-pass counting sort of the entries (v, e) by e >> EB_SHIFT: per-block shared histograms,
+// one scan, then a scatter in which each block counting-sorts a chunk in shared memory and
+// writes one run per bin.  The kill phase then reads the entries in edge-bin order, so the
+// alive bits (and the rows) it touches at a time cover ~one edge bin: L2 hits instead of
+// random DRAM granules.
+static constexpr int ES_CH = 4096;  // entries per chunk (scatter)
+
+__global__ void __launch_bounds__(256) esort_hist_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
+                                                         uint32_t nb, ull *ghist) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t b = threadIdx.x; b < nb; b += 256) sh[b] = 0;
+    __syncthreads();
+    const ull N = ld_cg_u64(pN);
+    for (ull i = blockIdx.x * 256ull + threadIdx.x; i < N; i += (ull)gridDim.x * 256)
+        atomicAdd(&sh[__ldcg(&F[i].y) >> EB_SHIFT], 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nb; b += 256)
+        if (sh[b]) atomicAdd(ghist + b, (ull)sh[b]);
+}
+
+__global__ void esort_scan_kernel(ull *ghist, ull *cursor, uint32_t nb) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        ull o = 0;
+        for (uint32_t b = 0; b < nb; b++) {
+            const ull c = ghist[b];
+            cursor[b] = o;
+            ghist[b] = 0;  // ready for the next round
+            o += c;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) esort_scatter_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
+                                                            uint32_t nb, ull *cursor, uint2 *out) {
+    extern __shared__ unsigned char smem_raw[];
+    uint2 *buf = (uint2 *)smem_raw;              // [ES_CH] the chunk, bin-sorted
+    ull *gpos = (ull *)(buf + ES_CH);            // [nb]
+    uint32_t *hist = (uint32_t *)(gpos + nb);    // [nb]
+    uint32_t *offs = hist + nb;                  // [nb]
+    uint32_t *fill = offs + nb;                  // [nb]
+    const ull N = ld_cg_u64(pN);
+    for (ull c0 = (ull)blockIdx.x * ES_CH; c0 < N; c0 += (ull)gridDim.x * ES_CH) {
+        const uint32_t ne = (uint32_t)min((ull)ES_CH, N - c0);
+        for (uint32_t b = threadIdx.x; b < nb; b += 256) { hist[b] = 0; fill[b] = 0; }
+        __syncthreads();
+        uint2 v[ES_CH / 256];
+        #pragma unroll
+        for (int j = 0; j < ES_CH / 256; j++) {
+            const uint32_t i = j * 256 + threadIdx.x;
+            v[j] = i < ne ? __ldcs(F + c0 + i) : make_uint2(0u, 0u);
+            if (i < ne) atomicAdd(&hist[v[j].y >> EB_SHIFT], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // exclusive scan of hist (nb <= 1024): one warp
+            const uint32_t per = (nb + 31) / 32;
+            uint32_t loc = 0;
+            for (uint32_t q = 0; q < per; q++) {
+                const uint32_t b = threadIdx.x * per + q;
+                loc += b < nb ? hist[b] : 0;
+            }
+            uint32_t x = loc;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if ((int)threadIdx.x >= o) x += y;
+            }
+            uint32_t run = x - loc;
+            for (uint32_t q = 0; q < per; q++) {
+                const uint32_t b = threadIdx.x * per + q;
+                if (b < nb) { offs[b] = run; run += hist[b]; }
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nb; b += 256)
+            if (hist[b]) gpos[b] = atomicAdd(cursor + b, (ull)hist[b]);
+        #pragma unroll
+        for (int j = 0; j < ES_CH / 256; j++) {
+            const uint32_t i = j * 256 + threadIdx.x;
+            if (i < ne) {
+                const uint32_t b = v[j].y >> EB_SHIFT;
+                buf[offs[b] + atomicAdd(&fill[b], 1u)] = v[j];
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < ne; i += 256) {
+            const uint2 x = buf[i];
+            const uint32_t b = x.y >> EB_SHIFT;
+            out[gpos[b] + (i - offs[b])] = x;
+        }
+        __syncthreads();
+    }
+}
+
+static size_t esort_scatter_smem(uint32_t nb) {
+    return sizeof(uint2) * ES_CH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nb;
 }
 
 static size_t kill_partition_smem(int r, uint32_t nbins) {
@@ -1632,6 +1737,17 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         kb = kb < 1 ? 1 : kb;
         db = db < 1 ? 1 : db;
         if (const char *ev = getenv("PEEL_D_BPS")) db = std::min(db, std::max(1, atoi(ev)));
+        // frontier sort by edge bin before each kill phase (PEEL_ESORT=0 disables, for A/B)
+        const char *esv = getenv("PEEL_ESORT");
+        const bool esort = !(esv && atoi(esv) == 0);
+        const uint32_t enb = (uint32_t)((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT);
+        ull *ehist = (ull *)(ws + L.esort), *ecur = ehist + enb + 1;
+        const size_t essmem = esort_scatter_smem(enb);
+        if (esort) {
+            PEEL_CUDA(cudaMemsetAsync(ehist, 0, sizeof(ull) * (enb + 1), s));
+            PEEL_CUDA(cudaFuncSetAttribute(esort_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)essmem));
+        }
+        br.Fsrc = nullptr;
         uint32_t t = 1;
         for (;;) {
             Ctl h;
@@ -1646,6 +1762,19 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             PEEL_CUDA(cudaMemsetAsync(cursor, 0, sizeof(ull) * L.nbins, s));
             PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
             br.t = t;
+            br.Fsrc = nullptr;
+            if (esort && m) {
+                const uint2 *src = (const uint2 *)a.F[(t - 1) & 1];
+                uint2 *dst = (uint2 *)a.F[t & 1];  // free until this round's apply writes F_{t+1}
+                const ull *pN = &ctl->ne[(t - 1) % 3];
+                ProfScope ps("frontier_edge_sort", s);
+                esort_hist_kernel<<<grid_for(nE, 8), 256, sizeof(uint32_t) * enb, s>>>(src, pN, enb, ehist);
+                esort_scan_kernel<<<1, 32, 0, s>>>(ehist, ecur, enb);
+                const uint64_t chunks = (nE + ES_CH - 1) / ES_CH;
+                const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * 4);
+                esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>(src, pN, enb, ecur, dst);
+                br.Fsrc = dst;
+            }
             {
                 ProfScope ps("round_kill_partition", s);
                 round_kill_partition_kernel<R><<<num_sms() * kb, PART_BLOCK, ksmem, s>>>(a, br);

@@ -645,6 +645,8 @@ struct BinRound {
     ull *work;          // D work-item counter
     uint32_t t;         // the round
     const uint2 *Fsrc;  // K: the round's frontier entries (edge-sorted copy), or null: F[(t-1)&1]
+    ull *ehist;         // D: histogram of F_{t+1} by edge bin for the next round's sort, or null
+    uint32_t enb;       // D: edge bins
 };
 
 template <int R>
@@ -883,10 +885,13 @@ typedef BlockQueueT<uint2, 2 * PEEL_BLOCK, PEEL_BLOCK> ApplyQ;
 __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, BinRound br) {
     extern __shared__ unsigned char smem_raw[];
     uint32_t *pre = (uint32_t *)smem_raw;  // [nbins + 1] prefix of work items per bin
+    uint32_t *ehs = pre + br.nbins + 1;    // [enb] F_{t+1} by edge bin (when br.ehist)
     __shared__ ApplyQ q;
     __shared__ ull item;
     Ctl *ctl = a.ctl;
     const uint32_t t = br.t, nbins = br.nbins, k = a.k;
+    if (br.ehist)
+        for (uint32_t b = threadIdx.x; b < br.enb; b += PEEL_BLOCK) ehs[b] = 0;
     if (threadIdx.x == 0) {
         uint32_t acc = 0;
         for (uint32_t b = 0; b < nbins; b++) {
@@ -950,13 +955,20 @@ __global__ void __launch_bounds__(PEEL_BLOCK) round_apply_kernel(PeelArgs a, Bin
             if (i < nin && count_of(old[r]) == k) {
                 crossed++;
                 const uint32_t u = (uint32_t)(a.v0 + (b << BIN_SHIFT)) + (uint32_t)(x[r] & mask);
+                const uint32_t e2 = idsum_of(old[r]) - (uint32_t)(x[r] >> 32);
                 if (a.peel_round) a.peel_round[u] = t + 1;
-                bq_push(q, slot, make_uint2(u, idsum_of(old[r]) - (uint32_t)(x[r] >> 32)), Fn, cn);
+                if (br.ehist) atomicAdd(&ehs[e2 >> EB_SHIFT], 1u);
+                bq_push(q, slot, make_uint2(u, e2), Fn, cn);
             }
         }
         bq_flush(q, slot, Fn, cn);
         slot ^= 1;
         __syncthreads();  // item is rewritten next iteration
+    }
+    if (br.ehist) {
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < br.enb; b += PEEL_BLOCK)
+            if (ehs[b]) atomicAdd(br.ehist + b, (ull)ehs[b]);
     }
     block_add<PEEL_BLOCK>(&ctl->nf[t % 3], crossed);
 }
@@ -1732,15 +1744,18 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                                        (int)ksmem));
         int kb = 0, db = 0;
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, round_kill_partition_kernel<R>, PART_BLOCK, ksmem));
-        const size_t dsmem = sizeof(uint32_t) * (br.nbins + 1);
+        // frontier sort by edge bin before each kill phase (PEEL_ESORT=0 disables, for A/B)
+        const char *esv = getenv("PEEL_ESORT");
+        const bool esort = !(esv && atoi(esv) == 0) && m > 0;
+        const uint32_t enb = (uint32_t)((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT);
+        // D also histograms F_{t+1} by edge bin, so rounds after the first skip the hist pass
+        const size_t dsmem = sizeof(uint32_t) * (br.nbins + 1) + (esort ? sizeof(uint32_t) * enb : 0);
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
         kb = kb < 1 ? 1 : kb;
         db = db < 1 ? 1 : db;
         if (const char *ev = getenv("PEEL_D_BPS")) db = std::min(db, std::max(1, atoi(ev)));
-        // frontier sort by edge bin before each kill phase (PEEL_ESORT=0 disables, for A/B)
-        const char *esv = getenv("PEEL_ESORT");
-        const bool esort = !(esv && atoi(esv) == 0);
-        const uint32_t enb = (uint32_t)((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT);
+        br.ehist = nullptr;
+        br.enb = enb;
         ull *ehist = (ull *)(ws + L.esort), *ecur = ehist + enb + 1;
         const size_t essmem = esort_scatter_smem(enb);
         if (esort) {
@@ -1763,17 +1778,19 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
             br.t = t;
             br.Fsrc = nullptr;
-            if (esort && m) {
+            if (esort) {
                 const uint2 *src = (const uint2 *)a.F[(t - 1) & 1];
                 uint2 *dst = (uint2 *)a.F[t & 1];  // free until this round's apply writes F_{t+1}
                 const ull *pN = &ctl->ne[(t - 1) % 3];
                 ProfScope ps("frontier_edge_sort", s);
-                esort_hist_kernel<<<grid_for(nE, 8), 256, sizeof(uint32_t) * enb, s>>>(src, pN, enb, ehist);
+                if (!br.ehist)  // round 1: F_1 came from the build; later rounds' D made the histogram
+                    esort_hist_kernel<<<grid_for(nE, 8), 256, sizeof(uint32_t) * enb, s>>>(src, pN, enb, ehist);
                 esort_scan_kernel<<<1, 32, 0, s>>>(ehist, ecur, enb);
                 const uint64_t chunks = (nE + ES_CH - 1) / ES_CH;
                 const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * 4);
                 esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>(src, pN, enb, ecur, dst);
                 br.Fsrc = dst;
+                br.ehist = ehist;
             }
             {
                 ProfScope ps("round_kill_partition", s);

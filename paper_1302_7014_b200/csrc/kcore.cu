@@ -124,7 +124,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         L.bin_base = o; o += al(sizeof(ull) * L.nbins);
         L.bin_cap = o; o += al(sizeof(ull) * L.nbins);
         L.entries = o; o += al(sizeof(ull) * L.total_cap);
-        L.esort = o; o += al(sizeof(ull) * 2 * (((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT) + 1));
+        L.esort = o; o += al(sizeof(ull) * 3 * (((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT) + 1));
     }
     L.total = o;
     return L;
@@ -791,26 +791,38 @@ __global__ void __launch_bounds__(256) esort_hist_kernel(const uint2 *__restrict
         if (sh[b]) atomicAdd(ghist + b, (ull)sh[b]);
 }
 
-__global__ void esort_scan_kernel(ull *ghist, ull *cursor, uint32_t nb) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        ull o = 0;
-        for (uint32_t b = 0; b < nb; b++) {
-            const ull c = ghist[b];
-            cursor[b] = o;
-            ghist[b] = 0;  // ready for the next round
-            o += c;
-        }
-    }
-}
-
+// ghist: the entries per edge bin (complete before the launch); cursor: zeroed.  Every block
+// derives the bins' start offsets from ghist itself (no separate scan launch).
 __global__ void __launch_bounds__(256) esort_scatter_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
-                                                            uint32_t nb, ull *cursor, uint2 *out) {
+                                                            uint32_t nb, const ull *__restrict__ ghist, ull *cursor,
+                                                            uint2 *out) {
     extern __shared__ unsigned char smem_raw[];
     uint2 *buf = (uint2 *)smem_raw;              // [ES_CH] the chunk, bin-sorted
     ull *gpos = (ull *)(buf + ES_CH);            // [nb]
-    uint32_t *hist = (uint32_t *)(gpos + nb);    // [nb]
+    ull *gstart = gpos + nb;                     // [nb] exclusive prefix of ghist
+    uint32_t *hist = (uint32_t *)(gstart + nb);  // [nb]
     uint32_t *offs = hist + nb;                  // [nb]
     uint32_t *fill = offs + nb;                  // [nb]
+    if (threadIdx.x < 32) {
+        const uint32_t per = (nb + 31) / 32;
+        ull loc = 0;
+        for (uint32_t q = 0; q < per; q++) {
+            const uint32_t b = threadIdx.x * per + q;
+            loc += b < nb ? ghist[b] : 0;
+        }
+        ull x = loc;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const ull y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((int)threadIdx.x >= o) x += y;
+        }
+        ull run = x - loc;
+        for (uint32_t q = 0; q < per; q++) {
+            const uint32_t b = threadIdx.x * per + q;
+            if (b < nb) { gstart[b] = run; run += ghist[b]; }
+        }
+    }
+    __syncthreads();
     const ull N = ld_cg_u64(pN);
     for (ull c0 = (ull)blockIdx.x * ES_CH; c0 < N; c0 += (ull)gridDim.x * ES_CH) {
         const uint32_t ne = (uint32_t)min((ull)ES_CH, N - c0);
@@ -845,7 +857,7 @@ __global__ void __launch_bounds__(256) esort_scatter_kernel(const uint2 *__restr
         }
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < nb; b += 256)
-            if (hist[b]) gpos[b] = atomicAdd(cursor + b, (ull)hist[b]);
+            if (hist[b]) gpos[b] = gstart[b] + atomicAdd(cursor + b, (ull)hist[b]);
         #pragma unroll
         for (int j = 0; j < ES_CH / 256; j++) {
             const uint32_t i = j * 256 + threadIdx.x;
@@ -865,7 +877,7 @@ __global__ void __launch_bounds__(256) esort_scatter_kernel(const uint2 *__restr
 }
 
 static size_t esort_scatter_smem(uint32_t nb) {
-    return sizeof(uint2) * ES_CH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nb;
+    return sizeof(uint2) * ES_CH + (2 * sizeof(ull) + 3 * sizeof(uint32_t)) * nb;
 }
 
 static size_t kill_partition_smem(int r, uint32_t nbins) {
@@ -1756,10 +1768,12 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         if (const char *ev = getenv("PEEL_D_BPS")) db = std::min(db, std::max(1, atoi(ev)));
         br.ehist = nullptr;
         br.enb = enb;
-        ull *ehist = (ull *)(ws + L.esort), *ecur = ehist + enb + 1;
+        // F_t's edge-bin histogram lives in ehist[t & 1]; round t's D fills ehist[(t + 1) & 1]
+        ull *ehist[2] = {(ull *)(ws + L.esort), (ull *)(ws + L.esort) + enb + 1};
+        ull *ecur = ehist[1] + enb + 1;
         const size_t essmem = esort_scatter_smem(enb);
         if (esort) {
-            PEEL_CUDA(cudaMemsetAsync(ehist, 0, sizeof(ull) * (enb + 1), s));
+            PEEL_CUDA(cudaMemsetAsync(ehist[1], 0, sizeof(ull) * (enb + 1), s));
             PEEL_CUDA(cudaFuncSetAttribute(esort_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)essmem));
         }
         br.Fsrc = nullptr;
@@ -1784,13 +1798,14 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                 const ull *pN = &ctl->ne[(t - 1) % 3];
                 ProfScope ps("frontier_edge_sort", s);
                 if (!br.ehist)  // round 1: F_1 came from the build; later rounds' D made the histogram
-                    esort_hist_kernel<<<grid_for(nE, 8), 256, sizeof(uint32_t) * enb, s>>>(src, pN, enb, ehist);
-                esort_scan_kernel<<<1, 32, 0, s>>>(ehist, ecur, enb);
+                    esort_hist_kernel<<<grid_for(nE, 8), 256, sizeof(uint32_t) * enb, s>>>(src, pN, enb, ehist[t & 1]);
+                PEEL_CUDA(cudaMemsetAsync(ecur, 0, sizeof(ull) * enb, s));
+                PEEL_CUDA(cudaMemsetAsync(ehist[(t + 1) & 1], 0, sizeof(ull) * enb, s));  // for this round's D
                 const uint64_t chunks = (nE + ES_CH - 1) / ES_CH;
                 const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * 4);
-                esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>(src, pN, enb, ecur, dst);
+                esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>(src, pN, enb, ehist[t & 1], ecur, dst);
                 br.Fsrc = dst;
-                br.ehist = ehist;
+                br.ehist = ehist[(t + 1) & 1];
             }
             {
                 ProfScope ps("round_kill_partition", s);

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
     for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {
         const int ne = (int)min((uint64_t)CH, m - c0);
         const int nw = ne * R;
-        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
         // stage the chunk's words (the chunk starts at word c0 R; 16-byte loads where aligned)
         const uint32_t *src = edges + c0 * R;
         if ((((uintptr_t)src) & 15) == 0) {
@@ -241,11 +241,20 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
         }
         __syncthreads();
         // a shard keeps only its endpoints [v0, v1), binned by the local id u - v0
-        for (int i = threadIdx.x; i < nw; i += PART_BLOCK) {
-            const uint64_t w = words[i];
-            const bool mine = okb[i / R] && w >= v0 && w < v1;
-            words[i] = mine ? (uint32_t)(w - v0) : 0xFFFFFFFFu;  // local id, or "not kept"
-            if (mine) atomicAdd(&hist[(uint32_t)(w - v0) >> BIN_SHIFT], 1u);
+        // the histogram atomic's return value is the entry's rank within its bin in this
+        // chunk: kept in registers for the scatter (one shared atomic per entry, not two)
+        constexpr int WPT = (CWP + PART_BLOCK - 1) / PART_BLOCK;  // words per thread
+        uint32_t rank[WPT];
+        #pragma unroll
+        for (int q = 0; q < WPT; q++) {
+            const int i = q * PART_BLOCK + threadIdx.x;
+            rank[q] = 0;
+            if (i < nw) {
+                const uint64_t w = words[i];
+                const bool mine = okb[i / R] && w >= v0 && w < v1;
+                words[i] = mine ? (uint32_t)(w - v0) : 0xFFFFFFFFu;  // local id, or "not kept"
+                if (mine) rank[q] = atomicAdd(&hist[(uint32_t)(w - v0) >> BIN_SHIFT], 1u);
+            }
         }
         __syncthreads();
         // exclusive scan of hist over nbins (<= 1024): one warp
@@ -276,12 +285,14 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
                 if (g + hist[b] > cap[b]) atomicOr(binovf, 1u);
                 gpos[b] = g;
             }
-        for (int i = threadIdx.x; i < nw; i += PART_BLOCK) {
+        #pragma unroll
+        for (int q = 0; q < WPT; q++) {
+            const int i = q * PART_BLOCK + threadIdx.x;
+            if (i >= nw) continue;
             const int ed = i / R;
             const uint32_t u = words[i];
             if (!okb[ed] || (u == 0xFFFFFFFFu && v1 - v0 <= 0xFFFFFFFFull)) continue;
-            const uint32_t b = u >> BIN_SHIFT;
-            sent[offs[b] + atomicAdd(&fill[b], 1u)] = ((c0 + ed) << 32) | u;
+            sent[offs[u >> BIN_SHIFT] + rank[q]] = ((c0 + ed) << 32) | u;
         }
         __syncthreads();
         const uint32_t tot = total;

@@ -57,6 +57,11 @@ peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ ull ld_cg_u64(const ull *p) { return __ldcg(p); }
 
+// bulk prefetch of [p, p + bytes) into L2 (p and bytes multiples of 16)
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // %globaltimer (ns): per-round device timestamps for profiling
 __device__ __forceinline__ ull globaltimer() {
     ull t;

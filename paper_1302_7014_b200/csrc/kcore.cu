@@ -219,6 +219,15 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
         // stage the chunk's words (the chunk starts at word c0 R; 16-byte loads where aligned)
         const uint32_t *src = edges + c0 * R;
+        if (threadIdx.x == 0) {  // the block's next chunk: into L2 while this one is sorted
+            const uint64_t c1 = c0 + (uint64_t)gridDim.x * CH;
+            if (c1 < m) {
+                const uint64_t w1 = min((uint64_t)CW, (m - c1) * R);
+                const uintptr_t p0 = (uintptr_t)(edges + c1 * R) & ~(uintptr_t)15;
+                const uintptr_t p1 = ((uintptr_t)(edges + c1 * R + w1) + 15) & ~(uintptr_t)15;
+                if (p1 > p0) prefetch_l2((const void *)p0, (uint32_t)(p1 - p0));
+            }
+        }
         if ((((uintptr_t)src) & 15) == 0) {
             const int nv = nw / 4;
             for (int i = threadIdx.x; i < nv; i += PART_BLOCK)
@@ -895,9 +904,6 @@ static size_t kill_partition_smem(int r, uint32_t nbins) {
     return 2 * sizeof(ull) * (size_t)(r - 1) * KCH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
 }
 
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // phase D: apply the round's decrements bin-major; work items of DCH entries are taken in
 // bin order from a global counter, so the blocks in flight share one or two bins (L2-resident).

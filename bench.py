@@ -370,21 +370,29 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
     m_all, seeds_all = S.paper_trials(T, n=n)
     lo, hi = S.shard(T, ws, rank)
     m, seeds = m_all[lo:hi], seeds_all[lo:hi]
-    batch = 64
+    batch = 128  # measured: 32 / 64 / 128 / 256 / 512 -> 2177 / 1756 / 1547 / 1970 / 2346 ms for 10^4 trials
     wsb = int(pk.lib().peel_sweep_workspace_bytes(n, int(m_all.max()), r, k, batch))
     wsp = torch.empty((wsb,), dtype=torch.uint8, device=dev)
-    for _ in range(max(args.warmup, 1)):
-        rounds, core = pk.sweep(n, r, k, m[: 2 * batch], seeds[: 2 * batch], batch=batch, ws=wsp)
+    for _ in range(max(args.warmup, 3)):
+        rounds, core = pk.sweep(n, r, k, m, seeds, batch=batch, ws=wsp)
     clk = ClockSampler(local)
     barrier()
     clk.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    pk.profile_enable(True)
+    per_kernel, launches = {}, 0
     e0.record(stream)
     for _ in range(args.steps):
         rounds, core = pk.sweep(n, r, k, m, seeds, batch=batch, ws=wsp)
+        launches += pk.last_launches()
+        for name, ms_, nl in pk.profile_read():
+            a_ = per_kernel.setdefault(name, [0.0, 0])
+            a_[0] += ms_
+            a_[1] += nl
     e1.record(stream)
     barrier()
+    pk.profile_enable(False)
     clocks = clk.stop()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -408,7 +416,7 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
             cpu = {"value": 8 / dt, "unit": "trials/s", "cores": 1, "kind": "oracle",
                    "sample": f"8 trials (gen + literal peel) spread over the c grid, {dt:.1f} s"}
         line = {"metric": SWEEP_METRIC, "value": value, "unit": "trials/s", "n_gpus": ws,
-                "steps": args.steps, "warmup": max(args.warmup, 1),
+                "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": round(t.item() / args.steps, 3), "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u32/u64 integer",
                 "data": "synthetic G^r_{n,cn} trials (generation on device inside the timed region)",
@@ -417,7 +425,15 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
                 "result": {"failure_fraction_crosses_half_at_c": cross, "c_star_2_3": 0.818469,
                            "mean_rounds_c0.70": float(R[:100].mean()), "mean_rounds_c0.898": float(R[-100:].mean()),
                            "max_mean_rounds": float(max(R[j == q].mean() for q in range(j.max() + 1)))},
-                "cpu_baseline": cpu, "e2e": None, "clocks": clocks}
+                "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 3),
+                                 "launches_per_step": v[1] / args.steps} for nm, v in per_kernel.items()},
+                "gpu_launches": launches,
+                # pk.sweep is the public call: it takes the (m_t, seed_t) arrays from the host and
+                # returns each trial's rounds and core size to the host, inside the timed region
+                "e2e": {"value": value, "unit": "trials/s", "h2d_bytes_per_step": 16 * (hi - lo),
+                        "d2h_bytes_per_step": 12 * (hi - lo),
+                        "api": "peel_sweep (host trial parameters in, host per-trial results out)"},
+                "cpu_baseline": cpu, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -165,7 +165,7 @@ peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, uint64_t m, 
  * out_core[t] (host u64: k-core vertices; "Failed" in Table 1 iff > 0).
  * m[], seeds[] are host arrays.  Trials are processed `batch` at a time as one
  * disjoint-union hypergraph (the synchronous peel of a disjoint union is the
- * trials' synchronous peels in lockstep), so batch * n <= 2^32 and
+ * trials' synchronous peels in lockstep), so 1 <= batch <= 1024, batch * n <= 2^32 and
  * batch * max(m) < 2^32.  Multi-GPU sweeps shard the trial index range across
  * ranks (no data-path collective); see paper_1302_7014_b200/trials.py.
  * workspace: dev, peel_sweep_workspace_bytes(n, max(m), r, k, batch) bytes.

@@ -245,7 +245,7 @@ def peel_kcore_host(edges_host: np.ndarray, n: int, k: int, flags: int = 0, cap:
 # ---------------------------------------------------------------------------
 # trial sweeps (e1)
 # ---------------------------------------------------------------------------
-def sweep(n: int, r: int, k: int, m, seeds, batch: int = 32, device=None, ws: torch.Tensor | None = None,
+def sweep(n: int, r: int, k: int, m, seeds, batch: int = 128, device=None, ws: torch.Tensor | None = None,
           stream=None):
     """Per-trial (rounds, core vertices) for trials (m[t], seeds[t]) of G^r_{n,m[t]} (peel.h peel_sweep)."""
     m = np.ascontiguousarray(m, dtype=np.uint64)

@@ -36,6 +36,7 @@ void prof_pre(const char *name, cudaStream_t s);          // before a kernel lau
 void prof_post(const char *name, cudaStream_t s);         // after it (counts the launch)
 int prof_collect();                                       // after stream sync: resolve events
 bool prof_enabled();
+void prof_hold(bool on);  // nest public calls inside one report (peel_sweep)
 void prof_set_rounds(const std::vector<double> &ms);      // per-round device time of the last peel
 
 struct ProfScope {
@@ -51,6 +52,8 @@ int num_sms();
 // generator launch shared by peel_gen_hypergraph and peel_sweep (gen.cu)
 peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, uint32_t *edges, uint32_t voff,
                              cudaStream_t s);
+peel_status launch_gen_batch(uint64_t n, uint32_t r, uint32_t B, const uint64_t *mpre, const uint64_t *seeds,
+                             uint64_t total, uint32_t *edges, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // device helpers

@@ -21,6 +21,29 @@ __device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32
     }
 }
 
+// edge e of G^r_{n,.}(seed): r distinct vertices (see the header comment)
+template <int R>
+__device__ __forceinline__ void gen_one_edge(uint64_t e, uint64_t n, uint32_t k0, uint32_t k1, uint32_t (&acc)[R]) {
+    int na = 0;
+    uint32_t w[4];
+    for (uint32_t j = 0; na < R; j++) {
+        if ((j & 1) == 0) {
+            w[0] = (uint32_t)e; w[1] = (uint32_t)(e >> 32); w[2] = j >> 1; w[3] = 0x45444745u;
+            philox4x32_10(w, k0, k1);
+        }
+        uint64_t d = (j & 1) ? (((uint64_t)w[3] << 32) | w[2]) : (((uint64_t)w[1] << 32) | w[0]);
+        uint32_t v = (uint32_t)__umul64hi(d, n);
+        bool dup = false;
+        #pragma unroll
+        for (int i = 0; i < R; i++) dup |= (i < na) && (acc[i] == v);
+        if (!dup) {
+            #pragma unroll
+            for (int i = 0; i < R; i++) if (i == na) acc[i] = v;
+            na++;
+        }
+    }
+}
+
 template <int R>
 __global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, uint64_t seed,
                                                         uint32_t *__restrict__ edges, uint32_t voff) {
@@ -28,26 +51,36 @@ __global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, 
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
          e += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t acc[R];
-        int na = 0;
-        uint32_t w[4];
-        for (uint32_t j = 0; na < R; j++) {
-            if ((j & 1) == 0) {
-                w[0] = (uint32_t)e; w[1] = (uint32_t)(e >> 32); w[2] = j >> 1; w[3] = 0x45444745u;
-                philox4x32_10(w, k0, k1);
-            }
-            uint64_t d = (j & 1) ? (((uint64_t)w[3] << 32) | w[2]) : (((uint64_t)w[1] << 32) | w[0]);
-            uint32_t v = (uint32_t)__umul64hi(d, n);
-            bool dup = false;
-            #pragma unroll
-            for (int i = 0; i < R; i++) dup |= (i < na) && (acc[i] == v);
-            if (!dup) {
-                #pragma unroll
-                for (int i = 0; i < R; i++) if (i == na) acc[i] = v;
-                na++;
-            }
-        }
+        gen_one_edge<R>(e, n, k0, k1, acc);
         #pragma unroll
         for (int i = 0; i < R; i++) edges[e * R + i] = acc[i] + voff;
+    }
+}
+
+// a batch of B trials in one launch (peel_sweep): edge g of the concatenation belongs to
+// trial b with mpre[b] <= g < mpre[b+1]; it is edge g - mpre[b] of G^r_{n,m_b}(seeds[b])
+// with every vertex shifted by b n -- the same edges as B gen_edges_kernel launches.
+static constexpr int GB_MAX = 1024;
+
+template <int R>
+__global__ void __launch_bounds__(256) gen_batch_kernel(uint64_t n, uint32_t B, const uint64_t *__restrict__ mpre,
+                                                        const uint64_t *__restrict__ seeds, uint32_t *__restrict__ edges) {
+    __shared__ uint64_t sp[GB_MAX + 1];
+    for (uint32_t i = threadIdx.x; i <= B; i += 256) sp[i] = mpre[i];
+    __syncthreads();
+    const uint64_t total = sp[B];
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total; g += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = B;  // trial b: sp[b] <= g < sp[b+1]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sp[mid] <= g) lo = mid; else hi = mid;
+        }
+        const uint64_t seed = seeds[lo];
+        uint32_t acc[R];
+        gen_one_edge<R>(g - sp[lo], n, (uint32_t)seed, (uint32_t)(seed >> 32), acc);
+        const uint32_t voff = (uint32_t)(lo * n);
+        #pragma unroll
+        for (int i = 0; i < R; i++) edges[g * R + i] = acc[i] + voff;
     }
 }
 
@@ -105,6 +138,29 @@ peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, 
         case 6: gen_edges_kernel<6><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
         case 7: gen_edges_kernel<7><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
         case 8: gen_edges_kernel<8><<<g, 256, 0, s>>>(n, m, seed, edges, voff); break;
+        default: return PEEL_EINVAL;
+    }
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
+}
+}  // namespace peel
+
+namespace peel {
+// the B trials' edges, concatenated (mpre: B+1 prefix sums of m, device; seeds: B, device)
+peel_status launch_gen_batch(uint64_t n, uint32_t r, uint32_t B, const uint64_t *mpre, const uint64_t *seeds,
+                             uint64_t total, uint32_t *edges, cudaStream_t s) {
+    if (B > GB_MAX) return PEEL_EINVAL;
+    if (total == 0) return PEEL_OK;
+    unsigned g = grid_for(total);
+    ProfScope ps("gen_edges_batch", s);
+    switch (r) {
+        case 2: gen_batch_kernel<2><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
+        case 3: gen_batch_kernel<3><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
+        case 4: gen_batch_kernel<4><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
+        case 5: gen_batch_kernel<5><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
+        case 6: gen_batch_kernel<6><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
+        case 7: gen_batch_kernel<7><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
+        case 8: gen_batch_kernel<8><<<g, 256, 0, s>>>(n, B, mpre, seeds, edges); break;
         default: return PEEL_EINVAL;
     }
     PEEL_CUDA(cudaGetLastError());

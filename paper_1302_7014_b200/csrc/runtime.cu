@@ -49,9 +49,12 @@ static ProfEntry take_pair(const char *name) {
 // (collecting) call, so an async iblt_insert followed by a blocking iblt_peel report
 // together.
 static bool g_collected = true;
+static int g_hold = 0;  // > 0 inside a call made of public calls (peel_sweep): one report
+
+void prof_hold(bool on) { g_hold += on ? 1 : -1; }
 
 void prof_begin_call() {
-    if (!g_collected) return;
+    if (!g_collected || g_hold) return;
     g_collected = false;
     g_launches = 0;
     g_round_ms.clear();
@@ -73,6 +76,7 @@ void prof_post(const char *name, cudaStream_t s) {
 }
 
 int prof_collect() {
+    if (g_hold) return 0;
     g_collected = true;
     g_res_names.clear();
     g_res_ms.clear();

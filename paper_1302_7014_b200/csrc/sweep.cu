@@ -14,17 +14,22 @@ namespace peel {
 
 static inline size_t al2(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// per trial b = blockIdx.y: max removal round and core size over its n vertices; blocks
+// blockIdx.x split the trial into SR_CH-vertex chunks and combine with atomics (outputs zeroed)
+static constexpr uint32_t SR_CH = 8192;
+
 __global__ void __launch_bounds__(256) sweep_reduce_kernel(const uint32_t *__restrict__ peel_round,
                                                            const uint8_t *__restrict__ mask, uint64_t n,
                                                            ull *out_rounds, ull *out_core) {
-    const uint64_t b = blockIdx.x;
+    const uint64_t b = blockIdx.y;
+    const uint64_t lo = (uint64_t)blockIdx.x * SR_CH, hi = min(n, lo + SR_CH);
     const uint32_t *pr = peel_round + b * n;
     const uint8_t *mk = mask + b * n;
     uint32_t mx = 0;
     ull core = 0;
-    for (uint64_t v = threadIdx.x; v < n; v += blockDim.x) {
-        mx = max(mx, pr[v]);
-        core += mk[v];
+    for (uint64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+        mx = max(mx, __ldcs(pr + v));
+        core += __ldcs(mk + v);
     }
     __shared__ uint32_t smx[8];
     __shared__ ull score[8];
@@ -37,13 +42,13 @@ __global__ void __launch_bounds__(256) sweep_reduce_kernel(const uint32_t *__res
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < 8; w++) { mx = max(mx, smx[w]); core += score[w]; }
-        out_rounds[b] = mx;
-        out_core[b] = core;
+        if (mx) atomicMax(out_rounds + b, (ull)mx);
+        if (core) atomicAdd(out_core + b, core);
     }
 }
 
 struct SweepLayout {
-    size_t edges, mask, pr, res, kws, total;
+    size_t edges, mask, pr, res, par, kws, total;
     size_t kws_bytes;
 };
 
@@ -54,6 +59,7 @@ static SweepLayout sweep_layout(uint64_t n, uint64_t max_m, uint32_t r, uint32_t
     L.mask = o; o += al2(n * batch);
     L.pr = o; o += al2(sizeof(uint32_t) * n * batch);
     L.res = o; o += al2(sizeof(ull) * 2 * batch);
+    L.par = o; o += al2(sizeof(ull) * (2 * batch + 1));  // trial m prefix sums and seeds (device copy)
     L.kws_bytes = peel_kcore_workspace_bytes(n * batch, max_m * batch, r, k, 0);
     L.kws = o; o += al2(L.kws_bytes);
     L.total = L.kws_bytes ? o : 0;
@@ -65,14 +71,14 @@ static SweepLayout sweep_layout(uint64_t n, uint64_t max_m, uint32_t r, uint32_t
 using namespace peel;
 
 extern "C" size_t peel_sweep_workspace_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
-    if (batch == 0 || n < r || n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return 0;
+    if (batch == 0 || batch > 1024 || n < r || n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return 0;
     return sweep_layout(n, max_m, r, k, batch).total;
 }
 
 extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
                                   uint64_t ntrials, uint32_t batch, uint32_t *out_rounds, uint64_t *out_core,
                                   void *workspace, size_t ws_bytes, void *stream) {
-    if (!m || !seeds || !out_rounds || !out_core || !workspace || batch == 0 || r < 2 || r > 8 || n < r)
+    if (!m || !seeds || !out_rounds || !out_core || !workspace || batch == 0 || batch > 1024 || r < 2 || r > 8 || n < r)
         return PEEL_EINVAL;
     uint64_t max_m = 0;
     for (uint64_t t = 0; t < ntrials; t++) max_m = m[t] > max_m ? m[t] : max_m;
@@ -86,22 +92,40 @@ extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint
     uint8_t *mask = (uint8_t *)(ws + L.mask);
     uint32_t *pr = (uint32_t *)(ws + L.pr);
     ull *res = (ull *)(ws + L.res);
-    std::vector<ull> hres(2 * batch);
+    std::vector<ull> hres(2 * batch), hpar(2 * batch + 1);
+    ull *par = (ull *)(ws + L.par);
+    prof_begin_call();
+    prof_hold(true);  // the batches' peel_kcore calls report as this one call
+    struct Release {
+        ~Release() {
+            prof_hold(false);
+            prof_collect();
+        }
+    } release;
     for (uint64_t t0 = 0; t0 < ntrials; t0 += batch) {
         const uint32_t B = (uint32_t)(ntrials - t0 < batch ? ntrials - t0 : batch);
-        uint64_t off = 0;
+        // one generator launch for the batch: prefix sums of m and the seeds go to the device
+        hpar[0] = 0;
         for (uint32_t b = 0; b < B; b++) {
-            if (m[t0 + b]) {
-                peel_status st = launch_gen_edges(n, m[t0 + b], r, seeds[t0 + b], edges + off * r, (uint32_t)(b * n), s);
-                if (st != PEEL_OK) return st;
-            }
-            off += m[t0 + b];
+            hpar[b + 1] = hpar[b] + m[t0 + b];
+            hpar[batch + 1 + b] = seeds[t0 + b];
+        }
+        const uint64_t off = hpar[B];
+        PEEL_CUDA(cudaMemcpyAsync(par, hpar.data(), sizeof(ull) * (2 * batch + 1), cudaMemcpyHostToDevice, s));
+        {
+            peel_status st = launch_gen_batch(n, r, B, (const uint64_t *)par, (const uint64_t *)par + batch + 1, off,
+                                              edges, s);
+            if (st != PEEL_OK) return st;
         }
         uint32_t rounds = 0;
         peel_status st = peel_kcore(edges, n * B, off, r, k, 0, mask, &rounds, nullptr, nullptr, 0, pr,
                                     ws + L.kws, L.kws_bytes, stream);
         if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
-        sweep_reduce_kernel<<<B, 256, 0, s>>>(pr, mask, n, res, res + batch);
+        PEEL_CUDA(cudaMemsetAsync(res, 0, sizeof(ull) * 2 * batch, s));
+        {
+            ProfScope ps("sweep_reduce", s);
+            sweep_reduce_kernel<<<dim3((unsigned)((n + SR_CH - 1) / SR_CH), B), 256, 0, s>>>(pr, mask, n, res, res + batch);
+        }
         PEEL_CUDA(cudaGetLastError());
         PEEL_CUDA(cudaMemcpyAsync(hres.data(), res, sizeof(ull) * 2 * batch, cudaMemcpyDeviceToHost, s));
         PEEL_CUDA(cudaStreamSynchronize(s));

@@ -57,7 +57,7 @@ def run_sweep(runner, m: np.ndarray, seeds: np.ndarray, group=None, device=None)
     return R, C
 
 
-def gpu_runner(n: int, r: int, k: int, batch: int = 32, device=None):
+def gpu_runner(n: int, r: int, k: int, batch: int = 128, device=None):
     """runner for run_sweep backed by peel_sweep on this rank's GPU."""
     import paper_1302_7014_b200 as pk
 

@@ -1186,8 +1186,8 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
     uint32_t t = a.t0;
     for (;;) {
         const ull nF = ld_cg_u64(&ctl->nf[(t - 1) % 3]);
+        const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);  // issued before the branch: one round trip
         if (nF == 0) break;
-        const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
         if (tid == 0) {
             if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
             a.stats[2 * (t <= a.stat_cap ? t - 1 : a.stat_cap)] = nF;

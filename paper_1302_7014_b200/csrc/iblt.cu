@@ -239,11 +239,16 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                 const ull x = ent.y;
                 uint32_t h[R];
                 key_cells<R>(x, a.C, a.seed_h, a.subt, h);
+                // owner rule: the lowest-index round-start-pure cell among h_1..h_r is c (the
+                // r pure bits are loaded together, then scanned in order)
+                uint32_t pw[R];
+                #pragma unroll
+                for (int j = 0; j < R; j++) pw[j] = ld_cg_u32(pure_cur + (h[j] >> 5));
                 bool owner = false, found = false;
                 #pragma unroll
                 for (int j = 0; j < R; j++) {
                     if (!found && h[j] == c) { found = true; owner = true; }
-                    if (!found && (ld_cg_u32(pure_cur + (h[j] >> 5)) >> (h[j] & 31) & 1u)) break;
+                    if (!found && (pw[j] >> (h[j] & 31) & 1u)) found = true;
                 }
                 if (owner) {
                     recovered++;
@@ -251,17 +256,21 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                     bq_push(qk, slot, make_ulonglong2(x, neg ? 1ull : 0ull), (ulonglong2 *)nullptr, &ctl->nrec);
                     const uint32_t hx = checksum(x, a.seed_c);
                     const uint32_t delta = neg ? 1u : 0xFFFFFFFFu;  // remove: count -= sign
+                    // the r count atomics are issued before any result is used
+                    uint32_t now[R];
                     #pragma unroll
                     for (int j = 0; j < R; j++) {
                         Cell *p = a.cells + h[j];
-                        const uint32_t now = atomicAdd(&p->count, delta) + delta;
+                        now[j] = atomicAdd(&p->count, delta) + delta;
                         atomicXor(&p->keySum, x);
                         atomicXor(&p->hashSum, hx);
-                        if (now == 1u || (SIGNED && now == 0xFFFFFFFFu)) {
+                    }
+                    #pragma unroll
+                    for (int j = 0; j < R; j++)
+                        if (now[j] == 1u || (SIGNED && now[j] == 0xFFFFFFFFu)) {
                             const uint32_t bit = 1u << (h[j] & 31);
                             if (!(atomicOr(a.cand + (h[j] >> 5), bit) & bit)) bq_push(qc, slot, h[j], a.clist, ccnt);
                         }
-                    }
                 }
             }
             bq_flush_with(qk, slot, &ctl->nrec, a.cap_keys, write_key);

@@ -1782,7 +1782,6 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
         kb = kb < 1 ? 1 : kb;
         db = db < 1 ? 1 : db;
-        if (const char *ev = getenv("PEEL_D_BPS")) db = std::min(db, std::max(1, atoi(ev)));
         br.ehist = nullptr;
         br.enb = enb;
         // F_t's edge-bin histogram lives in ehist[t & 1]; round t's D fills ehist[(t + 1) & 1]

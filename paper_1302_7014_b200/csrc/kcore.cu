@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
                                                                       ull *cursor, const ull *__restrict__ base,
                                                                       const ull *__restrict__ cap, ull *entries,
                                                                       uint32_t *err, uint32_t *binovf,
-                                                                      uint64_t v0, uint64_t v1) {
+                                                                      uint64_t v0, uint64_t v1, uint64_t e0) {
     constexpr int CH = PART_ENTRIES / R;  // edges per chunk
     constexpr int CW = CH * R;            // edge words per chunk
     constexpr int CWP = (CW + 3) & ~3;    // padded: keeps every array below 16-byte aligned
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(PART_BLOCK, 4) bin_partition_kernel(const uint
     uint8_t *okb = (uint8_t *)(fill + nbins);     // [CH]  edge valid
     __shared__ uint32_t total;
     const ull mask = (1ull << BIN_SHIFT) - 1;
-    for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {
+    for (uint64_t c0 = e0 + (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {  // edges [e0, m)
         const int ne = (int)min((uint64_t)CH, m - c0);
         const int nw = ne * R;
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
@@ -1618,11 +1618,32 @@ static peel_status finish_kcore(uint64_t n, uint32_t cap, uint32_t *rounds, uint
     return (T > cap || T > STAT_CAP) ? PEEL_ETRUNC : PEEL_OK;
 }
 
+// peel_kcore_host: the edges arrive from host memory in chunks on a copy stream; the binned
+// build partitions each chunk as soon as its copy lands (the partition hides under the
+// host->device transfer).  Other paths wait for the whole copy.
+struct EdgeStream {
+    const uint32_t *host;   // the caller's edges (pinned for the copies to overlap)
+    uint32_t *dev;          // = edges of run_kcore
+    cudaStream_t copy;
+    std::vector<cudaEvent_t> done;  // one per chunk
+    uint64_t chunk;         // edges per chunk
+};
+
+static peel_status stream_all(const EdgeStream &es, uint64_t m, uint32_t r, cudaStream_t s) {
+    for (size_t i = 0; i < es.done.size(); i++) {
+        const uint64_t e0 = i * es.chunk, e1 = std::min(m, e0 + es.chunk);
+        PEEL_CUDA(cudaMemcpyAsync(es.dev + e0 * r, es.host + e0 * r, sizeof(uint32_t) * r * (e1 - e0),
+                                  cudaMemcpyHostToDevice, es.copy));
+        PEEL_CUDA(cudaEventRecord(es.done[i], es.copy));
+    }
+    return PEEL_OK;
+}
+
 template <int R>
 static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr, uint32_t flags,
                              uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
                              uint64_t *killed, uint32_t cap, uint32_t *peel_round, char *ws,
-                             const Layout &L, cudaStream_t s) {
+                             const Layout &L, cudaStream_t s, const EdgeStream *es = nullptr) {
     const bool subr = (flags & PEEL_FLAG_SUBROUNDS) != 0;
     Ctl *ctl = (Ctl *)(ws + L.ctl);
     ull *stats = (ull *)(ws + L.stats);
@@ -1644,6 +1665,12 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
     a.edges_vec = ((uintptr_t)edges & 15) == 0;
     if (peel_round) PEEL_CUDA(cudaMemsetAsync(peel_round, 0, sizeof(uint32_t) * n, s));
 
+    if (es) {
+        peel_status st = stream_all(*es, m, R, s);
+        if (st != PEEL_OK) return st;
+        if (csr || !L.nbins)  // only the binned build consumes the chunks as they land
+            for (auto ev : es->done) PEEL_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    }
     if (!csr && L.nbins) {
         // binned build: partition endpoint increments by vertex bin, accumulate each bin in L2
         ull *state = (ull *)(ws + L.state);
@@ -1659,11 +1686,20 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         int pblocks = 0;
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
         if (pblocks < 1) pblocks = 1;
-        if (m) {
+        if (m && !es) {
             ProfScope ps("bin_partition", s);
             bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)L.nbins, cursor, bbase,
                                                                                    bcap, entries, &ctl->err, &ctl->binovf,
-                                                                                   0ull, n);
+                                                                                   0ull, n, 0ull);
+        } else if (m) {  // chunk by chunk, each after its copy
+            for (size_t i = 0; i < es->done.size(); i++) {
+                const uint64_t e0 = i * es->chunk, e1 = std::min(m, e0 + es->chunk);
+                PEEL_CUDA(cudaStreamWaitEvent(s, es->done[i], 0));
+                ProfScope ps("bin_partition", s);
+                bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, e1, (uint32_t)L.nbins, cursor,
+                                                                                       bbase, bcap, entries, &ctl->err,
+                                                                                       &ctl->binovf, 0ull, n, e0);
+            }
         }
         PEEL_CUDA(cudaGetLastError());
         BinArgs bn;
@@ -1713,7 +1749,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                 ProfScope ps("bin_partition", s);
                 bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)L.nbins,
                                                                                        cursor, bbase, bcap, entries, &ctl->err,
-                                                                                       &ctl->binovf, 0ull, n);
+                                                                                       &ctl->binovf, 0ull, n, 0ull);
             }
             // a bin overflow (adversarial degree skew) only loses entries of the binned copy:
             // fall back to the direct histogram below if it happened (checked on the host)
@@ -1943,7 +1979,7 @@ static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, 
     if (m) {
         ProfScope ps("bin_partition", s);
         bin_partition_kernel<R><<<num_sms() * pb, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)B.nbins, cursor, base, cap,
-                                                                          entries, err, flag, v0, v1);
+                                                                          entries, err, flag, v0, v1, 0ull);
     }
     PEEL_CUDA(cudaGetLastError());
     uint32_t hflag = 0;
@@ -2041,11 +2077,24 @@ extern "C" size_t peel_kcore_workspace_bytes(uint64_t n, uint64_t m, uint32_t r,
     return layout(n, m, r, csr).total;
 }
 
+static peel_status kcore_entry(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k, uint32_t flags,
+                               uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors, uint64_t *killed,
+                               uint32_t cap, uint32_t *peel_round, void *workspace, size_t ws_bytes, void *stream,
+                               const EdgeStream *es);
+
 extern "C" peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r,
                                   uint32_t k, uint32_t flags, uint8_t *core_mask, uint32_t *rounds,
                                   uint64_t *survivors, uint64_t *killed, uint32_t cap,
                                   uint32_t *peel_round, void *workspace, size_t ws_bytes,
                                   void *stream) {
+    return kcore_entry(edges, n, m, r, k, flags, core_mask, rounds, survivors, killed, cap, peel_round, workspace,
+                       ws_bytes, stream, nullptr);
+}
+
+static peel_status kcore_entry(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r, uint32_t k, uint32_t flags,
+                               uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors, uint64_t *killed,
+                               uint32_t cap, uint32_t *peel_round, void *workspace, size_t ws_bytes, void *stream,
+                               const EdgeStream *es) {
     bool csr = use_csr(k, flags);
     if (!kcore_args_ok(n, m, r, csr) || !rounds) return PEEL_EINVAL;
     if ((m && !edges) || (n && !core_mask) || !workspace) return PEEL_EINVAL;
@@ -2058,15 +2107,16 @@ extern "C" peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m,
         *rounds = 0;
         return PEEL_OK;
     }
+    if (es && !m) es = nullptr;
     char *ws = (char *)workspace;
     switch (r) {
-        case 2: return run_kcore<2>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 3: return run_kcore<3>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 4: return run_kcore<4>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 5: return run_kcore<5>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 6: return run_kcore<6>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 7: return run_kcore<7>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
-        case 8: return run_kcore<8>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
+        case 2: return run_kcore<2>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
+        case 3: return run_kcore<3>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
+        case 4: return run_kcore<4>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
+        case 5: return run_kcore<5>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
+        case 6: return run_kcore<6>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
+        case 7: return run_kcore<7>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
+        case 8: return run_kcore<8>(edges, n, m, k, csr, flags, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s, es);
     }
     return PEEL_EINVAL;
 }
@@ -2090,9 +2140,32 @@ extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, u
     char *base = (char *)workspace;
     uint32_t *d_edges = (uint32_t *)(base + w);
     uint8_t *d_mask = (uint8_t *)(base + w + al(sizeof(uint32_t) * r * m));
-    if (m) PEEL_CUDA(cudaMemcpyAsync(d_edges, edges_host, sizeof(uint32_t) * r * m, cudaMemcpyHostToDevice, s));
-    peel_status st = peel_kcore(d_edges, n, m, r, k, flags, d_mask, rounds, survivors, killed, cap,
-                                nullptr, workspace, w, stream);
+    // the copy runs on a second stream in 16 chunks; the binned build partitions each chunk as
+    // it lands (the copy stream first waits for work already queued on s)
+    static std::mutex mu;
+    static std::map<int, std::pair<cudaStream_t, std::vector<cudaEvent_t>>> res;  // per device
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    PEEL_CUDA(cudaGetDevice(&dev));
+    auto &rs = res[dev];
+    if (!rs.first) {
+        PEEL_CUDA(cudaStreamCreateWithFlags(&rs.first, cudaStreamNonBlocking));
+        rs.second.resize(17);
+        for (auto &e : rs.second) PEEL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    EdgeStream es;
+    es.host = edges_host;
+    es.dev = d_edges;
+    es.copy = rs.first;
+    const uint64_t nchunks = m ? std::min<uint64_t>(16, m) : 0;
+    es.chunk = nchunks ? (m + nchunks - 1) / nchunks : 1;
+    es.done.assign(rs.second.begin(), rs.second.begin() + (nchunks ? (m + es.chunk - 1) / es.chunk : 0));
+    if (m) {
+        PEEL_CUDA(cudaEventRecord(rs.second[16], s));
+        PEEL_CUDA(cudaStreamWaitEvent(es.copy, rs.second[16], 0));
+    }
+    peel_status st = kcore_entry(d_edges, n, m, r, k, flags, d_mask, rounds, survivors, killed, cap, nullptr,
+                                 workspace, w, stream, m ? &es : nullptr);
     if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
     if (n) PEEL_CUDA(cudaMemcpyAsync(core_mask_host, d_mask, n, cudaMemcpyDeviceToHost, s));
     PEEL_CUDA(cudaStreamSynchronize(s));

@@ -185,14 +185,20 @@ def test_round_cap_truncation():
     assert res.survivors.tolist() == ref.survivors[:10].tolist()
 
 
-def test_host_buffer_entry_point():
-    n, m, r, k = 50021, 40000, 3, 2
+@pytest.mark.parametrize("n,m,r,k,pin", [(50021, 40000, 3, 2, True), ((1 << 23) + 4099, 6300000, 3, 2, True),
+                                         ((1 << 23) + 4099, 6300000, 3, 2, False), ((1 << 23) + 17, 9000000, 3, 3, True),
+                                         (3000, 17, 4, 2, True)])
+def test_host_buffer_entry_point(n, m, r, k, pin):
+    # peel_kcore_host copies the edges in 16 chunks on its own stream; n > 2^23 (binned build)
+    # partitions each chunk as it lands; k = 3 (CSR) and small n wait for the whole copy
     e_np = O.gen_hypergraph(n, m, r, 5)
     ref = O.sync_peel(e_np, n, k)
-    pinned = torch.from_numpy(e_np.view(np.int32)).pin_memory()
-    res = pk.peel_kcore_host(pinned, n, k)
-    assert res.rounds == ref.rounds and np.array_equal(res.core_mask, ref.core_mask)
-    assert res.survivors.tolist() == ref.survivors.tolist()
+    host = torch.from_numpy(e_np.view(np.int32))
+    host = host.pin_memory() if pin else host
+    for _ in range(2):
+        res = pk.peel_kcore_host(host, n, k)
+        assert res.rounds == ref.rounds and np.array_equal(res.core_mask, ref.core_mask)
+        assert res.survivors.tolist() == ref.survivors.tolist() and res.killed.tolist() == ref.killed.tolist()
 
 
 # ---- full-scale configs (BASELINE.json), checked against goldens + certificate -----------

@@ -2140,8 +2140,18 @@ extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, u
     char *base = (char *)workspace;
     uint32_t *d_edges = (uint32_t *)(base + w);
     uint8_t *d_mask = (uint8_t *)(base + w + al(sizeof(uint32_t) * r * m));
-    // the copy runs on a second stream in 16 chunks; the binned build partitions each chunk as
-    // it lands (the copy stream first waits for work already queued on s)
+    // binned builds: the copy runs on a second stream in 16 chunks, and the build partitions
+    // each chunk as it lands (the copy stream first waits for work already queued on s).
+    // Other paths (and small inputs, where the extra stream costs more than it hides): one copy.
+    if (use_csr(k, flags) || n <= BIN_MIN_N || (flags & PEEL_FLAG_SUBROUNDS)) {
+        if (m) PEEL_CUDA(cudaMemcpyAsync(d_edges, edges_host, sizeof(uint32_t) * r * m, cudaMemcpyHostToDevice, s));
+        peel_status st = peel_kcore(d_edges, n, m, r, k, flags, d_mask, rounds, survivors, killed, cap, nullptr,
+                                    workspace, w, stream);
+        if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
+        if (n) PEEL_CUDA(cudaMemcpyAsync(core_mask_host, d_mask, n, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        return st;
+    }
     static std::mutex mu;
     static std::map<int, std::pair<cudaStream_t, std::vector<cudaEvent_t>>> res;  // per device
     std::lock_guard<std::mutex> lock(mu);

@@ -246,6 +246,16 @@ peel_status iblt_build(uint64_t cells, uint32_t r, uint64_t seed, void *mem, siz
  * flattened index of the last subtable step that recovered a key and per_round[s-1] the
  * keys recovered at step s. */
 #define IBLT_FLAG_SUBTABLES 1u
+/* IBLT_FLAG_BLOCKED -- locality-aware hashing, the paper's open question (
+ * DESIGN.md reading R27): the table is nb blocks of B = 2^blog cells (B must divide cells,
+ * r <= B; blog = IBLT_BLOCK_LOG(flags), 0 meaning 16) and all r cells of key x lie in one
+ * block: b = umulhi64(mix64(x ^ seed_h ^ 0x9E6C63D0676A9A99), cells / B), cell j =
+ * b B + the j-th cell of the plain hash over B cells.  Recovery is the plain
+ * round-synchronous schedule; a block's cells are contiguous, so a round's atomics for the
+ * frontier entries in flight stay in a few blocks. */
+#define IBLT_FLAG_BLOCKED 2u
+#define IBLT_BLOCK_LOG_SHIFT 8
+#define IBLT_BLOCK_LOG(flags) (((flags) >> IBLT_BLOCK_LOG_SHIFT) & 0xFFu)
 peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags, void *mem,
                           size_t mem_bytes, void *stream, peel_iblt **out);
 

@@ -68,6 +68,10 @@ def lib() -> ctypes.CDLL:
             L.ora_iblt_new.restype = p
             L.ora_iblt_new_ex.argtypes = [u64, u32, u64, i32]
             L.ora_iblt_new_ex.restype = p
+            L.ora_iblt_new_blocked.argtypes = [u64, u32, u64, u32]
+            L.ora_iblt_new_blocked.restype = p
+            L.ora_cells_of_blocked.argtypes = [u64, u64, u32, u64, u32, p]
+            L.ora_cells_of_blocked.restype = i32
             L.ora_iblt_peel_subtables.argtypes = [p, p, u64, p, p, p, u32, p]
             L.ora_iblt_peel_subtables.restype = i32
             L.ora_cells_of_subtable.argtypes = [u64, u64, u32, u64, p]
@@ -157,6 +161,14 @@ def checksum(x: int, seed: int) -> int:
 def cells_of_subtable(x: int, C: int, r: int, seed: int) -> np.ndarray:
     out = np.zeros(r, dtype=np.uint64)
     lib().ora_cells_of_subtable(x, C, r, seed_h(seed), _ptr(out))
+    return out
+
+
+def cells_of_blocked(x: int, C: int, r: int, seed: int, blog: int) -> np.ndarray:
+    """The r cells of key x under blocked hashing (one block of 2^blog cells; R27)."""
+    out = np.zeros(r, dtype=np.uint64)
+    if lib().ora_cells_of_blocked(x, C, r, seed_h(seed), blog, _ptr(out)):
+        raise RuntimeError("cells_of_blocked: no r distinct cells")
     return out
 
 
@@ -256,11 +268,14 @@ class IbltResult:
 class Iblt:
     """IBLT with C cells and r hashes."""
 
-    def __init__(self, C: int, r: int, seed: int, subtables: bool = False):
-        self.C, self.r, self.seed, self.subtables = C, r, seed, subtables
-        self._t = lib().ora_iblt_new_ex(C, r, seed, 1 if subtables else 0)
+    def __init__(self, C: int, r: int, seed: int, subtables: bool = False, blog: int = 0):
+        self.C, self.r, self.seed, self.subtables, self.blog = C, r, seed, subtables, blog
+        if blog:
+            self._t = lib().ora_iblt_new_blocked(C, r, seed, blog)
+        else:
+            self._t = lib().ora_iblt_new_ex(C, r, seed, 1 if subtables else 0)
         if not self._t:
-            raise ValueError("bad IBLT arguments (need r>=2, C>=r, and r | C for subtables)")
+            raise ValueError("bad IBLT arguments (need r>=2, C>=r, r | C for subtables, 2^blog | C for blocks)")
 
     def __del__(self):
         t = getattr(self, "_t", None)

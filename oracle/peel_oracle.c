@@ -20,6 +20,7 @@
  *   - ora_subround_peel ........ the subround (subtable) peel
  *   - ora_iblt_* ............... IBLT insert / round-synchronous recovery
  *   - ora_iblt_serial_recover .. one-pure-cell-at-a-time recovery
+ *   - ora_cells_of_blocked ..... blocked (locality-aware) hashing, the paper's open question
  * Nothing here is blocked, fused or reordered beyond what the definitions state.
  */
 #include <stdint.h>
@@ -373,6 +374,7 @@ typedef struct {
     uint64_t C;
     uint32_t r;
     int subtables; /* 1: r subtables of C/r cells, one cell per subtable per key */
+    uint32_t blog; /* > 0: blocked hashing, all r cells in one block of 2^blog cells (R27) */
     uint64_t seed_h, seed_c;
     int64_t *count;
     uint64_t *keySum;
@@ -398,6 +400,26 @@ ora_iblt *ora_iblt_new_ex(uint64_t C, uint32_t r, uint64_t seed, int subtables) 
 
 ora_iblt *ora_iblt_new(uint64_t C, uint32_t r, uint64_t seed) { return ora_iblt_new_ex(C, r, seed, 0); }
 
+/* blocked table: C = nb 2^blog cells (R27) */
+ora_iblt *ora_iblt_new_blocked(uint64_t C, uint32_t r, uint64_t seed, uint32_t blog) {
+    if (blog < 4 || blog > 30 || C % (1ull << blog) || r > (1u << blog)) return NULL;
+    ora_iblt *t = ora_iblt_new_ex(C, r, seed, 0);
+    if (t) t->blog = blog;
+    return t;
+}
+
+/* Blocked hashing (locality-aware hashing, the paper's open question P:706-708; DESIGN.md
+ * reading R27): the key's block b = umulhi64(mix64(x ^ seed_h ^ 0x9E6C63D0676A9A99), C / B)
+ * with B = 2^blog, then r distinct cells of [b B, (b+1) B) drawn exactly as ora_cells_of
+ * draws them from [0, C) -- the same draws j = 0, 1, ... mapped into B cells instead of C. */
+int ora_cells_of_blocked(uint64_t x, uint64_t C, uint32_t r, uint64_t seed_h, uint32_t blog, uint64_t *out) {
+    const uint64_t B = 1ull << blog;
+    const uint64_t b = umulhi64(ora_mix64(x ^ seed_h ^ 0x9E6C63D0676A9A99ull), C / B);
+    if (ora_cells_of(x, B, r, seed_h, out) != 0) return -1;
+    for (uint32_t j = 0; j < r; j++) out[j] += b * B;
+    return 0;
+}
+
 /* subtable hashing ("hash each item into one cell in each subtable"):  */
 /* h_j(x) = j C/r + umulhi64(mix64(x ^ seed_h ^ (j+1) 0xD1B54A32D192ED03), C/r) */
 void ora_cells_of_subtable(uint64_t x, uint64_t C, uint32_t r, uint64_t seed_h, uint64_t *out) {
@@ -408,6 +430,7 @@ void ora_cells_of_subtable(uint64_t x, uint64_t C, uint32_t r, uint64_t seed_h, 
 
 static void key_cells(const ora_iblt *t, uint64_t x, uint64_t *cells) {
     if (t->subtables) ora_cells_of_subtable(x, t->C, t->r, t->seed_h, cells);
+    else if (t->blog) ora_cells_of_blocked(x, t->C, t->r, t->seed_h, t->blog, cells);
     else ora_cells_of(x, t->C, t->r, t->seed_h, cells);
 }
 
@@ -553,7 +576,8 @@ int ora_iblt_peel_subtables(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys, 
 /* subtracts, key and checksum fields XOR), the IBLT of the signed multiset   */
 /* A - B.  Both tables must share C, r and seed.                              */
 int ora_iblt_subtract(ora_iblt *a, const ora_iblt *b) {
-    if (a->C != b->C || a->r != b->r || a->seed_h != b->seed_h || a->subtables != b->subtables) return -1;
+    if (a->C != b->C || a->r != b->r || a->seed_h != b->seed_h || a->subtables != b->subtables || a->blog != b->blog)
+        return -1;
     for (uint64_t c = 0; c < a->C; c++) {
         a->count[c] -= b->count[c];
         a->keySum[c] ^= b->keySum[c];

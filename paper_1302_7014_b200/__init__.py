@@ -23,6 +23,8 @@ PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOV
 PEEL_FLAG_CSR = 1
 PEEL_FLAG_SUBROUNDS = 2
 IBLT_FLAG_SUBTABLES = 1
+IBLT_FLAG_BLOCKED = 2
+IBLT_BLOCK_LOG_SHIFT = 8
 
 _lib = None
 
@@ -350,8 +352,10 @@ class Iblt:
     """IBLT of `cells` 16-byte cells and r hashes in a torch-owned device buffer (peel.h iblt_*)."""
 
     def __init__(self, cells: int, r: int, seed: int, device=None, stream=None, mem: torch.Tensor | None = None,
-                 subtables: bool = False):
-        self.C, self.r, self.seed, self.subtables = cells, r, seed, subtables
+                 subtables: bool = False, blog: int = 0):
+        """blog > 0: blocked (locality-aware) hashing, all r cells of a key in one block of
+        2^blog cells (peel.h IBLT_FLAG_BLOCKED)."""
+        self.C, self.r, self.seed, self.subtables, self.blog = cells, r, seed, subtables, blog
         self.device = _dev(device) if mem is None else mem.device
         nb = int(_L().iblt_mem_bytes(cells, r))
         if nb == 0:
@@ -365,7 +369,10 @@ class Iblt:
         if self._h is not None and self._h.value:
             _L().iblt_destroy(self._h)
         h = ctypes.c_void_p(0)
-        _check(_L().iblt_build_ex(self.C, self.r, self.seed & (2**64 - 1), IBLT_FLAG_SUBTABLES if self.subtables else 0,
+        flags = IBLT_FLAG_SUBTABLES if self.subtables else 0
+        if self.blog:
+            flags |= IBLT_FLAG_BLOCKED | (self.blog << IBLT_BLOCK_LOG_SHIFT)
+        _check(_L().iblt_build_ex(self.C, self.r, self.seed & (2**64 - 1), flags,
                                   _ptr(self.mem), self.mem.numel(), _stream(stream), ctypes.byref(h)), "iblt_build_ex")
         self._h = h
 

@@ -90,9 +90,17 @@ __device__ __forceinline__ void cells_of(ull x, ull C, ull seed_h, uint32_t (&c)
 
 // subtable hashing ("hash each item into one cell in each subtable"):
 // h_j(x) = j C/r + umulhi64(mix64(x ^ seed_h ^ (j+1) 0xD1B54A32D192ED03), C/r)
+// blocked hashing (IBLT_FLAG_BLOCKED; R27): block b = umulhi64(mix64(x ^ seed_h ^ K_B), C / B),
+// then the plain r-distinct cells over B cells, offset by b B.  blog = 0: not blocked.
 template <int R>
-__device__ __forceinline__ void key_cells(ull x, ull C, ull seed_h, bool subt, uint32_t (&c)[R]) {
-    if (subt) {
+__device__ __forceinline__ void key_cells(ull x, ull C, ull seed_h, bool subt, uint32_t (&c)[R], uint32_t blog = 0) {
+    if (blog) {
+        const ull B = 1ull << blog;
+        const ull b = __umul64hi(mix64(x ^ seed_h ^ 0x9E6C63D0676A9A99ull), C >> blog);
+        cells_of<R>(x, B, seed_h, c);
+        #pragma unroll
+        for (int j = 0; j < R; j++) c[j] += (uint32_t)(b * B);
+    } else if (subt) {
         const ull cs = C / R;
         #pragma unroll
         for (int j = 0; j < R; j++)
@@ -120,11 +128,12 @@ __device__ __forceinline__ Cell ld_cell_cg(const Cell *p) {
 template <int R>
 __global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ull seed_h, ull seed_c,
                                                           const ull *__restrict__ keys, ull nkeys,
-                                                          uint32_t delta, bool subt, uint32_t lo, uint32_t hi) {
+                                                          uint32_t delta, bool subt, uint32_t lo, uint32_t hi,
+                                                          uint32_t blog) {
     for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
         const ull x = __ldg(keys + i);
         uint32_t c[R];
-        key_cells<R>(x, C, seed_h, subt, c);
+        key_cells<R>(x, C, seed_h, subt, c, blog);
         const uint32_t h = checksum(x, seed_c);
         #pragma unroll
         for (int j = 0; j < R; j++) {
@@ -139,10 +148,10 @@ __global__ void __launch_bounds__(256) iblt_update_kernel(Cell *cells, ull C, ul
 
 template <int R>
 __global__ void __launch_bounds__(256) iblt_edges_kernel(ull C, ull seed_h, const ull *__restrict__ keys,
-                                                         ull nkeys, uint32_t *edges, bool subt) {
+                                                         ull nkeys, uint32_t *edges, bool subt, uint32_t blog) {
     for (ull i = blockIdx.x * (ull)blockDim.x + threadIdx.x; i < nkeys; i += (ull)gridDim.x * blockDim.x) {
         uint32_t c[R];
-        key_cells<R>(__ldg(keys + i), C, seed_h, subt, c);
+        key_cells<R>(__ldg(keys + i), C, seed_h, subt, c, blog);
         #pragma unroll
         for (int j = 0; j < R; j++) edges[i * R + j] = c[j];
     }
@@ -162,6 +171,7 @@ struct IPeelArgs {
     int8_t *out_sign;   // signed recovery: +1 / -1 per recovered key
     ull cap_keys;
     bool subt;          // subtable hashing
+    uint32_t blog;      // blocked hashing: log2 block size, 0 = off
 };
 
 __device__ __forceinline__ bool is_pure(const Cell &c, ull seed_c) {
@@ -238,7 +248,7 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                 const bool neg = (ent.x >> 32) != 0;
                 const ull x = ent.y;
                 uint32_t h[R];
-                key_cells<R>(x, a.C, a.seed_h, a.subt, h);
+                key_cells<R>(x, a.C, a.seed_h, a.subt, h, a.blog);
                 // owner rule: the lowest-index round-start-pure cell among h_1..h_r is c (the
                 // r pure bits are loaded together, then scanned in order)
                 uint32_t pw[R];
@@ -451,6 +461,7 @@ struct peel_iblt {
     ull C;
     uint32_t r;
     bool subt;  // IBLT_FLAG_SUBTABLES
+    uint32_t blog;  // IBLT_FLAG_BLOCKED: log2 cells per block (0: plain hashing)
     ull seed, seed_h, seed_c;
     char *mem;
     ILayout L;
@@ -471,6 +482,12 @@ extern "C" peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, 
                                      size_t mem_bytes, void *stream, peel_iblt **out) {
     if (!out || !mem || r < 2 || r > 8 || cells < r || cells >= (1ull << 32)) return PEEL_EINVAL;
     if ((flags & IBLT_FLAG_SUBTABLES) && cells % r) return PEEL_EINVAL;
+    uint32_t blog = 0;
+    if (flags & IBLT_FLAG_BLOCKED) {
+        blog = IBLT_BLOCK_LOG(flags) ? IBLT_BLOCK_LOG(flags) : 16u;
+        if ((flags & IBLT_FLAG_SUBTABLES) || blog < 4 || blog > 30 || cells % (1ull << blog) || (1ull << blog) < r)
+            return PEEL_EINVAL;
+    }
     if (((uintptr_t)mem & 15) != 0) return PEEL_EINVAL;
     ILayout L = ilayout(cells);
     if (mem_bytes < L.total) return PEEL_ENOMEM;
@@ -481,6 +498,7 @@ extern "C" peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, 
     t->C = cells;
     t->r = r;
     t->subt = (flags & IBLT_FLAG_SUBTABLES) != 0;
+    t->blog = blog;
     t->seed = seed;
     const ull G = 0x9E3779B97F4A7C15ull;
     t->seed_h = host_mix64((seed ^ 0x6A09E667F3BCC909ull) + G);
@@ -513,13 +531,13 @@ static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkey
     for (uint64_t q = 0; q < npass; q++) {
         const uint32_t lo = (uint32_t)(q * t->C / npass), hi = (uint32_t)((q + 1) * t->C / npass);
         switch (t->r) {
-            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
-            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
-            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
-            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
-            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
-            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
-            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi); break;
+            case 2: iblt_update_kernel<2><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
+            case 3: iblt_update_kernel<3><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
+            case 4: iblt_update_kernel<4><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
+            case 5: iblt_update_kernel<5><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
+            case 6: iblt_update_kernel<6><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
+            case 7: iblt_update_kernel<7><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
+            case 8: iblt_update_kernel<8><<<g, 256, 0, s>>>(cells, t->C, t->seed_h, t->seed_c, (const ull *)keys, nkeys, delta, t->subt, lo, hi, t->blog); break;
         }
     }
     PEEL_CUDA(cudaGetLastError());
@@ -581,6 +599,7 @@ static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_
     a.out_sign = out_sign;
     a.cap_keys = cap_keys;
     a.subt = t->subt;
+    a.blog = t->blog;
     peel_status st = PEEL_EINVAL;
     switch (t->r) {
         case 2: st = run_iblt_peel<2>(t, a, sgn, s); break;
@@ -644,7 +663,8 @@ __global__ void __launch_bounds__(256) iblt_subtract_kernel(Cell *a, const Cell 
 }
 
 extern "C" peel_status iblt_subtract(peel_iblt *a, const peel_iblt *b, void *stream) {
-    if (!a || !b || a->C != b->C || a->r != b->r || a->seed != b->seed || a->subt != b->subt) return PEEL_EINVAL;
+    if (!a || !b || a->C != b->C || a->r != b->r || a->seed != b->seed || a->subt != b->subt || a->blog != b->blog)
+        return PEEL_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     prof_begin_call();
     {
@@ -669,13 +689,13 @@ extern "C" peel_status iblt_to_hypergraph(const peel_iblt *t, const uint64_t *ke
     {
         ProfScope ps("iblt_edges", s);
         switch (t->r) {
-            case 2: iblt_edges_kernel<2><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
-            case 3: iblt_edges_kernel<3><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
-            case 4: iblt_edges_kernel<4><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
-            case 5: iblt_edges_kernel<5><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
-            case 6: iblt_edges_kernel<6><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
-            case 7: iblt_edges_kernel<7><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
-            case 8: iblt_edges_kernel<8><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt); break;
+            case 2: iblt_edges_kernel<2><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
+            case 3: iblt_edges_kernel<3><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
+            case 4: iblt_edges_kernel<4><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
+            case 5: iblt_edges_kernel<5><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
+            case 6: iblt_edges_kernel<6><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
+            case 7: iblt_edges_kernel<7><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
+            case 8: iblt_edges_kernel<8><<<g, 256, 0, s>>>(t->C, t->seed_h, (const ull *)keys, nkeys, edges, t->subt, t->blog); break;
         }
     }
     PEEL_CUDA(cudaGetLastError());

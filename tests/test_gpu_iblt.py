@@ -199,3 +199,34 @@ def test_signed_peel_on_insert_only_equals_plain():
     pb, sg = b.peel_signed()
     assert pa.rounds == pb.rounds and pa.per_round.tolist() == pb.per_round.tolist()
     assert bool((sg == 1).all())
+
+
+# ---- blocked (locality-aware) hashing, R27 ---------------------------
+@pytest.mark.parametrize("r", [2, 3, 4])
+@pytest.mark.parametrize("blog,load", [(4, 0.5), (8, 0.75), (12, 0.8), (16, 0.83), (20, 0.75)])
+def test_blocked_recovery_vs_oracle(r, blog, load):
+    C = max(1 << 20, 1 << blog)
+    N = int(load * C)
+    keys = O.gen_keys(N, 70 + r + blog)
+    t = pk.Iblt(C, r, 13, device=DEV, blog=blog)
+    o = O.Iblt(C, r, 13, blog=blog)
+    t.insert(keys_dev(keys))
+    o.insert(keys)
+    cnt, ks, hs = dev_cells(t)
+    ocnt, oks, ohs = o.cells()
+    assert np.array_equal(cnt.astype(np.int32), ocnt.astype(np.int32)) and np.array_equal(ks, oks)
+    assert np.array_equal(hs, ohs)
+    res = t.peel(cap_keys=N)
+    ref = o.peel(cap_keys=N + 1)
+    assert res.rounds == ref.rounds and res.per_round.tolist() == ref.per_round.tolist()
+    assert res.complete == ref.complete
+    assert np.array_equal(np.sort(res.keys.cpu().numpy().view(np.uint64)), np.sort(ref.keys))
+    e = t.to_hypergraph(keys_dev(keys[:1000])).cpu().numpy().view(np.uint32)
+    assert np.array_equal(e, o.to_hypergraph(keys[:1000]))
+
+
+def test_blocked_rejects_bad_shapes():
+    with pytest.raises(pk.PeelError):
+        pk.Iblt(1000, 3, 1, device=DEV, blog=8)            # 2^8 does not divide 1000
+    with pytest.raises(pk.PeelError):
+        pk.Iblt(1 << 12, 3, 1, device=DEV, blog=8, subtables=True)

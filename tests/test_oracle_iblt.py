@@ -216,3 +216,59 @@ def test_subtract_is_cellwise_difference_and_inverse_of_insert():
     a.subtract(b)
     for x, y in zip(a.cells(), d.cells()):
         assert np.array_equal(x, y)
+
+
+# ---- blocked (locality-aware) hashing, R27 ---------------------------
+@pytest.mark.parametrize("blog", [4, 8, 12])
+def test_blocked_cells_stay_in_one_block_and_are_uniform(blog):
+    C, r, seed = 1 << 16, 3, 11
+    B = 1 << blog
+    nb = C // B
+    blocks = np.zeros(nb, dtype=np.int64)
+    offs = np.zeros(B, dtype=np.int64)
+    keys = O.gen_keys(20000, 5)
+    for x in keys:
+        c = O.cells_of_blocked(int(x), C, r, seed, blog)
+        assert len(set(c.tolist())) == r                      # r distinct cells
+        assert len(set((c // B).tolist())) == 1                # one block
+        blocks[int(c[0] // B)] += 1
+        for v in c:
+            offs[int(v % B)] += 1
+    # chi-square against uniform blocks and uniform in-block positions (4-sigma bounds)
+    for h, k in ((blocks, nb), (offs, B)):
+        e = h.sum() / k
+        chi = ((h - e) ** 2 / e).sum()
+        assert abs(chi - (k - 1)) < 4 * np.sqrt(2 * (k - 1)) + 8
+
+
+def test_blocked_with_one_block_is_the_plain_hash():
+    # B = C: the block index is 0 and the cells are exactly the plain cells
+    C, r, seed = 1 << 10, 4, 3
+    for x in O.gen_keys(500, 9):
+        assert np.array_equal(O.cells_of_blocked(int(x), C, r, seed, 10), O.cells_of(int(x), C, r, seed))
+    a, b = O.Iblt(C, r, seed), O.Iblt(C, r, seed, blog=10)
+    keys = O.gen_keys(700, 4)
+    a.insert(keys); b.insert(keys)
+    ra, rb = a.peel(), b.peel()
+    assert ra.rounds == rb.rounds and ra.per_round.tolist() == rb.per_round.tolist()
+    assert np.array_equal(np.sort(ra.keys), np.sort(rb.keys))
+
+
+@pytest.mark.parametrize("blog,load", [(6, 0.6), (8, 0.75), (10, 0.8), (12, 0.78)])
+def test_blocked_recovery_is_the_two_core_complement(blog, load):
+    # the blocked table is still an r-hypergraph on the cells: recovery = complement of the
+    # 2-core, per-round recovered = per-round 2-core kills (the F4 identity of the plain table)
+    C, r, seed = 1 << 14, 3, 21
+    N = int(load * C)
+    keys = O.gen_keys(N, blog)
+    t = O.Iblt(C, r, seed, blog=blog)
+    t.insert(keys)
+    e = t.to_hypergraph(keys)
+    assert np.all(e // (1 << blog) == (e[:, :1] // (1 << blog)))
+    ref = O.sync_peel(e, C, 2)
+    res = t.peel(cap_keys=N + 1)
+    core_edges = np.all(ref.core_mask[e.astype(np.int64)] == 1, axis=1)
+    assert np.array_equal(np.sort(res.keys), np.sort(keys[~core_edges]))
+    assert res.per_round.tolist() == ref.killed[ref.killed > 0].tolist()
+    assert res.complete == (ref.core_mask.sum() == 0)
+    assert ref.rounds in (res.rounds, res.rounds + 1)

@@ -311,6 +311,28 @@ peel_status iblt_to_hypergraph(const peel_iblt *t, const uint64_t *keys, uint64_
 /* Free the handle (not the caller's memory). */
 void iblt_destroy(peel_iblt *t);
 
+/* ---- cell-partitioned IBLT over P GPUs ------------------------------------
+ * One table of `cells` cells split by cell range over the communicator's P shards (ranks, or
+ * virtual shards of one GPU): shard q owns cells [q cs, (q+1) cs), cs = ceil(cells/P)
+ * rounded up to 32.  iblt_dist_recover inserts the nkeys keys (dev u64, the SAME array on
+ * every rank: each shard applies them to its own cells) and runs the round-synchronous
+ * recovery of iblt_peel: per round the shards gather each other's round-start pure cells
+ * (one allgather of a cells-bit bitmap), each key is found by the shard owning its
+ * lowest-index pure cell (the owner rule) and sent to the shards owning its cells, which
+ * XOR-delete it; then candidates are re-tested.  Results equal iblt_peel on one table.
+ * flags: 0 or IBLT_FLAG_BLOCKED (+ IBLT_BLOCK_LOG); seed, hashes as iblt_build.
+ * Outputs: out_keys (dev u64, cap_keys) receives the keys found by THIS rank (virtual: all
+ * shards), *nrecovered their number; rounds, per_round[0 .. min(rounds, cap)) (host, keys
+ * recovered per round over all shards) and *complete (all cells of all shards zero) are
+ * global.  mem: dev, iblt_dist_mem_bytes(c, cells, r) bytes (per rank; virtual: all shards).
+ * Collective over the communicator's ranks; blocking.  EINVAL: bad shape or flags (r in
+ * [2, 8], P <= 8); ENOMEM: mem too small; ETRUNC: cap_keys or cap exceeded; ENCCL. */
+size_t iblt_dist_mem_bytes(const peel_comm *c, uint64_t cells, uint32_t r);
+peel_status iblt_dist_recover(peel_comm *c, uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags,
+                              const uint64_t *keys, uint64_t nkeys, uint64_t *out_keys, uint64_t cap_keys,
+                              uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
+                              int *complete, void *mem, size_t mem_bytes, void *stream);
+
 /* ======================================================================= */
 /* Measurement support                                                      */
 /* ======================================================================= */

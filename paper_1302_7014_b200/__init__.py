@@ -69,6 +69,9 @@ def _L() -> ctypes.CDLL:
         L.peel_kcore_dist_workspace_bytes.argtypes = [p, u64, u64, u32, u32]
         L.peel_kcore_dist_workspace_bytes.restype = sz
         L.peel_kcore_dist.argtypes = [p, p, u64, u64, u32, u32, p, p, p, p, u32, p, sz, p]
+        L.iblt_dist_mem_bytes.argtypes = [p, u64, u32]
+        L.iblt_dist_mem_bytes.restype = sz
+        L.iblt_dist_recover.argtypes = [p, u64, u32, u64, u32, p, u64, p, u64, p, p, p, u32, p, p, sz, p]
         L.iblt_mem_bytes.argtypes = [u64, u32]
         L.iblt_mem_bytes.restype = sz
         L.iblt_build.argtypes = [u64, u32, u64, p, sz, p, ctypes.POINTER(p)]
@@ -90,6 +93,7 @@ def _L() -> ctypes.CDLL:
         L.peel_profile_rounds.restype = i32
         for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_gen_partitioned", "peel_kcore", "peel_kcore_host", "peel_sweep",
                   "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build", "iblt_build_ex",
+                  "iblt_dist_recover",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_subtract", "iblt_peel_signed", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
         _lib = L
@@ -436,6 +440,34 @@ class Iblt:
         _check(_L().iblt_to_hypergraph(self._h, _ptr(keys), keys.numel(), _ptr(edges), _stream(stream)),
                "iblt_to_hypergraph")
         return edges
+
+
+def iblt_dist_recover(comm: Comm, cells: int, r: int, seed: int, keys: torch.Tensor, blog: int = 0,
+                      cap_keys: int | None = None, cap: int = 65536, mem: torch.Tensor | None = None,
+                      stream=None) -> IbltResult:
+    """Cell-partitioned IBLT over the communicator's shards (peel.h iblt_dist_recover): insert
+    `keys` (the same device array on every rank) and recover.  keys of the result: those found
+    by this rank (virtual shards: all); rounds, per_round and complete are global."""
+    assert keys.dtype == torch.int64 and keys.is_cuda and keys.is_contiguous()
+    need = int(_L().iblt_dist_mem_bytes(comm._h, cells, r))
+    if need == 0:
+        raise PeelError(PEEL_EINVAL, "iblt_dist_mem_bytes")
+    if mem is None:
+        mem = workspace(need, keys.device)
+    cap_keys = keys.numel() if cap_keys is None else cap_keys
+    out = torch.empty((max(cap_keys, 1),), dtype=torch.int64, device=keys.device)
+    flags = (IBLT_FLAG_BLOCKED | (blog << IBLT_BLOCK_LOG_SHIFT)) if blog else 0
+    nrec = ctypes.c_uint64(0)
+    rounds = ctypes.c_uint32(0)
+    per_round = np.zeros(cap, dtype=np.uint64)
+    complete = ctypes.c_int(0)
+    st = _L().iblt_dist_recover(comm._h, cells, r, seed & (2**64 - 1), flags, _ptr(keys), keys.numel(), _ptr(out),
+                                cap_keys, ctypes.addressof(nrec), ctypes.addressof(rounds), per_round.ctypes.data, cap,
+                                ctypes.addressof(complete), _ptr(mem), mem.numel(), _stream(stream))
+    _check(st, "iblt_dist_recover")
+    t = rounds.value
+    return IbltResult(out[: min(nrec.value, cap_keys)], nrec.value, t, per_round[:min(t, cap)].copy(),
+                      bool(complete.value), st)
 
 
 # ---------------------------------------------------------------------------

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "shard.h"
+#include "comm.h"
 
 namespace peel {
 
@@ -428,27 +429,6 @@ static unsigned dgrid(uint64_t work) {
 
 using namespace peel;
 
-struct peel_comm {
-    int P;          // number of shards (ranks)
-    int rank;       // this process's rank (NCCL), -1 for virtual shards
-    bool virt;
-    ncclComm_t nccl;
-};
-
-#define PEEL_NCCL(call)                                                 \
-    do {                                                                \
-        ncclResult_t _r = (call);                                       \
-        if (_r != ncclSuccess) {                                        \
-            snprintf_nccl_error(_r, #call);                             \
-            return PEEL_ENCCL;                                          \
-        }                                                               \
-    } while (0)
-
-static void snprintf_nccl_error(ncclResult_t r, const char *where) {
-    (void)where;
-    peel::set_cuda_error(cudaErrorUnknown, ncclGetErrorString(r));
-}
-
 extern "C" peel_status peel_comm_unique_id(void *id128) {
     if (!id128) return PEEL_EINVAL;
     ncclUniqueId id;
@@ -468,7 +448,7 @@ extern "C" peel_status peel_comm_init(const void *id128, int nranks, int rank, p
     ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
     if (r != ncclSuccess) {
         delete c;
-        snprintf_nccl_error(r, "ncclCommInitRank");
+        peel::nccl_error(r);
         return PEEL_ENCCL;
     }
     *out = c;

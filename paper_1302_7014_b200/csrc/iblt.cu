@@ -25,18 +25,14 @@
 #include <vector>
 
 #include "common.cuh"
+#include "iblt_common.cuh"
 
 namespace peel {
 
 static constexpr uint32_t ISTAT_CAP = 65536;
 static constexpr int IB_BLOCK = 256;
 
-struct __align__(16) Cell {
-    uint32_t count;
-    uint32_t hashSum;
-    ull keySum;
-};
-static_assert(sizeof(Cell) == 16, "cell is 16 bytes");
+
 
 struct IbltCtl {
     ull fcnt[3];   // frontier sizes, F_t uses fcnt[(t-1)%3]
@@ -69,58 +65,6 @@ static ILayout ilayout(uint64_t C) {
     L.clist = o; o += al(sizeof(uint32_t) * C);
     L.total = o;
     return L;
-}
-
-// h_1(x)..h_r(x): r distinct cells
-template <int R>
-__device__ __forceinline__ void cells_of(ull x, ull C, ull seed_h, uint32_t (&c)[R]) {
-    int na = 0;
-    for (ull j = 0; na < R; j++) {
-        ull z = mix64(x ^ seed_h ^ ((j + 1) * 0xD1B54A32D192ED03ull));
-        uint32_t v = (uint32_t)__umul64hi(z, C);
-        bool dup = false;
-        #pragma unroll
-        for (int i = 0; i < R; i++) dup |= (i < na) && (c[i] == v);
-        if (!dup) {
-            #pragma unroll
-            for (int i = 0; i < R; i++) if (i == na) c[i] = v;
-            na++;
-        }
-    }
-}
-
-// subtable hashing ("hash each item into one cell in each subtable"):
-// h_j(x) = j C/r + umulhi64(mix64(x ^ seed_h ^ (j+1) 0xD1B54A32D192ED03), C/r)
-// blocked hashing (IBLT_FLAG_BLOCKED; R27): block b = umulhi64(mix64(x ^ seed_h ^ K_B), C / B),
-// then the plain r-distinct cells over B cells, offset by b B.  blog = 0: not blocked.
-template <int R>
-__device__ __forceinline__ void key_cells(ull x, ull C, ull seed_h, bool subt, uint32_t (&c)[R], uint32_t blog = 0) {
-    if (blog) {
-        const ull B = 1ull << blog;
-        const ull b = __umul64hi(mix64(x ^ seed_h ^ 0x9E6C63D0676A9A99ull), C >> blog);
-        cells_of<R>(x, B, seed_h, c);
-        #pragma unroll
-        for (int j = 0; j < R; j++) c[j] += (uint32_t)(b * B);
-    } else if (subt) {
-        const ull cs = C / R;
-        #pragma unroll
-        for (int j = 0; j < R; j++)
-            c[j] = (uint32_t)(j * cs + __umul64hi(mix64(x ^ seed_h ^ ((ull)(j + 1) * 0xD1B54A32D192ED03ull)), cs));
-    } else {
-        cells_of<R>(x, C, seed_h, c);
-    }
-}
-
-// checkSum(x)
-__device__ __forceinline__ uint32_t checksum(ull x, ull seed_c) { return (uint32_t)(mix64(x ^ seed_c) >> 32); }
-
-__device__ __forceinline__ Cell ld_cell_cg(const Cell *p) {
-    uint4 v = __ldcg(reinterpret_cast<const uint4 *>(p));
-    Cell c;
-    c.count = v.x;
-    c.hashSum = v.y;
-    c.keySum = ((ull)v.w << 32) | v.z;
-    return c;
 }
 
 // one pass of an insert/delete: the r cells of every key, restricted to cells in [lo, hi)
@@ -175,9 +119,6 @@ struct IPeelArgs {
     uint32_t blog;      // blocked hashing: log2 block size, 0 = off
 };
 
-__device__ __forceinline__ bool is_pure(const Cell &c, ull seed_c) {
-    return c.count == 1u && c.hashSum == checksum(c.keySum, seed_c);
-}
 
 // signed tables (set difference): pure = count +1 or -1 with a matching checksum; returns
 // +1 / -1, or 0 if not pure.  Unsigned recovery accepts only count == +1.

@@ -74,6 +74,15 @@ for (n, c, r, seed) in [(100003, 0.75, 3, 5), (50021, 0.85, 3, 6), (40009, 0.8, 
     assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist()
     assert res.killed.tolist() == ref.killed.tolist()
     assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
+for (C, r, load, blog) in [(100003, 3, 0.75, 0), (1 << 18, 3, 0.8, 12)]:
+    keys = O.gen_keys(int(load * C), 5)
+    o = O.Iblt(C, r, 3, blog=blog)
+    o.insert(keys)
+    ref = o.peel(cap_keys=keys.size + 1)
+    res = pk.iblt_dist_recover(comm, C, r, 3, torch.from_numpy(keys.view(np.int64)).cuda(), blog=blog)
+    assert res.rounds == ref.rounds and res.per_round.tolist() == ref.per_round.tolist()
+    assert res.complete == ref.complete
+    assert np.array_equal(np.sort(res.keys.cpu().numpy().view(np.uint64)), np.sort(ref.keys))
 del comm
 dist.destroy_process_group()
 print("NCCL_OK")
@@ -112,3 +121,33 @@ def test_binned_shard_build_vs_oracle(P):
     hub[:, 2] = np.where(hub[:, 2] == 7, 9, hub[:, 2])
     ok = (hub[:, 1] != hub[:, 2]) & (hub[:, 1] != 7) & (hub[:, 2] != 7)
     check(np.concatenate([hub[ok], e[400000:]]), n, 2, P)
+
+
+# ---- cell-partitioned IBLT -------------------------------------------------
+def iblt_check(C, r, seed, keys_np, P, blog=0):
+    o = O.Iblt(C, r, seed, blog=blog)
+    o.insert(keys_np)
+    ref = o.peel(cap_keys=keys_np.size + 1)
+    comm = pk.Comm.virtual_shards(P)
+    kd = torch.from_numpy(np.ascontiguousarray(keys_np).view(np.int64)).to(DEV)
+    res = pk.iblt_dist_recover(comm, C, r, seed, kd, blog=blog)
+    assert res.rounds == ref.rounds, (P, res.rounds, ref.rounds)
+    assert res.per_round.tolist() == ref.per_round.tolist()
+    assert res.complete == ref.complete
+    assert np.array_equal(np.sort(res.keys.cpu().numpy().view(np.uint64)), np.sort(ref.keys))
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("r,load", [(3, 0.75), (3, 0.85), (4, 0.7), (2, 0.4)])
+def test_iblt_dist_vs_oracle(P, r, load):
+    C = 100003
+    keys = synth.random_keys(int(load * C), 40 + P + r)
+    iblt_check(C, r, 5 + r, keys, P)
+
+
+@pytest.mark.parametrize("P", [2, 5])
+def test_iblt_dist_blocked_and_edges(P):
+    iblt_check(1 << 16, 3, 9, synth.random_keys(int(0.8 * (1 << 16)), 3), P, blog=12)
+    iblt_check(64, 3, 1, synth.random_keys(40, 4), P)       # shards of 32 cells, some empty
+    iblt_check(1000, 3, 1, np.zeros(0, dtype=np.uint64), P)  # no keys
+    iblt_check(1000, 3, 1, np.array([0, 7], dtype=np.uint64), P)

@@ -190,7 +190,7 @@ def run_reference(args):
                 "cpu_baseline": {"value": val, "unit": "trials/s", "cores": 1, "kind": "oracle",
                                  "sample": "each step = 2 trials of the C5s grid (n=10^6)"},
                 "e2e": {"value": val, "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        emit(line)
         return 0
     if kind == "kcore":
         e = O.gen_hypergraph(n, m, r, seed)
@@ -228,7 +228,7 @@ def run_reference(args):
                          "sample": f"each step = oracle peel of one n={n} instance of the same model"},
         "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -236,6 +236,64 @@ def iblt_bytes(C, N, r, nrec):
     """insert 8N + 16C (read keys, RMW cells once); peel 16C (round-1 scan) +
     per recovered key 16 (frontier entry) + 32r (RMW r cells) + 8 (output key)."""
     return 8 * N + 16 * C, 16 * C + nrec * (16 + 32 * r + 8)
+
+
+def run_iblt_dist(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, stream):
+    """C2 as ONE table partitioned by cell range over the ranks (iblt_dist_recover; SURVEY
+    §8 f3): NCCL under torchrun (--mode dist), or --virtual-shards P on one GPU.  Strong
+    scaling: the table and the key set are fixed."""
+    import torch
+    import torch.distributed as dist
+    if args.virtual_shards > 0:
+        comm = pk.Comm.virtual_shards(args.virtual_shards)
+        P = args.virtual_shards
+    else:
+        comm = pk.Comm.from_process_group(device=dev)
+        P = ws
+    keys = pk.gen_keys(N, seed, device=dev)  # the same keys on every rank
+    mem = torch.empty((int(pk.lib().iblt_dist_mem_bytes(comm._h, C, r)),), dtype=torch.uint8, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        res = pk.iblt_dist_recover(comm, C, r, seed, keys, mem=mem)
+    clk = ClockSampler(local)
+    barrier()
+    clk.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    pk.profile_enable(True)
+    per_kernel, launches = {}, 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = pk.iblt_dist_recover(comm, C, r, seed, keys, mem=mem)
+        launches += pk.last_launches()
+        for name, ms_, nl in pk.profile_read():
+            a_ = per_kernel.setdefault(name, [0.0, 0])
+            a_[0] += ms_
+            a_[1] += nl
+    e1.record(stream)
+    barrier()
+    pk.profile_enable(False)
+    clocks = clk.stop()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(res.nrecovered)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot)
+    value = tot.item() * args.steps / (t.item() / 1e3)
+    if rank == 0:
+        line = {"metric": IBLT_METRIC, "value": value, "unit": "keys/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": round(t.item() / args.steps, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32/u64 integer",
+                "data": "synthetic distinct 64-bit keys (SplitMix64 stream on device), replicated on every rank",
+                "config": {"workload": f"{args.config}: {text}", "cells": C, "keys": N, "r": r, "seed": seed,
+                           "rounds": res.rounds, "complete": res.complete,
+                           "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"cell-partitioned{P}")},
+                "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
+                "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
+        emit(line)
+    del comm
+    if dist.is_initialized():
+        dist.destroy_process_group()
+    return 0
 
 
 def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, stream):
@@ -354,7 +412,7 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
             "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 4)} for k, v in per_kernel.items()},
             "round_ms": round_ms, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -434,7 +492,7 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
                         "d2h_bytes_per_step": 12 * (hi - lo),
                         "api": "peel_sweep (host trial parameters in, host per-trial results out)"},
                 "cpu_baseline": cpu, "clocks": clocks}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ws > 1:
         dist.destroy_process_group()
     return 0
@@ -493,14 +551,30 @@ def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barri
                            "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"vertex-partitioned{P}")},
                 "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
                 "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
-        print(json.dumps(line), flush=True)
+        emit(line)
     del comm
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the real stdout (everything else -- library banners such as NCCL's
+    version line -- was redirected to stderr by main())."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # keep fd 1 for the JSON line only: native libraries (NCCL, CUDA) print to fd 1 directly
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -532,6 +606,7 @@ def main():
     dev = torch.device("cuda", local)
     if ws > 1 or (args.mode == "dist" and not args.virtual_shards):
         # --mode dist at N=1 runs the NCCL transport with world size 1 (plain or torchrun)
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # no version banner on stdout: one JSON line
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", str(rank))
@@ -547,6 +622,8 @@ def main():
         torch.cuda.synchronize()
 
     if kind == "iblt":
+        if args.virtual_shards > 0 or args.mode == "dist":
+            return run_iblt_dist(args, pk, dev, ws, rank, local, n, m, r, seed - rank, text, barrier, stream)
         return run_iblt(args, pk, dev, ws, rank, local, n, m, r, seed, text, barrier, stream)
     if kind == "sweep":
         return run_sweep_bench(args, pk, dev, ws, rank, local, n, m, r, k, text, barrier, stream)
@@ -728,7 +805,7 @@ def main():
             "kernel_alg_bytes": kb, "random_access_roofline": rand, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ws > 1:
         dist.destroy_process_group()
     return 0

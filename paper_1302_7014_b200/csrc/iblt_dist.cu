@@ -82,7 +82,7 @@ struct IDArgs {
     uint32_t *cand;        // local candidate bitmap
     uint32_t *clist;       // local candidate list (local ids)
     ulonglong2 *Fc, *Fn;   // frontier entries (global cell, key snapshot)
-    ull nF;
+    const ull *pnF;        // this round's frontier size (device: no host round trip)
     ull *send;             // P segments of cs keys
     ull *out;              // recovered keys (output)
     ull *outcnt;
@@ -147,11 +147,12 @@ __global__ void __launch_bounds__(IDB) idist_find_kernel(IDArgs a) {
     __syncthreads();
     ull found = 0;
     int slot = 0;
-    for (ull base = (ull)blockIdx.x * IDB; base < a.nF; base += (ull)gridDim.x * IDB) {
+    const ull nF = ld_cg_u64(a.pnF);
+    for (ull base = (ull)blockIdx.x * IDB; base < nF; base += (ull)gridDim.x * IDB) {
         const ull i = base + threadIdx.x;
         uint32_t dmask = 0;
         ull x = 0;
-        if (i < a.nF) {
+        if (i < nF) {
             const ulonglong2 ent = __ldcg(a.Fc + i);
             const uint32_t c = (uint32_t)ent.x;
             x = ent.y;
@@ -225,17 +226,19 @@ __global__ void __launch_bounds__(IDB) idist_apply_kernel(IDArgs a, const ull *_
 
 // retire this round's pure bits of the shard
 __global__ void __launch_bounds__(IDB) idist_clear_kernel(IDArgs a) {
-    for (ull i = blockIdx.x * (ull)IDB + threadIdx.x; i < a.nF; i += (ull)gridDim.x * IDB) {
+    const ull nF = ld_cg_u64(a.pnF);
+    for (ull i = blockIdx.x * (ull)IDB + threadIdx.x; i < nF; i += (ull)gridDim.x * IDB) {
         const uint32_t c = (uint32_t)__ldcg(&a.Fc[i].x);
         atomicAnd(a.pure + (c >> 5), ~(1u << (c & 31)));
     }
 }
 
 // retest: candidates still pure -> the next local frontier and pure bits
-__global__ void __launch_bounds__(IDB) idist_retest_kernel(IDArgs a, ull ncand) {
+__global__ void __launch_bounds__(IDB) idist_retest_kernel(IDArgs a) {
     __shared__ IDEntQ q;
     bq_init(q);
     __syncthreads();
+    const ull ncand = ld_cg_u64(&a.ctl->ccnt);
     ull *cnt = &a.ctl->fcnt[a.par];
     int slot = 0;
     for (ull base = (ull)blockIdx.x * IDB; base < ncand; base += (ull)gridDim.x * IDB) {
@@ -324,6 +327,7 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
         ulonglong2 *F[2] = {(ulonglong2 *)(d.base + L.F0), (ulonglong2 *)(d.base + L.F1)};
         a.Fc = F[cur];
         a.Fn = F[cur ^ 1];
+        a.pnF = &d.ctl->fcnt[cur];
         a.send = (ull *)(d.base + L.send);
         a.out = (ull *)out_keys;
         a.outcnt = outcnt;
@@ -390,15 +394,14 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
         if (!c->virt)
             PEEL_NCCL(ncclAllGather(pure + (size_t)c->rank * (cs / 32), pure, cs / 32 * sizeof(uint32_t), ncclUint8,
                                     c->nccl, s));
-        st = fetch();
-        if (st != PEEL_OK) return st;
-        // find
+        // find (frontier sizes are read on the device: hc[] still holds them from the end of
+        // the previous round, which sizes the grids)
         for (size_t i = 0; i < sh.size(); i++) {
             IDArgs a = args(sh[i], cur);
-            a.nF = hc[i].fcnt[cur];
-            if (!a.nF) continue;
+            const ull nF = hc[i].fcnt[cur];
+            if (!nF) continue;
             ProfScope ps("iblt_dist_find", s);
-            idist_find_kernel<R><<<idgrid(a.nF), IDB, 0, s>>>(a);
+            idist_find_kernel<R><<<idgrid(nF), IDB, 0, s>>>(a);
         }
         PEEL_CUDA(cudaGetLastError());
         st = fetch();
@@ -451,29 +454,19 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
         for (auto &h : hc) found += h.found;
         for (size_t i = 0; i < sh.size(); i++) {
             IDArgs a = args(sh[i], cur);
-            a.nF = hc[i].fcnt[cur];
             if (nrecv[i]) {
                 ProfScope ps("iblt_dist_apply", s);
                 idist_apply_kernel<R><<<idgrid(nrecv[i]), IDB, 0, s>>>(a, (const ull *)(sh[i].base + L.recv), nrecv[i]);
             }
         }
-        for (size_t i = 0; i < sh.size(); i++) {
-            IDArgs a = args(sh[i], cur);
-            a.nF = hc[i].fcnt[cur];
-            if (a.nF) {
-                ProfScope ps("iblt_dist_retest", s);
-                idist_clear_kernel<<<idgrid(a.nF), IDB, 0, s>>>(a);
-            }
-        }
-        st = fetch();
-        if (st != PEEL_OK) return st;
         ull nf = 0;
         for (size_t i = 0; i < sh.size(); i++) {
             IDArgs a = args(sh[i], cur);
-            if (hc[i].ccnt) {
-                ProfScope ps("iblt_dist_retest", s);
-                idist_retest_kernel<<<idgrid(hc[i].ccnt), IDB, 0, s>>>(a, hc[i].ccnt);
-            }
+            const ull nF = hc[i].fcnt[cur];
+            ProfScope ps("iblt_dist_retest", s);
+            if (nF) idist_clear_kernel<<<idgrid(nF), IDB, 0, s>>>(a);
+            // candidates <= keys received x r (sized from the host's receive count)
+            idist_retest_kernel<<<idgrid(std::min<ull>(nrecv[i] * R, sh[i].ncl)), IDB, 0, s>>>(a);
         }
         PEEL_CUDA(cudaGetLastError());
         st = fetch();

@@ -599,6 +599,11 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             binr[i] = d.binned && (double)a.nE >= dist_bin_frac(d.v1 - d.v0) * (double)(d.v1 - d.v0);
             if (binr[i]) {
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
+                // sort the local frontier by edge bin into the next-round buffer (free until
+                // shard_apply writes F_{t+1} there)
+                peel_status st3 = shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s);
+                if (st3 != PEEL_OK) return st3;
+                a.Fc = d.F[nxt];
                 PEEL_CUDA(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s));
                 const size_t sm = dist_stage_smem(R, bv.nbins);
                 PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));

@@ -1932,7 +1932,7 @@ static bool use_csr(uint32_t k, uint32_t flags) { return (flags & PEEL_FLAG_CSR)
 // ---- the binned build for one vertex shard (shard.h; used by dist.cu) --------------------
 struct ShardBins {
     uint64_t nbins, total_cap;
-    size_t cursor, base, cap, flag, ctl, entries, total;
+    size_t cursor, base, cap, flag, ctl, esort, entries, total;
 };
 
 static ShardBins shard_bins(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
@@ -1946,6 +1946,7 @@ static ShardBins shard_bins(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
     B.cap = o; o += al(sizeof(ull) * B.nbins);
     B.flag = o; o += al(sizeof(uint32_t) + 8 + sizeof(ull));  // overflow flag, then the D work counter
     B.ctl = o; o += al(sizeof(Ctl));                           // binned rounds: round_apply's counters
+    B.esort = o; o += al(sizeof(ull) * 2 * (((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT) + 1));  // edge sort
     B.entries = o; o += al(sizeof(ull) * B.total_cap);
     B.total = o;
     return B;
@@ -2009,7 +2010,27 @@ ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc,
     v.entries = (ull *)(scratch + B.entries);
     v.work = (ull *)(scratch + B.flag + 8);  // after the overflow flag, in the same 256-byte slot
     v.ctl = scratch + B.ctl;
+    v.esort = (ull *)(scratch + B.esort);
     return v;
+}
+
+// sort the shard's frontier entries (v, e) by edge bin into dst (see esort_scatter_kernel):
+// the shard's kill phase then reads alive bits and rows per edge bin, from L2
+peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint64_t nE_host, uint64_t m, void *dst,
+                            const ShardBinsView &v, cudaStream_t s) {
+    if (!nE_host || !m) return PEEL_OK;
+    const uint32_t enb = (uint32_t)((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT);
+    ull *hist = v.esort, *cur = v.esort + enb + 1;
+    const size_t essmem = esort_scatter_smem(enb);
+    PEEL_CUDA(cudaFuncSetAttribute(esort_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)essmem));
+    PEEL_CUDA(cudaMemsetAsync(v.esort, 0, sizeof(ull) * 2 * (enb + 1), s));
+    ProfScope ps("frontier_edge_sort", s);
+    esort_hist_kernel<<<grid_for(nE_host, 8), 256, sizeof(uint32_t) * enb, s>>>((const uint2 *)src, pN, enb, hist);
+    const uint64_t chunks = (nE_host + ES_CH - 1) / ES_CH;
+    const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * 4);
+    esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>((const uint2 *)src, pN, enb, hist, cur, (uint2 *)dst);
+    PEEL_CUDA(cudaGetLastError());
+    return PEEL_OK;
 }
 
 // phase D of a binned round on a shard: the decrements staged in the shard's bins (by

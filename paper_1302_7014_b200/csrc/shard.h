@@ -29,6 +29,7 @@ struct ShardBinsView {
     unsigned long long *entries;
     unsigned long long *work;
     char *ctl;
+    unsigned long long *esort;  // edge-sort histogram and cursors
 };
 ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc, char *scratch);
 
@@ -36,6 +37,11 @@ ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc,
 peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long long *state, void *Fn,
                         const ShardBinsView &v, uint32_t t, unsigned long long *out_nf, unsigned long long *out_ne,
                         cudaStream_t s);
+
+// the shard's frontier entries (v, e) [nE_host of them; *pN on the device] sorted by edge bin
+// into dst (same capacity), as the single-GPU binned rounds do before their kill phase
+peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint64_t nE_host, uint64_t m, void *dst,
+                            const ShardBinsView &v, cudaStream_t s);
 
 // BIN_SHIFT of kcore.cu (vertex bins of 2^22 local ids)
 constexpr int SHARD_BIN_SHIFT = 22;

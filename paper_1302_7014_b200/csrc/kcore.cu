@@ -184,7 +184,10 @@ __global__ void bin_init_kernel(uint64_t n, uint64_t nloc, uint64_t m, uint32_t 
 }
 
 static constexpr int PART_BLOCK = 256;
-static constexpr int PART_ENTRIES = 4096;  // endpoint entries staged per chunk
+#ifndef PEEL_PART_ENTRIES
+#define PEEL_PART_ENTRIES 4096
+#endif
+static constexpr int PART_ENTRIES = PEEL_PART_ENTRIES;  // endpoint entries staged per chunk
 
 // pass 1: partition the r m endpoint increments by vertex bin.  Per chunk of edges the
 // block stages the chunk's edge words in shared memory with 16-byte coalesced loads,
@@ -650,7 +653,10 @@ __global__ void __launch_bounds__(PEEL_BLOCK) bin_accumulate_kernel(PeelArgs a, 
 // L2-resident returning atomics while the next bin's state is prefetched into L2.  The
 // crossing rule (old count == k) and the (v, e) frontier entries are those of the persistent
 // kernel, so the schedule is unchanged.
-static constexpr int KU = 4;                      // frontier entries per thread per K iteration
+#ifndef PEEL_KU
+#define PEEL_KU 4
+#endif
+static constexpr int KU = PEEL_KU;                 // frontier entries per thread per K iteration
 static constexpr int KCH = PART_BLOCK * KU;       // entries per block iteration
 #ifndef PEEL_DCH
 #define PEEL_DCH 512

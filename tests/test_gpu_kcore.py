@@ -292,3 +292,19 @@ def test_small_instances_both_round_loops(path, monkeypatch):
     check_vs_oracle(e, n, 2, twice=False)
     e = pk.gen_hypergraph(100000, 70000, 3, 1, device=DEV)
     check_vs_oracle(e.cpu().numpy().view(np.uint32), 100000, 2, twice=False)
+
+
+@pytest.mark.parametrize("r,c", [(2, 0.45), (5, 0.62), (8, 0.3), (4, 0.8)])
+def test_binned_rounds_all_r_vs_oracle(r, c):
+    # n > 2^23: binned build, frontier edge sort, binned kill/apply rounds, then the
+    # persistent kernel -- for r other than 3 (row loads of 8 B and 16 B windows, R-wide rows)
+    n = (1 << 23) + 4097
+    m = int(c * n)
+    e = pk.gen_hypergraph(n, m, r, 60 + r, device=DEV)
+    e_np = e.cpu().numpy().view(np.uint32)
+    ref = O.sync_peel(e_np, n, 2, want_peel_round=True)
+    res = pk.peel_kcore(e, n, 2, want_peel_round=True)
+    assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist()
+    assert res.killed.tolist() == ref.killed.tolist()
+    assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
+    assert np.array_equal(res.peel_round.cpu().numpy().view(np.uint32), ref.peel_round)

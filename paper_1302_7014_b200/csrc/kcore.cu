@@ -1204,6 +1204,37 @@ __global__ void __launch_bounds__(PEEL_BLOCK, 4) peel_packed_kernel(PeelArgs a) 
         uint2 *Fn = (uint2 *)a.F[t & 1];
         ull *cn = &ctl->ne[t % 3];
         ull kills = 0, crossed = 0;
+        if (nE <= nthr) {
+            // a latency-bound round (small frontier, e.g. the tail of a near-threshold peel): one
+            // entry per thread over the whole grid, and its r-1 decrements issued together before
+            // any result is used -- the shortest dependent chain per round
+            const uint64_t i = tid;
+            const uint2 ent = i < nE ? __ldcg(Fc + i) : make_uint2(0u, 0u);
+            bool win = false;
+            if (i < nE) {
+                const uint32_t bit = 1u << (ent.y & 31);
+                win = (atomicAnd(a.alive + (ent.y >> 5), ~bit) & bit) != 0;
+            }
+            uint32_t ue[R];
+            if (win) load_row<R>(a.edges, ent.y, a.m, a.edges_vec, ue);
+            const ull dec = 0ull - (((ull)ent.y << 32) + 1ull);
+            ull old[R];
+            #pragma unroll
+            for (int r = 0; r < R; r++) {
+                old[r] = ~0ull;  // count 0xFFFFFFFF: never k
+                if (win && ue[r] != ent.x) old[r] = atomicAdd(a.state + ue[r], dec);
+            }
+            kills += win;
+            #pragma unroll
+            for (int r = 0; r < R; r++)
+                if (count_of(old[r]) == k) {
+                    crossed++;
+                    if (a.peel_round) a.peel_round[ue[r]] = t + 1;
+                    bq_push(q, slot, make_uint2(ue[r], idsum_of(old[r]) - ent.y), Fn, cn);
+                }
+            bq_flush(q, slot, Fn, cn);
+            slot ^= 1;
+        } else
         for (uint64_t base = (uint64_t)blockIdx.x * CHUNK; base < nE; base += (uint64_t)gridDim.x * CHUNK) {
             // U independent entries per thread, staged so their random accesses overlap
             uint2 ent[U];

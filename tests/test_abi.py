@@ -54,6 +54,13 @@ def test_workspace_queries():
     assert L.peel_kcore_workspace_bytes(2**32 + 1, 10, 3, 2, 0) == 0
     assert L.iblt_mem_bytes(10**7, 3) >= 16 * 10**7
     assert L.iblt_mem_bytes(2, 3) == 0
+    # cell-partitioned IBLT: per shard 16 B cells + 2 x 16 B frontier + 4 B list + 2 x 8 P B of
+    # message buffers per owned cell; virtual shards hold all P shards
+    for P in (1, 4, 8):
+        c = pk.Comm.virtual_shards(P)
+        b = L.iblt_dist_mem_bytes(c._h, 10**7, 3)
+        assert (52 + 16 * P) * 10**7 <= b < (52 + 16 * P) * 10**7 * 1.01 + (8 << 20)
+        assert L.iblt_dist_mem_bytes(c._h, 2, 3) == 0 and L.iblt_dist_mem_bytes(c._h, 10**7, 9) == 0
 
 
 def test_invalid_arguments_rejected_before_any_launch():

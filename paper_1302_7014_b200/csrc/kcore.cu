@@ -679,13 +679,11 @@ template <int R>
 __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelArgs a, BinRound br) {
     extern __shared__ unsigned char smem_raw[];
     const uint32_t nbins = br.nbins;
-    ull *sent = (ull *)smem_raw;                         // [(R-1) KCH] unsorted (e << 32 | u)
-    ull *sorted = sent + (R - 1) * KCH;                  // [(R-1) KCH]
+    ull *sorted = (ull *)smem_raw;                       // [(R-1) KCH] the chunk's decrements, bin-sorted
     ull *gpos = sorted + (R - 1) * KCH;                  // [nbins]
     uint32_t *hist = (uint32_t *)(gpos + nbins);         // [nbins]
     uint32_t *offs = hist + nbins;                       // [nbins]
-    uint32_t *fill = offs + nbins;                       // [nbins]
-    __shared__ uint32_t wsum[PART_BLOCK / 32], total;
+    __shared__ uint32_t total;
     Ctl *ctl = a.ctl;
     const uint32_t t = br.t;
     const ull nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
@@ -699,7 +697,7 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
     const ull mask = (1ull << BIN_SHIFT) - 1;
     ull kills = 0;
     for (uint64_t base = (uint64_t)blockIdx.x * KCH; base < nE; base += (uint64_t)gridDim.x * KCH) {
-        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) { hist[b] = 0; fill[b] = 0; }
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
         uint2 ent[KU];
         bool win[KU];
         #pragma unroll
@@ -717,48 +715,23 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
             }
         }
         uint32_t ue[KU][R];
-        uint32_t mine = 0;
         #pragma unroll
         for (int j = 0; j < KU; j++)
             if (win[j]) {
                 kills++;
-                mine += R - 1;
                 load_row<R>(a.edges, ent[j].y, a.m, a.edges_vec, ue[j]);
             }
-        // block exclusive scan of per-thread decrement counts -> staging positions
-        uint32_t x = mine;
-        #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if ((threadIdx.x & 31) >= (unsigned)o) x += y;
-        }
-        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            uint32_t w = threadIdx.x < PART_BLOCK / 32 ? wsum[threadIdx.x] : 0, z = w;
-            #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-                if (threadIdx.x >= (unsigned)o) z += y;
-            }
-            if (threadIdx.x < PART_BLOCK / 32) wsum[threadIdx.x] = z - w;
-            if (threadIdx.x == PART_BLOCK / 32 - 1) total = z;
-        }
-        __syncthreads();
-        uint32_t pos = wsum[threadIdx.x >> 5] + x - mine;
+        __syncthreads();  // hist zeroed
+        // the histogram atomic's return value is the decrement's rank within its bin: the
+        // decrements stay in registers until the bin offsets are known (no unsorted copy)
+        uint32_t rk[KU][R];
         #pragma unroll
         for (int j = 0; j < KU; j++)
-            if (win[j]) {
-                #pragma unroll
-                for (int r = 0; r < R; r++)
-                    if (ue[j][r] != ent[j].x) {
-                        sent[pos++] = ((ull)ent[j].y << 32) | ue[j][r];
-                        atomicAdd(&hist[ue[j][r] >> BIN_SHIFT], 1u);
-                    }
-            }
+            #pragma unroll
+            for (int r = 0; r < R; r++)
+                if (win[j] && ue[j][r] != ent[j].x) rk[j][r] = atomicAdd(&hist[ue[j][r] >> BIN_SHIFT], 1u);
         __syncthreads();
-        const uint32_t tot = total;
-        if (threadIdx.x < 32) {
+        if (threadIdx.x < 32) {  // exclusive scan of hist over the bins: one warp
             const uint32_t per = (nbins + 31) / 32;
             uint32_t loc = 0;
             for (uint32_t q2 = 0; q2 < per; q2++) {
@@ -776,16 +749,19 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
                 uint32_t b = threadIdx.x * per + q2;
                 if (b < nbins) { offs[b] = run; run += hist[b]; }
             }
+            if (threadIdx.x == 31) total = z;
         }
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)
             if (hist[b]) gpos[b] = atomicAdd(br.cursor + b, (ull)hist[b]);
-        for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
-            const ull v = sent[i];
-            const uint32_t b = (uint32_t)v >> BIN_SHIFT;
-            sorted[offs[b] + atomicAdd(&fill[b], 1u)] = v;
-        }
+        #pragma unroll
+        for (int j = 0; j < KU; j++)
+            #pragma unroll
+            for (int r = 0; r < R; r++)
+                if (win[j] && ue[j][r] != ent[j].x)
+                    sorted[offs[ue[j][r] >> BIN_SHIFT] + rk[j][r]] = ((ull)ent[j].y << 32) | ue[j][r];
         __syncthreads();
+        const uint32_t tot = total;
         for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
             const ull v = sorted[i];
             const uint32_t b = (uint32_t)v >> BIN_SHIFT;
@@ -907,7 +883,7 @@ static size_t esort_scatter_smem(uint32_t nb) {
 }
 
 static size_t kill_partition_smem(int r, uint32_t nbins) {
-    return 2 * sizeof(ull) * (size_t)(r - 1) * KCH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
+    return sizeof(ull) * (size_t)(r - 1) * KCH + (sizeof(ull) + 2 * sizeof(uint32_t)) * nbins;
 }
 
 

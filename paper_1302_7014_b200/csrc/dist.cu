@@ -264,7 +264,7 @@ static constexpr int DKU = 4;                  // entries per thread per chunk
 static constexpr int DKCH = DB * DKU;          // entries per chunk
 
 static size_t dist_stage_smem(int r, uint32_t nbins) {
-    return 2 * sizeof(ull) * (size_t)r * DKCH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins;
+    return sizeof(ull) * (size_t)r * DKCH + (sizeof(ull) + 2 * sizeof(uint32_t)) * nbins;
 }
 
 template <int R, bool RECV>
@@ -273,14 +273,12 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
     extern __shared__ unsigned char smem_raw[];
     constexpr int SE = R * DKCH;
     const uint32_t nbins = bv.nbins;
-    ull *sent = (ull *)smem_raw;                  // [SE] unsorted (e << 32 | local u)
-    ull *sorted = sent + SE;                      // [SE]
+    ull *sorted = (ull *)smem_raw;                // [SE] the chunk's owned decrements, bin-sorted
     ull *gpos = sorted + SE;                      // [nbins]
     uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
     uint32_t *offs = hist + nbins;                // [nbins]
-    uint32_t *fill = offs + nbins;                // [nbins]
     __shared__ DIdQ qs[8];
-    __shared__ uint32_t wsum[DB / 32], total;
+    __shared__ uint32_t total;
     if (!RECV)
         for (int d = 0; d < 8; d++) bq_init(qs[d]);
     const ull nE = RECV ? nrecv : a.nE;
@@ -288,7 +286,7 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
     ull kills = 0;
     int slot = 0;
     for (uint64_t base = (uint64_t)blockIdx.x * DKCH; base < nE; base += (uint64_t)gridDim.x * DKCH) {
-        for (uint32_t b = threadIdx.x; b < nbins; b += DB) { hist[b] = 0; fill[b] = 0; }
+        for (uint32_t b = threadIdx.x; b < nbins; b += DB) hist[b] = 0;
         uint2 ent[DKU];
         bool win[DKU];
         #pragma unroll
@@ -307,7 +305,7 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             }
         }
         uint32_t u[DKU][R];
-        uint32_t mine = 0, sendm[DKU];
+        uint32_t sendm[DKU];
         #pragma unroll
         for (int j = 0; j < DKU; j++) {
             sendm[j] = 0;
@@ -317,9 +315,7 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             #pragma unroll
             for (int r = 0; r < R; r++) {
                 mn = min(mn, u[j][r]);
-                const bool own = u[j][r] >= a.v0 && u[j][r] < a.v1;
-                if (own && (RECV || u[j][r] != ent[j].x)) mine++;
-                if (!own) sendm[j] |= 1u << owner_of(u[j][r], a.n, a.P);
+                if (!(u[j][r] >= a.v0 && u[j][r] < a.v1)) sendm[j] |= 1u << owner_of(u[j][r], a.n, a.P);
             }
             if (owner_of(mn, a.n, a.P) == a.p) kills++;
         }
@@ -330,40 +326,17 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
                 for (int d = 0; d < a.P; d++)
                     if (sendm[j] >> d & 1u) bq_push(qs[d], slot, ent[j].y, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
         }
-        // block exclusive scan of per-thread staged counts -> staging positions
-        uint32_t x = mine;
-        #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if ((threadIdx.x & 31) >= (unsigned)o) x += y;
-        }
-        if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            uint32_t w = threadIdx.x < DB / 32 ? wsum[threadIdx.x] : 0, z = w;
-            #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-                if (threadIdx.x >= (unsigned)o) z += y;
-            }
-            if (threadIdx.x < DB / 32) wsum[threadIdx.x] = z - w;
-            if (threadIdx.x == DB / 32 - 1) total = z;
-        }
-        __syncthreads();
-        uint32_t pos = wsum[threadIdx.x >> 5] + x - mine;
+        __syncthreads();  // hist zeroed
+        // owned decrements stay in registers with their rank in the bin (the histogram atomic's
+        // return value) until the bin offsets are known (as round_kill_partition_kernel does)
+        uint32_t rk[DKU][R];
         #pragma unroll
         for (int j = 0; j < DKU; j++)
-            if (win[j]) {
-                #pragma unroll
-                for (int r = 0; r < R; r++)
-                    if (u[j][r] >= a.v0 && u[j][r] < a.v1 && (RECV || u[j][r] != ent[j].x)) {
-                        const uint32_t lu = (uint32_t)(u[j][r] - a.v0);
-                        sent[pos++] = ((ull)ent[j].y << 32) | lu;
-                        atomicAdd(&hist[lu >> SHARD_BIN_SHIFT], 1u);
-                    }
-            }
+            #pragma unroll
+            for (int r = 0; r < R; r++)
+                if (win[j] && u[j][r] >= a.v0 && u[j][r] < a.v1 && (RECV || u[j][r] != ent[j].x))
+                    rk[j][r] = atomicAdd(&hist[(uint32_t)(u[j][r] - a.v0) >> SHARD_BIN_SHIFT], 1u);
         __syncthreads();
-        const uint32_t tot = total;
         if (threadIdx.x < 32) {
             const uint32_t per = (nbins + 31) / 32;
             uint32_t loc = 0;
@@ -382,16 +355,21 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
                 uint32_t b = threadIdx.x * per + q2;
                 if (b < nbins) { offs[b] = run; run += hist[b]; }
             }
+            if (threadIdx.x == 31) total = z;
         }
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < nbins; b += DB)
             if (hist[b]) gpos[b] = atomicAdd(bv.cursor + b, (ull)hist[b]);
-        for (uint32_t i = threadIdx.x; i < tot; i += DB) {
-            const ull v = sent[i];
-            const uint32_t b = (uint32_t)v >> SHARD_BIN_SHIFT;
-            sorted[offs[b] + atomicAdd(&fill[b], 1u)] = v;
-        }
+        #pragma unroll
+        for (int j = 0; j < DKU; j++)
+            #pragma unroll
+            for (int r = 0; r < R; r++)
+                if (win[j] && u[j][r] >= a.v0 && u[j][r] < a.v1 && (RECV || u[j][r] != ent[j].x)) {
+                    const uint32_t lu = (uint32_t)(u[j][r] - a.v0);
+                    sorted[offs[lu >> SHARD_BIN_SHIFT] + rk[j][r]] = ((ull)ent[j].y << 32) | lu;
+                }
         __syncthreads();
+        const uint32_t tot = total;
         for (uint32_t i = threadIdx.x; i < tot; i += DB) {
             const ull v = sorted[i];
             const uint32_t b = (uint32_t)v >> SHARD_BIN_SHIFT;
@@ -607,6 +585,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 PEEL_CUDA(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s));
                 const size_t sm = dist_stage_smem(R, bv.nbins);
                 PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
                 int kb = 0;
                 PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, false>, DB, sm));
                 ProfScope ps("dist_kill_binned", s);
@@ -683,6 +662,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 if (nrecv[i]) {
                     const size_t sm = dist_stage_smem(R, bv.nbins);
                     PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                    PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
                     int kb = 0;
                     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, true>, DB, sm));
                     ProfScope ps("dist_recv_binned", s);

@@ -123,6 +123,27 @@ def ncu_traffic(config, kernel):
     return int(k["traffic_per_launch"]), f"profiles/r01_traffic_{config}.json (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
 
 
+def dram_step(config, per_kernel, steps, ms_step, hbm):
+    """Whole-step real DRAM traffic: the committed ncu bytes of every kernel this step launched
+    (profiles/r01_traffic_<config>.json, per step) over this run's step time, or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))["kernels"]
+    except Exception:
+        return None
+    alias = {"peel_rounds_packed": "peel_packed", "frontier_edge_sort": ("esort_hist", "esort_scatter")}
+    tot, missing = 0.0, []
+    for name in per_kernel:
+        keys = alias.get(name, name)
+        keys = keys if isinstance(keys, tuple) else (keys,)
+        found = [d[k] for k in keys if k in d]
+        if not found:
+            missing.append(name)
+        tot += sum(f["dram_read_bytes_per_step"] + f["dram_write_bytes_per_step"] for f in found)
+    return {"bytes": int(tot), "frac_of_peak": round(tot / (ms_step / 1e3) / 1e9 / hbm, 4),
+            "kernels_without_traffic": missing,
+            "source": f"profiles/r01_traffic_{config}.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -801,6 +822,7 @@ def main():
             "rounds": res.rounds,
             "hbm_roofline_step": {"alg_bytes": step_alg, "frac_of_measured": round(step_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
                                   "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},
+            "dram_step": dram_step(args.config, per_kernel, args.steps, ms_step, hbm),
             "roofline": roof, "kernels": kernels, "round_ms": round_ms,
             "kernel_alg_bytes": kb, "random_access_roofline": rand, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,

@@ -16,6 +16,7 @@
 // Same recovered set, rounds and per-round counts as the single-GPU table by construction
 // (the owner rule and the round snapshot are identical); the tests check it against the oracle.
 #include <nccl.h>
+#include <stddef.h>
 #include <string.h>
 
 #include <algorithm>
@@ -38,6 +39,8 @@ struct IDCtl {
     uint32_t nonzero;
     uint32_t pad;
 };
+// the per-round reset clears ccnt .. found with one memset
+static_assert(offsetof(IDCtl, found) == offsetof(IDCtl, ccnt) + 9 * sizeof(ull), "per-round counters contiguous");
 
 static inline size_t ial(size_t x) { return (x + 255) & ~(size_t)255; }
 

@@ -19,6 +19,7 @@
 // the decrements of its killed edges, and F_{t+1} is the set of k -> k-1 crossings.
 #include <nccl.h>
 #include <stdlib.h>
+#include <stddef.h>
 #include <string.h>
 
 #include <algorithm>
@@ -41,6 +42,9 @@ struct DCtl {
     uint32_t err;
     uint32_t pad;
 };
+
+// the per-round reset clears kills and nsend[8] with one memset
+static_assert(offsetof(DCtl, nsend) == offsetof(DCtl, kills) + sizeof(ull), "per-round counters contiguous");
 
 static inline size_t dal(size_t x) { return (x + 255) & ~(size_t)255; }
 

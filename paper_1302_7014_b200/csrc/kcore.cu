@@ -778,7 +778,10 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
 // writes one run per bin.  The kill phase then reads the entries in edge-bin order, so the
 // alive bits (and the rows) it touches at a time cover ~one edge bin: L2 hits instead of
 // random DRAM granules.
-static constexpr int ES_CH = 4096;  // entries per chunk (scatter)
+#ifndef PEEL_ES_CH
+#define PEEL_ES_CH 4096
+#endif
+static constexpr int ES_CH = PEEL_ES_CH;  // entries per chunk (scatter)
 
 __global__ void __launch_bounds__(256) esort_hist_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
                                                          uint32_t nb, ull *ghist) {

@@ -37,6 +37,8 @@ void prof_post(const char *name, cudaStream_t s);         // after it (counts th
 int prof_collect();                                       // after stream sync: resolve events
 bool prof_enabled();
 void prof_hold(bool on);  // nest public calls inside one report (peel_sweep)
+void prof_add_launches(uint32_t n);  // kernels launched inside a replayed CUDA graph
+void prof_capture(bool on);          // suppress profiling while a stream is being captured
 void prof_set_rounds(const std::vector<double> &ms);      // per-round device time of the last peel
 
 struct ProfScope {

@@ -1655,12 +1655,97 @@ static peel_status stream_all(const EdgeStream &es, uint64_t m, uint32_t r, cuda
     return PEEL_OK;
 }
 
+// Small instances (the one-cluster path) are launch-bound: the call's memsets, build and round
+// loop are captured once per (device, stream, buffers, shape) into a CUDA graph and replayed
+// (PEEL_GRAPH=0 disables).  A few entries are kept; a new shape or buffer evicts the oldest.
+struct SmallGraph {
+    int dev;
+    const void *edges, *mask, *pr, *ws;
+    cudaStream_t s;
+    uint64_t n, m;
+    uint32_t r, k;
+    cudaGraphExec_t exec;
+};
+
+static bool graphs_on() {
+    const char *e = getenv("PEEL_GRAPH");
+    return !(e && atoi(e) == 0);
+}
+
 template <int R>
 static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr, uint32_t flags,
                              uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
                              uint64_t *killed, uint32_t cap, uint32_t *peel_round, char *ws,
-                             const Layout &L, cudaStream_t s, const EdgeStream *es = nullptr) {
+                             const Layout &L, cudaStream_t s, const EdgeStream *es = nullptr,
+                             bool capturing = false);
+
+template <int R>
+static peel_status run_small_graph(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, uint8_t *core_mask,
+                                   uint32_t *rounds, uint64_t *survivors, uint64_t *killed, uint32_t cap,
+                                   uint32_t *peel_round, char *ws, const Layout &L, cudaStream_t s) {
+    static std::mutex mu;
+    static std::vector<SmallGraph> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    PEEL_CUDA(cudaGetDevice(&dev));
+    cudaGraphExec_t exec = nullptr;
+    for (auto &g : cache)
+        if (g.dev == dev && g.edges == edges && g.mask == core_mask && g.pr == peel_round && g.ws == ws && g.s == s &&
+            g.n == n && g.m == m && g.r == (uint32_t)R && g.k == k) {
+            exec = g.exec;
+            break;
+        }
+    if (!exec) {
+        // captured on a private stream (the caller's may be the legacy default stream, which
+        // cannot be captured); the graph is then launched into the caller's stream
+        static std::map<int, cudaStream_t> cap_stream;
+        if (!cap_stream.count(dev)) {
+            cudaStream_t cs = nullptr;
+            PEEL_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            cap_stream[dev] = cs;
+        }
+        cudaStream_t cs = cap_stream[dev];
+        cudaGraph_t graph = nullptr;
+        PEEL_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        prof_capture(true);
+        peel_status st = run_kcore<R>(edges, n, m, k, false, 0u, core_mask, rounds, survivors, killed, cap, peel_round,
+                                      ws, L, cs, nullptr, true);
+        prof_capture(false);
+        const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+        if (st != PEEL_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (ce != cudaSuccess) { set_cuda_error(ce, "cudaStreamEndCapture"); return PEEL_ECUDA; }
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) { set_cuda_error(ie, "cudaGraphInstantiate"); return PEEL_ECUDA; }
+        if (cache.size() >= 8) {
+            cudaGraphExecDestroy(cache.front().exec);
+            cache.erase(cache.begin());
+        }
+        cache.push_back({dev, edges, core_mask, peel_round, ws, s, n, m, (uint32_t)R, k, exec});
+    }
+    {
+        ProfScope ps("peel_small_graph", s);
+        PEEL_CUDA(cudaGraphLaunch(exec, s));
+    }
+    prof_add_launches(m ? 1 : 0);  // build + round loop inside the graph (ProfScope counted one)
+    PeelArgs a;
+    memset(&a, 0, sizeof a);
+    a.rtime = (ull *)(ws + L.rtime);
+    return finish_kcore(n, cap, rounds, survivors, killed, ws, L, a, s);
+}
+
+template <int R>
+static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, bool csr, uint32_t flags,
+                             uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
+                             uint64_t *killed, uint32_t cap, uint32_t *peel_round, char *ws,
+                             const Layout &L, cudaStream_t s, const EdgeStream *es, bool capturing) {
     const bool subr = (flags & PEEL_FLAG_SUBROUNDS) != 0;
+    if (!capturing && !csr && !subr && !es && !L.nbins && graphs_on() &&
+        cluster_eligible(n, m, (const void *)peel_cluster_kernel<R>))
+        return run_small_graph<R>(edges, n, m, k, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s);
     Ctl *ctl = (Ctl *)(ws + L.ctl);
     ull *stats = (ull *)(ws + L.stats);
     uint32_t *alive = (uint32_t *)(ws + L.alive);
@@ -1913,6 +1998,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                 ProfScope ps("peel_rounds_cluster", s);
                 PEEL_CUDA(cudaLaunchKernelEx(&cfg, peel_cluster_kernel<R>, a, shp));
             }
+            if (capturing) return PEEL_OK;  // run_small_graph launches the graph, then finishes
             return finish_kcore(n, cap, rounds, survivors, killed, ws, L, a, s);
         }
     }

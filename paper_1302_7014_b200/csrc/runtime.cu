@@ -52,6 +52,9 @@ static bool g_collected = true;
 static int g_hold = 0;  // > 0 inside a call made of public calls (peel_sweep): one report
 
 void prof_hold(bool on) { g_hold += on ? 1 : -1; }
+void prof_add_launches(uint32_t n) { g_launches += n; }
+static bool g_capture = false;  // inside a stream capture: no events, no counts (the replay is timed)
+void prof_capture(bool on) { g_capture = on; }
 
 void prof_begin_call() {
     if (!g_collected || g_hold) return;
@@ -63,13 +66,14 @@ void prof_begin_call() {
 }
 
 void prof_pre(const char *name, cudaStream_t s) {
-    if (!g_prof_on) return;
+    if (!g_prof_on || g_capture) return;
     ProfEntry p = take_pair(name);
     cudaEventRecord(p.a, s);
     g_prof.push_back(p);
 }
 
 void prof_post(const char *name, cudaStream_t s) {
+    if (g_capture) return;
     g_launches++;
     if (!g_prof_on) return;
     if (!g_prof.empty() && g_prof.back().name == name) cudaEventRecord(g_prof.back().b, s);

@@ -308,3 +308,22 @@ def test_binned_rounds_all_r_vs_oracle(r, c):
     assert res.killed.tolist() == ref.killed.tolist()
     assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
     assert np.array_equal(res.peel_round.cpu().numpy().view(np.uint32), ref.peel_round)
+
+
+def test_small_graph_replay_follows_buffer_contents(monkeypatch):
+    """The small-instance path replays a captured CUDA graph keyed by buffers and shape: new
+    contents in the same buffers must give the new results; PEEL_GRAPH=0 gives the same."""
+    n, m, r = 30011, 21000, 3
+    ws = torch.empty((pk.kcore_workspace_bytes(n, m, r, 2),), dtype=torch.uint8, device=DEV)
+    mask = torch.empty((n,), dtype=torch.uint8, device=DEV)
+    e = torch.empty((m, r), dtype=torch.int32, device=DEV)
+    for seed in (1, 2, 3):
+        e_np = O.gen_hypergraph(n, m, r, seed)
+        e.copy_(torch.from_numpy(e_np.view(np.int32)))
+        ref = O.sync_peel(e_np, n, 2)
+        for graph in ("1", "0"):
+            monkeypatch.setenv("PEEL_GRAPH", graph)
+            res = pk.peel_kcore(e, n, 2, core_mask=mask, ws=ws)
+            assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist()
+            assert res.killed.tolist() == ref.killed.tolist()
+            assert np.array_equal(mask.cpu().numpy(), ref.core_mask)

@@ -27,6 +27,34 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+L2_FLUSH_BELOW = 252 << 20  # 2x the B200 L2 (126 MB)
+
+
+def timed_loop(steps, stream, dev, footprint, body):
+    """Run body(i) for i < steps and return (device ms over the steps, l2 note).  A working set
+    below 2x L2 gets a 256 MB L2 flush before every step, outside the timed intervals (each step
+    is then timed alone with CUDA events on `stream`); a larger one is timed as one interval."""
+    import torch
+    flush = torch.empty((256 << 20,), dtype=torch.uint8, device=dev) if footprint < L2_FLUSH_BELOW else None
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps if flush is not None else 1)]
+    if flush is None:
+        evs[0][0].record(stream)
+    for i in range(steps):
+        if flush is not None:
+            flush.fill_(i & 0xff)
+            evs[i][0].record(stream)
+        body(i)
+        if flush is not None:
+            evs[i][1].record(stream)
+    if flush is None:
+        evs[0][1].record(stream)
+    torch.cuda.synchronize()
+    note = (f"working set {footprint / 1e6:.0f} MB < 2x L2: 256 MB L2 flush before each step, outside the timed intervals"
+            if flush is not None else f"working set {footprint / 1e9:.2f} GB > 2x L2; no flush needed")
+    return sum(a.elapsed_time(b) for a, b in evs), note
+
+
 CONFIGS = {
     # name: (kind, n_or_cells, m_or_keys, r, k, seed, BASELINE.json config text)
     "C1": ("kcore", 100_000, 70_000, 3, 2, 1, "k-core peel r=3 k=2 n=100,000 c=0.7"),
@@ -278,23 +306,23 @@ def run_iblt_dist(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, 
     clk = ClockSampler(local)
     barrier()
     clk.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     pk.profile_enable(True)
     per_kernel, launches = {}, 0
-    e0.record(stream)
-    for _ in range(args.steps):
+    res = None
+
+    def body(i):
+        nonlocal res, launches
         res = pk.iblt_dist_recover(comm, C, r, seed, keys, mem=mem)
         launches += pk.last_launches()
         for name, ms_, nl in pk.profile_read():
             a_ = per_kernel.setdefault(name, [0.0, 0])
             a_[0] += ms_
             a_[1] += nl
-    e1.record(stream)
+    ms_total, l2_note = timed_loop(args.steps, stream, dev, 16 * C // P + 8 * N, body)
     barrier()
     pk.profile_enable(False)
     clocks = clk.stop()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     tot = torch.tensor([float(res.nrecovered)], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -307,7 +335,8 @@ def run_iblt_dist(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, 
                 "data": "synthetic distinct 64-bit keys (SplitMix64 stream on device), replicated on every rank",
                 "config": {"workload": f"{args.config}: {text}", "cells": C, "keys": N, "r": r, "seed": seed,
                            "rounds": res.rounds, "complete": res.complete,
-                           "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"cell-partitioned{P}")},
+                           "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"cell-partitioned{P}"),
+                           "l2": l2_note},
                 "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
                 "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
         emit(line)
@@ -338,23 +367,22 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
     clk = ClockSampler(local)
     barrier()
     clk.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     per_kernel, launches = {}, 0
-    e0.record(stream)
-    for _ in range(args.steps):
+    res = None
+
+    def body(i):
+        nonlocal res, launches
         res, ins = step()
         launches += pk.last_launches()  # insert + peel launches
         for name, ms_, nl in ins + pk.profile_read():
             a = per_kernel.setdefault(name, [0.0, 0])
             a[0] += ms_
             a[1] += nl
-    e1.record(stream)
+    ms_total, l2_note = timed_loop(args.steps, stream, dev, 16 * C + 8 * N, body)
     barrier()
     clocks = clk.stop()
     round_ms = [round(x, 4) for x in pk.profile_rounds()]
     pk.profile_enable(False)
-    ms_total = e0.elapsed_time(e1)
     t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -427,7 +455,7 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
             "data": "synthetic distinct 64-bit keys (SplitMix64 stream on device)",
             "config": {"workload": f"C2: {text}", "cells": C, "keys": N, "r": r, "seed": seed,
                        "rounds": res.rounds, "complete": res.complete,
-                       "l2": "table 160 MB ~ L2; between steps the table is rebuilt (zeroed) and re-inserted"},
+                       "l2": l2_note + "; each step zeroes the table, re-inserts the keys and recovers them"},
             "paper_context": "Tesla C2070, 2^24 cells, r=3, load 0.75: recovery 0.33 s + insert 0.31 s (P:539)",
             "roofline": roof,
             "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 4)} for k, v in per_kernel.items()},
@@ -539,23 +567,22 @@ def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barri
     clk = ClockSampler(local)
     barrier()
     clk.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
     pk.profile_enable(True)
     per_kernel, launches = {}, 0
-    e0.record(stream)
-    for _ in range(args.steps):
+
+    def body(i):
+        nonlocal res, launches
         res = pk.peel_kcore_dist(comm, edges, n, k, ws=wsp, cap=4096)
         launches += pk.last_launches()
         for name, ms_, nl in pk.profile_read():
             a = per_kernel.setdefault(name, [0.0, 0])
             a[0] += ms_
             a[1] += nl
-    e1.record(stream)
+    ms_total, l2_note = timed_loop(args.steps, stream, dev, 4 * r * m + (8 * n + n // 8) // P, body)
     barrier()
     pk.profile_enable(False)
     clocks = clk.stop()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     cores = torch.tensor([float(n_core_local)], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -569,7 +596,8 @@ def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barri
                 "data": "synthetic G^r_{n,cn}, edge list replicated on every rank",
                 "config": {"workload": f"{args.config}: {text}", "n": n, "m": m, "r": r, "k": k, "seed": seed,
                            "rounds": res.rounds, "core_vertices": int(cores.item()), "peeled_edges": peeled,
-                           "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"vertex-partitioned{P}")},
+                           "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"vertex-partitioned{P}"),
+                           "l2": l2_note},
                 "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
                 "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
         emit(line)
@@ -678,24 +706,23 @@ def main():
     clk = ClockSampler(local)
     barrier()
     clk.start()
-    t_ev0 = torch.cuda.Event(enable_timing=True)
-    t_ev1 = torch.cuda.Event(enable_timing=True)
     per_kernel = {}
     launches = 0
-    t_ev0.record(stream)
-    for _ in range(args.steps):
+    res = None
+
+    def body(i):
+        nonlocal res, launches
         res = step()
         launches += pk.last_launches()
         for name, ms, nl in pk.profile_read():
             a = per_kernel.setdefault(name, [0.0, 0])
             a[0] += ms
             a[1] += nl
-    t_ev1.record(stream)
+    ms_total, l2_note = timed_loop(args.steps, stream, dev, 4 * r * m + 8 * n + n // 8, body)
     barrier()
     clocks = clk.stop()
     round_ms = [round(x, 3) for x in pk.profile_rounds()]
     pk.profile_enable(False)
-    ms_total = t_ev0.elapsed_time(t_ev1)
     ms_step = ms_total / args.steps
     t_max = torch.tensor([ms_total], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -818,7 +845,7 @@ def main():
             "config": {"workload": f"{args.config}: {text}", "n": n, "m": m, "r": r, "k": k, "seed": seed - rank,
                        "rounds": res.rounds, "core_vertices": n_core, "peeled_edges": peeled,
                        "parallelism": f"replicas{ws}" if ws > 1 else "single",
-                       "l2": "inputs (edges 4rm B, state 8n B) larger than L2; no flush needed"},
+                       "l2": l2_note},
             "rounds": res.rounds,
             "hbm_roofline_step": {"alg_bytes": step_alg, "frac_of_measured": round(step_alg / (ms_step / 1e3) / 1e9 / hbm, 4),
                                   "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},

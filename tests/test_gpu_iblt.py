@@ -230,3 +230,34 @@ def test_blocked_rejects_bad_shapes():
         pk.Iblt(1000, 3, 1, device=DEV, blog=8)            # 2^8 does not divide 1000
     with pytest.raises(pk.PeelError):
         pk.Iblt(1 << 12, 3, 1, device=DEV, blog=8, subtables=True)
+
+
+@pytest.mark.parametrize("mode", ["plain", "subtables", "blocked"])
+def test_large_table_beyond_2pow31_cells(mode):
+    """C = 9 * 2^28 (2.4e9 cells > 2^31, 38 GB of cells; iblt_mem_bytes ~ 125 GB): cell
+    indices above the signed 32-bit range.  The oracle cannot hold this table, but the hash
+    (cells_of*) is per key: every key's r predicted cells must carry exactly its multiplicity
+    of counts, the whole table must hold r*N counts (so nothing landed elsewhere), and the
+    recovery of N << C keys is complete and returns exactly the inserted set (a unique result)."""
+    C, r, N, seed = 9 << 28, 3, 100_000, 77
+    keys = synth.random_keys(N, seed=5)
+    blog = 16 if mode == "blocked" else 0
+    t = pk.Iblt(C, r, seed, device=DEV, subtables=(mode == "subtables"), blog=blog)
+    t.insert(keys_dev(keys))
+    if mode == "plain":
+        pred = np.stack([O.cells_of(int(x), C, r, seed) for x in keys])
+    elif mode == "subtables":
+        pred = np.stack([O.cells_of_subtable(int(x), C, r, seed) for x in keys])
+    else:
+        pred = np.stack([O.cells_of_blocked(int(x), C, r, seed, blog) for x in keys])
+    assert pred.max() >= (1 << 31)  # the test really reaches the upper half
+    cells, mult = np.unique(pred.ravel(), return_counts=True)
+    cnt = t.cells()[:, 0]
+    got = cnt[torch.from_numpy(cells.astype(np.int64)).to(DEV)].cpu().numpy()
+    assert np.array_equal(got, mult.astype(np.int32))
+    assert int(cnt.sum(dtype=torch.int64).item()) == r * N
+    res = t.peel(cap_keys=N + 1)
+    assert res.complete and res.nrecovered == N
+    assert np.array_equal(np.sort(res.keys.cpu().numpy().view(np.uint64)), np.sort(keys))
+    del t, cnt
+    torch.cuda.empty_cache()

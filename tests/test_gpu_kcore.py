@@ -327,3 +327,34 @@ def test_small_graph_replay_follows_buffer_contents(monkeypatch):
             assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist()
             assert res.killed.tolist() == ref.killed.tolist()
             assert np.array_equal(mask.cpu().numpy(), ref.core_mask)
+
+
+@pytest.mark.parametrize("k,flags,c", [(2, 0, 0.7), (2, 0, 0.9), (2, "csr", 0.9), (3, 0, 1.6)])
+def test_maximum_vertex_range(k, flags, c):
+    """n = 2^32 (the largest vertex range peel.h allows): a compact random hypergraph on n0
+    vertices, relabelled injectively into [0, 2^32) so that ids 0, 2^32-1 and ids either side
+    of 2^22-vertex bin boundaries occur.  Peeling is label-invariant, so the oracle runs on
+    the compact graph; the 2^32 - n0 isolated vertices all leave in round 1 on the GPU, so
+    rounds, survivors[t] and killed[t] must agree exactly, and the core mask must be the
+    oracle's at the mapped ids and empty elsewhere."""
+    flags = pk.PEEL_FLAG_CSR if flags == "csr" else 0
+    n0, r, N = 100_000, 3, 1 << 32
+    rng = np.random.default_rng(7 + k)
+    fixed = np.array([0, N - 1, N - 2, 1 << 22, (1 << 22) - 1, (1 << 31), (1 << 31) - 1, N - (1 << 22)],
+                     dtype=np.uint64)
+    rest = np.setdiff1d(np.unique(rng.integers(0, N, size=2 * n0, dtype=np.uint64)), fixed)
+    ids = rng.permutation(np.concatenate([fixed, rng.permutation(rest)[: n0 - fixed.size]]))
+    assert np.unique(ids).size == n0
+    e0 = O.gen_hypergraph(n0, int(c * n0), r, 40 + k)
+    ref = O.sync_peel(e0, n0, k)
+    mask = torch.empty((N,), dtype=torch.uint8, device=DEV)
+    res = pk.peel_kcore(to_dev(ids[e0.astype(np.int64)].astype(np.uint32)), N, k, flags=flags, core_mask=mask)
+    assert res.rounds == ref.rounds
+    assert res.survivors.tolist() == ref.survivors.tolist()
+    assert res.killed.tolist() == ref.killed.tolist()
+    got = mask[torch.from_numpy(ids.astype(np.int64)).to(DEV)].cpu().numpy()
+    assert np.array_equal(got, ref.core_mask)
+    assert int(mask.sum(dtype=torch.int64).item()) == int(ref.core_mask.sum())
+    del mask, res
+    pk._ws_cache.clear()
+    torch.cuda.empty_cache()

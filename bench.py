@@ -137,6 +137,12 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# bench.py's per-call profiling names -> the kernel (tools/ncu_traffic.py short name) doing the work
+NCU_KERNEL = {"peel_rounds_packed": ("peel_packed",), "peel_rounds_csr": ("peel_csr",), "iblt_peel_rounds": ("iblt_peel",),
+              "peel_small_graph": ("build_packed", "peel_cluster"), "peel_rounds_cluster": ("peel_cluster",),
+              "iblt_insert": ("iblt_update",), "frontier_edge_sort": ("esort_hist", "esort_scatter")}
+
+
 def ncu_traffic(config, kernel):
     """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture of
     this config (profiles/r01_traffic_<config>.json, tools/ncu_traffic.py), else None."""
@@ -144,11 +150,12 @@ def ncu_traffic(config, kernel):
         d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))
     except Exception:
         return None, None
-    kname = kernel.replace("peel_rounds_packed", "peel_packed")
-    k = d.get("kernels", {}).get(kname)
-    if not k:
+    ks = [d.get("kernels", {}).get(x) for x in NCU_KERNEL.get(kernel, (kernel,))]
+    if not ks or not all(ks):
         return None, None
-    return int(k["traffic_per_launch"]), f"profiles/r01_traffic_{config}.json (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
+    per_step = sum(k["dram_read_bytes_per_step"] + k["dram_write_bytes_per_step"] for k in ks)
+    return int(per_step / ks[-1]["launches_per_step"]), \
+        f"profiles/r01_traffic_{config}.json (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
 
 
 def dram_step(config, per_kernel, steps, ms_step, hbm):
@@ -158,11 +165,9 @@ def dram_step(config, per_kernel, steps, ms_step, hbm):
         d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))["kernels"]
     except Exception:
         return None
-    alias = {"peel_rounds_packed": "peel_packed", "frontier_edge_sort": ("esort_hist", "esort_scatter")}
     tot, missing = 0.0, []
     for name in per_kernel:
-        keys = alias.get(name, name)
-        keys = keys if isinstance(keys, tuple) else (keys,)
+        keys = NCU_KERNEL.get(name, (name,))
         found = [d[k] for k in keys if k in d]
         if not found:
             missing.append(name)
@@ -398,9 +403,13 @@ def run_iblt(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, strea
     name, (ms_sum, nl) = max(per_kernel.items(), key=lambda kv: kv[1][0])
     alg = b_peel if "peel" in name else b_ins
     ach = alg / (ms_sum / nl / 1e3) / 1e9
+    traffic, tsrc = ncu_traffic(args.config, name)
     roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(ach / hbm, 4), "traffic": None, "alg_bytes_per_launch": alg,
-            "avg_launch_ms": round(ms_sum / nl, 4),
+            "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc,
+            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else
+            "fallback (B200_PROFILING.md 6.65 TB/s)",
+            "dram_frac_of_peak": (round(traffic / (ms_sum / nl / 1e3) / 1e9 / hbm, 4) if traffic else None),
+            "alg_bytes_per_launch": alg, "avg_launch_ms": round(ms_sum / nl, 4),
             "note": "160 MB table ~ L2-sized: L2-atomic/latency bound, HBM roofline is a loose bound"}
     # e2e through the public API: pinned host keys -> device, insert, recover, recovered keys -> host
     e2e = None
@@ -767,13 +776,16 @@ def main():
         name, (ms_sum, nl) = dom
         avg_ms = ms_sum / max(nl, 1)
         alg = kb.get(name)  # bytes per STEP of this kernel (all its launches)
-        if alg is None:  # CSR path: whole-step formula over the whole-step time of its kernels
+        if alg is None:  # CSR path / graph replay: whole-step formula over the whole-step time of its kernels
             alg = b_build + b_rounds
             avg_ms = sum(v[0] for v in per_kernel.values()) / args.steps
+            ds = dram_step(args.config, per_kernel, args.steps, avg_ms, hbm)
+            traffic, tsrc = ((ds["bytes"], ds["source"] + ", whole step") if ds and not ds["kernels_without_traffic"]
+                             else (None, None))
         else:
             alg = alg / max(nl / args.steps, 1.0)  # per launch, like avg_ms
+            traffic, tsrc = ncu_traffic(args.config, name)
         ach = alg / (avg_ms / 1e3) / 1e9
-        traffic, tsrc = ncu_traffic(args.config, name)
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
                 # the same kernel's real DRAM bytes (ncu) over its time here: random 8-12 B accesses move

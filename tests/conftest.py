@@ -12,7 +12,7 @@ TESTS = os.path.dirname(os.path.abspath(__file__))
 if TESTS not in sys.path:
     sys.path.insert(0, TESTS)
 
-from peeltest_util import load_goldens  # noqa: E402
+from peeltest_util import load_goldens, load_oracle_goldens  # noqa: E402
 
 
 def pytest_configure(config):
@@ -24,4 +24,11 @@ def pytest_configure(config):
 
 @pytest.fixture(scope="session")
 def goldens():
+    """SURVEY §8 c3's independent goldens: used by the oracle pins (-m "not gpu")."""
     return load_goldens()
+
+
+@pytest.fixture(scope="session")
+def oracle_goldens():
+    """tools/make_oracle_goldens.py's oracle-computed values: the GPU tests' expected values."""
+    return load_oracle_goldens()

@@ -18,5 +18,13 @@ def load_table(name):
 
 
 def load_goldens():
+    """The independent implementation's goldens quoted by SURVEY.md §8 c3 (pins for the oracle)."""
     with open(os.path.join(GOLDEN, "survey_c3_goldens.json")) as f:
+        return json.load(f)
+
+
+def load_oracle_goldens():
+    """Full-size results written by tools/make_oracle_goldens.py from oracle/ alone (the
+    expected values of the GPU tests; checked against load_goldens() on CPU)."""
+    with open(os.path.join(GOLDEN, "oracle_goldens.json")) as f:
         return json.load(f)

@@ -108,9 +108,9 @@ def test_key_cap_truncation():
     assert ei.value.status == pk.PEEL_ETRUNC
 
 
-def test_c2_full_config(goldens):
+def test_c2_full_config(oracle_goldens):
     """BASELINE.json configs[1]: 10^7 cells, 7.5e6 keys, r=3, seed=2."""
-    g = goldens["C2"]
+    g = oracle_goldens["C2"]
     keys = pk.gen_keys(g["nkeys"], g["seed"], device=DEV)
     t = pk.Iblt(g["cells"], g["r"], g["seed"], device=DEV)
     t.insert(keys)

@@ -45,15 +45,15 @@ def test_generator_matches_oracle(n, m, r, seed):
     assert np.array_equal(got, O.gen_hypergraph(n, m, r, seed))
 
 
-def test_generator_c1_digest(goldens):
-    g = goldens["C1"]
+def test_generator_c1_digest(oracle_goldens):
+    g = oracle_goldens["C1"]
     got = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV).cpu().numpy().view(np.uint32)
     assert hashlib.sha256(got.tobytes()).hexdigest() == g["sha256"]
 
 
-def test_generator_sampled_at_full_scale(goldens):
+def test_generator_sampled_at_full_scale(oracle_goldens):
     # C5 (n=10^9, m=7.5e8): the oracle computes any edge on its own; compare 2000 sampled edges
-    g = goldens["C5"]
+    g = oracle_goldens["C5"]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
     rng = np.random.default_rng(0)
     idx = np.concatenate([[0, 1, g["m"] - 1], rng.integers(0, g["m"], 2000)])
@@ -148,8 +148,8 @@ def test_binned_build_overflow_fallback():
     check_vs_oracle(e_np, n, 2, twice=False)
 
 
-def test_c1_golden_and_oracle(goldens):
-    g = goldens["C1"]
+def test_c1_golden_and_oracle(oracle_goldens):
+    g = oracle_goldens["C1"]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
     res = pk.peel_kcore(e, g["n"], g["k"])
     assert res.rounds == g["rounds"] and res.survivors.tolist() == g["survivors"]
@@ -158,8 +158,8 @@ def test_c1_golden_and_oracle(goldens):
 
 
 @pytest.mark.parametrize("name", ["C4a_small", "C4b_small"])
-def test_reduced_c4_vs_oracle(goldens, name):
-    g = goldens[name]
+def test_reduced_c4_vs_oracle(oracle_goldens, name):
+    g = oracle_goldens[name]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
     e_np = e.cpu().numpy().view(np.uint32)
     assert hashlib.sha256(e_np.tobytes()).hexdigest() == g["sha256"]
@@ -228,8 +228,8 @@ def schedule_certificate_torch(edges: torch.Tensor, n: int, k: int, peel_round: 
 
 
 @pytest.mark.parametrize("name", ["C3", "C4a", "C4b"])
-def test_full_scale_1e8_goldens_and_certificate(goldens, name):
-    g = goldens[name]
+def test_full_scale_1e8_goldens_and_certificate(oracle_goldens, name):
+    g = oracle_goldens[name]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
     assert e[0].cpu().numpy().view(np.uint32).tolist() == g["edges_head"][0]
     res = pk.peel_kcore(e, g["n"], g["k"], want_peel_round=True)
@@ -256,9 +256,9 @@ def test_full_scale_1e8_goldens_and_certificate(goldens, name):
     torch.cuda.empty_cache()
 
 
-def test_full_scale_c5_north_star(goldens):
+def test_full_scale_c5_north_star(oracle_goldens):
     """n = 10^9, m = 7.5e8, r=3, k=2 (the bench workload): goldens + certificate pieces."""
-    g = goldens["C5"]
+    g = oracle_goldens["C5"]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)
     res = pk.peel_kcore(e, g["n"], g["k"])
     assert res.rounds == g["rounds"]

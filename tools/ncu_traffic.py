@@ -27,10 +27,13 @@ def main():
     rows = [r for r in csv.reader(open(a.csv)) if len(r) > 10]
     h = rows[0]
     iid, iname, imet, ival = h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    iunit = h.index("Metric Unit")
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
     per = collections.OrderedDict()
     for r in rows[1:]:
         d = per.setdefault(int(r[iid]), {"kernel": short(r[iname])})
-        d[r[imet]] = float(r[ival].replace(",", ""))
+        d[r[imet]] = float(r[ival].replace(",", "")) * scale[r[iunit]]  # bytes; durations in ms
     by = collections.defaultdict(list)
     for d in per.values():
         by[d["kernel"]].append(d)
@@ -41,9 +44,8 @@ def main():
         rd = sum(x.get("dram__bytes_read.sum", 0) for x in last)
         wr = sum(x.get("dram__bytes_write.sum", 0) for x in last)
         ms = sum(x.get("gpu__time_duration.sum", 0) for x in last)
-        unit_ms = 1e-6 if ms > 1e4 else 1.0  # ns or ms depending on the ncu version
         out[k] = {"launches_per_step": n, "dram_read_bytes_per_step": rd, "dram_write_bytes_per_step": wr,
-                  "traffic_per_launch": (rd + wr) / n, "ncu_ms_per_step": ms * unit_ms}
+                  "traffic_per_launch": (rd + wr) / n, "ncu_ms_per_step": ms}
     print(json.dumps({"source": a.csv, "method": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                       "gpu__time_duration.sum --clock-control none (single pass, no replay)", "kernels": out},
                      indent=1))

@@ -22,7 +22,11 @@ def test_oracle_goldens_match_independent(name):
     s, o = SURVEY[name], ORACLE[name]
     checked = 0
     for key, val in s.items():
-        if key in o:
+        if key == "edges_head":  # leading edges; the two files keep different numbers of rows
+            L = min(len(val), len(o[key]))
+            assert L >= 1 and o[key][:L] == val[:L], (name, key)
+            checked += 1
+        elif key in o:
             assert o[key] == val, (name, key)
             checked += 1
         elif key.endswith("_head"):

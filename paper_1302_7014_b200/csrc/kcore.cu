@@ -534,20 +534,37 @@ __device__ __forceinline__ uint32_t idsum_of(ull w) { return (uint32_t)(w >> 32)
 
 template <bool CSR>
 __device__ void write_core_mask(const PeelArgs &a, uint64_t tid, uint64_t nthr) {
-    // core_mask[v] = count(v) >= k (counts only decrease); 16 vertices -> one 16-byte store
+    // core_mask[v] = count(v) >= k (counts only decrease).  Warp-coalesced: each thread turns
+    // one 16-byte load (2 packed states / 4 CSR degrees) into one 2- / 4-byte mask store, so a
+    // warp instruction moves 512 B of state and 64 / 128 B of mask; UM loads are issued before
+    // any store so enough bytes are in flight to stream at HBM rate.
+    constexpr int UM = 4;
+    constexpr uint64_t VPL = CSR ? 4 : 2;  // vertices per 16-byte load
     const uint32_t k = a.k;
-    const uint64_t n16 = a.mask_vec ? a.n / 16 : 0;
-    for (uint64_t w = tid; w < n16; w += nthr) {
-        uint32_t bytes[4] = {0, 0, 0, 0};
+    const uint4 *src = CSR ? reinterpret_cast<const uint4 *>(a.deg) : reinterpret_cast<const uint4 *>(a.state);
+    const uint64_t nv = (a.mask_vec && ((uintptr_t)src & 15) == 0) ? a.n / VPL : 0;  // whole 16-byte groups
+    for (uint64_t w0 = tid; w0 < nv; w0 += UM * nthr) {
+        uint4 x[UM];
         #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            const uint64_t v = w * 16 + i;
-            uint32_t c = CSR ? ld_cg_u32(a.deg + v) : count_of(ld_cg_u64(a.state + v));
-            bytes[i >> 2] |= (uint32_t)(c >= k) << (8 * (i & 3));
+        for (int j = 0; j < UM; j++) {
+            const uint64_t w = w0 + j * nthr;
+            x[j] = w < nv ? __ldcs(src + w) : make_uint4(0u, 0u, 0u, 0u);
         }
-        reinterpret_cast<uint4 *>(a.core_mask)[w] = make_uint4(bytes[0], bytes[1], bytes[2], bytes[3]);
+        #pragma unroll
+        for (int j = 0; j < UM; j++) {
+            const uint64_t w = w0 + j * nthr;
+            if (w >= nv) break;
+            if (CSR) {
+                const uint32_t b = (uint32_t)(x[j].x >= k) | (uint32_t)(x[j].y >= k) << 8 |
+                                   (uint32_t)(x[j].z >= k) << 16 | (uint32_t)(x[j].w >= k) << 24;
+                reinterpret_cast<uint32_t *>(a.core_mask)[w] = b;
+            } else {  // packed state: the count is the low 32-bit word of each u64
+                const uint16_t b = (uint16_t)((x[j].x >= k) | (x[j].z >= k) << 8);
+                reinterpret_cast<uint16_t *>(a.core_mask)[w] = b;
+            }
+        }
     }
-    for (uint64_t v = n16 * 16 + tid; v < a.n; v += nthr) {
+    for (uint64_t v = nv * VPL + tid; v < a.n; v += nthr) {
         uint32_t c = CSR ? ld_cg_u32(a.deg + v) : count_of(ld_cg_u64(a.state + v));
         a.core_mask[v] = c >= k ? 1 : 0;
     }

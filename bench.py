@@ -333,6 +333,52 @@ def run_iblt_dist(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot)
     value = tot.item() * args.steps / (t.item() / 1e3)
+    # roofline: the whole step per rank against this rank's 1/P share of SURVEY §8 d0's bytes
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = peaks.get("hbm_gbs") or 6650.0
+    b_ins, b_peel = iblt_bytes(C, N, r, N)
+    alg = (b_ins + b_peel) / (1 if args.virtual_shards else P)
+    k_ms = sum(v[0] for v in per_kernel.values()) / args.steps
+    roof = None
+    if k_ms > 0:
+        roof = {"bound": "hbm", "kernel": "whole step per rank (all shard kernels)",
+                "achieved": round(alg / (k_ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(alg / (k_ms / 1e3) / 1e9 / hbm, 4), "traffic": None,
+                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else
+                "fallback (B200_PROFILING.md 6.65 TB/s)", "alg_bytes_per_launch": int(alg),
+                "avg_launch_ms": round(k_ms, 4)}
+    # e2e through the public call: pinned host keys -> every rank, each rank's recovered keys -> host
+    e2e = None
+    if not args.no_e2e:
+        k_host = torch.empty((N,), dtype=torch.int64, pin_memory=True)
+        k_host.copy_(keys)
+        o_host = torch.empty((N,), dtype=torch.int64, pin_memory=True)
+
+        def e2e_step():
+            keys.copy_(k_host, non_blocking=True)
+            rr = pk.iblt_dist_recover(comm, C, r, seed, keys, mem=mem)
+            o_host[:rr.keys.numel()].copy_(rr.keys, non_blocking=True)
+            return rr
+        e2e_step()
+        barrier()
+        h0 = torch.cuda.Event(enable_timing=True)
+        h1 = torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(args.e2e_steps):
+            rr = e2e_step()
+        h1.record(stream)
+        barrier()
+        te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        assert rr.complete
+        e2e = {"value": tot.item() * args.e2e_steps / (te.item() / 1e3), "unit": "keys/s",
+               "h2d_bytes_per_step": 8 * N * ws, "d2h_bytes_per_step": 8 * N, "steps": args.e2e_steps,
+               "api": "iblt_dist_recover (C-ABI); pinned host keys -> every rank, recovered keys -> host"}
     if rank == 0:
         line = {"metric": IBLT_METRIC, "value": value, "unit": "keys/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": round(t.item() / args.steps, 4),
@@ -343,7 +389,7 @@ def run_iblt_dist(args, pk, dev, ws, rank, local, C, N, r, seed, text, barrier, 
                            "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"cell-partitioned{P}"),
                            "l2": l2_note},
                 "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
-                "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
+                "gpu_launches": launches, "clocks": clocks, "roofline": roof, "cpu_baseline": None, "e2e": e2e}
         emit(line)
     del comm
     if dist.is_initialized():
@@ -598,6 +644,61 @@ def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barri
         dist.all_reduce(cores)
     peeled = int(sum(res.killed))
     value = peeled * args.steps / (t.item() / 1e3)
+    # roofline: the whole step per rank (the shard kernels have no per-kernel byte formula): this
+    # rank's 1/P share of the instance's algorithmic bytes over its kernel time
+    roof = None
+    n_core_all = int(cores.item())
+    if per_kernel and n_core_all == 0:  # m_core = 0 for an empty core; otherwise it needs every slice
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except Exception:
+            pass
+        hbm = peaks.get("hbm_gbs") or 6650.0
+        bb, br = algorithmic_bytes(r, n, m, 0, 0, k)
+        alg = (bb + br) / (1 if args.virtual_shards else P)  # virtual shards: all P shards on this GPU
+        k_ms = sum(v[0] for v in per_kernel.values()) / args.steps
+        ach = alg / (k_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": "whole step per rank (all shard kernels)", "achieved": round(ach, 1),
+                "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4), "traffic": None,
+                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)" if peaks.get("hbm_gbs") else
+                "fallback (B200_PROFILING.md 6.65 TB/s)",
+                "alg_bytes_per_launch": int(alg), "avg_launch_ms": round(k_ms, 4)}
+    # e2e through the public call: every rank copies the (replicated) edge list from pinned host
+    # memory into its device buffer, peels, and reads its core-mask slice back, per step
+    e2e = None
+    if not args.no_e2e:
+        try:
+            e_host = torch.empty((m, r), dtype=torch.int32, pin_memory=True)
+            e_host.copy_(edges)
+            m_host = torch.empty((res.core_mask.numel(),), dtype=torch.uint8, pin_memory=True)
+
+            def e2e_step():
+                edges.copy_(e_host, non_blocking=True)
+                rr = pk.peel_kcore_dist(comm, edges, n, k, ws=wsp, cap=4096)
+                m_host.copy_(rr.core_mask, non_blocking=True)
+                return rr
+            e2e_step()
+            barrier()
+            h0 = torch.cuda.Event(enable_timing=True)
+            h1 = torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            for _ in range(args.e2e_steps):
+                rr = e2e_step()
+            h1.record(stream)
+            barrier()
+            te = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
+            if ws > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            assert int(sum(rr.killed)) == peeled
+            e2e = {"value": peeled * args.e2e_steps / (te.item() / 1e3), "unit": "edges/s",
+                   "h2d_bytes_per_step": 4 * r * m * ws, "d2h_bytes_per_step": n,
+                   "steps": args.e2e_steps,
+                   "api": "peel_kcore_dist (C-ABI); pinned host edges -> every rank, core-mask slices -> host"}
+            del e_host, m_host
+        except Exception as ex:  # pragma: no cover
+            e2e = {"value": None, "unit": "edges/s", "error": repr(ex)[:200],
+                   "h2d_bytes_per_step": 4 * r * m * ws, "d2h_bytes_per_step": n}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": round(t.item() / args.steps, 4),
@@ -608,7 +709,7 @@ def run_dist_bench(args, pk, dev, ws, rank, local, n, m, r, k, seed, text, barri
                            "parallelism": (f"virtual{P} (1 GPU)" if args.virtual_shards else f"vertex-partitioned{P}"),
                            "l2": l2_note},
                 "kernels": {nm: {"ms_per_step": round(v[0] / args.steps, 4)} for nm, v in per_kernel.items()},
-                "gpu_launches": launches, "clocks": clocks, "roofline": None, "cpu_baseline": None, "e2e": None}
+                "gpu_launches": launches, "clocks": clocks, "roofline": roof, "cpu_baseline": None, "e2e": e2e}
         emit(line)
     del comm
     if dist.is_initialized():

@@ -1444,7 +1444,10 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_subround_kernel(PeelArgs a) {
 // other endpoints.  The adjacency list (the static one: dead edges included) is walked in
 // chunks of CV entries whose loads, alive tests, kills, row gathers and decrements are each
 // issued together, so a chunk costs ~5 dependent memory trips instead of ~2 per entry.
-static constexpr int CV = 8;
+#ifndef PEEL_CV
+#define PEEL_CV 4  // C4b rounds: 2/3/4/6/8/16 -> 7.54/7.41/7.36/7.64/7.68/8.94 ms
+#endif
+static constexpr int CV = PEEL_CV;
 template <int R>
 __device__ __forceinline__ ull csr_visit(const PeelArgs &a, uint32_t v, uint32_t k, uint32_t t,
                                          BlockQueue<uint32_t> &q, int slot, uint32_t *Fn, ull *cn) {
@@ -1527,16 +1530,12 @@ __global__ void __launch_bounds__(PEEL_BLOCK) peel_csr_kernel(PeelArgs a) {
         uint32_t *Fn = (uint32_t *)a.F[t & 1];
         ull *cn = &ctl->ne[t % 3];
         ull kills = 0;
-        // one frontier vertex per thread; a small round (nF <= grid threads) spreads its
-        // vertices over the whole grid, so no thread walks more than one adjacency list
-        const uint64_t per = nF <= nthr ? 1 : U;
-        const uint64_t span = per * PEEL_BLOCK;
-        for (uint64_t base = (uint64_t)blockIdx.x * span; base < nF; base += (uint64_t)gridDim.x * span) {
-            #pragma unroll 1
-            for (uint64_t j = 0; j < per; j++) {
-                const uint64_t i = base + j * PEEL_BLOCK + threadIdx.x;
-                if (i < nF) kills += csr_visit<R>(a, ld_cg_u32(Fc + i), k, t, q, slot, Fn, cn);
-            }
+        // one frontier vertex per thread per iteration, grid-stride (C4b rounds: 1/2/4/8 vertices
+        // per thread per iteration -> 7.27/7.28/7.37/7.72 ms): no thread walks two adjacency
+        // lists in a round that the grid could spread
+        for (uint64_t base = (uint64_t)blockIdx.x * PEEL_BLOCK; base < nF; base += (uint64_t)gridDim.x * PEEL_BLOCK) {
+            const uint64_t i = base + threadIdx.x;
+            if (i < nF) kills += csr_visit<R>(a, ld_cg_u32(Fc + i), k, t, q, slot, Fn, cn);
             bq_flush(q, slot, Fn, cn);
             slot ^= 1;
         }

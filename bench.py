@@ -144,8 +144,15 @@ NCU_KERNEL = {"peel_rounds_packed": ("peel_packed",), "peel_rounds_csr": ("peel_
 
 
 def ncu_traffic(config, kernel):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu capture of
-    this config (profiles/r01_traffic_<config>.json, tools/ncu_traffic.py), else None."""
+    """DRAM bytes (read + write) per launch of `kernel`: from the committed `ncu --set full`
+    capture of this config's kernel (profiles/r01_ncu_full_<kernel>_<config>.json) when there
+    is one, else from the committed launch list (profiles/r01_traffic_<config>.json,
+    tools/ncu_traffic.py), else None."""
+    full = os.path.join(ROOT, "profiles", f"r01_ncu_full_{kernel}_{config}.json")
+    if os.path.exists(full):
+        d = json.load(open(full))
+        return int(d["dram_gb_per_launch"] * 1e9), \
+            f"profiles/r01_ncu_full_{kernel}_{config}.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))
     except Exception:

@@ -95,6 +95,27 @@ static DLayout dlayout(uint64_t n, uint64_t m, uint32_t r, int P, uint64_t nloc)
 typedef BlockQueueT<uint2, DQ, DB> DEntQ;
 typedef BlockQueueT<uint32_t, DQ, DB> DIdQ;
 
+// flush the P per-destination send queues with two block barriers in all (bq_flush per
+// queue would take two each): thread 0 reserves every non-empty queue's output range, then
+// the block copies them out.  Every thread of the block must call it.
+__device__ __forceinline__ void flush_sends(DIdQ *qs, int slot, uint32_t P, uint32_t *send, uint64_t nloc,
+                                            ull *nsend) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (uint32_t d = 0; d < P; d++) {
+            const uint32_t c = min(qs[d].n[slot], (uint32_t)DQ);
+            qs[d].cnt = c;
+            qs[d].base = c ? atomicAdd(nsend + d, (ull)c) : 0ull;
+            qs[d].n[slot] = 0;
+        }
+    __syncthreads();
+    for (uint32_t d = 0; d < P; d++) {
+        const uint32_t c = qs[d].cnt;
+        const ull b = qs[d].base;
+        for (uint32_t i = threadIdx.x; i < c; i += DB) send[(uint64_t)d * nloc + b + i] = qs[d].buf[slot][i];
+    }
+}
+
 template <int R>
 __device__ __forceinline__ bool dload_edge(const uint32_t *__restrict__ edges, uint64_t e, uint64_t n,
                                            uint32_t (&u)[R]) {
@@ -218,7 +239,7 @@ __global__ void __launch_bounds__(DB) dist_kill_kernel(DKArgs a) {
             }
         }
         bq_flush(q, slot, a.Fn, cn);
-        for (int d = 0; d < a.P; d++) bq_flush(qs[d], slot, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
+        flush_sends(qs, slot, a.P, a.send, a.nloc, a.ctl->nsend);
         slot ^= 1;
     }
     block_add<DB>(&a.ctl->nf[a.par], crossed);
@@ -380,7 +401,7 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             bv.entries[bv.base[b] + gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ lmask);
         }
         if (!RECV)
-            for (int d = 0; d < a.P; d++) bq_flush(qs[d], slot, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
+            flush_sends(qs, slot, a.P, a.send, a.nloc, a.ctl->nsend);
         slot ^= 1;
         __syncthreads();
     }

@@ -300,7 +300,11 @@ peel_status iblt_peel_signed(peel_iblt *t, uint64_t *out_keys, int8_t *out_sign,
                              uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
                              int *complete, void *stream);
 
-/* Device pointer to the 16-byte cell array (for tests and serialisation). */
+/* Device pointer to the 16-byte cell array (for tests and serialisation).  The pointer
+ * is writable, so the call marks the table as no longer insert-only: later iblt_peel
+ * calls take the general path (three atomics per cell of a recovered key) instead of
+ * clearing round-start-pure cells with a plain store.  iblt_delete and iblt_subtract
+ * (on a) do the same. */
 void *iblt_cells(const peel_iblt *t);
 
 /* edges[i][j] (dev u32 [nkeys][r]) = j-th cell of keys[i]: the IBLT's

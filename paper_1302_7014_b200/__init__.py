@@ -395,7 +395,9 @@ class Iblt:
         _check(_L().iblt_delete(self._h, _ptr(keys), keys.numel(), _stream(stream)), "iblt_delete")
 
     def cells(self) -> torch.Tensor:
-        """[C, 4] int32 view (count, hashSum, keySum_lo, keySum_hi) of the device cells."""
+        """[C, 4] int32 view (count, hashSum, keySum_lo, keySum_hi) of the device cells.
+        Read-only by contract: iblt_peel's insert-only fast path assumes the cells hold
+        exactly what iblt_insert wrote (use delete() / subtract() to change them)."""
         return self.mem[: 16 * self.C].view(torch.int32).view(self.C, 4)
 
     def peel(self, cap_keys: int | None = None, cap: int = 65536, out: torch.Tensor | None = None,

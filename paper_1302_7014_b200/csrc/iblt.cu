@@ -117,6 +117,7 @@ struct IPeelArgs {
     ull cap_keys;
     bool subt;          // subtable hashing
     uint32_t blog;      // blocked hashing: log2 block size, 0 = off
+    bool insert_only;   // every count is the true number of keys in its cell (no delete/subtract)
 };
 
 
@@ -208,11 +209,19 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                     bq_push(qk, slot, make_ulonglong2(x, neg ? 1ull : 0ull), (ulonglong2 *)nullptr, &ctl->nrec);
                     const uint32_t hx = checksum(x, a.seed_c);
                     const uint32_t delta = neg ? 1u : 0xFFFFFFFFu;  // remove: count -= sign
-                    // the r count atomics are issued before any result is used
+                    // the r count atomics are issued before any result is used.  In an
+                    // insert-only table a round-start-pure cell holds x alone, and no other
+                    // key recovered this round can be in it: x's deletion leaves it zero,
+                    // a plain 16-byte store instead of three atomics.
                     uint32_t now[R];
                     #pragma unroll
                     for (int j = 0; j < R; j++) {
                         Cell *p = a.cells + h[j];
+                        if (!SIGNED && a.insert_only && (pw[j] >> (h[j] & 31) & 1u)) {
+                            __stcg(reinterpret_cast<uint4 *>(p), make_uint4(0u, 0u, 0u, 0u));
+                            now[j] = 0u;
+                            continue;
+                        }
                         now[j] = atomicAdd(&p->count, delta) + delta;
                         atomicXor(&p->keySum, x);
                         atomicXor(&p->hashSum, hx);
@@ -404,6 +413,7 @@ struct peel_iblt {
     uint32_t r;
     bool subt;  // IBLT_FLAG_SUBTABLES
     uint32_t blog;  // IBLT_FLAG_BLOCKED: log2 cells per block (0: plain hashing)
+    mutable bool insert_only;  // no delete, no subtract, no raw cell access since the build
     ull seed, seed_h, seed_c;
     char *mem;
     ILayout L;
@@ -441,6 +451,7 @@ extern "C" peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, 
     t->r = r;
     t->subt = (flags & IBLT_FLAG_SUBTABLES) != 0;
     t->blog = blog;
+    t->insert_only = true;
     t->seed = seed;
     const ull G = 0x9E3779B97F4A7C15ull;
     t->seed_h = host_mix64((seed ^ 0x6A09E667F3BCC909ull) + G);
@@ -461,6 +472,7 @@ static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkey
     if (!t) return PEEL_EINVAL;
     if (nkeys == 0) return PEEL_OK;
     if (!keys) return PEEL_EINVAL;
+    if (delta != 1u) t->insert_only = false;
     cudaStream_t s = (cudaStream_t)stream;
     prof_begin_call();
     Cell *cells = (Cell *)(t->mem + t->L.cells);
@@ -544,6 +556,7 @@ static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_
     a.cap_keys = cap_keys;
     a.subt = t->subt;
     a.blog = t->blog;
+    a.insert_only = t->insert_only;
     peel_status st = PEEL_EINVAL;
     switch (t->r) {
         case 2: st = run_iblt_peel<2>(t, a, sgn, s); break;
@@ -609,6 +622,7 @@ __global__ void __launch_bounds__(256) iblt_subtract_kernel(Cell *a, const Cell 
 extern "C" peel_status iblt_subtract(peel_iblt *a, const peel_iblt *b, void *stream) {
     if (!a || !b || a->C != b->C || a->r != b->r || a->seed != b->seed || a->subt != b->subt || a->blog != b->blog)
         return PEEL_EINVAL;
+    a->insert_only = false;
     cudaStream_t s = (cudaStream_t)stream;
     prof_begin_call();
     {
@@ -620,7 +634,12 @@ extern "C" peel_status iblt_subtract(peel_iblt *a, const peel_iblt *b, void *str
     return PEEL_OK;
 }
 
-extern "C" void *iblt_cells(const peel_iblt *t) { return t ? (void *)(t->mem + t->L.cells) : nullptr; }
+// raw (writable) access: the table may no longer be insert-only
+extern "C" void *iblt_cells(const peel_iblt *t) {
+    if (!t) return nullptr;
+    t->insert_only = false;
+    return (void *)(t->mem + t->L.cells);
+}
 
 extern "C" peel_status iblt_to_hypergraph(const peel_iblt *t, const uint64_t *keys, uint64_t nkeys,
                                           uint32_t *edges, void *stream) {

@@ -130,6 +130,13 @@ __device__ __forceinline__ int pure_sign(const Cell &c, ull seed_c) {
     return c.count == 1u ? 1 : -1;
 }
 
+// w[0, nwords) = 0 over the whole grid (w is 256-byte aligned: 16-byte stores, then the tail)
+__device__ __forceinline__ void zero_words(uint32_t *w, ull nwords, ull tid, ull nthr) {
+    const ull n4 = nwords / 4;
+    for (ull i = tid; i < n4; i += nthr) __stcg(reinterpret_cast<uint4 *>(w) + i, make_uint4(0u, 0u, 0u, 0u));
+    for (ull i = n4 * 4 + tid; i < nwords; i += nthr) w[i] = 0u;
+}
+
 static constexpr int IQ = 2 * IB_BLOCK;
 typedef BlockQueueT<ulonglong2, IQ, IB_BLOCK> EntQ;
 typedef BlockQueueT<ull, IQ, IB_BLOCK> KeyQ;
@@ -241,12 +248,20 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
         block_add<IB_BLOCK>(&a.per_round[t <= ISTAT_CAP ? t - 1 : ISTAT_CAP], recovered);
         grid.sync();
         // ---- phase B: retire this round's pure bits, re-test candidates ----
-        for (ull i = tid; i < nF; i += nthr) {
-            const uint32_t c = (uint32_t)__ldcg(&Fc[i].x);
-            atomicAnd(a.pure[(t - 1) & 1] + (c >> 5), ~(1u << (c & 31)));
-        }
+        // pure[(t-1)&1] holds exactly F_t's bits and cand exactly this round's candidates:
+        // a large round zeroes the whole bitmap with coalesced stores (C/8 bytes) instead of
+        // one random atomicAnd per entry
+        const ull nwords = (a.C + 31) / 32;
+        if (nF * 8 >= nwords) zero_words(a.pure[(t - 1) & 1], nwords, tid, nthr);
+        else
+            for (ull i = tid; i < nF; i += nthr) {
+                const uint32_t c = (uint32_t)__ldcg(&Fc[i].x);
+                atomicAnd(a.pure[(t - 1) & 1] + (c >> 5), ~(1u << (c & 31)));
+            }
         if (tid == 0) ctl->ccnt[(t + 1) & 1] = 0;
         const ull nC = ld_cg_u64(ccnt);
+        const bool cand_bulk = nC * 8 >= nwords;
+        if (cand_bulk) zero_words(a.cand, nwords, tid, nthr);
         ulonglong2 *Fn = a.F[t & 1];
         ull *fn = &ctl->fcnt[t % 3];
         uint32_t *pure_next = a.pure[t & 1];
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
             const ull i = base + threadIdx.x;
             if (i < nC) {
                 const uint32_t c = ld_cg_u32(a.clist + i);
-                atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
+                if (!cand_bulk) atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
                 Cell v = ld_cell_cg(a.cells + c);
                 const int sg = pure_sign<SIGNED>(v, a.seed_c);
                 if (sg) {

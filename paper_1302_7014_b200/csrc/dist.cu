@@ -420,7 +420,11 @@ static double dist_bin_frac(uint64_t nloc) {
         const double f = atof(e);
         return f > 0.0 ? f : 2.0;  // 0 disables (no frontier reaches 2 nloc)
     }
-    return 8.0 * (double)nloc >= 2e9 ? 0.02 : 0.05;
+    // unlike the single-GPU path, a small local frontier costs the shard random kills, send
+    // queues AND a random receive pass: binned rounds pay off from 0.02 nloc once the shard
+    // state is >= 0.8 GB (C5 virtual 8 shards 338 -> 311 ms, 4 shards 231 -> 197 ms; C3 at
+    // P = 1 19.2 -> 17.6 ms; C3 / C4a over 4 shards of 2.5e7 stay faster at 0.05)
+    return 8.0 * (double)nloc >= 8e8 ? 0.02 : 0.05;
 }
 
 static unsigned dgrid(uint64_t work) {

@@ -148,6 +148,23 @@ def test_binned_build_overflow_fallback():
     check_vs_oracle(e_np, n, 2, twice=False)
 
 
+def test_csr_binned_high_degree():
+    # k = 3 (CSR) with n > 2^23 (binned CSR build): random edges, then the same with hubs of
+    # degree ~1023-1025 (a 10-bit rank field's edge) and ~3000 added
+    n, m = (1 << 23) + 4321, 9000000
+    e_np = pk.gen_hypergraph(n, m, 3, 31, device=DEV).cpu().numpy().view(np.uint32).copy()
+    check_vs_oracle(e_np, n, 3, twice=False)
+    row = 0
+    for hub, extra in ((7, 3000), (5000003, 1025), (6000011, 1023)):
+        e_np[row:row + extra, 0] = hub
+        row += extra
+    bad = (e_np[:, 1] == e_np[:, 0]) | (e_np[:, 2] == e_np[:, 0])
+    e_np[bad, 0] = 1  # keep the r vertices distinct
+    e_np[bad & ((e_np[:, 1] == 1) | (e_np[:, 2] == 1)), 0] = 2
+    assert np.all((e_np[:, 0] != e_np[:, 1]) & (e_np[:, 0] != e_np[:, 2]) & (e_np[:, 1] != e_np[:, 2]))
+    check_vs_oracle(e_np, n, 3, twice=False)
+
+
 def test_c1_golden_and_oracle(oracle_goldens):
     g = oracle_goldens["C1"]
     e = pk.gen_hypergraph(g["n"], g["m"], g["r"], g["seed"], device=DEV)

@@ -199,17 +199,17 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                 const ull x = ent.y;
                 uint32_t h[R];
                 key_cells<R>(x, a.C, a.seed_h, a.subt, h, a.blog);
-                // owner rule: the lowest-index round-start-pure cell among h_1..h_r is c (the
-                // r pure bits are loaded together, then scanned in order)
+                // owner rule: c is one of x's cells and none of x's cells of lower index was
+                // pure at round start (only those pure bits are loaded, together)
                 uint32_t pw[R];
                 #pragma unroll
-                for (int j = 0; j < R; j++) pw[j] = ld_cg_u32(pure_cur + (h[j] >> 5));
-                bool owner = false, found = false;
+                for (int j = 0; j < R; j++) pw[j] = h[j] < c ? ld_cg_u32(pure_cur + (h[j] >> 5)) : 0u;
+                bool owner = false;
                 #pragma unroll
-                for (int j = 0; j < R; j++) {
-                    if (!found && h[j] == c) { found = true; owner = true; }
-                    if (!found && (pw[j] >> (h[j] & 31) & 1u)) found = true;
-                }
+                for (int j = 0; j < R; j++) owner |= h[j] == c;
+                #pragma unroll
+                for (int j = 0; j < R; j++)
+                    if (h[j] < c && (pw[j] >> (h[j] & 31) & 1u)) owner = false;
                 if (owner) {
                     recovered++;
                     // <= one push per thread per iteration < IQ: the queue never takes its overflow path
@@ -217,14 +217,14 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
                     const uint32_t hx = checksum(x, a.seed_c);
                     const uint32_t delta = neg ? 1u : 0xFFFFFFFFu;  // remove: count -= sign
                     // the r count atomics are issued before any result is used.  In an
-                    // insert-only table a round-start-pure cell holds x alone, and no other
-                    // key recovered this round can be in it: x's deletion leaves it zero,
-                    // a plain 16-byte store instead of three atomics.
+                    // insert-only table the round-start-pure cell c holds x alone, and no
+                    // other key recovered this round can be in it: x's deletion leaves it
+                    // zero, a plain 16-byte store instead of three atomics.
                     uint32_t now[R];
                     #pragma unroll
                     for (int j = 0; j < R; j++) {
                         Cell *p = a.cells + h[j];
-                        if (!SIGNED && a.insert_only && (pw[j] >> (h[j] & 31) & 1u)) {
+                        if (!SIGNED && a.insert_only && h[j] == c) {
                             __stcg(reinterpret_cast<uint4 *>(p), make_uint4(0u, 0u, 0u, 0u));
                             now[j] = 0u;
                             continue;

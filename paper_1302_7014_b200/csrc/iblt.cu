@@ -19,6 +19,7 @@
 //             (a candidate may have dropped to 0 in the same round) and emit
 //             the next frontier.
 //   stop      at the first round with an empty frontier.
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -143,8 +144,11 @@ typedef BlockQueueT<ull, IQ, IB_BLOCK> KeyQ;
 typedef BlockQueueT<uint32_t, IQ, IB_BLOCK> CellQ;
 
 // entry.x = cell | (negative sign) << 32, entry.y = key snapshot
+// 5 resident blocks per SM (48 registers; shared queues 36 KB per block): C2 peel 1.38 ms at
+// 4 blocks (64 registers), 1.35 ms at 5; 6 and 8 blocks spill or lose to the smaller queues
+// of registers: 1.60 / 1.64 ms
 template <int R, bool SIGNED>
-__global__ void __launch_bounds__(IB_BLOCK) iblt_peel_kernel(IPeelArgs a) {
+__global__ void __launch_bounds__(IB_BLOCK, 5) iblt_peel_kernel(IPeelArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ EntQ qe;
     __shared__ EntQ qk;  // recovered (key, sign)

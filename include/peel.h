@@ -276,6 +276,10 @@ peel_status iblt_delete(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, void
  * with the lowest hash index among the key's cells), deletes every recovered
  * key from its r cells, and stops at the first round recovering nothing.
  * DESTRUCTIVE: the table holds the unrecovered remainder afterwards.
+ * A table that has only seen iblt_insert since iblt_build (no iblt_delete, no
+ * iblt_subtract into it, no iblt_cells) is insert-only: its counts are the true
+ * key counts, so the owner's pure cell is zeroed with one store instead of an
+ * XOR-delete.  The result is identical either way.
  * out: out_keys dev u64 [cap_keys], recovered keys in unspecified order;
  *      nrecovered host u64 (may exceed cap_keys: then PEEL_ETRUNC and only
  *      cap_keys were stored); rounds host u32; per_round host u64 [cap]

@@ -799,6 +799,9 @@ __global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelAr
 #define PEEL_ES_CH 4096
 #endif
 static constexpr int ES_CH = PEEL_ES_CH;  // entries per chunk (scatter)
+// 5 resident scatter blocks per SM (48 registers) and a grid of 5 per SM: C5 sort 5.6 -> 5.25
+// ms; 4 blocks at 64 registers 5.6, 6 at 40 (spilling) 5.3, 8 per SM 6.5 ms
+static constexpr int ES_BLOCKS = 5;
 
 __global__ void __launch_bounds__(256) esort_hist_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
                                                          uint32_t nb, ull *ghist) {
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(256) esort_hist_kernel(const uint2 *__restrict
 
 // ghist: the entries per edge bin (complete before the launch); cursor: zeroed.  Every block
 // derives the bins' start offsets from ghist itself (no separate scan launch).
-__global__ void __launch_bounds__(256) esort_scatter_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
+__global__ void __launch_bounds__(256, ES_BLOCKS) esort_scatter_kernel(const uint2 *__restrict__ F, const ull *__restrict__ pN,
                                                             uint32_t nb, const ull *__restrict__ ghist, ull *cursor,
                                                             uint2 *out) {
     extern __shared__ unsigned char smem_raw[];
@@ -2002,7 +2005,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                 PEEL_CUDA(cudaMemsetAsync(ecur, 0, sizeof(ull) * enb, s));
                 PEEL_CUDA(cudaMemsetAsync(ehist[(t + 1) & 1], 0, sizeof(ull) * enb, s));  // for this round's D
                 const uint64_t chunks = (nE + ES_CH - 1) / ES_CH;
-                const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * 4);
+                const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * ES_BLOCKS);
                 esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>(src, pN, enb, ehist[t & 1], ecur, dst);
                 br.Fsrc = dst;
                 br.ehist = ehist[(t + 1) & 1];
@@ -2176,7 +2179,7 @@ peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint6
     ProfScope ps("frontier_edge_sort", s);
     esort_hist_kernel<<<grid_for(nE_host, 8), 256, sizeof(uint32_t) * enb, s>>>((const uint2 *)src, pN, enb, hist);
     const uint64_t chunks = (nE_host + ES_CH - 1) / ES_CH;
-    const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * 4);
+    const unsigned sg = (unsigned)std::min<uint64_t>(chunks, (uint64_t)num_sms() * ES_BLOCKS);
     esort_scatter_kernel<<<sg ? sg : 1, 256, essmem, s>>>((const uint2 *)src, pN, enb, hist, cur, (uint2 *)dst);
     PEEL_CUDA(cudaGetLastError());
     return PEEL_OK;

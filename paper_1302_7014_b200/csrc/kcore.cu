@@ -675,8 +675,13 @@ __global__ void __launch_bounds__(PEEL_BLOCK) bin_accumulate_kernel(PeelArgs a, 
 // L2-resident returning atomics while the next bin's state is prefetched into L2.  The
 // crossing rule (old count == k) and the (v, e) frontier entries are those of the persistent
 // kernel, so the schedule is unchanged.
+// 3 entries per thread at 5 resident blocks per SM (48 registers): C5 kill 24.4-24.8 ->
+// 24.0 ms against 4 at 4 blocks (62 registers); 2 at 6 blocks: 27.6 ms
 #ifndef PEEL_KU
-#define PEEL_KU 4
+#define PEEL_KU 3
+#endif
+#ifndef PEEL_KILL_MINB
+#define PEEL_KILL_MINB 5
 #endif
 static constexpr int KU = PEEL_KU;                 // frontier entries per thread per K iteration
 static constexpr int KCH = PART_BLOCK * KU;       // entries per block iteration
@@ -698,7 +703,7 @@ struct BinRound {
 };
 
 template <int R>
-__global__ void __launch_bounds__(PART_BLOCK) round_kill_partition_kernel(PeelArgs a, BinRound br) {
+__global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) round_kill_partition_kernel(PeelArgs a, BinRound br) {
     extern __shared__ unsigned char smem_raw[];
     const uint32_t nbins = br.nbins;
     ull *sorted = (ull *)smem_raw;                       // [(R-1) KCH] the chunk's decrements, bin-sorted

@@ -614,7 +614,9 @@ struct BinArgs {
 };
 
 template <int R>
-__global__ void __launch_bounds__(PEEL_BLOCK) bin_accumulate_kernel(PeelArgs a, BinArgs bn) {
+// 6 resident blocks per SM (40 registers): C5 18.7 -> 18.5 ms against the compiler's 48
+// registers (5 blocks)
+__global__ void __launch_bounds__(PEEL_BLOCK, 6) bin_accumulate_kernel(PeelArgs a, BinArgs bn) {
     cg::grid_group grid = cg::this_grid();
     __shared__ BlockQueue<uint2> q;
     Ctl *ctl = a.ctl;

@@ -38,7 +38,10 @@ typedef enum {
     PEEL_ECUDA = 3,     /* a CUDA runtime error (peel_last_cuda_error() has the text) */
     PEEL_ETRUNC = 4,    /* more rounds than the caller's `cap`; rounds and the first cap entries are valid */
     PEEL_ENCCL = 5,     /* an NCCL error (multi-GPU entry points) */
-    PEEL_EOVERFLOW = 6  /* packed k<=2 state cannot hold this degree x edge-id range (see peel_kcore) */
+    PEEL_EOVERFLOW = 6, /* packed k<=2 state cannot hold this degree x edge-id range (see peel_kcore) */
+    PEEL_EPEER = 7      /* multi-rank calls: another rank of the communicator failed; every rank
+                           leaves the call at the same collective (the failing rank returns its
+                           own status) */
 } peel_status;
 
 /* Human-readable name of a status code (static storage). */
@@ -47,7 +50,7 @@ const char *peel_strerror(int status);
 const char *peel_last_cuda_error(void);
 /* ABI version of this header (bumped on any signature change). */
 int peel_abi_version(void);
-#define PEEL_ABI_VERSION 1
+#define PEEL_ABI_VERSION 2
 
 /* ======================================================================= */
 /* a1 -- generator: G^r_{n,cn} and IBLT keys (counter-based) */
@@ -194,6 +197,23 @@ peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, co
  * peel_comm_init_virtual: P shards inside ONE process on ONE GPU, the
  *   all-to-all done by device copies through the same send/receive buffers
  *   and kernels -- the partitioning logic testable without P GPUs.
+ * peel_comm_init_host: a rank communicator whose collectives go through three
+ *   caller-supplied HOST callbacks (every rank one process; e.g. torch.distributed
+ *   gloo), with device<->host staging inside the library.  It runs exactly the
+ *   per-rank protocol of the NCCL communicator (count exchange, per-peer payload,
+ *   allreduce, error word) and needs no GPU per rank: no kernel waits on another
+ *   rank, so several ranks may share one GPU.  Callbacks return 0 on success
+ *   (else the call fails with PEEL_ENCCL) and must be collective: every rank
+ *   calls them in the same order.
+ *     allreduce(ctx, vals, count): vals[count] (host u64) <- elementwise sum.
+ *     allgather(ctx, send, recv, bytes): recv[P bytes] <- each rank's send[bytes].
+ *     alltoallv(ctx, send, sbytes[P], recv, rbytes[P]): rank me sends sbytes[d]
+ *       bytes to every rank d (segments packed in increasing d in send; sbytes[me]
+ *       = 0) and receives rbytes[q] bytes from every q, packed in increasing q.
+ * Errors (all partitioned calls): a rank that fails locally keeps taking part in
+ *   the collectives with an error word set; every rank then leaves at the same
+ *   collective -- the failing rank with its status, the others with PEEL_EPEER --
+ *   so no rank is left blocked in a collective.
  * peel_kcore_dist: edges dev u32 [m][r] (replicated); core_mask dev u8: the
  *   rank's slice [v1 - v0] (NCCL) or all n (virtual); rounds/survivors/killed
  *   host, global (identical on every rank); workspace dev,
@@ -201,8 +221,15 @@ peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, co
  *   Blocking (host-driven rounds: two stream syncs per round).
  */
 typedef struct peel_comm peel_comm;
+typedef int (*peel_host_allreduce_fn)(void *ctx, uint64_t *vals, uint64_t count);
+typedef int (*peel_host_allgather_fn)(void *ctx, const void *send, void *recv, uint64_t bytes);
+typedef int (*peel_host_alltoallv_fn)(void *ctx, const void *send, const uint64_t *sbytes, void *recv,
+                                      const uint64_t *rbytes);
 peel_status peel_comm_unique_id(void *id128);
 peel_status peel_comm_init(const void *id128, int nranks, int rank, peel_comm **out);
+peel_status peel_comm_init_host(int nranks, int rank, peel_host_allreduce_fn allreduce,
+                                peel_host_allgather_fn allgather, peel_host_alltoallv_fn alltoallv, void *ctx,
+                                peel_comm **out);
 peel_status peel_comm_init_virtual(int nshards, peel_comm **out);
 void peel_comm_destroy(peel_comm *c);
 size_t peel_kcore_dist_workspace_bytes(const peel_comm *c, uint64_t n, uint64_t m, uint32_t r, uint32_t k);
@@ -334,8 +361,18 @@ void iblt_destroy(peel_iblt *t);
  * recovered per round over all shards) and *complete (all cells of all shards zero) are
  * global.  mem: dev, iblt_dist_mem_bytes(c, cells, r) bytes (per rank; virtual: all shards).
  * Collective over the communicator's ranks; blocking.  EINVAL: bad shape or flags (r in
- * [2, 8], P <= 8); ENOMEM: mem too small; ETRUNC: cap_keys or cap exceeded; ENCCL. */
+ * [2, 8], P <= 8); ENOMEM: mem too small; ETRUNC: cap_keys or cap exceeded, or 65536
+ * rounds; ENCCL; EPEER.
+ * iblt_dist_recover_cells: the same recovery of an EXISTING table: cells_in (dev, `cells`
+ * 16-byte cells laid out as iblt_cells() returns them -- e.g. a subtracted, deserialized or
+ * received table; the same bytes on every rank) instead of keys to insert; each shard copies
+ * its own cell range.  Unsigned recovery (count +1).  R28: a cell is pure when
+ * its count is 1, its checksum matches and it is one of its key's cells. */
 size_t iblt_dist_mem_bytes(const peel_comm *c, uint64_t cells, uint32_t r);
+peel_status iblt_dist_recover_cells(peel_comm *c, const void *cells_in, uint64_t cells, uint32_t r, uint64_t seed,
+                                    uint32_t flags, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
+                                    uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete, void *mem,
+                                    size_t mem_bytes, void *stream);
 peel_status iblt_dist_recover(peel_comm *c, uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags,
                               const uint64_t *keys, uint64_t nkeys, uint64_t *out_keys, uint64_t cap_keys,
                               uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,

@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
             L.ora_iblt_delete.argtypes = [p, p, u64]
             L.ora_iblt_delete.restype = i32
             L.ora_iblt_dump.argtypes = [p, p, p, p]
+            L.ora_iblt_load.argtypes = [p, p, p, p]
             L.ora_iblt_peel.argtypes = [p, p, u64, p, p, p, u32, p]
             L.ora_iblt_peel.restype = i32
             L.ora_iblt_serial_recover.argtypes = [p, p, u64, p, p]
@@ -258,11 +259,12 @@ def queue_peel(edges: np.ndarray, n: int, k: int) -> np.ndarray:
 # IBLT
 # ---------------------------------------------------------------------------
 class IbltResult:
-    def __init__(self, keys, rounds, per_round, complete):
+    def __init__(self, keys, rounds, per_round, complete, truncated=False):
         self.keys = keys
         self.rounds = rounds
         self.per_round = per_round
         self.complete = complete
+        self.truncated = truncated
 
 
 class Iblt:
@@ -298,8 +300,17 @@ class Iblt:
         lib().ora_iblt_dump(self._t, _ptr(count), _ptr(keysum), _ptr(hashsum))
         return count, keysum, hashsum
 
-    def peel(self, cap_keys: int | None = None, cap: int = 1 << 16) -> IbltResult:
-        """Round-synchronous recovery, destructive."""
+    def load_cells(self, count, keysum, hashsum):
+        """Overwrite every cell (a serialized table; tests forge cells with it)."""
+        count = np.ascontiguousarray(count, dtype=np.int64)
+        keysum = np.ascontiguousarray(keysum, dtype=np.uint64)
+        hashsum = np.ascontiguousarray(hashsum, dtype=np.uint32)
+        assert count.size == keysum.size == hashsum.size == self.C
+        lib().ora_iblt_load(self._t, _ptr(count), _ptr(keysum), _ptr(hashsum))
+
+    def peel(self, cap_keys: int | None = None, cap: int = 1 << 16, allow_trunc: bool = False) -> IbltResult:
+        """Round-synchronous recovery, destructive.  allow_trunc: a truncated
+        recovery (cap, cap_keys or the 65536-round limit) is returned with .truncated set."""
         cap_keys = self.C * 2 if cap_keys is None else cap_keys
         out = np.zeros(max(cap_keys, 1), dtype=np.uint64)
         nrec = ctypes.c_uint64(0)
@@ -311,10 +322,11 @@ class Iblt:
                                  ctypes.addressof(complete))
         if st < 0:
             raise MemoryError("oracle iblt_peel")
-        if st == 1:
+        if st == 1 and not allow_trunc:
             raise OverflowError("cap exceeded")
         t = rounds.value
-        return IbltResult(out[:nrec.value].copy(), t, per_round[:t].copy(), bool(complete.value))
+        k = min(nrec.value, cap_keys)
+        return IbltResult(out[:k].copy(), t, per_round[:min(t, cap)].copy(), bool(complete.value), st == 1)
 
     def peel_subtables(self, cap_keys: int | None = None, cap: int = 1 << 16) -> IbltResult:
         """Subtable recovery, destructive; rounds = flattened index of the last
@@ -338,9 +350,11 @@ class Iblt:
         if lib().ora_iblt_subtract(self._t, other._t):
             raise ValueError("tables differ in C, r, seed or layout")
 
-    def peel_signed(self, cap_keys: int | None = None, cap: int = 1 << 16):
-        """Recovery of a signed table: pure = count +-1 with a matching checksum.
-        Returns (IbltResult, signs) with signs[i] = +1 (key of A only) or -1 (key of B only)."""
+    def peel_signed(self, cap_keys: int | None = None, cap: int = 1 << 16, allow_trunc: bool = False):
+        """Recovery of a signed table: pure = count +-1, a matching checksum, and the cell is
+        one of the key's cells (R26, R28); a key found in several pure cells is recovered
+        once, with the sign of the lowest such cell.  Returns (IbltResult, signs) with
+        signs[i] = +1 (key of A only) or -1 (key of B only)."""
         cap_keys = self.C * 2 if cap_keys is None else cap_keys
         out = np.zeros(max(cap_keys, 1), dtype=np.uint64)
         sg = np.zeros(max(cap_keys, 1), dtype=np.int8)
@@ -350,10 +364,14 @@ class Iblt:
         complete = ctypes.c_int(0)
         st = lib().ora_iblt_peel_signed(self._t, _ptr(out), _ptr(sg), cap_keys, ctypes.addressof(nrec),
                                         ctypes.addressof(rounds), _ptr(per), cap, ctypes.addressof(complete))
-        if st != 0:
+        if st < 0:
+            raise MemoryError("oracle iblt_peel_signed")
+        if st == 1 and not allow_trunc:
             raise OverflowError("cap exceeded")
         t = rounds.value
-        return IbltResult(out[:nrec.value].copy(), t, per[:t].copy(), bool(complete.value)), sg[:nrec.value].copy()
+        k = min(nrec.value, cap_keys)
+        return (IbltResult(out[:k].copy(), t, per[:min(t, cap)].copy(), bool(complete.value), st == 1),
+                sg[:k].copy())
 
     def serial_recover(self):
         """One-pure-cell-at-a-time recovery, destructive."""

@@ -472,16 +472,41 @@ void ora_iblt_dump(const ora_iblt *t, int64_t *count, uint64_t *keySum, uint32_t
     memcpy(hashSum, t->hashSum, t->C * sizeof(uint32_t));
 }
 
+/* Overwrite every cell (a serialized table; tests also forge cells with it). */
+void ora_iblt_load(ora_iblt *t, const int64_t *count, const uint64_t *keySum, const uint32_t *hashSum) {
+    memcpy(t->count, count, t->C * sizeof(int64_t));
+    memcpy(t->keySum, keySum, t->C * sizeof(uint64_t));
+    memcpy(t->hashSum, hashSum, t->C * sizeof(uint32_t));
+}
+
 static int cmp_u64(const void *a, const void *b) {
     uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
     return (x > y) - (x < y);
 }
 
-/* pure cell ("cells that only contain one item"): count == 1 and the  */
-/* checksum field equals checkSum(key field).                     */
-static int iblt_pure(const ora_iblt *t, uint64_t c) {
-    return t->count[c] == 1 && t->hashSum[c] == ora_checksum(t->keySum[c], t->seed_c);
+/* A pure cell "only contain[s] one item", x = its key field.  This   */
+/* build's test (reading R28): count == 1, the checksum field       */
+/* equals checkSum(x), and c is one of x's own cells h_1(x) ..    */
+/* h_r(x) -- a cell holding only x is necessarily one of x's     */
+/* cells, so a cell failing that test holds more than one item whatever its   */
+/* other fields say (a checksum collision, a forged or corrupted table).      */
+static int cell_of_key(const ora_iblt *t, uint64_t c, uint64_t x) {
+    uint64_t cells[16];
+    key_cells(t, x, cells);
+    for (uint32_t j = 0; j < t->r; j++)
+        if (cells[j] == c) return 1;
+    return 0;
 }
+
+static int iblt_pure(const ora_iblt *t, uint64_t c) {
+    return t->count[c] == 1 && t->hashSum[c] == ora_checksum(t->keySum[c], t->seed_c) &&
+           cell_of_key(t, c, t->keySum[c]);
+}
+
+/* At most this many rounds (steps, for the subtable schedule) are run; a     */
+/* table still holding pure cells after the last one is reported truncated    */
+/* (status 1).  Forged signed tables are not known to terminate (DESIGN R28). */
+#define ORA_IBLT_ROUND_LIMIT 65536u
 
 /* Round-synchronous recovery: each round snapshots the set of    */
 /* pure cells, recovers the SET of their keys (set semantics: a key seen in   */
@@ -502,6 +527,7 @@ int ora_iblt_peel(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *
         for (uint64_t c = 0; c < C; c++)
             if (iblt_pure(t, c)) X[nX++] = t->keySum[c];
         if (nX == 0) break;
+        if (rt == ORA_IBLT_ROUND_LIMIT) { status = 1; break; }
         qsort(X, nX, sizeof(uint64_t), cmp_u64);
         uint64_t u = 0;
         for (uint64_t i = 0; i < nX; i++)
@@ -541,6 +567,7 @@ int ora_iblt_peel_subtables(ora_iblt *t, uint64_t *out_keys, uint64_t cap_keys, 
     int status = 0;
     for (;;) {
         int any = 0;
+        if (flat + t->r > ORA_IBLT_ROUND_LIMIT) { status = 1; break; }
         for (uint32_t j = 0; j < t->r; j++) {
             flat++;
             uint64_t nX = 0;
@@ -587,19 +614,23 @@ int ora_iblt_subtract(ora_iblt *a, const ora_iblt *b) {
 }
 
 /* Round-synchronous recovery of a signed table: a cell is pure when its     */
-/* count is +1 or -1 and its checksum field equals checkSum(key field); each */
-/* round recovers the SET of (key, sign) of the round-start pure cells and   */
-/* removes each (deleting a +1 key, re-inserting a -1 key).  out_sign[i] is  */
-/* +1 for keys of A \ B, -1 for keys of B \ A.                              */
+/* count is +1 or -1, its checksum field equals checkSum(key field) and it is */
+/* one of that key's cells (R26, R28).  Each round recovers every distinct    */
+/* key x of the round-start pure cells ONCE, with the sign of the lowest-     */
+/* index round-start pure cell holding x (R28), and removes it (deleting a +1 */
+/* key, re-inserting a -1 key).  out_sign[i] is +1 for keys of A \ B, -1 for */
+/* keys of B \ A.                                                           */
 static int iblt_pure_signed(const ora_iblt *t, uint64_t c, int *sign) {
-    if ((t->count[c] == 1 || t->count[c] == -1) && t->hashSum[c] == ora_checksum(t->keySum[c], t->seed_c)) {
+    if ((t->count[c] == 1 || t->count[c] == -1) && t->hashSum[c] == ora_checksum(t->keySum[c], t->seed_c) &&
+        cell_of_key(t, c, t->keySum[c])) {
         *sign = (int)t->count[c];
         return 1;
     }
     return 0;
 }
 
-static int cmp_key_sign(const void *a, const void *b) {
+/* (key, cell, sign + 1) triples ordered by key, then cell */
+static int cmp_key_cell(const void *a, const void *b) {
     const uint64_t *x = (const uint64_t *)a, *y = (const uint64_t *)b;
     if (x[0] != y[0]) return (x[0] > y[0]) - (x[0] < y[0]);
     return (x[1] > y[1]) - (x[1] < y[1]);
@@ -609,7 +640,7 @@ int ora_iblt_peel_signed(ora_iblt *t, uint64_t *out_keys, int8_t *out_sign, uint
                          uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
                          int *complete) {
     uint64_t C = t->C;
-    uint64_t *X = (uint64_t *)malloc(2 * C * sizeof(uint64_t));  /* (key, sign + 1) pairs */
+    uint64_t *X = (uint64_t *)malloc(3 * C * sizeof(uint64_t));  /* (key, cell, sign + 1) */
     if (!X) return -1;
     uint64_t nrec = 0;
     uint32_t rt = 0;
@@ -618,21 +649,24 @@ int ora_iblt_peel_signed(ora_iblt *t, uint64_t *out_keys, int8_t *out_sign, uint
         uint64_t nX = 0;
         for (uint64_t c = 0; c < C; c++) {
             int sg;
-            if (iblt_pure_signed(t, c, &sg)) { X[2 * nX] = t->keySum[c]; X[2 * nX + 1] = (uint64_t)(sg + 1); nX++; }
+            if (iblt_pure_signed(t, c, &sg)) {
+                X[3 * nX] = t->keySum[c]; X[3 * nX + 1] = c; X[3 * nX + 2] = (uint64_t)(sg + 1); nX++;
+            }
         }
         if (nX == 0) break;
-        qsort(X, nX, 2 * sizeof(uint64_t), cmp_key_sign);
-        uint64_t u = 0;
+        if (rt == ORA_IBLT_ROUND_LIMIT) { status = 1; break; }
+        qsort(X, nX, 3 * sizeof(uint64_t), cmp_key_cell);
+        uint64_t u = 0;  /* first (lowest-cell) triple of every key */
         for (uint64_t i = 0; i < nX; i++)
-            if (i == 0 || X[2 * i] != X[2 * (i - 1)] || X[2 * i + 1] != X[2 * (i - 1) + 1]) {
-                X[2 * u] = X[2 * i]; X[2 * u + 1] = X[2 * i + 1]; u++;
+            if (i == 0 || X[3 * i] != X[3 * (i - 1)]) {
+                X[3 * u] = X[3 * i]; X[3 * u + 1] = X[3 * i + 1]; X[3 * u + 2] = X[3 * i + 2]; u++;
             }
         nX = u;
         rt += 1;
         for (uint64_t i = 0; i < nX; i++) {
-            int sg = (int)X[2 * i + 1] - 1;
-            iblt_apply(t, X[2 * i], -sg);
-            if (nrec < cap_keys) { out_keys[nrec] = X[2 * i]; out_sign[nrec] = (int8_t)sg; } else status = 1;
+            int sg = (int)X[3 * i + 2] - 1;
+            iblt_apply(t, X[3 * i], -sg);
+            if (nrec < cap_keys) { out_keys[nrec] = X[3 * i]; out_sign[nrec] = (int8_t)sg; } else status = 1;
             nrec++;
         }
         if (rt <= cap) per_round[rt - 1] = nX; else status = 1;

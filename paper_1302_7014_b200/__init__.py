@@ -19,7 +19,7 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PEEL_LIB") or os.path.join(_PKG, "libpeel.so")  # PEEL_LIB: A/B builds
 
-PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOVERFLOW = range(7)
+PEEL_OK, PEEL_EINVAL, PEEL_ENOMEM, PEEL_ECUDA, PEEL_ETRUNC, PEEL_ENCCL, PEEL_EOVERFLOW, PEEL_EPEER = range(8)
 PEEL_FLAG_CSR = 1
 PEEL_FLAG_SUBROUNDS = 2
 IBLT_FLAG_SUBTABLES = 1
@@ -27,6 +27,12 @@ IBLT_FLAG_BLOCKED = 2
 IBLT_BLOCK_LOG_SHIFT = 8
 
 _lib = None
+
+# host-transport callbacks (peel.h peel_comm_init_host)
+_AR_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64)
+_AG_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64)
+_A2A_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                           ctypes.c_void_p)
 
 
 class PeelError(RuntimeError):
@@ -65,6 +71,7 @@ def _L() -> ctypes.CDLL:
         L.peel_comm_unique_id.argtypes = [p]
         L.peel_comm_init.argtypes = [p, i32, i32, ctypes.POINTER(p)]
         L.peel_comm_init_virtual.argtypes = [i32, ctypes.POINTER(p)]
+        L.peel_comm_init_host.argtypes = [i32, i32, _AR_FN, _AG_FN, _A2A_FN, p, ctypes.POINTER(p)]
         L.peel_comm_destroy.argtypes = [p]
         L.peel_kcore_dist_workspace_bytes.argtypes = [p, u64, u64, u32, u32]
         L.peel_kcore_dist_workspace_bytes.restype = sz
@@ -72,6 +79,7 @@ def _L() -> ctypes.CDLL:
         L.iblt_dist_mem_bytes.argtypes = [p, u64, u32]
         L.iblt_dist_mem_bytes.restype = sz
         L.iblt_dist_recover.argtypes = [p, u64, u32, u64, u32, p, u64, p, u64, p, p, p, u32, p, p, sz, p]
+        L.iblt_dist_recover_cells.argtypes = [p, p, u64, u32, u64, u32, p, u64, p, p, p, u32, p, p, sz, p]
         L.iblt_mem_bytes.argtypes = [u64, u32]
         L.iblt_mem_bytes.restype = sz
         L.iblt_build.argtypes = [u64, u32, u64, p, sz, p, ctypes.POINTER(p)]
@@ -93,7 +101,7 @@ def _L() -> ctypes.CDLL:
         L.peel_profile_rounds.restype = i32
         for f in ("peel_gen_hypergraph", "peel_gen_keys", "peel_gen_partitioned", "peel_kcore", "peel_kcore_host", "peel_sweep",
                   "peel_comm_unique_id", "peel_comm_init", "peel_comm_init_virtual", "peel_kcore_dist", "iblt_build", "iblt_build_ex",
-                  "iblt_dist_recover",
+                  "iblt_dist_recover", "iblt_dist_recover_cells", "peel_comm_init_host",
                   "iblt_insert", "iblt_delete", "iblt_peel", "iblt_subtract", "iblt_peel_signed", "iblt_to_hypergraph"):
             getattr(L, f).restype = i32
         _lib = L
@@ -304,6 +312,71 @@ class Comm:
         _check(_L().peel_comm_init(idb.ctypes.data, world, rank, ctypes.byref(h)), "peel_comm_init")
         return cls(h, world, rank, False)
 
+    @classmethod
+    def host_transport(cls, group=None):
+        """Rank communicator whose collectives run through torch.distributed on the HOST
+        (e.g. a gloo group; peel.h peel_comm_init_host): the per-rank protocol of the NCCL
+        path with device<->host staging, so several ranks may share one GPU.  The callbacks
+        only move bytes between the library's pinned buffers and the process group."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def u8(ptr, nbytes):
+            return np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(ptr)) if nbytes else \
+                np.zeros(0, dtype=np.uint8)
+
+        def allreduce(_ctx, vals, count):
+            try:
+                a = u8(vals, 8 * count).view(np.int64)
+                t = torch.from_numpy(a.copy())
+                dist.all_reduce(t, group=group)
+                a[:] = t.numpy()
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a transport failure
+                return 1
+
+        def allgather(_ctx, send, recv, nbytes):
+            try:
+                t = torch.from_numpy(u8(send, nbytes).copy())
+                out = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(out, t, group=group)
+                u8(recv, nbytes * world)[:] = torch.cat(out).numpy()
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        def alltoallv(_ctx, send, sbytes, recv, rbytes):
+            try:
+                sb = np.ctypeslib.as_array((ctypes.c_uint64 * world).from_address(sbytes)).astype(np.int64)
+                rb = np.ctypeslib.as_array((ctypes.c_uint64 * world).from_address(rbytes)).astype(np.int64)
+                so = np.concatenate([[0], np.cumsum(sb)])
+                ro = np.concatenate([[0], np.cumsum(rb)])
+                sall = u8(send, int(so[-1]))
+                reqs, bufs = [], []
+                for q in range(world):
+                    if q != rank and rb[q]:
+                        b = torch.empty(int(rb[q]), dtype=torch.uint8)
+                        bufs.append((q, b))
+                        reqs.append(dist.irecv(b, src=q, group=group))
+                for q in range(world):
+                    if q != rank and sb[q]:
+                        reqs.append(dist.isend(torch.from_numpy(sall[so[q]:so[q + 1]].copy()), dst=q, group=group))
+                for rq in reqs:
+                    rq.wait()
+                rall = u8(recv, int(ro[-1]))
+                for q, b in bufs:
+                    rall[ro[q]:ro[q + 1]] = b.numpy()
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        fns = (_AR_FN(allreduce), _AG_FN(allgather), _A2A_FN(alltoallv))
+        h = ctypes.c_void_p(0)
+        _check(_L().peel_comm_init_host(world, rank, *fns, None, ctypes.byref(h)), "peel_comm_init_host")
+        c = cls(h, world, rank, False)
+        c._fns = fns  # the library keeps the function pointers: keep them alive
+        return c
+
     def shard(self, n: int, q: int | None = None) -> tuple[int, int]:
         q = self.rank if q is None else q
         return q * n // self.P, (q + 1) * n // self.P
@@ -395,13 +468,19 @@ class Iblt:
         _check(_L().iblt_delete(self._h, _ptr(keys), keys.numel(), _stream(stream)), "iblt_delete")
 
     def cells(self) -> torch.Tensor:
-        """[C, 4] int32 view (count, hashSum, keySum_lo, keySum_hi) of the device cells.
-        Read-only by contract: iblt_peel's insert-only fast path assumes the cells hold
-        exactly what iblt_insert wrote (use delete() / subtract() to change them)."""
-        return self.mem[: 16 * self.C].view(torch.int32).view(self.C, 4)
+        """[C, 4] int32 COPY (count, hashSum, keySum_lo, keySum_hi) of the device cells."""
+        return self.mem[: 16 * self.C].view(torch.int32).view(self.C, 4).clone()
+
+    def load_cells(self, cells: torch.Tensor):
+        """Overwrite every cell with `cells` ([C, 4] int32, the layout of cells()): a
+        serialized or received table.  Goes through iblt_cells(), so recovery no longer
+        assumes an insert-only table (peel.h)."""
+        ptr = _L().iblt_cells(self._h)
+        assert ptr == self.mem.data_ptr()
+        self.mem[: 16 * self.C].view(torch.int32).view(self.C, 4).copy_(cells)
 
     def peel(self, cap_keys: int | None = None, cap: int = 65536, out: torch.Tensor | None = None,
-             stream=None) -> IbltResult:
+             stream=None, allow_trunc: bool = False) -> IbltResult:
         cap_keys = self.C if cap_keys is None else cap_keys
         if out is None:
             out = torch.empty((max(cap_keys, 1),), dtype=torch.int64, device=self.device)
@@ -411,7 +490,7 @@ class Iblt:
         complete = ctypes.c_int(0)
         st = _L().iblt_peel(self._h, _ptr(out), cap_keys, ctypes.addressof(nrec), ctypes.addressof(rounds),
                             per_round.ctypes.data, cap, ctypes.addressof(complete), _stream(stream))
-        _check(st, "iblt_peel")
+        _check(st, "iblt_peel", ok=(PEEL_OK, PEEL_ETRUNC) if allow_trunc else (PEEL_OK,))
         t = rounds.value
         return IbltResult(out[: min(nrec.value, cap_keys)], nrec.value, t, per_round[:min(t, cap)].copy(),
                           bool(complete.value), st)
@@ -420,7 +499,7 @@ class Iblt:
         """self <- self - other cell-wise: the IBLT of the signed difference (peel.h iblt_subtract)."""
         _check(_L().iblt_subtract(self._h, other._h, _stream(stream)), "iblt_subtract")
 
-    def peel_signed(self, cap_keys: int | None = None, cap: int = 65536, stream=None):
+    def peel_signed(self, cap_keys: int | None = None, cap: int = 65536, stream=None, allow_trunc: bool = False):
         """Recovery of a signed table (peel.h iblt_peel_signed): returns (IbltResult, signs)."""
         cap_keys = self.C if cap_keys is None else cap_keys
         out = torch.empty((max(cap_keys, 1),), dtype=torch.int64, device=self.device)
@@ -432,7 +511,7 @@ class Iblt:
         st = _L().iblt_peel_signed(self._h, _ptr(out), _ptr(sg), cap_keys, ctypes.addressof(nrec),
                                    ctypes.addressof(rounds), per_round.ctypes.data, cap, ctypes.addressof(complete),
                                    _stream(stream))
-        _check(st, "iblt_peel_signed")
+        _check(st, "iblt_peel_signed", ok=(PEEL_OK, PEEL_ETRUNC) if allow_trunc else (PEEL_OK,))
         t = rounds.value
         k = min(nrec.value, cap_keys)
         return IbltResult(out[:k], nrec.value, t, per_round[:min(t, cap)].copy(), bool(complete.value), st), sg[:k]
@@ -467,6 +546,34 @@ def iblt_dist_recover(comm: Comm, cells: int, r: int, seed: int, keys: torch.Ten
                                 cap_keys, ctypes.addressof(nrec), ctypes.addressof(rounds), per_round.ctypes.data, cap,
                                 ctypes.addressof(complete), _ptr(mem), mem.numel(), _stream(stream))
     _check(st, "iblt_dist_recover")
+    t = rounds.value
+    return IbltResult(out[: min(nrec.value, cap_keys)], nrec.value, t, per_round[:min(t, cap)].copy(),
+                      bool(complete.value), st)
+
+
+def iblt_dist_recover_cells(comm: Comm, cells: torch.Tensor, r: int, seed: int, blog: int = 0,
+                            cap_keys: int | None = None, cap: int = 65536, mem: torch.Tensor | None = None,
+                            stream=None) -> IbltResult:
+    """Cell-partitioned recovery of an existing table (peel.h iblt_dist_recover_cells): cells
+    is the [C, 4] int32 device table (Iblt.cells() layout), the same on every rank."""
+    assert cells.is_cuda and cells.is_contiguous() and cells.dim() == 2 and cells.shape[1] == 4
+    C = cells.shape[0]
+    need = int(_L().iblt_dist_mem_bytes(comm._h, C, r))
+    if need == 0:
+        raise PeelError(PEEL_EINVAL, "iblt_dist_mem_bytes")
+    if mem is None:
+        mem = workspace(need, cells.device)
+    cap_keys = C if cap_keys is None else cap_keys
+    out = torch.empty((max(cap_keys, 1),), dtype=torch.int64, device=cells.device)
+    flags = (IBLT_FLAG_BLOCKED | (blog << IBLT_BLOCK_LOG_SHIFT)) if blog else 0
+    nrec = ctypes.c_uint64(0)
+    rounds = ctypes.c_uint32(0)
+    per_round = np.zeros(cap, dtype=np.uint64)
+    complete = ctypes.c_int(0)
+    st = _L().iblt_dist_recover_cells(comm._h, _ptr(cells), C, r, seed & (2**64 - 1), flags, _ptr(out), cap_keys,
+                                      ctypes.addressof(nrec), ctypes.addressof(rounds), per_round.ctypes.data, cap,
+                                      ctypes.addressof(complete), _ptr(mem), mem.numel(), _stream(stream))
+    _check(st, "iblt_dist_recover_cells")
     t = rounds.value
     return IbltResult(out[: min(nrec.value, cap_keys)], nrec.value, t, per_round[:min(t, cap)].copy(),
                       bool(complete.value), st)

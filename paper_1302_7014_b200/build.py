@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libpeel.so")
-SOURCES = ["runtime.cu", "gen.cu", "kcore.cu", "iblt.cu", "sweep.cu", "dist.cu", "iblt_dist.cu"]
+SOURCES = ["runtime.cu", "gen.cu", "kcore.cu", "iblt.cu", "sweep.cu", "comm.cu", "dist.cu", "iblt_dist.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr"]
 

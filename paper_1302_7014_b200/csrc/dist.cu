@@ -39,9 +39,12 @@ struct DCtl {
     ull ne[2];      // frontier entry counts
     ull kills;      // edges killed this round, counted at the owner of the smallest endpoint
     ull nsend[8];   // per-destination queue lengths this round
+    ull fail;       // this rank failed locally (host status != OK): the error word of the
+                    // count exchange, right after nsend (one 9-word allgather per round)
     uint32_t err;
     uint32_t pad;
 };
+static_assert(offsetof(DCtl, fail) == offsetof(DCtl, nsend) + 8 * sizeof(ull), "count row = nsend[8], fail");
 
 // the per-round reset clears kills and nsend[8] with one memset
 static_assert(offsetof(DCtl, nsend) == offsetof(DCtl, kills) + sizeof(ull), "per-round counters contiguous");
@@ -79,7 +82,7 @@ static DLayout dlayout(uint64_t n, uint64_t m, uint32_t r, int P, uint64_t nloc)
     DLayout L;
     size_t o = 0;
     L.ctl = o; o += dal(sizeof(DCtl));
-    L.scratch = o; o += dal(sizeof(ull) * (4 + 64));  // NCCL staging: 3 sums + the P x P count matrix
+    L.scratch = o; o += dal(sizeof(ull) * (8 + 9 * 8 + 5 * 8));  // collective staging: sums, P count rows, pack words
     L.state = o; o += dal(sizeof(ull) * nloc);
     L.alive = o; o += dal(sizeof(uint32_t) * ((m + 31) / 32));
     L.F0 = o; o += dal(sizeof(uint2) * nloc);
@@ -436,47 +439,14 @@ static unsigned dgrid(uint64_t work) {
 
 using namespace peel;
 
-extern "C" peel_status peel_comm_unique_id(void *id128) {
-    if (!id128) return PEEL_EINVAL;
-    ncclUniqueId id;
-    PEEL_NCCL(ncclGetUniqueId(&id));
-    memcpy(id128, &id, sizeof(id));
-    return PEEL_OK;
-}
-
-extern "C" peel_status peel_comm_init(const void *id128, int nranks, int rank, peel_comm **out) {
-    if (!id128 || !out || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return PEEL_EINVAL;
-    ncclUniqueId id;
-    memcpy(&id, id128, sizeof(id));
-    peel_comm *c = new peel_comm;
-    c->P = nranks;
-    c->rank = rank;
-    c->virt = false;
-    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
-    if (r != ncclSuccess) {
-        delete c;
-        peel::nccl_error(r);
-        return PEEL_ENCCL;
-    }
-    *out = c;
-    return PEEL_OK;
-}
-
-extern "C" peel_status peel_comm_init_virtual(int nshards, peel_comm **out) {
-    if (!out || nshards < 1 || nshards > 8) return PEEL_EINVAL;
-    peel_comm *c = new peel_comm;
-    c->P = nshards;
-    c->rank = -1;
-    c->virt = true;
-    c->nccl = nullptr;
-    *out = c;
-    return PEEL_OK;
-}
-
-extern "C" void peel_comm_destroy(peel_comm *c) {
-    if (!c) return;
-    if (!c->virt && c->nccl) ncclCommDestroy(c->nccl);
-    delete c;
+// the end-of-round words of a shard: [0..3] reduced over ranks (|F_{t+1}|, kills, bad-vertex
+// bits, failure), [4] local (frontier entries of round t+1, sizes the next kill grid)
+__global__ void dist_pack_kernel(const DCtl *ctl, int par, ull *out) {
+    out[0] = ctl->nf[par];
+    out[1] = ctl->kills;
+    out[2] = ctl->err;
+    out[3] = ctl->fail;
+    out[4] = ctl->ne[par];
 }
 
 static uint64_t max_shard(uint64_t n, int P) {
@@ -518,20 +488,45 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         d.binned = false;
         sh.push_back(d);
     }
+    // Error protocol (peel.h "Errors"): a rank's first local failure is kept in lst; from then
+    // on it launches nothing but still takes part in every collective with its failure word
+    // set, and every rank leaves at the next exchange.  Virtual shards have no peers: return.
+    peel_status lst = PEEL_OK;
+    auto cu = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && lst == PEEL_OK) {
+            set_cuda_error(e, what);
+            lst = PEEL_ECUDA;
+        }
+        return lst == PEEL_OK;
+    };
+    auto step = [&](peel_status st2) {
+        if (st2 != PEEL_OK && lst == PEEL_OK) lst = st2;
+        return lst == PEEL_OK;
+    };
+    ull *dsum = (ull *)(ws + L.scratch);  // device staging for the collectives (8 + 8 P words)
+    ull one = 1;
+    // the failure word of the count exchange (device, read by the gather)
+    auto mark_fail = [&]() {
+        for (auto &d : sh) cudaMemcpyAsync(&d.ctl->fail, &one, sizeof(ull), cudaMemcpyHostToDevice, s);
+    };
+    auto leave = [&](bool peer_failed) -> peel_status {
+        if (lst != PEEL_OK) return lst;
+        return peer_failed ? PEEL_EPEER : PEEL_OK;
+    };
+
     for (auto &d : sh) {
-        PEEL_CUDA(cudaMemsetAsync(d.ctl, 0, sizeof(DCtl), s));
-        PEEL_CUDA(cudaMemsetAsync(d.alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s));
+        if (!cu(cudaMemsetAsync(d.ctl, 0, sizeof(DCtl), s), "memset ctl")) break;
+        if (!cu(cudaMemsetAsync(d.alive, 0xFF, sizeof(uint32_t) * ((m + 31) / 32), s), "memset alive")) break;
         // large shards: the binned build of kcore.cu restricted to the shard's endpoints
         bool direct = true;
         d.binned = false;
         if (L.bins_bytes && d.v1 - d.v0 > 0) {
             char *b = ws + (c->virt ? (size_t)d.q * L.total : 0);
-            peel_status st = shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct);
-            if (st != PEEL_OK) return st;
+            if (!step(shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct))) break;
         }
         d.binned = !direct;  // bins usable by the binned rounds (no overflow)
         if (direct) {  // small shard, or a bin overflowed
-            PEEL_CUDA(cudaMemsetAsync(d.state, 0, sizeof(ull) * (d.v1 - d.v0), s));
+            if (!cu(cudaMemsetAsync(d.state, 0, sizeof(ull) * (d.v1 - d.v0), s), "memset state")) break;
             if (m) {
                 ProfScope ps("dist_build", s);
                 dist_build_kernel<R><<<dgrid(m), DB, 0, s>>>(edges, n, m, d.v0, d.v1, d.state, d.ctl);
@@ -540,43 +535,44 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         ProfScope ps("dist_scan", s);
         dist_scan_kernel<<<dgrid(d.v1 - d.v0), DB, 0, s>>>(d.state, d.v0, d.v1 - d.v0, k, d.F[1], d.ctl);
     }
-    PEEL_CUDA(cudaGetLastError());
+    cu(cudaGetLastError(), "build launch");
+    if (lst != PEEL_OK && c->virt) return lst;
 
-    // host-side views of the per-shard control blocks
-    std::vector<DCtl> hc(sh.size());
-    auto fetch_ctl = [&]() -> peel_status {
-        for (size_t i = 0; i < sh.size(); i++)
-            PEEL_CUDA(cudaMemcpyAsync(&hc[i], sh[i].ctl, sizeof(DCtl), cudaMemcpyDeviceToHost, s));
-        PEEL_CUDA(cudaStreamSynchronize(s));
-        return PEEL_OK;
-    };
-    // global sums of (|F|, kills, err) over all shards/ranks
-    ull *dsum = (ull *)(ws + L.scratch);  // device staging for the NCCL collectives (3 words)
-    auto global_sums = [&](int par, ull out[3]) -> peel_status {
-        peel_status st = fetch_ctl();
-        if (st != PEEL_OK) return st;
-        ull loc[3] = {0, 0, 0};
-        for (auto &h : hc) { loc[0] += h.nf[par]; loc[1] += h.kills; loc[2] |= h.err; }
-        if (c->virt) {
-            memcpy(out, loc, sizeof loc);
-            return PEEL_OK;
+    // end-of-round words: g[0] = |F_{t+1}|, g[1] = kills, g[2] = bad-vertex bits, g[3] =
+    // failed ranks (all global); ne[i] = shard i's frontier entries (local).  ONE stream sync
+    // (virtual: the shards' words summed on the host; ranks: one allreduce).
+    std::vector<ull> ne(sh.size(), 0), pk(5 * sh.size());
+    auto end_round = [&](int par, ull g[4]) -> peel_status {
+        if (lst != PEEL_OK) mark_fail();
+        for (size_t i = 0; i < sh.size(); i++) dist_pack_kernel<<<1, 1, 0, s>>>(sh[i].ctl, par, dsum + 8 + 5 * i);
+        if (!c->virt && !c->host) {  // NCCL: reduce the device words in place, one copy back
+            cudaMemcpyAsync(dsum, dsum + 8, sizeof(ull) * 4, cudaMemcpyDeviceToDevice, s);
+            ncclResult_t nr = ncclAllReduce(dsum, dsum, 4, ncclUint64, ncclSum, c->nccl, s);
+            if (nr != ncclSuccess) { nccl_error(nr); return PEEL_ENCCL; }
+            cudaMemcpyAsync(g, dsum, sizeof(ull) * 4, cudaMemcpyDeviceToHost, s);
         }
-        PEEL_CUDA(cudaMemcpyAsync(dsum, loc, sizeof loc, cudaMemcpyHostToDevice, s));
-        PEEL_NCCL(ncclAllReduce(dsum, dsum, 3, ncclUint64, ncclSum, c->nccl, s));
-        PEEL_CUDA(cudaMemcpyAsync(out, dsum, sizeof loc, cudaMemcpyDeviceToHost, s));
-        PEEL_CUDA(cudaStreamSynchronize(s));
+        if (cudaMemcpyAsync(pk.data(), dsum + 8, sizeof(ull) * 5 * sh.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) {
+            cu(cudaGetLastError(), "end of round");
+            return lst;
+        }
+        for (size_t i = 0; i < sh.size(); i++) ne[i] = pk[5 * i + 4];
+        if (!c->virt && !c->host) return PEEL_OK;
+        g[0] = g[1] = g[2] = g[3] = 0;
+        for (size_t i = 0; i < sh.size(); i++) {
+            g[0] += pk[5 * i]; g[1] += pk[5 * i + 1]; g[2] |= pk[5 * i + 2]; g[3] += pk[5 * i + 3];
+        }
+        if (lst != PEEL_OK) g[3] = 1;
+        if (c->host) return comm_allreduce_sum(c, g, 4, dsum, s);
         return PEEL_OK;
     };
 
-    ull g[3];
-    peel_status st = global_sums(1, g);
-    if (st != PEEL_OK) return st;
+    ull g[4];
+    if (!step(end_round(1, g)) || g[3]) return leave(g[3] != 0);
     if (g[2]) return PEEL_EINVAL;
     uint64_t alive_v = n;
     uint32_t t = 0;
-    std::vector<ull> cnt_mat((size_t)P * P);
-    std::vector<ull> loc_cnt(P);
-    ull *dcnt = dsum + 4;  // P x P count matrix
+    std::vector<ull> cnt_mat((size_t)P * P), rows((size_t)P * 9);
     while (g[0] > 0) {
         t++;
         alive_v -= g[0];
@@ -584,39 +580,41 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             if (survivors) survivors[t - 1] = alive_v;
         }
         const int cur = t & 1, nxt = cur ^ 1;  // round t's entries live at parity (t&1): round 1 uses F[1]
-        // reset next-round counters and per-destination queues
-        for (auto &d : sh) {
-            PEEL_CUDA(cudaMemsetAsync(&d.ctl->nf[nxt], 0, sizeof(ull), s));
-            PEEL_CUDA(cudaMemsetAsync(&d.ctl->ne[nxt], 0, sizeof(ull), s));
-            PEEL_CUDA(cudaMemsetAsync(&d.ctl->kills, 0, sizeof(ull) * 9, s));  // kills + nsend[8]
+        if (comm_fault(c, t) && lst == PEEL_OK) {
+            set_cuda_error(cudaErrorUnknown, "PEEL_FAULT injected failure");
+            lst = PEEL_ECUDA;
         }
-        st = fetch_ctl();
-        if (st != PEEL_OK) return st;
+        // reset next-round counters and per-destination queues (ne[] came with the last sums)
+        for (auto &d : sh) {
+            cu(cudaMemsetAsync(&d.ctl->nf[nxt], 0, sizeof(ull), s), "memset nf");
+            cu(cudaMemsetAsync(&d.ctl->ne[nxt], 0, sizeof(ull), s), "memset ne");
+            cu(cudaMemsetAsync(&d.ctl->kills, 0, sizeof(ull) * 9, s), "memset kills");  // kills + nsend[8]
+        }
         // kill: binned (decrements staged in the shard's bins) while the local frontier is large
         std::vector<char> binr(sh.size(), 0);
-        for (size_t i = 0; i < sh.size(); i++) {
+        for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
             DShard &d = sh[i];
             DKArgs a;
             a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
             a.edges_vec = ((uintptr_t)edges & 15) == 0;
             a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
             a.state = d.state; a.alive = d.alive;
-            a.Fc = d.F[cur]; a.nE = hc[i].ne[cur]; a.Fn = d.F[nxt];
+            a.Fc = d.F[cur]; a.nE = ne[i]; a.Fn = d.F[nxt];
             a.send = d.send; a.ctl = d.ctl; a.par = nxt;
             binr[i] = d.binned && (double)a.nE >= dist_bin_frac(d.v1 - d.v0) * (double)(d.v1 - d.v0);
             if (binr[i]) {
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
                 // sort the local frontier by edge bin into the next-round buffer (free until
                 // shard_apply writes F_{t+1} there)
-                peel_status st3 = shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s);
-                if (st3 != PEEL_OK) return st3;
+                if (!step(shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s))) break;
                 a.Fc = d.F[nxt];
-                PEEL_CUDA(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s));
+                cu(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s), "memset cursor");
                 const size_t sm = dist_stage_smem(R, bv.nbins);
-                PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
+                cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "attr");
+                cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 72), "attr");
                 int kb = 0;
-                PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, false>, DB, sm));
+                cu(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, false>, DB, sm), "occupancy");
+                if (lst != PEEL_OK) break;
                 ProfScope ps("dist_kill_binned", s);
                 dist_kill_bin_kernel<R, false><<<num_sms() * (kb < 1 ? 1 : kb), DB, sm, s>>>(a, nullptr, 0, bv);
             } else {
@@ -624,20 +622,57 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 dist_kill_kernel<R><<<dgrid(a.nE), DB, 0, s>>>(a);
             }
         }
-        PEEL_CUDA(cudaGetLastError());
-        st = fetch_ctl();
-        if (st != PEEL_OK) return st;
-        // exchange: counts matrix cnt_mat[src * P + dst]
+        cu(cudaGetLastError(), "kill launch");
+        // count exchange: cnt_mat[src * P + dst], plus every rank's failure word -- ONE sync
+        // (virtual: the shards' rows; ranks: one allgather of the 9-word rows nsend[8], fail)
+        if (lst != PEEL_OK) mark_fail();
+        bool peer_failed = false;
         if (c->virt) {
-            for (int q = 0; q < P; q++)
-                for (int d = 0; d < P; d++) cnt_mat[(size_t)q * P + d] = hc[q].nsend[d];
+            for (size_t i = 0; i < sh.size(); i++)
+                cu(cudaMemcpyAsync(&rows[(size_t)sh[i].q * 9], sh[i].ctl->nsend, sizeof(ull) * 9, cudaMemcpyDeviceToHost, s), "rows");
+            cu(cudaStreamSynchronize(s), "sync");
+            if (lst != PEEL_OK) return lst;
         } else {
-            for (int d = 0; d < P; d++) loc_cnt[d] = hc[0].nsend[d];
-            PEEL_CUDA(cudaMemcpyAsync(dcnt + (size_t)c->rank * P, loc_cnt.data(), sizeof(ull) * P,
-                                      cudaMemcpyHostToDevice, s));
-            PEEL_NCCL(ncclAllGather(dcnt + (size_t)c->rank * P, dcnt, P, ncclUint64, c->nccl, s));
-            PEEL_CUDA(cudaMemcpyAsync(cnt_mat.data(), dcnt, sizeof(ull) * P * P, cudaMemcpyDeviceToHost, s));
-            PEEL_CUDA(cudaStreamSynchronize(s));
+            if (!cu(cudaMemcpyAsync(dsum + 8 + 9 * c->rank, sh[0].ctl->nsend, sizeof(ull) * 9, cudaMemcpyDeviceToDevice, s), "rows")) {
+                // the local row cannot be staged: still take part, with the failure word only
+                std::vector<ull> fr(9, 0);
+                fr[8] = 1;
+                cudaMemcpyAsync(dsum + 8 + 9 * c->rank, fr.data(), sizeof(ull) * 9, cudaMemcpyHostToDevice, s);
+            }
+            peel_status sg;
+            if (c->host) {
+                std::vector<ull> mine(9);
+                if (cudaMemcpyAsync(mine.data(), dsum + 8 + 9 * c->rank, sizeof(ull) * 9, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                    cudaStreamSynchronize(s) != cudaSuccess) {
+                    cu(cudaGetLastError(), "rows");
+                    mine.assign(9, 0);
+                }
+                if (lst != PEEL_OK) mine[8] = 1;
+                sg = comm_allgather_u64(c, mine.data(), rows.data(), 9, dsum + 8, s);
+            } else {
+                // NCCL: gather the device rows in place, then one copy back
+                sg = PEEL_OK;
+                ncclResult_t nr = ncclAllGather(dsum + 8 + 9 * c->rank, dsum + 8, 9, ncclUint64, c->nccl, s);
+                if (nr != ncclSuccess) { nccl_error(nr); sg = PEEL_ENCCL; }
+                if (sg == PEEL_OK && (cudaMemcpyAsync(rows.data(), dsum + 8, sizeof(ull) * 9 * P, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+                                      cudaStreamSynchronize(s) != cudaSuccess)) {
+                    cu(cudaGetLastError(), "rows");
+                    sg = PEEL_ECUDA;
+                }
+            }
+            if (sg != PEEL_OK) return lst != PEEL_OK ? lst : sg;  // the transport itself failed
+            for (int q = 0; q < P; q++) peer_failed |= rows[(size_t)q * 9 + 8] != 0;
+            if (lst != PEEL_OK || peer_failed) return leave(peer_failed);
+        }
+        for (int q = 0; q < P; q++)
+            for (int d = 0; d < P; d++) cnt_mat[(size_t)q * P + d] = rows[(size_t)q * 9 + d];
+        // capacity: checked for EVERY receiver from the gathered matrix, so all ranks agree and
+        // leave together (never from inside an open transport group)
+        for (int dst = 0; dst < P; dst++) {
+            ull tot = 0;
+            for (int src = 0; src < P; src++)
+                if (src != dst) tot += cnt_mat[(size_t)src * P + dst];
+            if (tot > n) return PEEL_ENOMEM;
         }
         // payload: shard dst receives, from each src != dst, cnt[src][dst] ids into recv at running offsets
         std::vector<ull> nrecv(sh.size(), 0);
@@ -647,37 +682,30 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 for (int src = 0; src < P; src++) {
                     if (src == dst) continue;
                     ull cntv = cnt_mat[(size_t)src * P + dst];
-                    if (off + cntv > n) return PEEL_ENOMEM;
                     if (cntv)
-                        PEEL_CUDA(cudaMemcpyAsync(sh[dst].recv + off, sh[src].send + (uint64_t)dst * nl_max,
-                                                  sizeof(uint32_t) * cntv, cudaMemcpyDeviceToDevice, s));
+                        cu(cudaMemcpyAsync(sh[dst].recv + off, sh[src].send + (uint64_t)dst * nl_max,
+                                           sizeof(uint32_t) * cntv, cudaMemcpyDeviceToDevice, s), "virtual exchange");
                     off += cntv;
                 }
                 nrecv[dst] = off;
             }
         } else {
             const int me = c->rank;
-            PEEL_NCCL(ncclGroupStart());
+            std::vector<const char *> sp(P);
+            std::vector<ull> sb(P), rb(P);
             ull off = 0;
-            for (int src = 0; src < P; src++) {
-                if (src == me) continue;
-                ull cin = cnt_mat[(size_t)src * P + me];
-                if (off + cin > n) { ncclGroupEnd(); return PEEL_ENOMEM; }
-                if (cin) PEEL_NCCL(ncclRecv(sh[0].recv + off, cin * sizeof(uint32_t), ncclUint8, src, c->nccl, s));
-                off += cin;
+            for (int q = 0; q < P; q++) {
+                sp[q] = (const char *)(sh[0].send + (uint64_t)q * nl_max);
+                sb[q] = q == me ? 0 : sizeof(uint32_t) * cnt_mat[(size_t)me * P + q];
+                rb[q] = q == me ? 0 : sizeof(uint32_t) * cnt_mat[(size_t)q * P + me];
+                off += rb[q] / sizeof(uint32_t);
             }
-            for (int dst = 0; dst < P; dst++) {
-                if (dst == me) continue;
-                ull cout = cnt_mat[(size_t)me * P + dst];
-                if (cout)
-                    PEEL_NCCL(ncclSend(sh[0].send + (uint64_t)dst * nl_max, cout * sizeof(uint32_t), ncclUint8, dst,
-                                       c->nccl, s));
-            }
-            PEEL_NCCL(ncclGroupEnd());
+            peel_status sx = comm_alltoallv(c, sp.data(), sb.data(), (char *)sh[0].recv, rb.data(), s);
+            if (sx != PEEL_OK) return sx;  // the transport failed (every rank sees its own error)
             nrecv[0] = off;
         }
         // receive (binned shards stage the received kills, then apply the round's bins)
-        for (size_t i = 0; i < sh.size(); i++) {
+        for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
             DShard &d = sh[i];
             DKArgs a;
             a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
@@ -690,24 +718,24 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
                 if (nrecv[i]) {
                     const size_t sm = dist_stage_smem(R, bv.nbins);
-                    PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                    PEEL_CUDA(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
+                    cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "attr");
+                    cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 72), "attr");
                     int kb = 0;
-                    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, true>, DB, sm));
+                    cu(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, true>, DB, sm), "occupancy");
+                    if (lst != PEEL_OK) break;
                     ProfScope ps("dist_recv_binned", s);
                     dist_kill_bin_kernel<R, true><<<num_sms() * (kb < 1 ? 1 : kb), DB, sm, s>>>(a, d.recv, nrecv[i], bv);
                 }
-                peel_status st2 = shard_apply(d.v1 - d.v0, d.v0, k, d.state, d.F[nxt], bv, t, &d.ctl->nf[nxt], &d.ctl->ne[nxt], s);
-                if (st2 != PEEL_OK) return st2;
+                step(shard_apply(d.v1 - d.v0, d.v0, k, d.state, d.F[nxt], bv, t, &d.ctl->nf[nxt], &d.ctl->ne[nxt], s));
                 continue;
             }
             if (!nrecv[i]) continue;
             ProfScope ps("dist_recv", s);
             dist_recv_kernel<R><<<dgrid(nrecv[i]), DB, 0, s>>>(a, d.recv, nrecv[i]);
         }
-        PEEL_CUDA(cudaGetLastError());
-        st = global_sums(nxt, g);
-        if (st != PEEL_OK) return st;
+        cu(cudaGetLastError(), "receive launch");
+        if (lst != PEEL_OK && c->virt) return lst;
+        if (!step(end_round(nxt, g)) || g[3]) return leave(g[3] != 0);
         if (t <= cap && killed) killed[t - 1] = g[1];
     }
     *rounds = t;
@@ -726,11 +754,15 @@ extern "C" peel_status peel_kcore_dist(peel_comm *c, const uint32_t *edges, uint
                                        uint32_t k, uint8_t *core_mask, uint32_t *rounds, uint64_t *survivors,
                                        uint64_t *killed, uint32_t cap, void *workspace, size_t ws_bytes,
                                        void *stream) {
-    size_t need = peel_kcore_dist_workspace_bytes(c, n, m, r, k);
-    if (!need || !rounds || !workspace || (m && !edges) || !core_mask) return PEEL_EINVAL;
-    if (ws_bytes < need) return PEEL_ENOMEM;
-    prof_begin_call();
+    if (!c) return PEEL_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
+    size_t need = peel_kcore_dist_workspace_bytes(c, n, m, r, k);
+    peel_status v = PEEL_OK;
+    if (!need || !rounds || !workspace || (m && !edges) || !core_mask) v = PEEL_EINVAL;
+    else if (ws_bytes < need) v = PEEL_ENOMEM;
+    v = comm_agree(c, v, s);  // every rank leaves together if any rank rejects its arguments
+    if (v != PEEL_OK) return v;
+    prof_begin_call();
     char *ws = (char *)workspace;
     switch (r) {
         case 2: return run_dist<2>(c, edges, n, m, k, core_mask, rounds, survivors, killed, cap, ws, s);

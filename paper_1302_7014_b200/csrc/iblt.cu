@@ -42,7 +42,7 @@ struct IbltCtl {
     ull rounds;
     ull scnt[16];  // subtable mode: list lengths [subtable j][round parity b] at j * 2 + b
     uint32_t nonzero;
-    uint32_t pad;
+    uint32_t trunc;  // the round limit (ISTAT_CAP rounds / subtable steps) stopped recovery
 };
 
 struct ILayout {
@@ -122,13 +122,15 @@ struct IPeelArgs {
 };
 
 
-// signed tables (set difference): pure = count +1 or -1 with a matching checksum; returns
-// +1 / -1, or 0 if not pure.  Unsigned recovery accepts only count == +1.
-template <bool SIGNED>
-__device__ __forceinline__ int pure_sign(const Cell &c, ull seed_c) {
-    const bool cnt = SIGNED ? (c.count == 1u || c.count == 0xFFFFFFFFu) : (c.count == 1u);
-    if (!cnt || c.hashSum != checksum(c.keySum, seed_c)) return 0;
-    return c.count == 1u ? 1 : -1;
+// signed tables (set difference): pure = count +1 or -1 with a matching checksum, and cell c
+// is one of the key's cells (R26, R28); returns +1 / -1, or 0 if not pure.  Unsigned recovery
+// accepts only count == +1.
+template <int R, bool SIGNED>
+__device__ __forceinline__ int pure_sign(const Cell &v, uint32_t c, const IPeelArgs &a) {
+    const bool cnt = SIGNED ? (v.count == 1u || v.count == 0xFFFFFFFFu) : (v.count == 1u);
+    if (!cnt || v.hashSum != checksum(v.keySum, a.seed_c)) return 0;
+    if (!cell_of_key<R>(c, v.keySum, a.C, a.seed_h, a.subt, a.blog)) return 0;
+    return v.count == 1u ? 1 : -1;
 }
 
 // w[0, nwords) = 0 over the whole grid (w is 256-byte aligned: 16-byte stores, then the tail)
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(IB_BLOCK, 5) iblt_peel_kernel(IPeelArgs a) {
         const ull c = base + threadIdx.x;
         if (c < a.C) {
             Cell v = ld_cell_cg(a.cells + c);
-            const int sg = pure_sign<SIGNED>(v, a.seed_c);
+            const int sg = pure_sign<R, SIGNED>(v, (uint32_t)c, a);
             if (sg) {
                 bq_push(qe, slot, make_ulonglong2(c | ((ull)(sg < 0) << 32), v.keySum), a.F[0], &ctl->fcnt[0]);
                 atomicOr(a.pure[0] + (c >> 5), 1u << (c & 31));
@@ -185,6 +187,10 @@ __global__ void __launch_bounds__(IB_BLOCK, 5) iblt_peel_kernel(IPeelArgs a) {
     for (;;) {
         const ull nF = ld_cg_u64(&ctl->fcnt[(t - 1) % 3]);
         if (nF == 0) break;
+        if (t > ISTAT_CAP) {  // round limit (R28: forged signed tables can cycle)
+            if (tid == 0) ctl->trunc = 1u;
+            break;
+        }
         if (tid == 0) {
             ctl->fcnt[(t + 1) % 3] = 0;
             if (t <= ISTAT_CAP) a.rtime[t - 1] = globaltimer();
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(IB_BLOCK, 5) iblt_peel_kernel(IPeelArgs a) {
                 const uint32_t c = ld_cg_u32(a.clist + i);
                 if (!cand_bulk) atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
                 Cell v = ld_cell_cg(a.cells + c);
-                const int sg = pure_sign<SIGNED>(v, a.seed_c);
+                const int sg = pure_sign<R, SIGNED>(v, c, a);
                 if (sg) {
                     bq_push(qe, slot, make_ulonglong2(c | ((ull)(sg < 0) << 32), v.keySum), Fn, fn);
                     atomicOr(pure_next + (c >> 5), 1u << (c & 31));
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_subtable_peel_kernel(IPeelArgs 
         bool p = false;
         if (c < a.C) {
             Cell v = ld_cell_cg(a.cells + c);
-            p = is_pure(v, a.seed_c);
+            p = is_pure(v, a.seed_c) && cell_of_key<R>((uint32_t)c, v.keySum, a.C, a.seed_h, true, 0u);
             if (p) atomicOr(a.cand + (c >> 5), 1u << (c & 31));
         }
         const uint32_t jc = (uint32_t)(c / cs);
@@ -349,6 +355,10 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_subtable_peel_kernel(IPeelArgs 
     for (uint32_t i = 0;; i++) {
         bool any = false;
         const uint32_t b = i & 1u;
+        if (flat + (uint32_t)R > ISTAT_CAP) {  // step limit, as the oracle's
+            if (tid == 0) ctl->trunc = 1u;
+            break;
+        }
         #pragma unroll 1
         for (uint32_t j = 0; j < (uint32_t)R; j++) {
             flat++;
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(IB_BLOCK) iblt_subtable_peel_kernel(IPeelArgs 
                     const uint32_t c = ld_cg_u32(Lc + q);
                     atomicAnd(a.cand + (c >> 5), ~(1u << (c & 31)));
                     Cell v = ld_cell_cg(a.cells + c);
-                    if (is_pure(v, a.seed_c)) {
+                    if (is_pure(v, a.seed_c) && cell_of_key<R>(c, v.keySum, a.C, a.seed_h, true, 0u)) {
                         x = v.keySum;
                         recovered++;
                         bq_push(qk, slot, x, a.out, &ctl->nrec);
@@ -606,7 +616,7 @@ static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_
     if (nstore > ISTAT_CAP) nstore = ISTAT_CAP;
     if (per_round && nstore)
         PEEL_CUDA(cudaMemcpy(per_round, a.per_round, sizeof(ull) * nstore, cudaMemcpyDeviceToHost));
-    if (h.nrec > cap_keys || h.rounds > cap || h.rounds > ISTAT_CAP) return PEEL_ETRUNC;
+    if (h.nrec > cap_keys || h.rounds > cap || h.rounds > ISTAT_CAP || h.trunc) return PEEL_ETRUNC;
     return PEEL_OK;
 }
 

@@ -68,4 +68,19 @@ __device__ __forceinline__ bool is_pure(const Cell &c, ull seed_c) {
     return c.count == 1u && c.hashSum == checksum(c.keySum, seed_c);
 }
 
+// DESIGN.md R28 ("cells that only contain one item"): a cell holding one item x is one
+// of x's own cells, so purity also requires cell id c in h(keySum) -- a cell whose count and
+// checksum say "pure" but whose key does not hash to it (a checksum collision, a forged or
+// corrupted table) holds several items and is never recovered.  The hashes are computed only
+// for cells that passed the count and checksum tests.
+template <int R>
+__device__ __forceinline__ bool cell_of_key(uint32_t c, ull x, ull C, ull seed_h, bool subt, uint32_t blog) {
+    uint32_t h[R];
+    key_cells<R>(x, C, seed_h, subt, h, blog);
+    bool in = false;
+    #pragma unroll
+    for (int j = 0; j < R; j++) in |= h[j] == c;
+    return in;
+}
+
 }  // namespace peel

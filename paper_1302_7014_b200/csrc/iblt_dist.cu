@@ -59,7 +59,7 @@ static IDLayout id_layout(uint64_t C, int P) {
     size_t o = 0;
     L.pure = o; o += ial(sizeof(uint32_t) * (P * cs / 32));
     L.outcnt = o; o += ial(sizeof(ull));
-    L.scratch = o; o += ial(sizeof(ull) * (4 + 64));
+    L.scratch = o; o += ial(sizeof(ull) * (4 + 9 * 8));
     L.common = o;
     o = 0;
     L.ctl = o; o += ial(sizeof(IDCtl));
@@ -117,7 +117,14 @@ __global__ void __launch_bounds__(IDB) idist_insert_kernel(IDArgs a, const ull *
     }
 }
 
+// pure (R28): count 1, matching checksum, and c (global id) is one of the key's cells
+template <int R>
+__device__ __forceinline__ bool id_pure(const Cell &v, uint32_t c, const IDArgs &a) {
+    return is_pure(v, a.seed_c) && cell_of_key<R>(c, v.keySum, a.C, a.seed_h, false, a.blog);
+}
+
 // round 1: the shard's pure cells -> frontier entries and pure bits
+template <int R>
 __global__ void __launch_bounds__(IDB) idist_scan_kernel(IDArgs a) {
     __shared__ IDEntQ q;
     bq_init(q);
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(IDB) idist_scan_kernel(IDArgs a) {
         const ull l = base + threadIdx.x;
         if (l < a.ncl) {
             const Cell v = ld_cell_cg(a.cells + l);
-            if (is_pure(v, a.seed_c)) {
+            if (id_pure<R>(v, a.c0 + (uint32_t)l, a)) {
                 const uint32_t c = a.c0 + (uint32_t)l;
                 bq_push(q, slot, make_ulonglong2(c, v.keySum), a.Fn, cnt);
                 atomicOr(a.pure + (c >> 5), 1u << (c & 31));
@@ -237,6 +244,7 @@ __global__ void __launch_bounds__(IDB) idist_clear_kernel(IDArgs a) {
 }
 
 // retest: candidates still pure -> the next local frontier and pure bits
+template <int R>
 __global__ void __launch_bounds__(IDB) idist_retest_kernel(IDArgs a) {
     __shared__ IDEntQ q;
     bq_init(q);
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(IDB) idist_retest_kernel(IDArgs a) {
             const uint32_t l = __ldcg(a.clist + i);
             atomicAnd(a.cand + (l >> 5), ~(1u << (l & 31)));
             const Cell v = ld_cell_cg(a.cells + l);
-            if (is_pure(v, a.seed_c)) {
+            if (id_pure<R>(v, a.c0 + l, a)) {
                 const uint32_t c = a.c0 + l;
                 bq_push(q, slot, make_ulonglong2(c, v.keySum), a.Fn, cnt);
                 atomicOr(a.pure + (c >> 5), 1u << (c & 31));
@@ -290,9 +298,9 @@ struct IDShard {
 
 template <int R>
 static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32_t blog, const uint64_t *keys,
-                                 uint64_t nkeys, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,
-                                 uint32_t *rounds, uint64_t *per_round, uint32_t cap, int *complete, char *mem,
-                                 cudaStream_t s) {
+                                 uint64_t nkeys, const Cell *cells_in, uint64_t *out_keys, uint64_t cap_keys,
+                                 uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
+                                 int *complete, char *mem, cudaStream_t s) {
     const int P = c->P;
     const uint64_t cs = id_cs(C, P);
     const IDLayout L = id_layout(C, P);
@@ -339,123 +347,153 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
         a.par = cur ^ 1;
         return a;
     };
+    // error protocol as dist.cu's (peel.h "Errors"): local failures are carried in the
+    // failure words of the collectives, every rank leaves at the same one
+    peel_status lst = PEEL_OK;
+    auto cu = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && lst == PEEL_OK) {
+            set_cuda_error(e, what);
+            lst = PEEL_ECUDA;
+        }
+        return lst == PEEL_OK;
+    };
     // zero the common area and every local shard's control block, cells and candidate bits
-    PEEL_CUDA(cudaMemsetAsync(mem, 0, L.common, s));
+    cu(cudaMemsetAsync(mem, 0, L.common, s), "memset");
     for (auto &d : sh) {
-        PEEL_CUDA(cudaMemsetAsync(d.base, 0, L.F0, s));  // ctl, cells, cand
-        IDArgs a = args(d, 1);                            // round 1's frontier goes to F[0]
-        if (nkeys) {
+        if (!cu(cudaMemsetAsync(d.base, 0, L.F0, s), "memset")) break;  // ctl, cells, cand
+        IDArgs a = args(d, 1);                                          // round 1's frontier goes to F[0]
+        if (cells_in) {
+            if (!cu(cudaMemcpyAsync(a.cells, cells_in + d.c0, sizeof(Cell) * d.ncl, cudaMemcpyDeviceToDevice, s), "cells_in"))
+                break;
+        } else if (nkeys) {
             ProfScope ps("iblt_dist_insert", s);
             idist_insert_kernel<R><<<idgrid(nkeys), IDB, 0, s>>>(a, (const ull *)keys, nkeys);
         }
         ProfScope ps("iblt_dist_scan", s);
-        idist_scan_kernel<<<idgrid(d.ncl), IDB, 0, s>>>(a);
+        idist_scan_kernel<R><<<idgrid(d.ncl), IDB, 0, s>>>(a);
     }
-    PEEL_CUDA(cudaGetLastError());
+    cu(cudaGetLastError(), "build launch");
+    if (lst != PEEL_OK && c->virt) return lst;
 
     std::vector<IDCtl> hc(sh.size());
-    auto fetch = [&]() -> peel_status {
+    auto fetch = [&]() {
         for (size_t i = 0; i < sh.size(); i++)
-            PEEL_CUDA(cudaMemcpyAsync(&hc[i], sh[i].ctl, sizeof(IDCtl), cudaMemcpyDeviceToHost, s));
-        PEEL_CUDA(cudaStreamSynchronize(s));
-        return PEEL_OK;
+            cu(cudaMemcpyAsync(&hc[i], sh[i].ctl, sizeof(IDCtl), cudaMemcpyDeviceToHost, s), "fetch");
+        cu(cudaStreamSynchronize(s), "fetch");
     };
-    // global sums over shards / ranks of (v0, v1)
-    auto gsum = [&](ull v0, ull v1, ull out[2]) -> peel_status {
-        if (c->virt) {
-            out[0] = v0;
-            out[1] = v1;
-            return PEEL_OK;
-        }
-        ull loc[2] = {v0, v1};
-        PEEL_CUDA(cudaMemcpyAsync(dsum, loc, sizeof loc, cudaMemcpyHostToDevice, s));
-        PEEL_NCCL(ncclAllReduce(dsum, dsum, 2, ncclUint64, ncclSum, c->nccl, s));
-        PEEL_CUDA(cudaMemcpyAsync(out, dsum, sizeof loc, cudaMemcpyDeviceToHost, s));
-        PEEL_CUDA(cudaStreamSynchronize(s));
-        return PEEL_OK;
+    // global sums over shards / ranks of (v0, v1) and the failure word: out[2] = failed ranks
+    auto gsum = [&](ull v0, ull v1, ull out[3]) -> peel_status {
+        out[0] = v0;
+        out[1] = v1;
+        out[2] = lst != PEEL_OK ? 1 : 0;
+        if (c->virt) return PEEL_OK;
+        return comm_allreduce_sum(c, out, 3, dsum, s);
     };
-    peel_status st = fetch();
-    if (st != PEEL_OK) return st;
-    ull g[2];
+    auto leave = [&](bool peer_failed) -> peel_status {
+        if (lst != PEEL_OK) return lst;
+        return peer_failed ? PEEL_EPEER : PEEL_OK;
+    };
+    fetch();
+    if (lst != PEEL_OK && c->virt) return lst;
+    ull g[3];
     {
         ull f = 0;
         for (auto &h : hc) f += h.fcnt[0];
-        st = gsum(f, 0, g);
+        peel_status st = gsum(f, 0, g);
         if (st != PEEL_OK) return st;
+        if (g[2]) return leave(true);
     }
     uint32_t t = 0;
-    std::vector<ull> cnt_mat((size_t)P * P), loc_cnt(P);
-    ull *dcnt = dsum + 4;
+    std::vector<ull> cnt_mat((size_t)P * P), rows((size_t)P * (P + 1));
+    bool trunc = false;
     while (g[0] > 0) {
+        if (t == 65536u) {  // round limit, as iblt_peel's (R28: forged signed tables can cycle)
+            trunc = true;
+            break;
+        }
         t++;
         const int cur = (t - 1) & 1;  // round t's frontier: F[(t-1) & 1]
-        for (auto &d : sh) {
-            PEEL_CUDA(cudaMemsetAsync(&d.ctl->fcnt[cur ^ 1], 0, sizeof(ull), s));
-            PEEL_CUDA(cudaMemsetAsync(&d.ctl->ccnt, 0, sizeof(ull) * 10, s));  // ccnt, nsend[8], found
+        if (comm_fault(c, t) && lst == PEEL_OK) {
+            set_cuda_error(cudaErrorUnknown, "PEEL_FAULT injected failure");
+            lst = PEEL_ECUDA;
         }
-        // pure bits of every shard (NCCL: in-place allgather of the slices)
-        if (!c->virt)
-            PEEL_NCCL(ncclAllGather(pure + (size_t)c->rank * (cs / 32), pure, cs / 32 * sizeof(uint32_t), ncclUint8,
-                                    c->nccl, s));
+        for (auto &d : sh) {
+            cu(cudaMemsetAsync(&d.ctl->fcnt[cur ^ 1], 0, sizeof(ull), s), "memset");
+            cu(cudaMemsetAsync(&d.ctl->ccnt, 0, sizeof(ull) * 10, s), "memset");  // ccnt, nsend[8], found
+        }
+        // pure bits of every shard (ranks: in-place allgather of the slices)
+        if (!c->virt) {
+            peel_status sg = comm_allgather_dev(c, pure + (size_t)c->rank * (cs / 32), pure, cs / 32 * sizeof(uint32_t), s);
+            if (sg != PEEL_OK) return sg;
+        }
         // find (frontier sizes are read on the device: hc[] still holds them from the end of
         // the previous round, which sizes the grids)
-        for (size_t i = 0; i < sh.size(); i++) {
+        for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
             IDArgs a = args(sh[i], cur);
             const ull nF = hc[i].fcnt[cur];
             if (!nF) continue;
             ProfScope ps("iblt_dist_find", s);
             idist_find_kernel<R><<<idgrid(nF), IDB, 0, s>>>(a);
         }
-        PEEL_CUDA(cudaGetLastError());
-        st = fetch();
-        if (st != PEEL_OK) return st;
-        // exchange (self-delivery included): cnt_mat[src * P + dst]
+        cu(cudaGetLastError(), "find launch");
+        fetch();
+        if (lst != PEEL_OK && c->virt) return lst;
+        // exchange (self-delivery included): cnt_mat[src * P + dst]; every rank's row carries
+        // its failure word
         if (c->virt) {
             for (int q = 0; q < P; q++)
                 for (int d = 0; d < P; d++) cnt_mat[(size_t)q * P + d] = hc[q].nsend[d];
         } else {
-            for (int d = 0; d < P; d++) loc_cnt[d] = hc[0].nsend[d];
-            PEEL_CUDA(cudaMemcpyAsync(dcnt + (size_t)c->rank * P, loc_cnt.data(), sizeof(ull) * P, cudaMemcpyHostToDevice, s));
-            PEEL_NCCL(ncclAllGather(dcnt + (size_t)c->rank * P, dcnt, P, ncclUint64, c->nccl, s));
-            PEEL_CUDA(cudaMemcpyAsync(cnt_mat.data(), dcnt, sizeof(ull) * P * P, cudaMemcpyDeviceToHost, s));
-            PEEL_CUDA(cudaStreamSynchronize(s));
+            std::vector<ull> mine(P + 1, 0);
+            for (int d = 0; d < P; d++) mine[d] = hc[0].nsend[d];
+            mine[P] = lst != PEEL_OK ? 1 : 0;
+            peel_status sg = comm_allgather_u64(c, mine.data(), rows.data(), P + 1, dsum + 4, s);
+            if (sg != PEEL_OK) return lst != PEEL_OK ? lst : sg;
+            bool peer_failed = false;
+            for (int q = 0; q < P; q++) peer_failed |= rows[(size_t)q * (P + 1) + P] != 0;
+            if (lst != PEEL_OK || peer_failed) return leave(peer_failed);
+            for (int q = 0; q < P; q++)
+                for (int d = 0; d < P; d++) cnt_mat[(size_t)q * P + d] = rows[(size_t)q * (P + 1) + d];
         }
+        // capacity of every receiver, from the gathered matrix (all ranks agree)
+        for (int dst = 0; dst < P; dst++)
+            for (int src = 0; src < P; src++)
+                if (cnt_mat[(size_t)src * P + dst] > cs) return PEEL_ENOMEM;
         std::vector<ull> nrecv(sh.size(), 0);
         for (size_t i = 0; i < sh.size(); i++) {
             const int dst = sh[i].q;
             ull *recv = (ull *)(sh[i].base + L.recv);
+            // self-delivery (and every delivery between virtual shards) is a device copy, packed
+            // first; the other ranks' keys follow in increasing source rank
             ull off = 0;
-            if (!c->virt) PEEL_NCCL(ncclGroupStart());
             for (int src = 0; src < P; src++) {
+                if (!(c->virt || src == dst)) continue;
                 const ull cn = cnt_mat[(size_t)src * P + dst];
                 if (!cn) continue;
-                if (cn > cs) {
-                    if (!c->virt) ncclGroupEnd();
-                    return PEEL_ENOMEM;
-                }
-                if (c->virt || src == dst) {
-                    const char *sb = mem + L.common + (c->virt ? (size_t)src * L.shard : 0) + L.send;
-                    PEEL_CUDA(cudaMemcpyAsync(recv + off, (const ull *)sb + (size_t)dst * cs, sizeof(ull) * cn,
-                                              cudaMemcpyDeviceToDevice, s));
-                } else {
-                    PEEL_NCCL(ncclRecv(recv + off, cn * sizeof(ull), ncclUint8, src, c->nccl, s));
-                }
+                const char *sb = mem + L.common + (c->virt ? (size_t)src * L.shard : 0) + L.send;
+                cu(cudaMemcpyAsync(recv + off, (const ull *)sb + (size_t)dst * cs, sizeof(ull) * cn,
+                                   cudaMemcpyDeviceToDevice, s), "self delivery");
                 off += cn;
             }
             if (!c->virt) {
+                std::vector<const char *> sp(P);
+                std::vector<ull> sbytes(P), rbytes(P);
                 const ull *sb = (const ull *)(sh[i].base + L.send);
-                for (int d = 0; d < P; d++) {
-                    const ull cn = cnt_mat[(size_t)dst * P + d];
-                    if (cn && d != dst) PEEL_NCCL(ncclSend(sb + (size_t)d * cs, cn * sizeof(ull), ncclUint8, d, c->nccl, s));
+                for (int q = 0; q < P; q++) {
+                    sp[q] = (const char *)(sb + (size_t)q * cs);
+                    sbytes[q] = q == dst ? 0 : sizeof(ull) * cnt_mat[(size_t)dst * P + q];
+                    rbytes[q] = q == dst ? 0 : sizeof(ull) * cnt_mat[(size_t)q * P + dst];
                 }
-                PEEL_NCCL(ncclGroupEnd());
+                peel_status sx = comm_alltoallv(c, sp.data(), sbytes.data(), (char *)(recv + off), rbytes.data(), s);
+                if (sx != PEEL_OK) return sx;
+                for (int q = 0; q < P; q++) off += rbytes[q] / sizeof(ull);
             }
             nrecv[i] = off;
         }
         // apply, retire the round's pure bits, retest the candidates
         ull found = 0;
         for (auto &h : hc) found += h.found;
-        for (size_t i = 0; i < sh.size(); i++) {
+        for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
             IDArgs a = args(sh[i], cur);
             if (nrecv[i]) {
                 ProfScope ps("iblt_dist_apply", s);
@@ -463,20 +501,21 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
             }
         }
         ull nf = 0;
-        for (size_t i = 0; i < sh.size(); i++) {
+        for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
             IDArgs a = args(sh[i], cur);
             const ull nF = hc[i].fcnt[cur];
             ProfScope ps("iblt_dist_retest", s);
             if (nF) idist_clear_kernel<<<idgrid(nF), IDB, 0, s>>>(a);
             // candidates <= keys received x r (sized from the host's receive count)
-            idist_retest_kernel<<<idgrid(std::min<ull>(nrecv[i] * R, sh[i].ncl)), IDB, 0, s>>>(a);
+            idist_retest_kernel<R><<<idgrid(std::min<ull>(nrecv[i] * R, sh[i].ncl)), IDB, 0, s>>>(a);
         }
-        PEEL_CUDA(cudaGetLastError());
-        st = fetch();
-        if (st != PEEL_OK) return st;
+        cu(cudaGetLastError(), "apply launch");
+        fetch();
+        if (lst != PEEL_OK && c->virt) return lst;
         for (auto &h : hc) nf += h.fcnt[cur ^ 1];
-        st = gsum(nf, found, g);
+        peel_status st = gsum(nf, found, g);
         if (st != PEEL_OK) return st;
+        if (g[2]) return leave(true);
         if (t <= cap && per_round) per_round[t - 1] = g[1];
     }
     // completeness: every cell of every shard zero
@@ -485,20 +524,21 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
         ProfScope ps("iblt_dist_nonzero", s);
         idist_nonzero_kernel<<<idgrid(d.ncl), IDB, 0, s>>>(a);
     }
-    PEEL_CUDA(cudaGetLastError());
-    st = fetch();
-    if (st != PEEL_OK) return st;
+    cu(cudaGetLastError(), "nonzero launch");
+    fetch();
     ull nz = 0, nout = 0;
     for (auto &h : hc) nz |= h.nonzero;
-    PEEL_CUDA(cudaMemcpyAsync(&nout, outcnt, sizeof(ull), cudaMemcpyDeviceToHost, s));
-    PEEL_CUDA(cudaStreamSynchronize(s));
+    cu(cudaMemcpyAsync(&nout, outcnt, sizeof(ull), cudaMemcpyDeviceToHost, s), "outcnt");
+    cu(cudaStreamSynchronize(s), "sync");
     prof_collect();
-    st = gsum(nz ? 1 : 0, 0, g);
+    if (lst != PEEL_OK && c->virt) return lst;
+    peel_status st = gsum(nz ? 1 : 0, 0, g);
     if (st != PEEL_OK) return st;
+    if (g[2]) return leave(true);
     *rounds = t;
     *nrecovered = nout;
     if (complete) *complete = g[0] ? 0 : 1;
-    if (nout > cap_keys || t > cap) return PEEL_ETRUNC;
+    if (nout > cap_keys || t > cap || trunc) return PEEL_ETRUNC;
     return PEEL_OK;
 }
 
@@ -512,30 +552,53 @@ extern "C" size_t iblt_dist_mem_bytes(const peel_comm *c, uint64_t cells, uint32
     return L.common + (c->virt ? (size_t)c->P : 1) * L.shard;
 }
 
+static peel_status idist_entry(peel_comm *c, uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags,
+                               const uint64_t *keys, uint64_t nkeys, const void *cells_in, uint64_t *out_keys,
+                               uint64_t cap_keys, uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round,
+                               uint32_t cap, int *complete, void *mem, size_t mem_bytes, void *stream) {
+    if (!c) return PEEL_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t need = iblt_dist_mem_bytes(c, cells, r);
+    peel_status v = PEEL_OK;
+    uint32_t blog = 0;
+    if (!need || !nrecovered || !rounds || !mem || (nkeys && !keys) || (cap_keys && !out_keys)) v = PEEL_EINVAL;
+    else if (cells_in && ((uintptr_t)cells_in & 15)) v = PEEL_EINVAL;
+    else if (flags & ~(IBLT_FLAG_BLOCKED | (0xFFu << IBLT_BLOCK_LOG_SHIFT))) v = PEEL_EINVAL;  // no subtables / signed
+    else if (flags & IBLT_FLAG_BLOCKED) {
+        blog = IBLT_BLOCK_LOG(flags) ? IBLT_BLOCK_LOG(flags) : 16u;
+        if (blog < 4 || blog > 30 || cells % (1ull << blog) || (1ull << blog) < r) v = PEEL_EINVAL;
+    }
+    if (v == PEEL_OK && mem_bytes < need) v = PEEL_ENOMEM;
+    v = comm_agree(c, v, s);  // every rank leaves together if any rank rejects its arguments
+    if (v != PEEL_OK) return v;
+    prof_begin_call();
+    char *m = (char *)mem;
+    const Cell *ci = (const Cell *)cells_in;
+    switch (r) {
+        case 2: return run_iblt_dist<2>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+        case 3: return run_iblt_dist<3>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+        case 4: return run_iblt_dist<4>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+        case 5: return run_iblt_dist<5>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+        case 6: return run_iblt_dist<6>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+        case 7: return run_iblt_dist<7>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+        case 8: return run_iblt_dist<8>(c, cells, seed, blog, keys, nkeys, ci, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
+    }
+    return PEEL_EINVAL;
+}
+
 extern "C" peel_status iblt_dist_recover(peel_comm *c, uint64_t cells, uint32_t r, uint64_t seed, uint32_t flags,
                                          const uint64_t *keys, uint64_t nkeys, uint64_t *out_keys, uint64_t cap_keys,
                                          uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round, uint32_t cap,
                                          int *complete, void *mem, size_t mem_bytes, void *stream) {
-    const size_t need = iblt_dist_mem_bytes(c, cells, r);
-    if (!need || !nrecovered || !rounds || !mem || (nkeys && !keys) || (cap_keys && !out_keys)) return PEEL_EINVAL;
-    if (flags & ~(IBLT_FLAG_BLOCKED | (0xFFu << IBLT_BLOCK_LOG_SHIFT))) return PEEL_EINVAL;  // no subtables / signed
-    uint32_t blog = 0;
-    if (flags & IBLT_FLAG_BLOCKED) {
-        blog = IBLT_BLOCK_LOG(flags) ? IBLT_BLOCK_LOG(flags) : 16u;
-        if (blog < 4 || blog > 30 || cells % (1ull << blog) || (1ull << blog) < r) return PEEL_EINVAL;
-    }
-    if (mem_bytes < need) return PEEL_ENOMEM;
-    prof_begin_call();
-    cudaStream_t s = (cudaStream_t)stream;
-    char *m = (char *)mem;
-    switch (r) {
-        case 2: return run_iblt_dist<2>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-        case 3: return run_iblt_dist<3>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-        case 4: return run_iblt_dist<4>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-        case 5: return run_iblt_dist<5>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-        case 6: return run_iblt_dist<6>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-        case 7: return run_iblt_dist<7>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-        case 8: return run_iblt_dist<8>(c, cells, seed, blog, keys, nkeys, out_keys, cap_keys, nrecovered, rounds, per_round, cap, complete, m, s);
-    }
-    return PEEL_EINVAL;
+    return idist_entry(c, cells, r, seed, flags, keys, nkeys, nullptr, out_keys, cap_keys, nrecovered, rounds,
+                       per_round, cap, complete, mem, mem_bytes, stream);
+}
+
+extern "C" peel_status iblt_dist_recover_cells(peel_comm *c, const void *cells_in, uint64_t cells, uint32_t r,
+                                               uint64_t seed, uint32_t flags, uint64_t *out_keys, uint64_t cap_keys,
+                                               uint64_t *nrecovered, uint32_t *rounds, uint64_t *per_round,
+                                               uint32_t cap, int *complete, void *mem, size_t mem_bytes,
+                                               void *stream) {
+    return idist_entry(c, cells, r, seed, flags, nullptr, 0, cells_in, out_keys, cap_keys, nrecovered, rounds,
+                       per_round, cap, complete, mem, mem_bytes, stream);
 }

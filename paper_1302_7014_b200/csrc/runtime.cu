@@ -130,6 +130,7 @@ const char *peel_strerror(int s) {
         case PEEL_ETRUNC: return "PEEL_ETRUNC: more rounds/keys than the caller's capacity";
         case PEEL_ENCCL: return "PEEL_ENCCL: NCCL error";
         case PEEL_EOVERFLOW: return "PEEL_EOVERFLOW: packed state overflow; use PEEL_FLAG_CSR";
+        case PEEL_EPEER: return "PEEL_EPEER: another rank of the communicator failed";
         default: return "unknown peel_status";
     }
 }

@@ -14,6 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_functions():
     src = open(os.path.join(ROOT, "include", "peel.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    src = re.sub(r"^typedef[^;]*;", "", src, flags=re.M | re.S)  # callback typedefs
     names = re.findall(r"^[A-Za-z_][\w \*]*?\b([a-z_][a-z0-9_]*)\s*\(", src, flags=re.M)
     return sorted(set(n for n in names if n not in ("if", "while")))
 
@@ -32,8 +33,8 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_strerror():
     L = pk.lib()
-    assert L.peel_abi_version() == 1
-    for s in range(7):
+    assert L.peel_abi_version() == 2
+    for s in range(8):
         assert L.peel_strerror(s).decode().startswith("PEEL_")
 
 
@@ -89,3 +90,16 @@ def test_library_does_not_link_the_oracle():
     import subprocess
     out = subprocess.run(["nm", "-D", pk.LIB_PATH], capture_output=True, text=True).stdout
     assert "ora_" not in out
+
+
+def test_host_comm_validation():
+    L = pk.lib()
+    h = ctypes.c_void_p(0)
+    null = pk._AR_FN()  # NULL function pointers
+    assert L.peel_comm_init_host(2, 0, null, pk._AG_FN(), pk._A2A_FN(), None, ctypes.byref(h)) == pk.PEEL_EINVAL
+    ok = pk._AR_FN(lambda c, v, n: 0), pk._AG_FN(lambda c, s, r, b: 0), pk._A2A_FN(lambda c, s, sb, r, rb: 0)
+    assert L.peel_comm_init_host(2, 2, *ok, None, ctypes.byref(h)) == pk.PEEL_EINVAL  # rank >= nranks
+    assert L.peel_comm_init_host(9, 0, *ok, None, ctypes.byref(h)) == pk.PEEL_EINVAL  # P > 8
+    assert L.peel_comm_init_host(2, 1, *ok, None, ctypes.byref(h)) == pk.PEEL_OK
+    assert L.iblt_dist_mem_bytes(h, 3 * 4096, 3) > 0
+    L.peel_comm_destroy(h)

@@ -16,7 +16,7 @@ from peeltest_util import cells_to_dev_layout, forge_foreign_cells, forge_sign_c
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0")
 
-MODES = [("plain", 0), ("subtables", 0), ("blocked", 8)]
+MODES = [("plain", 0), ("subtables", 0), ("blocked", 10)]
 
 
 def dev_table(C, r, seed, mode, blog, cells):
@@ -40,7 +40,7 @@ def remaining(t):
 @pytest.mark.parametrize("r", [3, 4])
 def test_foreign_cells(mode, blog, r):
     C, seed = 4096 * r, 31 + r
-    keys = synth.random_keys(int(0.7 * C), 200 + r)
+    keys = synth.random_keys(int(0.6 * C), 200 + r)  # below the blocked threshold at 2^10 cells too
     cells = honest_cells(O, keys, C, r, seed, mode, blog)
     forged = forge_foreign_cells(O, cells, C, r, seed, mode, 40, 9, blog)
     t = dev_table(C, r, seed, mode, blog, cells)

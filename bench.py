@@ -191,31 +191,79 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_baseline_kcore(r, k, c, target_s=12.0):
+def host_cpu():
+    """CPU model and core count of this host (for the cpu_baseline record)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+class OneCore:
+    """Pin this process to one core for the duration (the oracle is single-threaded by
+    definition; SURVEY §8 d0 `taskset -c 0`)."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.old)
+
+
+def cpu_baseline_kcore(r, k, c, target_s=12.0, config=None):
     """The oracle as it stands (single-threaded literal synchronous peel) on a bounded
-    sample: one instance of the same model (r, k, c) scaled down so it runs ~10-30 s."""
+    sample: instances of the same model (r, k, c) scaled down so they run ~10-30 s, pinned to
+    one core.  Also timed on the same instances: the serial queue peel (ora_queue_peel, the
+    work-efficient comparator of P:516's serial recovery).  The full-scale oracle run of the
+    workload, when tests/golden/oracle_goldens.json recorded one, is quoted beside them."""
     from oracle import oracle as O
     n = 2_000_000
-    t_total = 0.0
+    t_total = t_queue = 0.0
     peeled = 0
     runs = 0
-    while True:
-        m = int(round(c * n))
-        e = O.gen_hypergraph(n, m, r, 1000 + runs)
-        t0 = time.perf_counter()
-        res = O.sync_peel(e, n, k)
-        dt = time.perf_counter() - t0
-        inside = res.core_mask[e].all(axis=1)
-        peeled += int(m - inside.sum())
-        t_total += dt
-        runs += 1
-        if t_total > target_s or runs >= 4:
-            break
-        if dt < target_s / 4:
-            n *= 2
-    return {"value": peeled / t_total, "unit": "edges/s", "cores": 1, "kind": "oracle",
-            "sample": f"{runs} instance(s) of G^{r}_(n,cn), c={c}, k={k}, largest n={n} "
-                      f"(literal synchronous oracle, single thread, {t_total:.1f} s of peel)"}
+    with OneCore() as pin:
+        while True:
+            m = int(round(c * n))
+            e = O.gen_hypergraph(n, m, r, 1000 + runs)
+            t0 = time.perf_counter()
+            res = O.sync_peel(e, n, k)
+            dt = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            O.queue_peel(e, n, k)
+            t_queue += time.perf_counter() - t0
+            inside = res.core_mask[e].all(axis=1)
+            peeled += int(m - inside.sum())
+            t_total += dt
+            runs += 1
+            if t_total > target_s or runs >= 4:
+                break
+            if dt < target_s / 4:
+                n *= 2
+    out = {"value": peeled / t_total, "unit": "edges/s", "cores": 1, "kind": "oracle",
+           "sample": f"{runs} instance(s) of G^{r}_(n,cn), c={c}, k={k}, largest n={n} "
+                     f"(literal synchronous oracle, single thread pinned to core {pin.core}, {t_total:.1f} s of peel)",
+           "queue_peel": {"value": peeled / t_queue, "unit": "edges/s", "cores": 1,
+                          "kind": "serial queue peel (oracle/peel_oracle.c ora_queue_peel, CSR build included)",
+                          "seconds": round(t_queue, 2)}}
+    out.update(host_cpu())
+    try:
+        g = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_goldens.json")))[config]
+        if g.get("oracle_seconds"):
+            out["full_scale_oracle"] = {
+                "value": (g["m"] - g.get("core_edges", 0)) / g["oracle_seconds"] if g.get("core", 0) == 0 else None,
+                "unit": "edges/s", "seconds": g["oracle_seconds"],
+                "note": "tools/make_oracle_goldens.py on the build host (not this box), whole workload, one core"}
+    except Exception:
+        pass
+    return out
 
 
 def run_reference(args):
@@ -253,6 +301,8 @@ def run_reference(args):
                 "e2e": {"value": val, "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         emit(line)
         return 0
+    pin = OneCore()
+    pin.__enter__()  # single-threaded oracle on one core (released at exit)
     if kind == "kcore":
         e = O.gen_hypergraph(n, m, r, seed)
         for i in range(args.warmup + args.steps):
@@ -285,8 +335,9 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64 integer",
         "data": "synthetic (counter-based G^r_{n,cn} generator, oracle implementation)",
         "config": {"workload": f"{args.config}: {text}", "sample_n": n, "sample_m": m, "r": r, "k": k},
-        "cpu_baseline": {"value": val, "unit": unit, "cores": 1, "kind": "oracle",
-                         "sample": f"each step = oracle peel of one n={n} instance of the same model"},
+        "cpu_baseline": dict({"value": val, "unit": unit, "cores": 1, "kind": "oracle",
+                              "sample": f"each step = oracle peel of one n={n} instance of the same model, "
+                                        f"pinned to core {pin.core}"}, **host_cpu()),
         "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -954,7 +1005,7 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_kcore(r, k, m / n)
+        cpu = cpu_baseline_kcore(r, k, m / n, config=args.config)
 
     if rank == 0:
         line = {

@@ -55,6 +55,14 @@ struct Ctl {
     ull work;         // binned-round work-item counter
     uint32_t err;     // ERR_* bits
     uint32_t binovf;  // a vertex bin overflowed its capacity (binned build falls back)
+    ull nlive[2];     // compacted rounds: live vertices after round t at nlive[t & 1] (build: [0])
+};
+
+// compacted rounds (kcompact.cuh): group records, per-bin live counts, A-item counters,
+// per-edge-bin frontier regions and their counts
+struct CompactLayout {
+    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe;
+    uint64_t enb, fe_stride;
 };
 
 struct Layout {
@@ -62,6 +70,8 @@ struct Layout {
     size_t bins, bin_cursor, bin_base, bin_cap, entries;  // binned build (packed, n > BIN_MIN_N)
     size_t esort;                                          // binned rounds: edge-bin counters of the frontier sort
     uint64_t nbins, total_cap;
+    bool compact;                                          // packed, n > BIN_MIN_N: kcompact.cuh's rounds
+    CompactLayout cl;
     size_t total;
 };
 
@@ -125,6 +135,21 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         L.bin_cap = o; o += al(sizeof(ull) * L.nbins);
         L.entries = o; o += al(sizeof(ull) * L.total_cap);
         L.esort = o; o += al(sizeof(ull) * 3 * (((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT) + 1));
+    }
+    L.compact = !csr && n > BIN_MIN_N;
+    memset(&L.cl, 0, sizeof L.cl);
+    if (L.compact) {
+        CompactLayout &C = L.cl;
+        C.enb = (m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT;
+        if (C.enb == 0) C.enb = 1;
+        C.fe_stride = (uint64_t)r << EB_SHIFT;  // an edge bin's entries: <= r per edge (one per endpoint)
+        C.recs = o; o += al(16 * ((n + 63) / 64));
+        C.live0 = o; o += al(sizeof(ull) * L.nbins);
+        C.live1 = o; o += al(sizeof(ull) * L.nbins);
+        C.adone = o; o += al(sizeof(uint32_t) * L.nbins);
+        C.fecnt0 = o; o += al(sizeof(ull) * C.enb);
+        C.fecnt1 = o; o += al(sizeof(ull) * C.enb);
+        C.fe = o; o += al(sizeof(uint2) * C.enb * C.fe_stride);
     }
     L.total = o;
     return L;
@@ -1714,6 +1739,8 @@ static peel_status stream_all(const EdgeStream &es, uint64_t m, uint32_t r, cuda
     return PEEL_OK;
 }
 
+#include "kcompact.cuh"
+
 // Small instances (the one-cluster path) are launch-bound: the call's memsets, build and round
 // loop are captured once per (device, stream, buffers, shape) into a CUDA graph and replayed
 // (PEEL_GRAPH=0 disables).  A few entries are kept; a new shape or buffer evicts the oldest.
@@ -1831,6 +1858,18 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         if (csr || !L.nbins)  // only the binned build consumes the chunks as they land
             for (auto ev : es->done) PEEL_CUDA(cudaStreamWaitEvent(s, ev, 0));
     }
+    bool compact_done = false;
+    if (!csr && !subr && L.compact && compact_on()) {
+        bool fallback = false;
+        peel_status st = run_compact<R>(edges, n, m, k, core_mask, rounds, survivors, killed, cap, peel_round, ws, L, s,
+                                        es, a, &fallback);
+        if (!fallback) return st;
+        // a bin overflowed: the uncompacted binned path below rebuilds from scratch
+        PEEL_CUDA(cudaMemsetAsync(ws + L.ctl, 0, L.state - L.ctl, s));
+        es = nullptr;  // the copies have landed (the partition waited for every chunk)
+        compact_done = false;
+    }
+    (void)compact_done;
     if (!csr && L.nbins) {
         // binned build: partition endpoint increments by vertex bin, accumulate each bin in L2
         ull *state = (ull *)(ws + L.state);

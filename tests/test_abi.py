@@ -42,9 +42,12 @@ def test_workspace_queries():
     L = pk.lib()
     n, m = 10**9, 750 * 10**6
     ws = L.peel_kcore_workspace_bytes(n, m, 3, 2, 0)
-    # packed k=2 layout: 8n state + 2 x 8n (v, e) frontier entries + m/8 alive bits + stats,
-    # plus (n > 2^23) the binned build's 8-byte entry buffer: r m entries + ~0.3% slack
-    assert 24 * n + 8 * 3 * m < ws < 24 * n + 8 * 3 * m * 1.004 + m // 8 + (16 << 20)
+    # packed k=2 layout: 8n state + 2 x 8n (v, e) frontier entries (the compacted rounds' two
+    # state buffers) + m/8 alive bits + stats, plus (n > 2^23) the binned build's 8-byte entry
+    # buffer (r m entries + ~0.3% slack), the per-edge-bin frontier regions (r entries per edge,
+    # whole edge bins of 2^22) and the 16-byte records of 64-vertex groups
+    fe = 8 * 3 * (1 << 22) * ((m + (1 << 22) - 1) >> 22)
+    assert 24 * n + 8 * 3 * m + fe + n // 4 < ws < 24 * n + 8 * 3 * m * 1.004 + fe + n // 4 + m // 8 + (16 << 20)
     small = L.peel_kcore_workspace_bytes(10**6, 750000, 3, 2, 0)   # no binning below 2^23
     assert 24 * 10**6 < small < 24 * 10**6 + (8 << 20)
     # CSR: deg + end offsets + 2 frontiers (4n each) + adj 4rm, plus the binned entries (n > 2^23)

@@ -375,3 +375,30 @@ def test_maximum_vertex_range(k, flags, c):
     del mask, res
     pk._ws_cache.clear()
     torch.cuda.empty_cache()
+
+
+# ---- slot-compacted rounds (kcompact.cuh; n > 2^23, k <= 2) --------------------------------
+@pytest.mark.parametrize("tail,at", [("0", None), ("2", None), (None, None), ("2", "1.0"), ("2", "0")])
+@pytest.mark.parametrize("c,k,r", [(0.85, 2, 3), (0.75, 2, 3), (0.6, 1, 3), (0.77, 2, 4)])
+def test_compact_rounds_modes(monkeypatch, tail, at, c, k, r):
+    """The binned rounds with edge-bin frontier regions and slot compaction: handing over to
+    the persistent kernel at the first small frontier (tail 0), never (tail 2), or by the
+    default rule; compacting whenever the live set shrank at all (at 1.0), never (at 0), or at
+    the default halving -- and the uncompacted binned rounds (PEEL_COMPACT=0) on the same input,
+    all bit-exact against the oracle."""
+    n = (1 << 23) + 3 * 4097 + 5
+    m = int(c * n)
+    e = pk.gen_hypergraph(n, m, r, 70 + r, device=DEV)
+    ref = O.sync_peel(e.cpu().numpy().view(np.uint32), n, k, want_peel_round=True)
+    for name, val in (("PEEL_COMPACT_TAIL", tail), ("PEEL_COMPACT_AT", at)):
+        if val is None:
+            monkeypatch.delenv(name, raising=False)
+        else:
+            monkeypatch.setenv(name, val)
+    for compact in ("1", "0") if (tail, at) == (None, None) else ("1",):
+        monkeypatch.setenv("PEEL_COMPACT", compact)
+        res = pk.peel_kcore(e, n, k, want_peel_round=True)
+        assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist(), compact
+        assert res.killed.tolist() == ref.killed.tolist()
+        assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask)
+        assert np.array_equal(res.peel_round.cpu().numpy().view(np.uint32), ref.peel_round)

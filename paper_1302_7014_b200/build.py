@@ -36,15 +36,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines: list | None = None) -> str:
+    """Build libpeel.so (or, for A/B measurements, a variant at `out` with extra -D defines)."""
+    lib = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
     objs = []
-    os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
+    bdir = os.path.join(PKG, "build" if out is None else "build_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(bdir, exist_ok=True)
     procs = []
     for s in SOURCES:
-        obj = os.path.join(PKG, "build", s.replace(".cu", ".o"))
-        cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-c", os.path.join(CSRC, s), "-o", obj]
+        obj = os.path.join(bdir, s.replace(".cu", ".o"))
+        cmd = [_nvcc(), *NVCC_FLAGS, *["-D" + d for d in (defines or [])], "-I", INCLUDE, "-c",
+               os.path.join(CSRC, s), "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
     for cmd, p in procs:
@@ -54,12 +58,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
         if verbose:
             sys.stderr.write(out.decode())
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lnccl"]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python build.py [--force] [--out variants/libpeel_x.so -DNAME=VALUE ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose=out is None, out=out, defines=defs))

@@ -67,6 +67,11 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// prefetch the L2 line holding p (fire and forget)
+__device__ __forceinline__ void prefetch_line_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // %globaltimer (ns): per-round device timestamps for profiling
 __device__ __forceinline__ ull globaltimer() {
     ull t;

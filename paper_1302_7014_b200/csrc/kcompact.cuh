@@ -36,9 +36,35 @@ struct __align__(16) CRec {
 static_assert(sizeof(CRec) == 16, "16-byte group record");
 
 static constexpr int CB_BLOCK = 256;
-static constexpr int FE_CAP = 2048;  // frontier entries staged per block before an edge-bin sort
-static constexpr int GB = 4;         // groups per compaction batch (registers: 2 GB states per lane)
+static constexpr int GB = 4;         // compaction: groups per batch (registers: 2 GB states per lane)
 static constexpr int CGW = 32;       // compaction: groups per warp per item (8 CGW per block item)
+#ifndef PEEL_FE_CAP_A
+#define PEEL_FE_CAP_A 2048
+#endif
+#ifndef PEEL_FE_CAP_B
+#define PEEL_FE_CAP_B 2048
+#endif
+static constexpr int FE_CAP_A = PEEL_FE_CAP_A;  // apply: frontier entries staged per block before an edge-bin sort
+static constexpr int FE_CAP_B = PEEL_FE_CAP_B;  // build scan (F_1 is ~24% of n: longer runs per edge bin)
+#ifndef PEEL_KILL_SPEC
+#define PEEL_KILL_SPEC 0
+#endif
+#ifndef PEEL_APPLY_PF
+#define PEEL_APPLY_PF 1
+#endif
+#ifndef PEEL_KILL_EPF
+#define PEEL_KILL_EPF 1
+#endif
+#ifndef PEEL_CB_RU
+#define PEEL_CB_RU 8
+#endif
+#ifndef PEEL_CB_SU
+#define PEEL_CB_SU 4
+#endif
+#ifndef PEEL_CDCH
+#define PEEL_CDCH 512
+#endif
+static constexpr int CDCH = PEEL_CDCH;  // apply: decrement entries per work item
 
 __host__ __device__ inline uint64_t bin_groups(uint64_t n, uint64_t b) { return (bin_size(n, b) + 63) >> 6; }
 
@@ -110,25 +136,27 @@ struct FeView {
     uint32_t *n;  // staged entries
 };
 
+template <int CAP>
 __device__ __forceinline__ FeView fe_view(unsigned char *smem, uint32_t enb, uint32_t *n) {
     FeView f;
     f.buf = (uint2 *)smem;
-    f.gpos = (ull *)(f.buf + FE_CAP);
+    f.gpos = (ull *)(f.buf + CAP);
     f.hist = (uint32_t *)(f.gpos + enb);
     f.offs = f.hist + enb;
     f.n = n;
     return f;
 }
 
-static size_t fe_smem(uint32_t enb) { return sizeof(uint2) * FE_CAP + (sizeof(ull) + 2 * sizeof(uint32_t)) * enb; }
+static size_t fe_smem(int cap, uint32_t enb) { return sizeof(uint2) * cap + (sizeof(ull) + 2 * sizeof(uint32_t)) * enb; }
 
-// warp-aggregated push; past FE_CAP the entry goes straight to its region (one global atomic)
+// warp-aggregated push; past CAP the entry goes straight to its region (one global atomic)
+template <int CAP>
 __device__ __forceinline__ void fe_push(const FeView &f, const CArgs &a, uint2 v) {
     cg::coalesced_group g = cg::coalesced_threads();
     uint32_t pos = 0;
     if (g.thread_rank() == 0) pos = atomicAdd(f.n, (uint32_t)g.size());
     pos = g.shfl(pos, 0) + g.thread_rank();
-    if (pos < FE_CAP) {
+    if (pos < CAP) {
         f.buf[pos] = v;
     } else {
         const uint32_t j = v.y >> EB_SHIFT;
@@ -138,10 +166,11 @@ __device__ __forceinline__ void fe_push(const FeView &f, const CArgs &a, uint2 v
 }
 
 // every thread of the block calls it
+template <int CAP>
 __device__ void fe_flush(const FeView &f, const CArgs &a) {
-    constexpr int PER = FE_CAP / CB_BLOCK;
+    constexpr int PER = CAP / CB_BLOCK;
     __syncthreads();
-    const uint32_t cnt = min(*f.n, (uint32_t)FE_CAP);
+    const uint32_t cnt = min(*f.n, (uint32_t)CAP);
     if (cnt == 0) return;  // uniform: every thread read the same count after the barrier
     for (uint32_t j = threadIdx.x; j < a.enb; j += CB_BLOCK) f.hist[j] = 0;
     __syncthreads();
@@ -327,11 +356,11 @@ __global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_kernel(CArgs a) {
     __shared__ uint32_t fen;
     if (threadIdx.x == 0) fen = 0;
     __syncthreads();
-    const FeView f = fe_view(smem_raw, a.enb, &fen);
+    const FeView f = fe_view<FE_CAP_B>(smem_raw, a.enb, &fen);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     const ull mask = (1ull << BIN_SHIFT) - 1;
-    constexpr int SU = 4;  // states per thread per scan step
+    constexpr int SU = PEEL_CB_SU;  // states per thread per scan step
     ull leavers = 0, emitted = 0, kept = 0;
     for (uint32_t b = 0; b <= a.nbins; b++) {
         if (b > 0) {  // scan bin b-1 (still in L2), overlapped with zeroing bin b
@@ -354,11 +383,11 @@ __global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_kernel(CArgs a) {
                     if (a.peel_round) a.peel_round[v] = 1;
                     if (c == 1u) {  // k = 2: its one edge is the id sum
                         emitted++;
-                        fe_push(f, a, make_uint2((uint32_t)v, (uint32_t)(w[j] >> 32)));
+                        fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(w[j] >> 32)));
                     }
                 }
                 __syncthreads();  // every push of this step landed: one decision for the block
-                if (fen >= FE_CAP / 2) fe_flush(f, a);
+                if (fen >= FE_CAP_B - CB_BLOCK * SU) fe_flush<FE_CAP_B>(f, a);
                 __syncthreads();
             }
         }
@@ -370,17 +399,226 @@ __global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_kernel(CArgs a) {
         }
         grid.sync();
         if (b < a.nbins) {
+            // RU entry loads in flight per thread before their REDs (one load at a time left the
+            // loop waiting on DRAM latency: the load -> RED dependency was ncu's top stall)
+            constexpr int RU = PEEL_CB_RU;
             ull *st = a.X + ((uint64_t)b << BIN_SHIFT);
             const ull *ent = a.entries + a.base[b];
             const ull cnt = a.cursor[b];
-            for (ull i = tid; i < cnt; i += nthr) {
-                const ull x = __ldcs(ent + i);
-                atomicAdd(st + (x & mask), (x & ~0xFFFFFFFFull) + 1ull);
+            for (ull i0 = tid; i0 < cnt; i0 += RU * nthr) {
+                ull x[RU];
+                #pragma unroll
+                for (int u = 0; u < RU; u++) {
+                    const ull i = i0 + (ull)u * nthr;
+                    x[u] = i < cnt ? __ldcs(ent + i) : 0ull;
+                }
+                #pragma unroll
+                for (int u = 0; u < RU; u++)
+                    if (i0 + (ull)u * nthr < cnt) atomicAdd(st + (x[u] & mask), (x[u] & ~0xFFFFFFFFull) + 1ull);
             }
         }
         grid.sync();
     }
-    fe_flush(f, a);
+    fe_flush<FE_CAP_B>(f, a);
+    block_add<CB_BLOCK>(&a.ctl->nf[0], leavers);
+    block_add<CB_BLOCK>(&a.ctl->ne[0], emitted);
+    block_add<CB_BLOCK>(a.live_total, kept);
+}
+
+// ---- build as a dataflow (PEEL_BUILD_DF, default): the same three phases per bin -- zero
+// Z(b), REDs R(b), scan S(b) -- as work items handed out by a counter in the order
+// Z(0) R(0) | Z(1) R(1) S(0) | Z(2) R(2) S(1) | ... | S(nb-1), with no grid barrier: an R(b)
+// item waits (spinning on a per-bin counter) until Z(b) is done, an S(b) item until R(b) is.
+// Every wait is on items handed out earlier, so it always ends.  Bin b's scan overlaps bin
+// b+1's REDs and bin b+2's zeroing instead of waiting at a barrier for the slowest block.
+static constexpr uint32_t DZ_BYTES = 256u << 10;  // zeroed per Z item
+static constexpr uint32_t DR_ENT = 4096;          // entries per R item (16 per thread)
+static constexpr uint32_t DS_SU = 4;              // states per thread per scan step
+static constexpr uint32_t DS_STEPS = 4;           // scan steps per S item (4096 states)
+static_assert(CB_BLOCK * DS_SU * DS_STEPS == 4096, "an S item is 64 groups");
+
+__host__ __device__ inline uint32_t df_seg_kind(uint32_t s, uint32_t nb, uint32_t &b) {  // 0 Z, 1 R, 2 S
+    if (s == 0) { b = 0; return 0; }
+    if (s == 1) { b = 0; return 1; }
+    if (s == 3 * nb - 1) { b = nb - 1; return 2; }
+    const uint32_t q = (s + 1) / 3, r = (s + 1) % 3;  // s = 3q - 1 + r
+    if (r == 0) { b = q; return 0; }
+    if (r == 1) { b = q; return 1; }
+    b = q - 1;
+    return 2;
+}
+
+// COUT: the scan also lays out the bin's live states as compacted slots (CArgs::Y, records,
+// alloc = slots per bin), so the rounds start compacted: S items then cover 64 groups, warp w
+// taking 8 of them, lane = vertex within the group (two passes: count + emit, then write).
+template <int R, bool COUT>
+__global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_df_kernel(CArgs a, uint32_t *zdone, uint32_t *rdone) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ uint32_t fen;
+    __shared__ ull item;
+    const uint32_t nb = a.nbins, ns = 3 * nb;
+    const FeView f = fe_view<FE_CAP_B>(smem_raw, a.enb, &fen);
+    uint32_t *pre = (uint32_t *)(f.offs + a.enb);  // [3 nb + 1] items before segment s
+    auto nitems_of = [&](uint32_t kind, uint32_t b) -> uint32_t {
+        const uint64_t sz = bin_size(a.n, b);
+        if (kind == 0) return (uint32_t)((sz * sizeof(ull) + DZ_BYTES - 1) / DZ_BYTES);
+        if (kind == 1) return (uint32_t)((ld_cg_u64(a.cursor + b) + DR_ENT - 1) / DR_ENT);
+        return (uint32_t)((sz + 4095) / 4096);  // CB_BLOCK DS_SU DS_STEPS = 64 groups = 4096 states
+    };
+    if (threadIdx.x == 0) fen = 0;
+    for (uint32_t s = threadIdx.x; s < ns; s += CB_BLOCK) {
+        uint32_t b;
+        const uint32_t kind = df_seg_kind(s, nb, b);
+        pre[s] = nitems_of(kind, b);
+    }
+    block_excl_scan(pre, ns);
+    const uint32_t nitems = pre[ns];
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    ull leavers = 0, emitted = 0, kept = 0;
+    for (;;) {
+        if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
+        __syncthreads();
+        const ull c = item;
+        if (c >= nitems) break;
+        uint32_t lo = 0, hi = ns;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (pre[mid] <= c) lo = mid; else hi = mid;
+        }
+        uint32_t b;
+        const uint32_t kind = df_seg_kind(lo, nb, b), j = (uint32_t)c - pre[lo];
+        const uint64_t v0 = (uint64_t)b << BIN_SHIFT, sz = bin_size(a.n, b);
+        if (kind == 0) {  // zero bytes [j DZ, (j+1) DZ) of the bin's states
+            const uint64_t w0 = (uint64_t)j * (DZ_BYTES / 16), w1 = min(w0 + DZ_BYTES / 16, sz / 2);
+            ulonglong2 *z = reinterpret_cast<ulonglong2 *>(a.X + v0);
+            for (uint64_t i = w0 + threadIdx.x; i < w1; i += CB_BLOCK) z[i] = make_ulonglong2(0ull, 0ull);
+            if ((sz & 1) && threadIdx.x == 0 && w1 == sz / 2) a.X[v0 + sz - 1] = 0ull;
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd(zdone + b, 1u);
+        } else if (kind == 1) {  // REDs of entries [j DR, (j+1) DR)
+            if (threadIdx.x == 0) {
+                const uint32_t need = nitems_of(0, b);
+                while (*(volatile uint32_t *)(zdone + b) < need) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            const ull cnt = ld_cg_u64(a.cursor + b);
+            const ull *ent = a.entries + a.base[b] + (ull)j * DR_ENT;
+            const uint32_t nin = (uint32_t)min((ull)DR_ENT, cnt - (ull)j * DR_ENT);
+            ull *st = a.X + v0;
+            constexpr int U = DR_ENT / CB_BLOCK;
+            ull x[U];
+            #pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t i = u * CB_BLOCK + threadIdx.x;
+                x[u] = i < nin ? __ldcs(ent + i) : 0ull;
+            }
+            #pragma unroll
+            for (int u = 0; u < U; u++)
+                if (u * CB_BLOCK + threadIdx.x < nin) atomicAdd(st + (x[u] & mask), (x[u] & ~0xFFFFFFFFull) + 1ull);
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) atomicAdd(rdone + b, 1u);
+        } else {  // scan states [j 4096, (j+1) 4096): F_1 entries, leavers, survivors
+            if (threadIdx.x == 0) {
+                const uint32_t need = nitems_of(1, b);
+                while (*(volatile uint32_t *)(rdone + b) < need) __nanosleep(100);
+                __threadfence();
+            }
+            __syncthreads();
+            if (COUT) {
+                __shared__ uint32_t wsh[CB_BLOCK / 32 + 1];
+                const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                const uint64_t gb0 = v0 >> 6, gend = gb0 + bin_groups(a.n, b);
+                const uint64_t gw0 = gb0 + (uint64_t)j * 64 + (uint64_t)w * 8;  // this warp's 8 groups
+                uint32_t keepcnt = 0;
+                #pragma unroll 2
+                for (int gi = 0; gi < 8; gi++) {
+                    const uint64_t g = gw0 + gi;
+                    #pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const uint64_t v = (g << 6) + 32 * h + lane;
+                        const bool valid = g < gend && v < v0 + sz;
+                        const ull st = valid ? __ldcg(a.X + v) : 0ull;
+                        const uint32_t cn = (uint32_t)st;
+                        const bool keep = valid && cn >= a.k;
+                        keepcnt += __popc(__ballot_sync(0xffffffffu, keep));
+                        if (valid && !keep) {
+                            leavers++;
+                            if (a.peel_round) a.peel_round[v] = 1;
+                            if (cn == 1u) {
+                                emitted++;
+                                fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(st >> 32)));
+                            }
+                        }
+                    }
+                }
+                if (lane == 0) wsh[w] = keepcnt;
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    uint32_t tot = 0;
+                    for (int q = 0; q < CB_BLOCK / 32; q++) { const uint32_t cq = wsh[q]; wsh[q] = tot; tot += cq; }
+                    const ull bb = tot ? atomicAdd(a.alloc + b, (ull)tot) : 0ull;
+                    wsh[CB_BLOCK / 32] = (uint32_t)(v0 + bb);
+                }
+                __syncthreads();
+                uint32_t run = wsh[CB_BLOCK / 32] + wsh[w];
+                kept += lane == 0 ? keepcnt : 0;
+                #pragma unroll 2
+                for (int gi = 0; gi < 8; gi++) {
+                    const uint64_t g = gw0 + gi;
+                    ull st[2];
+                    bool kp[2];
+                    #pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        const uint64_t v = (g << 6) + 32 * h + lane;
+                        const bool valid = g < gend && v < v0 + sz;
+                        st[h] = valid ? __ldcg(a.X + v) : 0ull;
+                        kp[h] = valid && (uint32_t)st[h] >= a.k;
+                    }
+                    const uint32_t b0 = __ballot_sync(0xffffffffu, kp[0]), b1 = __ballot_sync(0xffffffffu, kp[1]);
+                    if (kp[0]) a.Y[run + __popc(b0 & lanemask_lt())] = st[0];
+                    if (kp[1]) a.Y[run + __popc(b0) + __popc(b1 & lanemask_lt())] = st[1];
+                    if (lane == 0 && g < gend)
+                        __stcg(reinterpret_cast<uint4 *>(a.recs + g), make_uint4(b0, b1, run, 0u));
+                    run += __popc(b0) + __popc(b1);
+                }
+                __syncthreads();  // every push of this item landed: one decision for the block
+                if (fen >= FE_CAP_B / 2) fe_flush<FE_CAP_B>(f, a);  // past FE_CAP_B: direct appends
+                __syncthreads();
+                continue;
+            }
+            const uint64_t lo2 = v0 + (uint64_t)j * CB_BLOCK * DS_SU * DS_STEPS;
+            const uint64_t hi2 = min(lo2 + CB_BLOCK * DS_SU * DS_STEPS, v0 + sz);
+            for (uint64_t base = lo2; base < hi2; base += CB_BLOCK * DS_SU) {
+                ull w[DS_SU];
+                #pragma unroll
+                for (int u = 0; u < (int)DS_SU; u++) {
+                    const uint64_t v = base + (uint64_t)u * CB_BLOCK + threadIdx.x;
+                    w[u] = v < hi2 ? __ldcg(a.X + v) : ~0ull;
+                }
+                #pragma unroll
+                for (int u = 0; u < (int)DS_SU; u++) {
+                    const uint64_t v = base + (uint64_t)u * CB_BLOCK + threadIdx.x;
+                    if (v >= hi2) continue;
+                    const uint32_t cn = (uint32_t)w[u];
+                    if (cn >= a.k) { kept++; continue; }
+                    leavers++;
+                    if (a.peel_round) a.peel_round[v] = 1;
+                    if (cn == 1u) {  // k = 2: its one edge is the id sum
+                        emitted++;
+                        fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(w[u] >> 32)));
+                    }
+                }
+                __syncthreads();  // every push of this step landed: one decision for the block
+                if (fen >= FE_CAP_B - CB_BLOCK * DS_SU) fe_flush<FE_CAP_B>(f, a);
+                __syncthreads();
+            }
+        }
+        __syncthreads();  // item is rewritten next iteration
+    }
+    fe_flush<FE_CAP_B>(f, a);
     block_add<CB_BLOCK>(&a.ctl->nf[0], leavers);
     block_add<CB_BLOCK>(&a.ctl->ne[0], emitted);
     block_add<CB_BLOCK>(a.live_total, kept);
@@ -420,11 +658,25 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
             const uint32_t mid = (lo + hi) >> 1;
             if (pre[mid] <= item) lo = mid; else hi = mid;
         }
-        const uint32_t j = lo;
-        const ull off = (ull)(item - pre[j]) * KCH;
-        const ull nE = min((ull)KCH, ld_cg_u64(c.fecur + j) - off);
-        const uint2 *Fc = c.fe + (ull)j * c.fe_stride + off;
-        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
+        const ull off = (ull)(item - pre[lo]) * KCH;
+        const ull nE = min((ull)KCH, ld_cg_u64(c.fecur + lo) - off);
+        const uint2 *Fc = c.fe + (ull)lo * c.fe_stride + off;
+#if PEEL_KILL_EPF
+        if (threadIdx.x == 32 && item + gridDim.x < nitems) {
+            // this block's next chunk of entries: into L2 while this one is processed
+            const uint32_t it2 = item + gridDim.x;
+            uint32_t l2 = lo, h2 = c.enb;
+            while (h2 - l2 > 1) {
+                const uint32_t mid = (l2 + h2) >> 1;
+                if (pre[mid] <= it2) l2 = mid; else h2 = mid;
+            }
+            const ull off2 = (ull)(it2 - pre[l2]) * KCH;
+            const ull n2 = min((ull)KCH, ld_cg_u64(c.fecur + l2) - off2);
+            const uintptr_t p0 = (uintptr_t)(c.fe + (ull)l2 * c.fe_stride + off2) & ~(uintptr_t)15;
+            const uintptr_t p1 = ((uintptr_t)(c.fe + (ull)l2 * c.fe_stride + off2 + n2) + 15) & ~(uintptr_t)15;
+            if (p1 > p0) prefetch_l2((const void *)p0, (uint32_t)(p1 - p0));
+        }
+#endif
         uint2 ent[KU];
         bool win[KU];
         #pragma unroll
@@ -432,22 +684,30 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
             const uint32_t i = q * PART_BLOCK + threadIdx.x;
             ent[q] = i < nE ? __ldcg(Fc + i) : make_uint2(0u, 0u);
         }
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
+        uint32_t oldw[KU];
         #pragma unroll
         for (int q = 0; q < KU; q++) {
             const uint32_t i = q * PART_BLOCK + threadIdx.x;
-            win[q] = false;
-            if (i < nE) {
-                const uint32_t e = ent[q].y, bit = 1u << (e & 31);
-                win[q] = (atomicAnd(a.alive + (e >> 5), ~bit) & bit) != 0;
-            }
+            oldw[q] = 0;
+            if (i < nE) oldw[q] = atomicAnd(a.alive + (ent[q].y >> 5), ~(1u << (ent[q].y & 31)));
         }
+        // the rows are loaded together with the test-and-clears, not after them: one dependent
+        // memory trip less per chunk (a losing entry's row -- its edge died already -- is ~10%
+        // of the rows, read for nothing)
         uint32_t ue[KU][R];
         #pragma unroll
-        for (int q = 0; q < KU; q++)
-            if (win[q]) {
-                kills++;
-                load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
-            }
+        for (int q = 0; q < KU; q++) {
+            const uint32_t i = q * PART_BLOCK + threadIdx.x;
+#if PEEL_KILL_SPEC
+            if (i < nE) load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
+#endif
+            win[q] = i < nE && ((oldw[q] >> (ent[q].y & 31)) & 1u);
+#if !PEEL_KILL_SPEC
+            if (win[q]) load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
+#endif
+            kills += win[q];
+        }
         __syncthreads();  // hist zeroed
         uint32_t rk[KU][R];
         #pragma unroll
@@ -477,8 +737,8 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
             if (threadIdx.x == 31) total = z;
         }
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)
-            if (hist[b]) gpos[b] = atomicAdd(br.cursor + b, (ull)hist[b]);
+        for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)  // absolute run starts
+            if (hist[b]) gpos[b] = br.base[b] + atomicAdd(br.cursor + b, (ull)hist[b]);
         #pragma unroll
         for (int q = 0; q < KU; q++)
             #pragma unroll
@@ -490,7 +750,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
         for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
             const ull v = sorted[i];
             const uint32_t b = (uint32_t)v >> BIN_SHIFT;
-            br.entries[br.base[b] + gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ mask);
+            br.entries[gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ mask);
         }
         __syncthreads();
     }
@@ -512,10 +772,10 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
     __shared__ uint32_t fen;
     __shared__ ull item;
     const uint32_t nb = a.nbins;
-    const FeView f = fe_view(smem_raw, a.enb, &fen);
+    const FeView f = fe_view<FE_CAP_A>(smem_raw, a.enb, &fen);
     uint32_t *pre = (uint32_t *)(f.offs + a.enb);  // [nb + 1] items before bin b
     if (threadIdx.x == 0) fen = 0;
-    for (uint32_t b = threadIdx.x; b < nb; b += CB_BLOCK) pre[b] = (uint32_t)((ld_cg_u64(a.cursor + b) + DCH - 1) / DCH);
+    for (uint32_t b = threadIdx.x; b < nb; b += CB_BLOCK) pre[b] = (uint32_t)((ld_cg_u64(a.cursor + b) + CDCH - 1) / CDCH);
     block_excl_scan(pre, nb);
     const uint32_t nitems = pre[nb];
     const ull mask = (1ull << BIN_SHIFT) - 1;
@@ -532,6 +792,22 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
             if (pre[mid] <= c) lo = mid; else hi = mid;
         }
         const uint32_t b = lo, j = (uint32_t)c - pre[b];
+#if PEEL_APPLY_PF
+        if (threadIdx.x == 32 && c + gridDim.x < nitems) {
+            // the entries of the item handed out one grid later: into L2 before it is claimed
+            const ull c2 = c + gridDim.x;
+            uint32_t l2 = lo, h2 = nb;
+            while (h2 - l2 > 1) {
+                const uint32_t mid = (l2 + h2) >> 1;
+                if (pre[mid] <= c2) l2 = mid; else h2 = mid;
+            }
+            const ull off2 = (ull)((uint32_t)c2 - pre[l2]) * CDCH;
+            const ull n2 = min((ull)CDCH, ld_cg_u64(a.cursor + l2) - off2);
+            const uintptr_t p0 = (uintptr_t)(a.entries + a.base[l2] + off2) & ~(uintptr_t)15;
+            const uintptr_t p1 = ((uintptr_t)(a.entries + a.base[l2] + off2 + n2) + 15) & ~(uintptr_t)15;
+            if (p1 > p0) prefetch_l2((const void *)p0, (uint32_t)(p1 - p0));
+        }
+#endif
         if (threadIdx.x == 0 && b + 1 < nb) {
             // slice j of the next bin's slots (and records) into L2
             const uint32_t nj = pre[b + 1] - pre[b];
@@ -549,13 +825,13 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
             }
         }
         const ull cnt = ld_cg_u64(a.cursor + b);
-        const ull *ent = a.entries + a.base[b] + (ull)j * DCH;
-        const uint32_t nin = (uint32_t)min((ull)DCH, cnt - (ull)j * DCH);
+        const ull *ent = a.entries + a.base[b] + (ull)j * CDCH;
+        const uint32_t nin = (uint32_t)min((ull)CDCH, cnt - (ull)j * CDCH);
         ull *st = a.X + ((uint64_t)b << BIN_SHIFT);
         const CRec *rb = a.recs + ((uint64_t)b << (BIN_SHIFT - 6));
         // all DU entries of a thread: loads, record lookups and returning atomics issued before
         // any result is used
-        constexpr int DU = DCH / CB_BLOCK;
+        constexpr int DU = CDCH / CB_BLOCK;
         ull x[DU], old[DU];
         #pragma unroll
         for (int r = 0; r < DU; r++) {
@@ -589,19 +865,19 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
                 crossed++;
                 const uint32_t u = (uint32_t)((b << BIN_SHIFT) + (uint32_t)(x[r] & mask));
                 if (a.peel_round) a.peel_round[u] = t + 1;
-                fe_push(f, a, make_uint2(u, idsum_of(old[r]) - (uint32_t)(x[r] >> 32)));
+                fe_push<FE_CAP_A>(f, a, make_uint2(u, idsum_of(old[r]) - (uint32_t)(x[r] >> 32)));
             }
         }
         __syncthreads();
-        if (fen >= FE_CAP / 2) fe_flush(f, a);
+        if (fen >= FE_CAP_A / 2) fe_flush<FE_CAP_A>(f, a);
         __syncthreads();  // item is rewritten next iteration
     }
-    fe_flush(f, a);
+    fe_flush<FE_CAP_A>(f, a);
     block_add<CB_BLOCK>(&a.ctl->nf[t % 3], crossed);
     block_add<CB_BLOCK>(&a.ctl->ne[t % 3], crossed);
 }
 
-static size_t capply_smem(uint32_t nbins, uint32_t enb) { return fe_smem(enb) + sizeof(uint32_t) * (nbins + 1); }
+static size_t capply_smem(uint32_t nbins, uint32_t enb) { return fe_smem(FE_CAP_A, enb) + sizeof(uint32_t) * (nbins + 1); }
 
 // ---- end of the path
 // core_mask[v] = count(slot(v)) >= k, 0 without a slot: one record per thread, 64 mask bytes
@@ -776,8 +1052,32 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     PEEL_CUDA(cudaMemsetAsync(fecnt[0], 0, sizeof(ull) * enb, s));
     c.fecnt = fecnt[0];
     c.live_total = &ctl->nlive[0];
-    {
-        const size_t bs = fe_smem(enb);
+    const char *dfe = getenv("PEEL_BUILD_DF");
+    const bool dataflow = dfe && atoi(dfe) == 1;  // measured slower than the cooperative build (97.3 vs 89.7 ms at C5)
+    // the dataflow build can lay out compacted slots itself (PEEL_BUILD_COMPACT, default on)
+    const char *bce = getenv("PEEL_BUILD_COMPACT");
+    const bool bcompact = dataflow && compact_on() && !(bce && atoi(bce) == 0);
+    if (bcompact) {
+        PEEL_CUDA(cudaMemsetAsync(slots[0], 0, sizeof(ull) * nbins, s));
+        c.Y = CB[0];
+        c.alloc = slots[0];
+    }
+    if (dataflow) {
+        // dataflow build: per-bin completion counters (zdone, rdone) in the A-item counter area
+        uint32_t *zdone = (uint32_t *)(ws + CL.adone), *rdone = zdone + nbins;
+        PEEL_CUDA(cudaMemsetAsync(zdone, 0, sizeof(uint32_t) * 2 * nbins, s));
+        PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
+        const size_t bs = fe_smem(FE_CAP_B, enb) + sizeof(uint32_t) * (3 * nbins + 1);
+        PEEL_CUDA(cudaFuncSetAttribute(cbuild_df_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
+        PEEL_CUDA(cudaFuncSetAttribute(cbuild_df_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
+        int per_sm = 0;
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cbuild_df_kernel<R, true>, CB_BLOCK, bs));
+        if (per_sm < 1) per_sm = 1;
+        ProfScope ps("bin_accumulate", s);
+        if (bcompact) cbuild_df_kernel<R, true><<<num_sms() * per_sm, CB_BLOCK, bs, s>>>(c, zdone, rdone);
+        else cbuild_df_kernel<R, false><<<num_sms() * per_sm, CB_BLOCK, bs, s>>>(c, zdone, rdone);
+    } else {
+        const size_t bs = fe_smem(FE_CAP_B, enb);
         PEEL_CUDA(cudaFuncSetAttribute(cbuild_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
         int per_sm = 0;
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cbuild_kernel<R>, CB_BLOCK, bs));
@@ -811,12 +1111,16 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     cb = cb < 1 ? 1 : cb;
     const double frac = bin_round_frac(n), tail = ctail_live_frac();
     const bool compaction = compact_on();
-    bool compacted = false;
+    bool compacted = bcompact;
     int cur = 0;             // compacted: the slots live in CB[cur], their counts per bin in slots[cur]
-    uint64_t nslots = n;     // slots laid out (identity: every vertex)
     PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
     PEEL_CUDA(cudaStreamSynchronize(s));
     uint64_t live = h.nlive[0];
+    uint64_t nslots = bcompact ? live : n;  // slots laid out (identity: every vertex)
+    if (bcompact) {
+        c.X = CB[0];
+        c.slots = slots[0];
+    }
     uint32_t t = 1;
     for (;;) {
         const ull nF = h.nf[(t - 1) % 3], nE = h.ne[(t - 1) % 3];
@@ -852,9 +1156,9 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
             // lay the live states out densely: CB[nxt], slot counts slots[nxt], new records
             const int nxt = compacted ? cur ^ 1 : 0;
             PEEL_CUDA(cudaMemsetAsync(slots[nxt], 0, sizeof(ull) * nbins, s));
-            PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
-            c.Y = CB[nxt];
+                c.Y = CB[nxt];
             c.alloc = slots[nxt];
+            PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
             {
                 ProfScope ps("compact_slots", s);
                 if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, s>>>(c);

@@ -146,7 +146,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         C.recs = o; o += al(16 * ((n + 63) / 64));
         C.live0 = o; o += al(sizeof(ull) * L.nbins);
         C.live1 = o; o += al(sizeof(ull) * L.nbins);
-        C.adone = o; o += al(sizeof(uint32_t) * L.nbins);
+        C.adone = o; o += al(sizeof(uint32_t) * 2 * L.nbins);  // dataflow build: zeroed / accumulated items per bin
         C.fecnt0 = o; o += al(sizeof(ull) * C.enb);
         C.fecnt1 = o; o += al(sizeof(ull) * C.enb);
         C.fe = o; o += al(sizeof(uint2) * C.enb * C.fe_stride);
@@ -321,11 +321,15 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
             if (threadIdx.x == 31) total = x;
         }
         __syncthreads();
+        // gpos[b] <- the run's absolute start in the entry buffer, and fill[b] <- how many of
+        // its entries still fit the bin (the write-out reads shared memory only)
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)
             if (hist[b]) {
-                ull g = atomicAdd(cursor + b, (ull)hist[b]);
-                if (g + hist[b] > cap[b]) atomicOr(binovf, 1u);
-                gpos[b] = g;
+                const ull g = atomicAdd(cursor + b, (ull)hist[b]);
+                const ull c = cap[b];
+                if (g + hist[b] > c) atomicOr(binovf, 1u);
+                gpos[b] = base[b] + g;
+                fill[b] = (uint32_t)(g >= c ? 0ull : min((ull)hist[b], c - g));
             }
         #pragma unroll
         for (int q = 0; q < WPT; q++) {
@@ -341,8 +345,8 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
         for (uint32_t i = threadIdx.x; i < tot; i += PART_BLOCK) {
             const ull x = sent[i];
             const uint32_t b = (uint32_t)x >> BIN_SHIFT;
-            const ull pos = gpos[b] + (i - offs[b]);
-            if (pos < cap[b]) entries[base[b] + pos] = x & ~(0xFFFFFFFFull ^ mask);
+            const uint32_t q = i - offs[b];
+            if (q < fill[b]) entries[gpos[b] + q] = x & ~(0xFFFFFFFFull ^ mask);
         }
         __syncthreads();
     }

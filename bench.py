@@ -140,7 +140,23 @@ class ClockSampler:
 # bench.py's per-call profiling names -> the kernel (tools/ncu_traffic.py short name) doing the work
 NCU_KERNEL = {"peel_rounds_packed": ("peel_packed",), "peel_rounds_csr": ("peel_csr",), "iblt_peel_rounds": ("iblt_peel",),
               "peel_small_graph": ("build_packed", "peel_cluster"), "peel_rounds_cluster": ("peel_cluster",),
-              "iblt_insert": ("iblt_update",), "frontier_edge_sort": ("esort_hist", "esort_scatter")}
+              "iblt_insert": ("iblt_update",), "frontier_edge_sort": ("esort_hist", "esort_scatter"),
+              # slot-compacted binned rounds (kcompact.cuh) for n > 2^23, k <= 2
+              "bin_accumulate": ("cbuild", "bin_accumulate"), "round_kill_partition": ("ckill", "round_kill_partition"),
+              "round_apply": ("capply", "round_apply"), "compact_slots": ("ccompact",),
+              "compact_core_mask": ("ctail", "cmask"), "compact_writeback": ("cdecompact",),
+              "compact_gather": ("cgather",)}
+PROFILE_ROUNDS = ("r02", "r01")  # newest first: profiles/<round>_traffic_<config>.json
+
+
+def profile_file(kind, config, kernel=None):
+    """The newest committed profile of this kind for the config (None if there is none)."""
+    for rnd in PROFILE_ROUNDS:
+        name = f"{rnd}_{kind}_{kernel}_{config}.json" if kernel else f"{rnd}_{kind}_{config}.json"
+        path = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(path):
+            return path
+    return None
 
 
 def ncu_traffic(config, kernel):
@@ -148,13 +164,14 @@ def ncu_traffic(config, kernel):
     capture of this config's kernel (profiles/r01_ncu_full_<kernel>_<config>.json) when there
     is one, else from the committed launch list (profiles/r01_traffic_<config>.json,
     tools/ncu_traffic.py), else None."""
-    full = os.path.join(ROOT, "profiles", f"r01_ncu_full_{kernel}_{config}.json")
-    if os.path.exists(full):
+    full = profile_file("ncu_full", config, kernel)
+    if full:
         d = json.load(open(full))
         return int(d["dram_gb_per_launch"] * 1e9), \
-            f"profiles/r01_ncu_full_{kernel}_{config}.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"
+            f"profiles/{os.path.basename(full)} (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"
+    tf = profile_file("traffic", config)
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))
+        d = json.load(open(tf))
     except Exception:
         return None, None
     ks = [d.get("kernels", {}).get(x) for x in NCU_KERNEL.get(kernel, (kernel,))]
@@ -162,14 +179,15 @@ def ncu_traffic(config, kernel):
         return None, None
     per_step = sum(k["dram_read_bytes_per_step"] + k["dram_write_bytes_per_step"] for k in ks)
     return int(per_step / ks[-1]["launches_per_step"]), \
-        f"profiles/r01_traffic_{config}.json (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
+        f"profiles/{os.path.basename(tf)} (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
 
 
 def dram_step(config, per_kernel, steps, ms_step, hbm):
     """Whole-step real DRAM traffic: the committed ncu bytes of every kernel this step launched
     (profiles/r01_traffic_<config>.json, per step) over this run's step time, or None."""
+    tf = profile_file("traffic", config)
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", f"r01_traffic_{config}.json")))["kernels"]
+        d = json.load(open(tf))["kernels"]
     except Exception:
         return None
     tot, missing = 0.0, []
@@ -181,7 +199,7 @@ def dram_step(config, per_kernel, steps, ms_step, hbm):
         tot += sum(f["dram_read_bytes_per_step"] + f["dram_write_bytes_per_step"] for f in found)
     return {"bytes": int(tot), "frac_of_peak": round(tot / (ms_step / 1e3) / 1e9 / hbm, 4),
             "kernels_without_traffic": missing,
-            "source": f"profiles/r01_traffic_{config}.json (ncu dram__bytes_read.sum + dram__bytes_write.sum)"}
+            "source": f"profiles/{os.path.basename(tf)} (ncu dram__bytes_read.sum + dram__bytes_write.sum)"}
 
 
 def dist_env():
@@ -929,6 +947,8 @@ def main():
         kb["round_apply"] = sum(16 * (r - 1) * kl[t] for t in range(min(nb, len(F))))
         kb["peel_rounds_packed"] = sum(8 * F[t] + (4 * r + 16 * (r - 1)) * kl[t] for t in range(nb, len(F))) + n
         kb["peel_rounds_cluster"] = kb["peel_rounds_packed"]
+        kb["compact_core_mask"] = n  # the mask of the compacted path (no persistent tail)
+        kb["compact_slots"] = 0      # compaction moves no compulsory bytes
     dom = max(per_kernel.items(), key=lambda kv: kv[1][0]) if per_kernel else None
     roof = None
     if dom:
@@ -951,22 +971,6 @@ def main():
                 # 64 B DRAM granules, so traffic >> algorithmic bytes by construction
                 "dram_frac_of_peak": (round(traffic / (avg_ms / 1e3) / 1e9 / hbm, 4) if traffic else None),
                 "alg_bytes_per_launch": int(alg), "avg_launch_ms": round(avg_ms, 4)}
-    # Supplementary roof for the persistent round kernel: the time its random DRAM operations
-    # need at the rates measured on this pool (microbench/membench.cu, profiles/r01_membench.jsonl:
-    # 8 B random read-modify-write 20.1 G/s, 8 B random gather 37.1 G/s, 4 B test-and-clear on a
-    # ~100 MB bitmap 55.3 G/s).  Per round t >= nb+1: |F_t| entries (one test-and-clear each; for
-    # t >= 2 every frontier vertex has an entry), killed_t edge gathers, (r-1) killed_t RMWs.
-    rand = None
-    if k <= 2 and "peel_rounds_packed" in per_kernel:
-        first = max(nb, 1)
-        E = sum(F[first:])
-        Kt = sum(kl[nb:])
-        floor_ms = 1e3 * (Kt * (r - 1) / 20.1e9 + Kt / 37.1e9 + E / 55.3e9)
-        ms_k = per_kernel["peel_rounds_packed"][0] / per_kernel["peel_rounds_packed"][1]
-        rand = {"kernel": "peel_rounds_packed", "random_rmw": Kt * (r - 1), "random_gathers": Kt,
-                "bitmap_test_and_clear": E, "floor_ms_at_measured_random_rates": round(floor_ms, 3),
-                "kernel_ms": round(ms_k, 3), "frac": round(floor_ms / ms_k, 4),
-                "rates_source": "profiles/r01_membench.jsonl (B200, this pool)"}
     step_alg = b_build + b_rounds
     kernels = {nm: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
                for nm, v in per_kernel.items()}
@@ -1022,7 +1026,7 @@ def main():
                                   "frac_of_8TBs": round(step_alg / (ms_step / 1e3) / 8e12, 4)},
             "dram_step": dram_step(args.config, per_kernel, args.steps, ms_step, hbm),
             "roofline": roof, "kernels": kernels, "round_ms": round_ms,
-            "kernel_alg_bytes": kb, "random_access_roofline": rand, "cpu_baseline": cpu, "e2e": e2e,
+            "kernel_alg_bytes": kb, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks,
         }
         emit(line)

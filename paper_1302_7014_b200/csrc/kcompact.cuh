@@ -982,6 +982,29 @@ static double ctail_live_frac() {
     return e ? atof(e) : 0.11;
 }
 
+// a per-device side stream and two events for work that overlaps the round kernels
+struct SideStream {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+static SideStream &side_stream() {
+    static std::mutex mu;
+    static std::map<int, SideStream> per;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); dev = 0; }
+    SideStream &sd = per[dev];
+    if (!sd.s2) {
+        if (cudaStreamCreateWithFlags(&sd.s2, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd.ev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd.ev[1], cudaEventDisableTiming) != cudaSuccess) {
+            set_cuda_error(cudaGetLastError(), "side stream");
+            sd.s2 = nullptr;
+        }
+    }
+    return sd;
+}
+
 // compact when the live set has halved since the slots were laid out and the bytes a round
 // would stop prefetching (8 per dropped slot) pay for the records pass (n / 2 bytes)
 static bool compact_now(uint64_t n, uint64_t slots, uint64_t live) {
@@ -1109,6 +1132,8 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     int cb = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cb, ccompact_kernel<true>, CB_BLOCK, 0));
     cb = cb < 1 ? 1 : cb;
+    SideStream &sd = side_stream();
+    if (!sd.s2) return PEEL_ECUDA;
     const double frac = bin_round_frac(n), tail = ctail_live_frac();
     const bool compaction = compact_on();
     bool compacted = bcompact;
@@ -1152,18 +1177,27 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
             }
             return finish_kcore(n, cap, rounds, survivors, killed, ws, L, a, s);
         }
+        bool comp_pending = false;
         if (compaction && compact_now(n, nslots, live)) {
-            // lay the live states out densely: CB[nxt], slot counts slots[nxt], new records
+            // lay the live states out densely: CB[nxt], slot counts slots[nxt], new records.  On a
+            // side stream: this round's kill does not touch the slots and runs concurrently; the
+            // apply waits for the compaction.
             const int nxt = compacted ? cur ^ 1 : 0;
-            PEEL_CUDA(cudaMemsetAsync(slots[nxt], 0, sizeof(ull) * nbins, s));
-                c.Y = CB[nxt];
-            c.alloc = slots[nxt];
-            PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
+            PEEL_CUDA(cudaEventRecord(sd.ev[0], s));
+            PEEL_CUDA(cudaStreamWaitEvent(sd.s2, sd.ev[0], 0));
+            PEEL_CUDA(cudaMemsetAsync(slots[nxt], 0, sizeof(ull) * nbins, sd.s2));
+            PEEL_CUDA(cudaMemsetAsync(&ctl->cwork, 0, sizeof(ull), sd.s2));
+            CArgs cc = c;
+            cc.Y = CB[nxt];
+            cc.alloc = slots[nxt];
+            cc.work = &ctl->cwork;
             {
-                ProfScope ps("compact_slots", s);
-                if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, s>>>(c);
-                else ccompact_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, s>>>(c);
+                ProfScope ps("compact_slots", sd.s2);
+                if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+                else ccompact_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
             }
+            PEEL_CUDA(cudaEventRecord(sd.ev[1], sd.s2));
+            comp_pending = true;
             compacted = true;
             cur = nxt;
             c.X = CB[cur];
@@ -1182,6 +1216,7 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
             ProfScope ps("round_kill_partition", s);
             ckill_kernel<R><<<num_sms() * kb, PART_BLOCK, ksmem, s>>>(a, br, c);
         }
+        if (comp_pending) PEEL_CUDA(cudaStreamWaitEvent(s, sd.ev[1], 0));
         {
             ProfScope ps("round_apply", s);
             if (compacted) capply_kernel<R, true><<<num_sms() * (ab[1] < 1 ? 1 : ab[1]), CB_BLOCK, asmem, s>>>(c);

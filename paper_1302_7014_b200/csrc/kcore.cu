@@ -56,6 +56,7 @@ struct Ctl {
     uint32_t err;     // ERR_* bits
     uint32_t binovf;  // a vertex bin overflowed its capacity (binned build falls back)
     ull nlive[2];     // compacted rounds: live vertices after round t at nlive[t & 1] (build: [0])
+    ull cwork;        // compacted rounds: the compaction pass's work-item counter (side stream)
 };
 
 // compacted rounds (kcompact.cuh): group records, per-bin live counts, A-item counters,

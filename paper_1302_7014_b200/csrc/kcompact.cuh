@@ -91,6 +91,7 @@ struct CArgs {
     const ull *entries;
     ull *work;
     ull *live_total;         // build: vertices with count >= k
+    const uint4 *rows16;     // PEEL_ROWPAD (r = 3): 16-byte-aligned rows, one load per gather
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -704,7 +705,16 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
 #endif
             win[q] = i < nE && ((oldw[q] >> (ent[q].y & 31)) & 1u);
 #if !PEEL_KILL_SPEC
-            if (win[q]) load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
+            if (win[q]) {
+                if (R == 3 && c.rows16) {
+                    const uint4 rw = __ldg(c.rows16 + ent[q].y);
+                    ue[q][0] = rw.x;
+                    ue[q][1 % R] = rw.y;
+                    ue[q][2 % R] = rw.z;
+                } else {
+                    load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
+                }
+            }
 #endif
             kills += win[q];
         }
@@ -1032,10 +1042,13 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     int pblocks = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
     if (pblocks < 1) pblocks = 1;
+    const char *rpe = getenv("PEEL_ROWPAD");
+    uint4 *rows16 = (R == 3 && L.cl.rows16 && rpe && atoi(rpe) == 1) ? (uint4 *)(ws + L.cl.rows16) : nullptr;
     if (m && !es) {
         ProfScope ps("bin_partition", s);
         bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, nbins, cursor, bbase, bcap,
-                                                                               entries, &ctl->err, &ctl->binovf, 0ull, n, 0ull);
+                                                                               entries, &ctl->err, &ctl->binovf, 0ull, n, 0ull,
+                                                                               rows16);
     } else if (m) {  // chunk by chunk, each after its copy
         for (size_t i = 0; i < es->done.size(); i++) {
             const uint64_t e0 = i * es->chunk, e1 = std::min(m, e0 + es->chunk);
@@ -1043,7 +1056,7 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
             ProfScope ps("bin_partition", s);
             bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, e1, nbins, cursor, bbase,
                                                                                    bcap, entries, &ctl->err,
-                                                                                   &ctl->binovf, 0ull, n, e0);
+                                                                                   &ctl->binovf, 0ull, n, e0, rows16);
         }
     }
     PEEL_CUDA(cudaGetLastError());
@@ -1071,6 +1084,7 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     c.cursor = cursor; c.base = bbase; c.entries = entries;
     c.work = &ctl->work;
     c.X = state;  // identity slots until the first compaction
+    c.rows16 = rows16;
     // build: the full states, F_1 into fecnt[0]
     PEEL_CUDA(cudaMemsetAsync(fecnt[0], 0, sizeof(ull) * enb, s));
     c.fecnt = fecnt[0];

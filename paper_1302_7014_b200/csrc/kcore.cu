@@ -62,7 +62,7 @@ struct Ctl {
 // compacted rounds (kcompact.cuh): group records, per-bin live counts, A-item counters,
 // per-edge-bin frontier regions and their counts
 struct CompactLayout {
-    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe;
+    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe, rows16;
     uint64_t enb, fe_stride;
 };
 
@@ -151,6 +151,8 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         C.fecnt0 = o; o += al(sizeof(ull) * C.enb);
         C.fecnt1 = o; o += al(sizeof(ull) * C.enb);
         C.fe = o; o += al(sizeof(uint2) * C.enb * C.fe_stride);
+        C.rows16 = 0;
+        if (r == 3) { C.rows16 = o; o += al(16 * m); }  // PEEL_ROWPAD: 16-byte rows for the kill
     }
     L.total = o;
     return L;
@@ -233,7 +235,8 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
                                                                       ull *cursor, const ull *__restrict__ base,
                                                                       const ull *__restrict__ cap, ull *entries,
                                                                       uint32_t *err, uint32_t *binovf,
-                                                                      uint64_t v0, uint64_t v1, uint64_t e0) {
+                                                                      uint64_t v0, uint64_t v1, uint64_t e0,
+                                                                      uint4 *rows16 = nullptr) {
     constexpr int CH = PART_ENTRIES / R;  // edges per chunk
     constexpr int CW = CH * R;            // edge words per chunk
     constexpr int CWP = (CW + 3) & ~3;    // padded: keeps every array below 16-byte aligned
@@ -280,6 +283,9 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
                 #pragma unroll
                 for (int q = j + 1; q < R; q++) ok &= words[i * R + j] != words[i * R + q];
             okb[i] = ok;
+            // r = 3: a 16-byte-aligned copy of the row for the kill phase's gathers (PEEL_ROWPAD)
+            if (R == 3 && rows16)
+                rows16[c0 + i] = make_uint4(words[i * R], words[i * R + (1 % R)], words[i * R + (2 % R)], 0u);
             if (!ok) atomicOr(err, ERR_BADVERTEX);
         }
         __syncthreads();

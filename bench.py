@@ -608,7 +608,7 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
     m_all, seeds_all = S.paper_trials(T, n=n)
     lo, hi = S.shard(T, ws, rank)
     m, seeds = m_all[lo:hi], seeds_all[lo:hi]
-    batch = 128  # measured: 32 / 64 / 128 / 256 / 512 -> 2177 / 1756 / 1547 / 1970 / 2346 ms for 10^4 trials
+    batch = int(os.environ.get("PEEL_SWEEP_BATCH", "128"))  # r01: 32 / 64 / 128 / 256 / 512 -> 2177 / 1756 / 1547 / 1970 / 2346 ms
     wsb = int(pk.lib().peel_sweep_workspace_bytes(n, int(m_all.max()), r, k, batch))
     wsp = torch.empty((wsb,), dtype=torch.uint8, device=dev)
     for _ in range(max(args.warmup, 3)):

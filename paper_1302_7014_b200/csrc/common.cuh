@@ -32,8 +32,8 @@ void set_cuda_error(cudaError_t e, const char *where);
 // per-call launch accounting + optional CUDA-event profiling (peel.h)
 // ---------------------------------------------------------------------------
 void prof_begin_call();                                   // resets the per-call tables
-void prof_pre(const char *name, cudaStream_t s);          // before a kernel launch
-void prof_post(const char *name, cudaStream_t s);         // after it (counts the launch)
+int prof_pre(const char *name, cudaStream_t s);           // before a kernel launch: its entry, or -1
+void prof_post(int entry, cudaStream_t s);                // after it (counts the launch)
 int prof_collect();                                       // after stream sync: resolve events
 bool prof_enabled();
 void prof_hold(bool on);  // nest public calls inside one report (peel_sweep)
@@ -44,12 +44,17 @@ void prof_set_rounds(const std::vector<double> &ms);      // per-round device ti
 struct ProfScope {
     const char *name;
     cudaStream_t s;
-    ProfScope(const char *n, cudaStream_t st) : name(n), s(st) { prof_pre(n, st); }
-    ~ProfScope() { prof_post(name, s); }
+    int entry;
+    ProfScope(const char *n, cudaStream_t st) : name(n), s(st) { entry = prof_pre(n, st); }
+    ~ProfScope() { prof_post(entry, s); }
 };
 
 // number of SMs and cooperative occupancy helpers
 int num_sms();
+
+// raise (never lower) a kernel's dynamic shared-memory limit on the current device: host threads
+// calling the library concurrently with different sizes must not lower another's launch limit
+cudaError_t raise_smem(const void *kern, size_t bytes);
 
 // generator launch shared by peel_gen_hypergraph and peel_sweep (gen.cu)
 peel_status launch_gen_edges(uint64_t n, uint64_t m, uint32_t r, uint64_t seed, uint32_t *edges, uint32_t voff,

@@ -610,7 +610,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 a.Fc = d.F[nxt];
                 cu(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s), "memset cursor");
                 const size_t sm = dist_stage_smem(R, bv.nbins);
-                cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "attr");
+                cu(raise_smem((const void *)dist_kill_bin_kernel<R, false>, sm), "attr");
                 cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 72), "attr");
                 int kb = 0;
                 cu(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, false>, DB, sm), "occupancy");
@@ -718,7 +718,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
                 if (nrecv[i]) {
                     const size_t sm = dist_stage_smem(R, bv.nbins);
-                    cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "attr");
+                    cu(raise_smem((const void *)dist_kill_bin_kernel<R, true>, sm), "attr");
                     cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 72), "attr");
                     int kb = 0;
                     cu(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, true>, DB, sm), "occupancy");

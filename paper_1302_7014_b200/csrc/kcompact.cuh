@@ -91,7 +91,6 @@ struct CArgs {
     const ull *entries;
     ull *work;
     ull *live_total;         // build: vertices with count >= k
-    const uint4 *rows16;     // PEEL_ROWPAD (r = 3): 16-byte-aligned rows, one load per gather
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -363,261 +362,65 @@ __global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_kernel(CArgs a) {
     const ull mask = (1ull << BIN_SHIFT) - 1;
     constexpr int SU = PEEL_CB_SU;  // states per thread per scan step
     ull leavers = 0, emitted = 0, kept = 0;
-    for (uint32_t b = 0; b <= a.nbins; b++) {
-        if (b > 0) {  // scan bin b-1 (still in L2), overlapped with zeroing bin b
-            const uint64_t lo = (uint64_t)(b - 1) << BIN_SHIFT, hi = lo + bin_size(a.n, b - 1);
-            for (uint64_t base = lo + (uint64_t)blockIdx.x * CB_BLOCK * SU; base < hi;
-                 base += (uint64_t)gridDim.x * CB_BLOCK * SU) {
-                ull w[SU];
-                #pragma unroll
-                for (int j = 0; j < SU; j++) {
-                    const uint64_t v = base + (uint64_t)j * CB_BLOCK + threadIdx.x;
-                    w[j] = v < hi ? __ldcg(a.X + v) : ~0ull;
-                }
-                #pragma unroll
-                for (int j = 0; j < SU; j++) {
-                    const uint64_t v = base + (uint64_t)j * CB_BLOCK + threadIdx.x;
-                    if (v >= hi) continue;
-                    const uint32_t c = (uint32_t)w[j];
-                    if (c >= a.k) { kept++; continue; }
-                    leavers++;
-                    if (a.peel_round) a.peel_round[v] = 1;
-                    if (c == 1u) {  // k = 2: its one edge is the id sum
-                        emitted++;
-                        fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(w[j] >> 32)));
-                    }
-                }
-                __syncthreads();  // every push of this step landed: one decision for the block
-                if (fen >= FE_CAP_B - CB_BLOCK * SU) fe_flush<FE_CAP_B>(f, a);
-                __syncthreads();
+    auto scan_bin = [&](uint32_t sb) {  // bin sb's states (in L2): F_1 entries, leavers, survivors
+        const uint64_t lo = (uint64_t)sb << BIN_SHIFT, hi = lo + bin_size(a.n, sb);
+        for (uint64_t base = lo + (uint64_t)blockIdx.x * CB_BLOCK * SU; base < hi;
+             base += (uint64_t)gridDim.x * CB_BLOCK * SU) {
+            ull w[SU];
+            #pragma unroll
+            for (int j = 0; j < SU; j++) {
+                const uint64_t v = base + (uint64_t)j * CB_BLOCK + threadIdx.x;
+                w[j] = v < hi ? __ldcg(a.X + v) : ~0ull;
             }
-        }
-        if (b < a.nbins) {
-            const uint64_t lo = (uint64_t)b << BIN_SHIFT, sz = bin_size(a.n, b);
-            ulonglong2 *z = reinterpret_cast<ulonglong2 *>(a.X + lo);  // lo is 2^22-aligned
-            for (uint64_t i = tid; i < sz / 2; i += nthr) z[i] = make_ulonglong2(0ull, 0ull);
-            if ((sz & 1) && tid == 0) a.X[lo + sz - 1] = 0ull;
-        }
-        grid.sync();
-        if (b < a.nbins) {
-            // RU entry loads in flight per thread before their REDs (one load at a time left the
-            // loop waiting on DRAM latency: the load -> RED dependency was ncu's top stall)
-            constexpr int RU = PEEL_CB_RU;
-            ull *st = a.X + ((uint64_t)b << BIN_SHIFT);
-            const ull *ent = a.entries + a.base[b];
-            const ull cnt = a.cursor[b];
-            for (ull i0 = tid; i0 < cnt; i0 += RU * nthr) {
-                ull x[RU];
-                #pragma unroll
-                for (int u = 0; u < RU; u++) {
-                    const ull i = i0 + (ull)u * nthr;
-                    x[u] = i < cnt ? __ldcs(ent + i) : 0ull;
+            #pragma unroll
+            for (int j = 0; j < SU; j++) {
+                const uint64_t v = base + (uint64_t)j * CB_BLOCK + threadIdx.x;
+                if (v >= hi) continue;
+                const uint32_t c = (uint32_t)w[j];
+                if (c >= a.k) { kept++; continue; }
+                leavers++;
+                if (a.peel_round) a.peel_round[v] = 1;
+                if (c == 1u) {  // k = 2: its one edge is the id sum
+                    emitted++;
+                    fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(w[j] >> 32)));
                 }
-                #pragma unroll
-                for (int u = 0; u < RU; u++)
-                    if (i0 + (ull)u * nthr < cnt) atomicAdd(st + (x[u] & mask), (x[u] & ~0xFFFFFFFFull) + 1ull);
             }
+            __syncthreads();  // every push of this step landed: one decision for the block
+            if (fen >= FE_CAP_B - CB_BLOCK * SU) fe_flush<FE_CAP_B>(f, a);
+            __syncthreads();
         }
-        grid.sync();
-    }
-    fe_flush<FE_CAP_B>(f, a);
-    block_add<CB_BLOCK>(&a.ctl->nf[0], leavers);
-    block_add<CB_BLOCK>(&a.ctl->ne[0], emitted);
-    block_add<CB_BLOCK>(a.live_total, kept);
-}
-
-// ---- build as a dataflow (PEEL_BUILD_DF, default): the same three phases per bin -- zero
-// Z(b), REDs R(b), scan S(b) -- as work items handed out by a counter in the order
-// Z(0) R(0) | Z(1) R(1) S(0) | Z(2) R(2) S(1) | ... | S(nb-1), with no grid barrier: an R(b)
-// item waits (spinning on a per-bin counter) until Z(b) is done, an S(b) item until R(b) is.
-// Every wait is on items handed out earlier, so it always ends.  Bin b's scan overlaps bin
-// b+1's REDs and bin b+2's zeroing instead of waiting at a barrier for the slowest block.
-static constexpr uint32_t DZ_BYTES = 256u << 10;  // zeroed per Z item
-static constexpr uint32_t DR_ENT = 4096;          // entries per R item (16 per thread)
-static constexpr uint32_t DS_SU = 4;              // states per thread per scan step
-static constexpr uint32_t DS_STEPS = 4;           // scan steps per S item (4096 states)
-static_assert(CB_BLOCK * DS_SU * DS_STEPS == 4096, "an S item is 64 groups");
-
-__host__ __device__ inline uint32_t df_seg_kind(uint32_t s, uint32_t nb, uint32_t &b) {  // 0 Z, 1 R, 2 S
-    if (s == 0) { b = 0; return 0; }
-    if (s == 1) { b = 0; return 1; }
-    if (s == 3 * nb - 1) { b = nb - 1; return 2; }
-    const uint32_t q = (s + 1) / 3, r = (s + 1) % 3;  // s = 3q - 1 + r
-    if (r == 0) { b = q; return 0; }
-    if (r == 1) { b = q; return 1; }
-    b = q - 1;
-    return 2;
-}
-
-// COUT: the scan also lays out the bin's live states as compacted slots (CArgs::Y, records,
-// alloc = slots per bin), so the rounds start compacted: S items then cover 64 groups, warp w
-// taking 8 of them, lane = vertex within the group (two passes: count + emit, then write).
-template <int R, bool COUT>
-__global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_df_kernel(CArgs a, uint32_t *zdone, uint32_t *rdone) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ uint32_t fen;
-    __shared__ ull item;
-    const uint32_t nb = a.nbins, ns = 3 * nb;
-    const FeView f = fe_view<FE_CAP_B>(smem_raw, a.enb, &fen);
-    uint32_t *pre = (uint32_t *)(f.offs + a.enb);  // [3 nb + 1] items before segment s
-    auto nitems_of = [&](uint32_t kind, uint32_t b) -> uint32_t {
-        const uint64_t sz = bin_size(a.n, b);
-        if (kind == 0) return (uint32_t)((sz * sizeof(ull) + DZ_BYTES - 1) / DZ_BYTES);
-        if (kind == 1) return (uint32_t)((ld_cg_u64(a.cursor + b) + DR_ENT - 1) / DR_ENT);
-        return (uint32_t)((sz + 4095) / 4096);  // CB_BLOCK DS_SU DS_STEPS = 64 groups = 4096 states
     };
-    if (threadIdx.x == 0) fen = 0;
-    for (uint32_t s = threadIdx.x; s < ns; s += CB_BLOCK) {
-        uint32_t b;
-        const uint32_t kind = df_seg_kind(s, nb, b);
-        pre[s] = nitems_of(kind, b);
-    }
-    block_excl_scan(pre, ns);
-    const uint32_t nitems = pre[ns];
-    const ull mask = (1ull << BIN_SHIFT) - 1;
-    ull leavers = 0, emitted = 0, kept = 0;
-    for (;;) {
-        if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
-        __syncthreads();
-        const ull c = item;
-        if (c >= nitems) break;
-        uint32_t lo = 0, hi = ns;
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (pre[mid] <= c) lo = mid; else hi = mid;
-        }
-        uint32_t b;
-        const uint32_t kind = df_seg_kind(lo, nb, b), j = (uint32_t)c - pre[lo];
-        const uint64_t v0 = (uint64_t)b << BIN_SHIFT, sz = bin_size(a.n, b);
-        if (kind == 0) {  // zero bytes [j DZ, (j+1) DZ) of the bin's states
-            const uint64_t w0 = (uint64_t)j * (DZ_BYTES / 16), w1 = min(w0 + DZ_BYTES / 16, sz / 2);
-            ulonglong2 *z = reinterpret_cast<ulonglong2 *>(a.X + v0);
-            for (uint64_t i = w0 + threadIdx.x; i < w1; i += CB_BLOCK) z[i] = make_ulonglong2(0ull, 0ull);
-            if ((sz & 1) && threadIdx.x == 0 && w1 == sz / 2) a.X[v0 + sz - 1] = 0ull;
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) atomicAdd(zdone + b, 1u);
-        } else if (kind == 1) {  // REDs of entries [j DR, (j+1) DR)
-            if (threadIdx.x == 0) {
-                const uint32_t need = nitems_of(0, b);
-                while (*(volatile uint32_t *)(zdone + b) < need) __nanosleep(100);
-                __threadfence();
-            }
-            __syncthreads();
-            const ull cnt = ld_cg_u64(a.cursor + b);
-            const ull *ent = a.entries + a.base[b] + (ull)j * DR_ENT;
-            const uint32_t nin = (uint32_t)min((ull)DR_ENT, cnt - (ull)j * DR_ENT);
-            ull *st = a.X + v0;
-            constexpr int U = DR_ENT / CB_BLOCK;
-            ull x[U];
+    auto zero_bin = [&](uint32_t zb) {
+        const uint64_t lo = (uint64_t)zb << BIN_SHIFT, sz = bin_size(a.n, zb);
+        ulonglong2 *z = reinterpret_cast<ulonglong2 *>(a.X + lo);  // lo is 2^22-aligned
+        for (uint64_t i = tid; i < sz / 2; i += nthr) z[i] = make_ulonglong2(0ull, 0ull);
+        if ((sz & 1) && tid == 0) a.X[lo + sz - 1] = 0ull;
+    };
+    auto red_bin = [&](uint32_t rb) {
+        // RU entry loads in flight per thread before their REDs (one load at a time left the
+        // loop waiting on DRAM latency: the load -> RED dependency was ncu's top stall)
+        constexpr int RU = PEEL_CB_RU;
+        ull *st = a.X + ((uint64_t)rb << BIN_SHIFT);
+        const ull *ent = a.entries + a.base[rb];
+        const ull cnt = a.cursor[rb];
+        for (ull i0 = tid; i0 < cnt; i0 += RU * nthr) {
+            ull x[RU];
             #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t i = u * CB_BLOCK + threadIdx.x;
-                x[u] = i < nin ? __ldcs(ent + i) : 0ull;
+            for (int u = 0; u < RU; u++) {
+                const ull i = i0 + (ull)u * nthr;
+                x[u] = i < cnt ? __ldcs(ent + i) : 0ull;
             }
             #pragma unroll
-            for (int u = 0; u < U; u++)
-                if (u * CB_BLOCK + threadIdx.x < nin) atomicAdd(st + (x[u] & mask), (x[u] & ~0xFFFFFFFFull) + 1ull);
-            __threadfence();
-            __syncthreads();
-            if (threadIdx.x == 0) atomicAdd(rdone + b, 1u);
-        } else {  // scan states [j 4096, (j+1) 4096): F_1 entries, leavers, survivors
-            if (threadIdx.x == 0) {
-                const uint32_t need = nitems_of(1, b);
-                while (*(volatile uint32_t *)(rdone + b) < need) __nanosleep(100);
-                __threadfence();
-            }
-            __syncthreads();
-            if (COUT) {
-                __shared__ uint32_t wsh[CB_BLOCK / 32 + 1];
-                const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-                const uint64_t gb0 = v0 >> 6, gend = gb0 + bin_groups(a.n, b);
-                const uint64_t gw0 = gb0 + (uint64_t)j * 64 + (uint64_t)w * 8;  // this warp's 8 groups
-                uint32_t keepcnt = 0;
-                #pragma unroll 2
-                for (int gi = 0; gi < 8; gi++) {
-                    const uint64_t g = gw0 + gi;
-                    #pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        const uint64_t v = (g << 6) + 32 * h + lane;
-                        const bool valid = g < gend && v < v0 + sz;
-                        const ull st = valid ? __ldcg(a.X + v) : 0ull;
-                        const uint32_t cn = (uint32_t)st;
-                        const bool keep = valid && cn >= a.k;
-                        keepcnt += __popc(__ballot_sync(0xffffffffu, keep));
-                        if (valid && !keep) {
-                            leavers++;
-                            if (a.peel_round) a.peel_round[v] = 1;
-                            if (cn == 1u) {
-                                emitted++;
-                                fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(st >> 32)));
-                            }
-                        }
-                    }
-                }
-                if (lane == 0) wsh[w] = keepcnt;
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    uint32_t tot = 0;
-                    for (int q = 0; q < CB_BLOCK / 32; q++) { const uint32_t cq = wsh[q]; wsh[q] = tot; tot += cq; }
-                    const ull bb = tot ? atomicAdd(a.alloc + b, (ull)tot) : 0ull;
-                    wsh[CB_BLOCK / 32] = (uint32_t)(v0 + bb);
-                }
-                __syncthreads();
-                uint32_t run = wsh[CB_BLOCK / 32] + wsh[w];
-                kept += lane == 0 ? keepcnt : 0;
-                #pragma unroll 2
-                for (int gi = 0; gi < 8; gi++) {
-                    const uint64_t g = gw0 + gi;
-                    ull st[2];
-                    bool kp[2];
-                    #pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        const uint64_t v = (g << 6) + 32 * h + lane;
-                        const bool valid = g < gend && v < v0 + sz;
-                        st[h] = valid ? __ldcg(a.X + v) : 0ull;
-                        kp[h] = valid && (uint32_t)st[h] >= a.k;
-                    }
-                    const uint32_t b0 = __ballot_sync(0xffffffffu, kp[0]), b1 = __ballot_sync(0xffffffffu, kp[1]);
-                    if (kp[0]) a.Y[run + __popc(b0 & lanemask_lt())] = st[0];
-                    if (kp[1]) a.Y[run + __popc(b0) + __popc(b1 & lanemask_lt())] = st[1];
-                    if (lane == 0 && g < gend)
-                        __stcg(reinterpret_cast<uint4 *>(a.recs + g), make_uint4(b0, b1, run, 0u));
-                    run += __popc(b0) + __popc(b1);
-                }
-                __syncthreads();  // every push of this item landed: one decision for the block
-                if (fen >= FE_CAP_B / 2) fe_flush<FE_CAP_B>(f, a);  // past FE_CAP_B: direct appends
-                __syncthreads();
-                continue;
-            }
-            const uint64_t lo2 = v0 + (uint64_t)j * CB_BLOCK * DS_SU * DS_STEPS;
-            const uint64_t hi2 = min(lo2 + CB_BLOCK * DS_SU * DS_STEPS, v0 + sz);
-            for (uint64_t base = lo2; base < hi2; base += CB_BLOCK * DS_SU) {
-                ull w[DS_SU];
-                #pragma unroll
-                for (int u = 0; u < (int)DS_SU; u++) {
-                    const uint64_t v = base + (uint64_t)u * CB_BLOCK + threadIdx.x;
-                    w[u] = v < hi2 ? __ldcg(a.X + v) : ~0ull;
-                }
-                #pragma unroll
-                for (int u = 0; u < (int)DS_SU; u++) {
-                    const uint64_t v = base + (uint64_t)u * CB_BLOCK + threadIdx.x;
-                    if (v >= hi2) continue;
-                    const uint32_t cn = (uint32_t)w[u];
-                    if (cn >= a.k) { kept++; continue; }
-                    leavers++;
-                    if (a.peel_round) a.peel_round[v] = 1;
-                    if (cn == 1u) {  // k = 2: its one edge is the id sum
-                        emitted++;
-                        fe_push<FE_CAP_B>(f, a, make_uint2((uint32_t)v, (uint32_t)(w[u] >> 32)));
-                    }
-                }
-                __syncthreads();  // every push of this step landed: one decision for the block
-                if (fen >= FE_CAP_B - CB_BLOCK * DS_SU) fe_flush<FE_CAP_B>(f, a);
-                __syncthreads();
-            }
+            for (int u = 0; u < RU; u++)
+                if (i0 + (ull)u * nthr < cnt) atomicAdd(st + (x[u] & mask), (x[u] & ~0xFFFFFFFFull) + 1ull);
         }
-        __syncthreads();  // item is rewritten next iteration
+    };
+    for (uint32_t b = 0; b <= a.nbins; b++) {
+        if (b > 0) scan_bin(b - 1);  // bin b-1 (still in L2), overlapped with zeroing bin b
+        if (b < a.nbins) zero_bin(b);
+        grid.sync();
+        if (b < a.nbins) red_bin(b);
+        grid.sync();
     }
     fe_flush<FE_CAP_B>(f, a);
     block_add<CB_BLOCK>(&a.ctl->nf[0], leavers);
@@ -705,16 +508,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
 #endif
             win[q] = i < nE && ((oldw[q] >> (ent[q].y & 31)) & 1u);
 #if !PEEL_KILL_SPEC
-            if (win[q]) {
-                if (R == 3 && c.rows16) {
-                    const uint4 rw = __ldg(c.rows16 + ent[q].y);
-                    ue[q][0] = rw.x;
-                    ue[q][1 % R] = rw.y;
-                    ue[q][2 % R] = rw.z;
-                } else {
-                    load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
-                }
-            }
+            if (win[q]) load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
 #endif
             kills += win[q];
         }
@@ -984,12 +778,20 @@ static bool compact_on() {
     return !(e && atoi(e) == 0);
 }
 
-// a small frontier with a large live set (above threshold) is cheaper on the persistent
-// kernel after one write-back of the full state: a compact round streams 16 B per live vertex
-// and 1/4 B per vertex of records, the write-back 8 B per vertex once
+// A small frontier with a large live set (above threshold) is cheaper on the persistent
+// kernel after one write-back of the full state (8 B per vertex, once): a compacted round
+// streams 8 B per SLOT whatever the frontier, the persistent kernel pays per frontier entry
+// (a few random 64 B DRAM granules).  Hand over when the live set is >= PEEL_COMPACT_TAIL n
+// (default 0.11) and there are >= PEEL_COMPACT_TAIL_RATIO (default 64) slots per entry.
+// Measured: C4a 9.70 ms compacted to the end against 7.11 handed over; C3 13.39 against 14.95
+// when the live-set rule alone handed its rounds over at the first 5% frontier.
 static double ctail_live_frac() {
     const char *e = getenv("PEEL_COMPACT_TAIL");
     return e ? atof(e) : 0.11;
+}
+static double ctail_ratio() {
+    const char *e = getenv("PEEL_COMPACT_TAIL_RATIO");
+    return e ? atof(e) : 64.0;
 }
 
 // a per-device side stream and two events for work that overlaps the round kernels
@@ -998,9 +800,9 @@ struct SideStream {
     cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 static SideStream &side_stream() {
-    static std::mutex mu;
-    static std::map<int, SideStream> per;
-    std::lock_guard<std::mutex> lock(mu);
+    // per host thread and device: concurrent calls from several threads (peel_sweep's batch
+    // workers) must not share the side stream's events
+    static thread_local std::map<int, SideStream> per;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); dev = 0; }
     SideStream &sd = per[dev];
@@ -1038,17 +840,14 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
         bin_init_kernel<<<1, 32, 0, s>>>(n, n, m, R, L.nbins, cursor, bbase, bcap);
     }
     const size_t smem = partition_smem(R, L.nbins);
-    PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PEEL_CUDA(raise_smem((const void *)bin_partition_kernel<R>, smem));
     int pblocks = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
     if (pblocks < 1) pblocks = 1;
-    const char *rpe = getenv("PEEL_ROWPAD");
-    uint4 *rows16 = (R == 3 && L.cl.rows16 && rpe && atoi(rpe) == 1) ? (uint4 *)(ws + L.cl.rows16) : nullptr;
     if (m && !es) {
         ProfScope ps("bin_partition", s);
         bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, m, nbins, cursor, bbase, bcap,
-                                                                               entries, &ctl->err, &ctl->binovf, 0ull, n, 0ull,
-                                                                               rows16);
+                                                                               entries, &ctl->err, &ctl->binovf, 0ull, n, 0ull);
     } else if (m) {  // chunk by chunk, each after its copy
         for (size_t i = 0; i < es->done.size(); i++) {
             const uint64_t e0 = i * es->chunk, e1 = std::min(m, e0 + es->chunk);
@@ -1056,7 +855,7 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
             ProfScope ps("bin_partition", s);
             bin_partition_kernel<R><<<num_sms() * pblocks, PART_BLOCK, smem, s>>>(edges, n, e1, nbins, cursor, bbase,
                                                                                    bcap, entries, &ctl->err,
-                                                                                   &ctl->binovf, 0ull, n, e0, rows16);
+                                                                                   &ctl->binovf, 0ull, n, e0);
         }
     }
     PEEL_CUDA(cudaGetLastError());
@@ -1084,38 +883,13 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     c.cursor = cursor; c.base = bbase; c.entries = entries;
     c.work = &ctl->work;
     c.X = state;  // identity slots until the first compaction
-    c.rows16 = rows16;
     // build: the full states, F_1 into fecnt[0]
     PEEL_CUDA(cudaMemsetAsync(fecnt[0], 0, sizeof(ull) * enb, s));
     c.fecnt = fecnt[0];
     c.live_total = &ctl->nlive[0];
-    const char *dfe = getenv("PEEL_BUILD_DF");
-    const bool dataflow = dfe && atoi(dfe) == 1;  // measured slower than the cooperative build (97.3 vs 89.7 ms at C5)
-    // the dataflow build can lay out compacted slots itself (PEEL_BUILD_COMPACT, default on)
-    const char *bce = getenv("PEEL_BUILD_COMPACT");
-    const bool bcompact = dataflow && compact_on() && !(bce && atoi(bce) == 0);
-    if (bcompact) {
-        PEEL_CUDA(cudaMemsetAsync(slots[0], 0, sizeof(ull) * nbins, s));
-        c.Y = CB[0];
-        c.alloc = slots[0];
-    }
-    if (dataflow) {
-        // dataflow build: per-bin completion counters (zdone, rdone) in the A-item counter area
-        uint32_t *zdone = (uint32_t *)(ws + CL.adone), *rdone = zdone + nbins;
-        PEEL_CUDA(cudaMemsetAsync(zdone, 0, sizeof(uint32_t) * 2 * nbins, s));
-        PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
-        const size_t bs = fe_smem(FE_CAP_B, enb) + sizeof(uint32_t) * (3 * nbins + 1);
-        PEEL_CUDA(cudaFuncSetAttribute(cbuild_df_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
-        PEEL_CUDA(cudaFuncSetAttribute(cbuild_df_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
-        int per_sm = 0;
-        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cbuild_df_kernel<R, true>, CB_BLOCK, bs));
-        if (per_sm < 1) per_sm = 1;
-        ProfScope ps("bin_accumulate", s);
-        if (bcompact) cbuild_df_kernel<R, true><<<num_sms() * per_sm, CB_BLOCK, bs, s>>>(c, zdone, rdone);
-        else cbuild_df_kernel<R, false><<<num_sms() * per_sm, CB_BLOCK, bs, s>>>(c, zdone, rdone);
-    } else {
+    {
         const size_t bs = fe_smem(FE_CAP_B, enb);
-        PEEL_CUDA(cudaFuncSetAttribute(cbuild_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
+        PEEL_CUDA(raise_smem((const void *)cbuild_kernel<R>, bs));
         int per_sm = 0;
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cbuild_kernel<R>, CB_BLOCK, bs));
         if (per_sm < 1) per_sm = 1;
@@ -1132,15 +906,15 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     br.entries = entries;
     br.work = &ctl->work;
     const size_t ksmem = ckill_smem(R, nbins, enb);
-    PEEL_CUDA(cudaFuncSetAttribute(ckill_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem));
+    PEEL_CUDA(raise_smem((const void *)ckill_kernel<R>, ksmem));
     PEEL_CUDA(cudaFuncSetAttribute(ckill_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
     int kb = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, ckill_kernel<R>, PART_BLOCK, ksmem));
     kb = kb < 1 ? 1 : kb;
     const size_t asmem = capply_smem(nbins, enb);
     int ab[2] = {0, 0};
-    PEEL_CUDA(cudaFuncSetAttribute(capply_kernel<R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
-    PEEL_CUDA(cudaFuncSetAttribute(capply_kernel<R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asmem));
+    PEEL_CUDA(raise_smem((const void *)capply_kernel<R, false>, asmem));
+    PEEL_CUDA(raise_smem((const void *)capply_kernel<R, true>, asmem));
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ab[0], capply_kernel<R, false>, CB_BLOCK, asmem));
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ab[1], capply_kernel<R, true>, CB_BLOCK, asmem));
     int cb = 0;
@@ -1148,24 +922,21 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     cb = cb < 1 ? 1 : cb;
     SideStream &sd = side_stream();
     if (!sd.s2) return PEEL_ECUDA;
-    const double frac = bin_round_frac(n), tail = ctail_live_frac();
+    const double frac = bin_round_frac(n), tail = ctail_live_frac(), tratio = ctail_ratio();
     const bool compaction = compact_on();
-    bool compacted = bcompact;
+    bool compacted = false;
     int cur = 0;             // compacted: the slots live in CB[cur], their counts per bin in slots[cur]
     PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
     PEEL_CUDA(cudaStreamSynchronize(s));
     uint64_t live = h.nlive[0];
-    uint64_t nslots = bcompact ? live : n;  // slots laid out (identity: every vertex)
-    if (bcompact) {
-        c.X = CB[0];
-        c.slots = slots[0];
-    }
+    uint64_t nslots = n;     // slots laid out (identity: every vertex)
     uint32_t t = 1;
     for (;;) {
         const ull nF = h.nf[(t - 1) % 3], nE = h.ne[(t - 1) % 3];
         if (t > 1) live -= nF;  // the vertices of F_t left L in round t-1
         if (nF == 0) break;
-        if ((double)nE < frac * (double)n && (double)live >= tail * (double)n) {
+        if ((double)nE < frac * (double)n && (double)live >= tail * (double)n &&
+            (double)nslots >= tratio * (double)nE) {
             // the persistent kernel takes the remaining rounds from round t
             if (compacted) {
                 ProfScope ps("compact_writeback", s);

@@ -62,7 +62,7 @@ struct Ctl {
 // compacted rounds (kcompact.cuh): group records, per-bin live counts, A-item counters,
 // per-edge-bin frontier regions and their counts
 struct CompactLayout {
-    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe, rows16;
+    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe;
     uint64_t enb, fe_stride;
 };
 
@@ -151,8 +151,6 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         C.fecnt0 = o; o += al(sizeof(ull) * C.enb);
         C.fecnt1 = o; o += al(sizeof(ull) * C.enb);
         C.fe = o; o += al(sizeof(uint2) * C.enb * C.fe_stride);
-        C.rows16 = 0;
-        if (r == 3) { C.rows16 = o; o += al(16 * m); }  // PEEL_ROWPAD: 16-byte rows for the kill
     }
     L.total = o;
     return L;
@@ -235,8 +233,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
                                                                       ull *cursor, const ull *__restrict__ base,
                                                                       const ull *__restrict__ cap, ull *entries,
                                                                       uint32_t *err, uint32_t *binovf,
-                                                                      uint64_t v0, uint64_t v1, uint64_t e0,
-                                                                      uint4 *rows16 = nullptr) {
+                                                                      uint64_t v0, uint64_t v1, uint64_t e0) {
     constexpr int CH = PART_ENTRIES / R;  // edges per chunk
     constexpr int CW = CH * R;            // edge words per chunk
     constexpr int CWP = (CW + 3) & ~3;    // padded: keeps every array below 16-byte aligned
@@ -283,9 +280,6 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
                 #pragma unroll
                 for (int q = j + 1; q < R; q++) ok &= words[i * R + j] != words[i * R + q];
             okb[i] = ok;
-            // r = 3: a 16-byte-aligned copy of the row for the kill phase's gathers (PEEL_ROWPAD)
-            if (R == 3 && rows16)
-                rows16[c0 + i] = make_uint4(words[i * R], words[i * R + (1 % R)], words[i * R + (2 % R)], 0u);
             if (!ok) atomicOr(err, ERR_BADVERTEX);
         }
         __syncthreads();
@@ -1650,14 +1644,10 @@ static int cluster_eligible(uint64_t n, uint64_t m, const void *kern) {
         if (shp.smem + 4096 > (size_t)optin[dev]) continue;  // + static shared memory
         const size_t smem4k = (shp.smem + 4095) & ~(size_t)4095;
         const auto key = std::make_tuple(dev, kern, cs, smem4k);
-        // the dynamic-smem attribute is per function and only ever raised here
-        static std::map<const void *, size_t> attr;
-        if (attr[kern] < smem4k) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4k) != cudaSuccess) {
-                cudaGetLastError();
-                continue;
-            }
-            attr[kern] = smem4k;
+        // the dynamic-smem attribute: per (device, function), only ever raised (raise_smem)
+        if (raise_smem((const void *)kern, smem4k) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
         }
         auto it = ok.find(key);
         if (it == ok.end()) {
@@ -1892,7 +1882,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
             bin_init_kernel<<<1, 32, 0, s>>>(n, n, m, R, L.nbins, cursor, bbase, bcap);
         }
         const size_t smem = partition_smem(R, L.nbins);
-        PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PEEL_CUDA(raise_smem((const void *)bin_partition_kernel<R>, smem));
         int pblocks = 0;
         PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
         if (pblocks < 1) pblocks = 1;
@@ -1951,7 +1941,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
                 bin_init_kernel<<<1, 32, 0, s>>>(n, n, m, R, L.nbins, cursor, bbase, bcap);
             }
             const size_t smem = partition_smem(R, L.nbins);
-            PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PEEL_CUDA(raise_smem((const void *)bin_partition_kernel<R>, smem));
             int pblocks = 0;
             PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pblocks, bin_partition_kernel<R>, PART_BLOCK, smem));
             pblocks = pblocks < 1 ? 1 : pblocks;
@@ -2015,8 +2005,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         br.entries = (ull *)(ws + L.entries);
         br.work = &ctl->work;
         const size_t ksmem = kill_partition_smem(R, br.nbins);
-        PEEL_CUDA(cudaFuncSetAttribute(round_kill_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ksmem));
+        PEEL_CUDA(raise_smem((const void *)round_kill_partition_kernel<R>, ksmem));
         // keep >= 60 KB of L1 for the row gathers: with the shared-memory carve-out at 86-100%
         // (28 KB L1 or less) the C5 kill phase takes 43 ms instead of 24.5 (72% and 58%: 24.5-24.7)
         PEEL_CUDA(cudaFuncSetAttribute(round_kill_partition_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 72));
@@ -2039,7 +2028,7 @@ static peel_status run_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint
         const size_t essmem = esort_scatter_smem(enb);
         if (esort) {
             PEEL_CUDA(cudaMemsetAsync(ehist[1], 0, sizeof(ull) * (enb + 1), s));
-            PEEL_CUDA(cudaFuncSetAttribute(esort_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)essmem));
+            PEEL_CUDA(raise_smem((const void *)esort_scatter_kernel, essmem));
         }
         br.Fsrc = nullptr;
         uint32_t t = 1;
@@ -2187,7 +2176,7 @@ static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, 
         bin_init_kernel<<<1, 32, 0, s>>>(n, nloc, m, R, B.nbins, cursor, base, cap);
     }
     const size_t smem = partition_smem(R, B.nbins);
-    PEEL_CUDA(cudaFuncSetAttribute(bin_partition_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PEEL_CUDA(raise_smem((const void *)bin_partition_kernel<R>, smem));
     int pb = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, bin_partition_kernel<R>, PART_BLOCK, smem));
     if (pb < 1) pb = 1;
@@ -2236,7 +2225,7 @@ peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint6
     const uint32_t enb = (uint32_t)((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT);
     ull *hist = v.esort, *cur = v.esort + enb + 1;
     const size_t essmem = esort_scatter_smem(enb);
-    PEEL_CUDA(cudaFuncSetAttribute(esort_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)essmem));
+    PEEL_CUDA(raise_smem((const void *)esort_scatter_kernel, essmem));
     PEEL_CUDA(cudaMemsetAsync(v.esort, 0, sizeof(ull) * 2 * (enb + 1), s));
     ProfScope ps("frontier_edge_sort", s);
     esort_hist_kernel<<<grid_for(nE_host, 8), 256, sizeof(uint32_t) * enb, s>>>((const uint2 *)src, pN, enb, hist);
@@ -2387,9 +2376,9 @@ extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, u
         PEEL_CUDA(cudaStreamSynchronize(s));
         return st;
     }
-    static std::mutex mu;
-    static std::map<int, std::pair<cudaStream_t, std::vector<cudaEvent_t>>> res;  // per device
-    std::lock_guard<std::mutex> lock(mu);
+    // per host thread and device: concurrent calls (distinct streams and workspaces, peel.h)
+    // each get their own copy stream and events, and no lock is held across the peel
+    static thread_local std::map<int, std::pair<cudaStream_t, std::vector<cudaEvent_t>>> res;
     int dev = 0;
     PEEL_CUDA(cudaGetDevice(&dev));
     auto &rs = res[dev];

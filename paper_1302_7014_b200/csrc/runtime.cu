@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -23,6 +24,9 @@ struct ProfEntry {
     cudaEvent_t a, b;
 };
 
+// the profiling tables are shared by every host thread (peel_sweep's batch workers call the
+// library concurrently): every access below holds g_mu
+static std::recursive_mutex g_mu;
 static bool g_prof_on = false;
 static std::vector<ProfEntry> g_prof;          // events of the current call
 static std::vector<ProfEntry> g_pool;          // recycled events
@@ -51,12 +55,12 @@ static ProfEntry take_pair(const char *name) {
 static bool g_collected = true;
 static int g_hold = 0;  // > 0 inside a call made of public calls (peel_sweep): one report
 
-void prof_hold(bool on) { g_hold += on ? 1 : -1; }
-void prof_add_launches(uint32_t n) { g_launches += n; }
+void prof_hold(bool on) { std::lock_guard<std::recursive_mutex> lk(g_mu); g_hold += on ? 1 : -1; }
+void prof_add_launches(uint32_t n) { std::lock_guard<std::recursive_mutex> lk(g_mu); g_launches += n; }
 static bool g_capture = false;  // inside a stream capture: no events, no counts (the replay is timed)
-void prof_capture(bool on) { g_capture = on; }
+void prof_capture(bool on) { std::lock_guard<std::recursive_mutex> lk(g_mu); g_capture = on; }
 
-void prof_begin_call() {
+void prof_begin_call() { std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (!g_collected || g_hold) return;
     g_collected = false;
     g_launches = 0;
@@ -65,21 +69,23 @@ void prof_begin_call() {
     g_prof.clear();
 }
 
-void prof_pre(const char *name, cudaStream_t s) {
-    if (!g_prof_on || g_capture) return;
+int prof_pre(const char *name, cudaStream_t s) { std::lock_guard<std::recursive_mutex> lk(g_mu);
+    if (!g_prof_on || g_capture) return -1;
     ProfEntry p = take_pair(name);
     cudaEventRecord(p.a, s);
     g_prof.push_back(p);
+    return (int)g_prof.size() - 1;
 }
 
-void prof_post(const char *name, cudaStream_t s) {
+// the entry index (not "the last entry"): concurrent threads interleave their entries
+void prof_post(int entry, cudaStream_t s) { std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (g_capture) return;
     g_launches++;
-    if (!g_prof_on) return;
-    if (!g_prof.empty() && g_prof.back().name == name) cudaEventRecord(g_prof.back().b, s);
+    if (!g_prof_on || entry < 0 || entry >= (int)g_prof.size()) return;
+    cudaEventRecord(g_prof[entry].b, s);
 }
 
-int prof_collect() {
+int prof_collect() { std::lock_guard<std::recursive_mutex> lk(g_mu);
     if (g_hold) return 0;
     g_collected = true;
     g_res_names.clear();
@@ -104,7 +110,21 @@ int prof_collect() {
 }
 
 bool prof_enabled() { return g_prof_on; }
-void prof_set_rounds(const std::vector<double> &ms) { g_round_ms = ms; }
+void prof_set_rounds(const std::vector<double> &ms) { std::lock_guard<std::recursive_mutex> lk(g_mu); g_round_ms = ms; }
+
+cudaError_t raise_smem(const void *kern, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> cur;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &c = cur[std::make_pair(dev, kern)];
+    if (bytes <= c) return cudaSuccess;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) c = bytes;
+    return e;
+}
 
 int num_sms() {
     static int sms = 0;

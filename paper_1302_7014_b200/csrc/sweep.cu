@@ -8,6 +8,12 @@
 // the union -- with its binned build, persistent round loop and all -- computes every
 // trial.  Per trial: rounds = max over its vertices of the removal round, core = number
 // of its vertices never removed (a segmented reduction over peel_round / core_mask).
+#include <stdlib.h>
+
+#include <string>
+#include <thread>
+#include <vector>
+
 #include "common.cuh"
 
 namespace peel {
@@ -70,9 +76,18 @@ static SweepLayout sweep_layout(uint64_t n, uint64_t max_m, uint32_t r, uint32_t
 
 using namespace peel;
 
+// Batches run on NW host worker threads, each with its own stream and workspace slice: the
+// GPU overlaps one batch's latency-bound tail rounds with another batch's build
+// (PEEL_SWEEP_WORKERS, default 2)
+static uint32_t sweep_workers() {
+    const char *e = getenv("PEEL_SWEEP_WORKERS");
+    const int w = e ? atoi(e) : 2;
+    return (uint32_t)(w < 1 ? 1 : (w > 8 ? 8 : w));
+}
+
 extern "C" size_t peel_sweep_workspace_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
     if (batch == 0 || batch > 1024 || n < r || n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return 0;
-    return sweep_layout(n, max_m, r, k, batch).total;
+    return sweep_layout(n, max_m, r, k, batch).total * sweep_workers();
 }
 
 extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
@@ -85,15 +100,16 @@ extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint
     if (n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return PEEL_EINVAL;
     SweepLayout L = sweep_layout(n, max_m, r, k, batch);
     if (!L.total) return PEEL_EINVAL;
-    if (ws_bytes < L.total) return PEEL_ENOMEM;
+    const uint64_t nbatches = (ntrials + batch - 1) / batch;
+    uint32_t NW = sweep_workers();
+    if (ws_bytes < L.total * NW) {
+        if (ws_bytes < L.total) return PEEL_ENOMEM;
+        NW = 1;  // a workspace sized for one worker (the caller's own query of another setting)
+    }
+    if (NW > nbatches) NW = (uint32_t)(nbatches ? nbatches : 1);
     cudaStream_t s = (cudaStream_t)stream;
-    char *ws = (char *)workspace;
-    uint32_t *edges = (uint32_t *)(ws + L.edges);
-    uint8_t *mask = (uint8_t *)(ws + L.mask);
-    uint32_t *pr = (uint32_t *)(ws + L.pr);
-    ull *res = (ull *)(ws + L.res);
-    std::vector<ull> hres(2 * batch), hpar(2 * batch + 1);
-    ull *par = (ull *)(ws + L.par);
+    int dev = 0;
+    PEEL_CUDA(cudaGetDevice(&dev));
     prof_begin_call();
     prof_hold(true);  // the batches' peel_kcore calls report as this one call
     struct Release {
@@ -102,37 +118,73 @@ extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint
             prof_collect();
         }
     } release;
-    for (uint64_t t0 = 0; t0 < ntrials; t0 += batch) {
-        const uint32_t B = (uint32_t)(ntrials - t0 < batch ? ntrials - t0 : batch);
-        // one generator launch for the batch: prefix sums of m and the seeds go to the device
-        hpar[0] = 0;
-        for (uint32_t b = 0; b < B; b++) {
-            hpar[b + 1] = hpar[b] + m[t0 + b];
-            hpar[batch + 1 + b] = seeds[t0 + b];
+    // worker w: batches w, w + NW, ...; its own stream (after the caller's stream's prior work)
+    cudaEvent_t start = nullptr;
+    PEEL_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    PEEL_CUDA(cudaEventRecord(start, s));
+    std::vector<peel_status> st(NW, PEEL_OK);
+    std::vector<std::string> err(NW);
+    auto worker = [&](uint32_t w) {
+        if (cudaSetDevice(dev) != cudaSuccess) { st[w] = PEEL_ECUDA; return; }
+        cudaStream_t ws_s = nullptr;
+        if (cudaStreamCreateWithFlags(&ws_s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamWaitEvent(ws_s, start, 0) != cudaSuccess) {
+            st[w] = PEEL_ECUDA;
+            return;
         }
-        const uint64_t off = hpar[B];
-        PEEL_CUDA(cudaMemcpyAsync(par, hpar.data(), sizeof(ull) * (2 * batch + 1), cudaMemcpyHostToDevice, s));
-        {
-            peel_status st = launch_gen_batch(n, r, B, (const uint64_t *)par, (const uint64_t *)par + batch + 1, off,
-                                              edges, s);
-            if (st != PEEL_OK) return st;
-        }
-        uint32_t rounds = 0;
-        peel_status st = peel_kcore(edges, n * B, off, r, k, 0, mask, &rounds, nullptr, nullptr, 0, pr,
-                                    ws + L.kws, L.kws_bytes, stream);
-        if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
-        PEEL_CUDA(cudaMemsetAsync(res, 0, sizeof(ull) * 2 * batch, s));
-        {
-            ProfScope ps("sweep_reduce", s);
-            sweep_reduce_kernel<<<dim3((unsigned)((n + SR_CH - 1) / SR_CH), B), 256, 0, s>>>(pr, mask, n, res, res + batch);
-        }
-        PEEL_CUDA(cudaGetLastError());
-        PEEL_CUDA(cudaMemcpyAsync(hres.data(), res, sizeof(ull) * 2 * batch, cudaMemcpyDeviceToHost, s));
-        PEEL_CUDA(cudaStreamSynchronize(s));
-        for (uint32_t b = 0; b < B; b++) {
-            out_rounds[t0 + b] = (uint32_t)hres[b];
-            out_core[t0 + b] = hres[batch + b];
-        }
-    }
+        char *ws = (char *)workspace + (size_t)w * L.total;
+        uint32_t *edges = (uint32_t *)(ws + L.edges);
+        uint8_t *mask = (uint8_t *)(ws + L.mask);
+        uint32_t *pr = (uint32_t *)(ws + L.pr);
+        ull *res = (ull *)(ws + L.res);
+        ull *par = (ull *)(ws + L.par);
+        std::vector<ull> hres(2 * batch), hpar(2 * batch + 1);
+        auto run = [&]() -> peel_status {
+            for (uint64_t bi = w; bi < nbatches; bi += NW) {
+                const uint64_t t0 = bi * batch;
+                const uint32_t B = (uint32_t)(ntrials - t0 < batch ? ntrials - t0 : batch);
+                // one generator launch for the batch: prefix sums of m and the seeds go to the device
+                hpar[0] = 0;
+                for (uint32_t b = 0; b < B; b++) {
+                    hpar[b + 1] = hpar[b] + m[t0 + b];
+                    hpar[batch + 1 + b] = seeds[t0 + b];
+                }
+                const uint64_t off = hpar[B];
+                PEEL_CUDA(cudaMemcpyAsync(par, hpar.data(), sizeof(ull) * (2 * batch + 1), cudaMemcpyHostToDevice, ws_s));
+                peel_status st2 = launch_gen_batch(n, r, B, (const uint64_t *)par, (const uint64_t *)par + batch + 1,
+                                                   off, edges, ws_s);
+                if (st2 != PEEL_OK) return st2;
+                uint32_t rounds = 0;
+                st2 = peel_kcore(edges, n * B, off, r, k, 0, mask, &rounds, nullptr, nullptr, 0, pr, ws + L.kws,
+                                 L.kws_bytes, ws_s);
+                if (st2 != PEEL_OK && st2 != PEEL_ETRUNC) return st2;
+                PEEL_CUDA(cudaMemsetAsync(res, 0, sizeof(ull) * 2 * batch, ws_s));
+                {
+                    ProfScope ps("sweep_reduce", ws_s);
+                    sweep_reduce_kernel<<<dim3((unsigned)((n + SR_CH - 1) / SR_CH), B), 256, 0, ws_s>>>(pr, mask, n, res,
+                                                                                                    res + batch);
+                }
+                PEEL_CUDA(cudaGetLastError());
+                PEEL_CUDA(cudaMemcpyAsync(hres.data(), res, sizeof(ull) * 2 * batch, cudaMemcpyDeviceToHost, ws_s));
+                PEEL_CUDA(cudaStreamSynchronize(ws_s));
+                for (uint32_t b = 0; b < B; b++) {
+                    out_rounds[t0 + b] = (uint32_t)hres[b];
+                    out_core[t0 + b] = hres[batch + b];
+                }
+            }
+            return PEEL_OK;
+        };
+        st[w] = run();
+        if (st[w] != PEEL_OK) err[w] = peel_last_cuda_error();
+        cudaStreamSynchronize(ws_s);
+        cudaStreamDestroy(ws_s);
+    };
+    std::vector<std::thread> th;
+    for (uint32_t w = 1; w < NW; w++) th.emplace_back(worker, w);
+    worker(0);
+    for (auto &x : th) x.join();
+    cudaEventDestroy(start);
+    for (uint32_t w = 0; w < NW; w++)
+        if (st[w] != PEEL_OK) return st[w];
     return PEEL_OK;
 }

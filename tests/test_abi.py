@@ -46,8 +46,7 @@ def test_workspace_queries():
     # state buffers) + m/8 alive bits + stats, plus (n > 2^23) the binned build's 8-byte entry
     # buffer (r m entries + ~0.3% slack), the per-edge-bin frontier regions (r entries per edge,
     # whole edge bins of 2^22) and the 16-byte records of 64-vertex groups
-    # (r = 3 also reserves a 16-byte-aligned row copy for PEEL_ROWPAD: 16 m)
-    fe = 8 * 3 * (1 << 22) * ((m + (1 << 22) - 1) >> 22) + 16 * m
+    fe = 8 * 3 * (1 << 22) * ((m + (1 << 22) - 1) >> 22)
     assert 24 * n + 8 * 3 * m + fe + n // 4 < ws < 24 * n + 8 * 3 * m * 1.004 + fe + n // 4 + m // 8 + (16 << 20)
     small = L.peel_kcore_workspace_bytes(10**6, 750000, 3, 2, 0)   # no binning below 2^23
     assert 24 * 10**6 < small < 24 * 10**6 + (8 << 20)

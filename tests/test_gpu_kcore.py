@@ -390,7 +390,8 @@ def test_compact_rounds_modes(monkeypatch, tail, at, c, k, r):
     m = int(c * n)
     e = pk.gen_hypergraph(n, m, r, 70 + r, device=DEV)
     ref = O.sync_peel(e.cpu().numpy().view(np.uint32), n, k, want_peel_round=True)
-    for name, val in (("PEEL_COMPACT_TAIL", tail), ("PEEL_COMPACT_AT", at)):
+    ratio = "0" if tail == "0" else None  # tail 0: hand over at the first small frontier
+    for name, val in (("PEEL_COMPACT_TAIL", tail), ("PEEL_COMPACT_AT", at), ("PEEL_COMPACT_TAIL_RATIO", ratio)):
         if val is None:
             monkeypatch.delenv(name, raising=False)
         else:

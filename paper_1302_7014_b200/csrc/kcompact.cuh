@@ -68,6 +68,26 @@ static constexpr int CDCH = PEEL_CDCH;  // apply: decrement entries per work ite
 
 __host__ __device__ inline uint64_t bin_groups(uint64_t n, uint64_t b) { return (bin_size(n, b) + 63) >> 6; }
 
+// Device-side round control (the rounds run without a host sync each: see run_compact).  One
+// thread of cround_ctl_kernel decides, before every round, whether the peel is done, whether
+// the tail goes to the persistent kernel or the slots are due for compaction (the host's
+// work), or the round runs -- then zeroes the round's counters.  Every round kernel exits at
+// once when `stop` is set.
+enum : uint32_t { RC_RUN = 0, RC_DONE = 1, RC_TAIL = 2, RC_COMPACT = 3 };
+struct RoundCtl {
+    uint32_t t;       // the round to run next
+    uint32_t stop;    // RC_*
+    uint32_t ran;     // the round t was launched (t advances at the next decision)
+    uint32_t live_t;  // the round whose |F_t| was last taken off `live`
+    ull live;         // vertices with count >= k after the last completed round
+    ull nslots;       // slots laid out
+};
+struct RoundRule {    // the thresholds (compact_at, ctail_live_frac, ctail_ratio)
+    uint64_t n;
+    double frac, tail, tratio, at;
+    int compaction;
+};
+
 struct CArgs {
     const uint32_t *edges;
     uint64_t n, m;
@@ -91,6 +111,8 @@ struct CArgs {
     const ull *entries;
     ull *work;
     ull *live_total;         // build: vertices with count >= k
+    RoundCtl *rc;            // rounds: the round index and the stop flag (device-side loop)
+    ull *fec[2];             // rounds: per-edge-bin entry counts by round parity
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -133,12 +155,14 @@ struct FeView {
     uint2 *buf;
     ull *gpos;
     uint32_t *hist, *offs;
-    uint32_t *n;  // staged entries
+    uint32_t *n;   // staged entries
+    ull *fecnt;    // the regions' entry counts being written (F_{t+1})
 };
 
 template <int CAP>
-__device__ __forceinline__ FeView fe_view(unsigned char *smem, uint32_t enb, uint32_t *n) {
+__device__ __forceinline__ FeView fe_view(unsigned char *smem, uint32_t enb, uint32_t *n, ull *fecnt) {
     FeView f;
+    f.fecnt = fecnt;
     f.buf = (uint2 *)smem;
     f.gpos = (ull *)(f.buf + CAP);
     f.hist = (uint32_t *)(f.gpos + enb);
@@ -160,7 +184,7 @@ __device__ __forceinline__ void fe_push(const FeView &f, const CArgs &a, uint2 v
         f.buf[pos] = v;
     } else {
         const uint32_t j = v.y >> EB_SHIFT;
-        const ull p = atomicAdd(a.fecnt + j, 1ull);
+        const ull p = atomicAdd(f.fecnt + j, 1ull);
         a.fe[(ull)j * a.fe_stride + p] = v;
     }
 }
@@ -206,7 +230,7 @@ __device__ void fe_flush(const FeView &f, const CArgs &a) {
     }
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < a.enb; j += CB_BLOCK)
-        if (f.hist[j]) f.gpos[j] = atomicAdd(a.fecnt + j, (ull)f.hist[j]);
+        if (f.hist[j]) f.gpos[j] = atomicAdd(f.fecnt + j, (ull)f.hist[j]);
     #pragma unroll
     for (int q = 0; q < PER; q++) {
         const uint32_t i = q * CB_BLOCK + threadIdx.x;
@@ -356,7 +380,7 @@ __global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_kernel(CArgs a) {
     __shared__ uint32_t fen;
     if (threadIdx.x == 0) fen = 0;
     __syncthreads();
-    const FeView f = fe_view<FE_CAP_B>(smem_raw, a.enb, &fen);
+    const FeView f = fe_view<FE_CAP_B>(smem_raw, a.enb, &fen, a.fecnt);
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
     const ull mask = (1ull << BIN_SHIFT) - 1;
@@ -441,9 +465,11 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
     uint32_t *pre = offs + nbins;                        // [enb + 1] chunks before edge bin j
     __shared__ uint32_t total;
     Ctl *ctl = a.ctl;
-    const uint32_t t = br.t;
+    if (c.rc && *(volatile uint32_t *)&c.rc->stop) return;  // uniform: the loop stopped before this round
+    const uint32_t t = c.rc ? *(volatile uint32_t *)&c.rc->t : br.t;
+    const ull *fecur = c.rc ? (((t - 1) & 1) ? c.fec[1] : c.fec[0]) : c.fecur;
     for (uint32_t j = threadIdx.x; j < c.enb; j += PART_BLOCK)
-        pre[j] = (uint32_t)((ld_cg_u64(c.fecur + j) + KCH - 1) / KCH);
+        pre[j] = (uint32_t)((ld_cg_u64(fecur + j) + KCH - 1) / KCH);
     block_excl_scan(pre, c.enb);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
@@ -463,7 +489,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
             if (pre[mid] <= item) lo = mid; else hi = mid;
         }
         const ull off = (ull)(item - pre[lo]) * KCH;
-        const ull nE = min((ull)KCH, ld_cg_u64(c.fecur + lo) - off);
+        const ull nE = min((ull)KCH, ld_cg_u64(fecur + lo) - off);
         const uint2 *Fc = c.fe + (ull)lo * c.fe_stride + off;
 #if PEEL_KILL_EPF
         if (threadIdx.x == 32 && item + gridDim.x < nitems) {
@@ -475,7 +501,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
                 if (pre[mid] <= it2) l2 = mid; else h2 = mid;
             }
             const ull off2 = (ull)(it2 - pre[l2]) * KCH;
-            const ull n2 = min((ull)KCH, ld_cg_u64(c.fecur + l2) - off2);
+            const ull n2 = min((ull)KCH, ld_cg_u64(fecur + l2) - off2);
             const uintptr_t p0 = (uintptr_t)(c.fe + (ull)l2 * c.fe_stride + off2) & ~(uintptr_t)15;
             const uintptr_t p1 = ((uintptr_t)(c.fe + (ull)l2 * c.fe_stride + off2 + n2) + 15) & ~(uintptr_t)15;
             if (p1 > p0) prefetch_l2((const void *)p0, (uint32_t)(p1 - p0));
@@ -576,14 +602,18 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
     __shared__ uint32_t fen;
     __shared__ ull item;
     const uint32_t nb = a.nbins;
-    const FeView f = fe_view<FE_CAP_A>(smem_raw, a.enb, &fen);
+    if (a.rc && *(volatile uint32_t *)&a.rc->stop) return;  // uniform: the loop stopped before this round
+    const uint32_t t = a.rc ? *(volatile uint32_t *)&a.rc->t : a.t;
+    // (a select, not a.fec[t & 1]: a dynamic index into a kernel parameter copies the whole
+    // parameter struct to local memory -- 248 bytes of stack, +6 ms of apply at C5)
+    const FeView f = fe_view<FE_CAP_A>(smem_raw, a.enb, &fen, a.rc ? ((t & 1) ? a.fec[1] : a.fec[0]) : a.fecnt);
     uint32_t *pre = (uint32_t *)(f.offs + a.enb);  // [nb + 1] items before bin b
     if (threadIdx.x == 0) fen = 0;
     for (uint32_t b = threadIdx.x; b < nb; b += CB_BLOCK) pre[b] = (uint32_t)((ld_cg_u64(a.cursor + b) + CDCH - 1) / CDCH);
     block_excl_scan(pre, nb);
     const uint32_t nitems = pre[nb];
     const ull mask = (1ull << BIN_SHIFT) - 1;
-    const uint32_t k = a.k, t = a.t;
+    const uint32_t k = a.k;
     ull crossed = 0;
     for (;;) {
         if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
@@ -766,6 +796,35 @@ __global__ void __launch_bounds__(256) cgather_kernel(const uint2 *__restrict__ 
     }
 }
 
+// the decision before round t (see RoundCtl); one block
+__global__ void __launch_bounds__(256) cround_ctl_kernel(Ctl *ctl, RoundCtl *rc, RoundRule rule, ull *cursor,
+                                                         uint32_t nbins, ull *fec0, ull *fec1, uint32_t enb, ull *work) {
+    __shared__ uint32_t go, tt;
+    if (threadIdx.x == 0) {
+        go = 0;
+        if (!rc->stop) {
+            if (rc->ran) { rc->t++; rc->ran = 0; }
+            const uint32_t t = rc->t;
+            const ull nF = ld_cg_u64(&ctl->nf[(t - 1) % 3]), nE = ld_cg_u64(&ctl->ne[(t - 1) % 3]);
+            if (t > 1 && rc->live_t != t) { rc->live -= nF; rc->live_t = t; }  // F_t left L in round t-1
+            const double live = (double)rc->live, slots = (double)rc->nslots, n = (double)rule.n;
+            if (nF == 0) rc->stop = RC_DONE;
+            else if ((double)nE < rule.frac * n && live >= rule.tail * n && slots >= rule.tratio * (double)nE)
+                rc->stop = RC_TAIL;
+            else if (rule.compaction && live <= rule.at * slots && 8.0 * (slots - live) >= 0.5 * n)
+                rc->stop = RC_COMPACT;
+            else { go = 1; rc->ran = 1; }
+            tt = t;
+        }
+    }
+    __syncthreads();
+    if (!go) return;
+    ull *fn = (tt & 1) ? fec1 : fec0;
+    for (uint32_t i = threadIdx.x; i < nbins; i += 256) cursor[i] = 0ull;
+    for (uint32_t i = threadIdx.x; i < enb; i += 256) fn[i] = 0ull;
+    if (threadIdx.x == 0) *work = 0ull;
+}
+
 // rounds, and the timer that closes the last round (profiling), once the frontier is empty
 __global__ void ctail_kernel(Ctl *ctl, ull *rtime, uint32_t T, uint32_t stat_cap) {
     ctl->rounds = T;
@@ -817,13 +876,19 @@ static SideStream &side_stream() {
     return sd;
 }
 
-// compact when the live set has halved since the slots were laid out and the bytes a round
-// would stop prefetching (8 per dropped slot) pay for the records pass (n / 2 bytes)
-static bool compact_now(uint64_t n, uint64_t slots, uint64_t live) {
+static double compact_at() {
     const char *e = getenv("PEEL_COMPACT_AT");  // live / slots ratio that triggers (A/B; 0: never)
-    const double at = e ? atof(e) : 0.5;
-    return (double)live <= at * (double)slots && 8.0 * (double)(slots - live) >= 0.5 * (double)n;
+    return e ? atof(e) : 0.5;
 }
+static int rounds_per_sync() {
+    const char *e = getenv("PEEL_ROUNDS_PER_SYNC");
+    const int k = e ? atoi(e) : 4;
+    return k < 1 ? 1 : (k > 64 ? 64 : k);
+}
+
+// compaction rule (cround_ctl_kernel): compact when the live set has halved since the slots
+// were laid out (PEEL_COMPACT_AT) and the bytes a round would stop prefetching (8 per dropped
+// slot) pay for the records pass (n / 2 bytes)
 
 template <int R>
 static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t k, uint8_t *core_mask,
@@ -930,14 +995,53 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     PEEL_CUDA(cudaStreamSynchronize(s));
     uint64_t live = h.nlive[0];
     uint64_t nslots = n;     // slots laid out (identity: every vertex)
+    // The rounds run as a device-side loop: cround_ctl_kernel decides before each round (done /
+    // tail hand-over / compaction due / run) and zeroes its counters; the host launches
+    // PEEL_ROUNDS_PER_SYNC rounds (default 4) at a time and syncs once per batch -- rounds
+    // after a stop exit at once -- and does only the work the device cannot: the compaction
+    // (a buffer swap) and the hand-over.
+    RoundCtl *rc = (RoundCtl *)(ws + CL.rc);
+    RoundCtl hrc;
+    memset(&hrc, 0, sizeof hrc);
+    hrc.t = 1;
+    hrc.live_t = 1;  // round 1's F_1 left L in the build: live is already after it
+    hrc.live = live;
+    hrc.nslots = nslots;
+    PEEL_CUDA(cudaMemcpyAsync(rc, &hrc, sizeof hrc, cudaMemcpyHostToDevice, s));
+    c.rc = rc;
+    c.fec[0] = fecnt[0];
+    c.fec[1] = fecnt[1];
+    const RoundRule rule = {n, frac, tail, tratio, compact_at(), compaction ? 1 : 0};
+    const int K = rounds_per_sync();
+    bool comp_pending = false;
     uint32_t t = 1;
     for (;;) {
-        const ull nF = h.nf[(t - 1) % 3], nE = h.ne[(t - 1) % 3];
-        if (t > 1) live -= nF;  // the vertices of F_t left L in round t-1
-        if (nF == 0) break;
-        if ((double)nE < frac * (double)n && (double)live >= tail * (double)n &&
-            (double)nslots >= tratio * (double)nE) {
+        for (int i = 0; i < K; i++) {
+            cround_ctl_kernel<<<1, 256, 0, s>>>(ctl, rc, rule, cursor, nbins, fecnt[0], fecnt[1], enb, &ctl->work);
+            {
+                ProfScope ps("round_kill_partition", s);
+                ckill_kernel<R><<<num_sms() * kb, PART_BLOCK, ksmem, s>>>(a, br, c);
+            }
+            if (comp_pending) {
+                PEEL_CUDA(cudaStreamWaitEvent(s, sd.ev[1], 0));
+                comp_pending = false;
+            }
+            {
+                ProfScope ps("round_apply", s);
+                if (compacted) capply_kernel<R, true><<<num_sms() * (ab[1] < 1 ? 1 : ab[1]), CB_BLOCK, asmem, s>>>(c);
+                else capply_kernel<R, false><<<num_sms() * (ab[0] < 1 ? 1 : ab[0]), CB_BLOCK, asmem, s>>>(c);
+            }
+        }
+        PEEL_CUDA(cudaGetLastError());
+        PEEL_CUDA(cudaMemcpyAsync(&hrc, rc, sizeof hrc, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        t = hrc.t;
+        if (hrc.stop == RC_RUN) continue;
+        if (hrc.stop == RC_DONE) break;
+        if (hrc.stop == RC_TAIL) {
             // the persistent kernel takes the remaining rounds from round t
+            const ull nE = h.ne[(t - 1) % 3];
             if (compacted) {
                 ProfScope ps("compact_writeback", s);
                 cdecompact_kernel<<<grid_for(n), 256, 0, s>>>(c.recs, c.X, n, k, state);
@@ -962,55 +1066,32 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
             }
             return finish_kcore(n, cap, rounds, survivors, killed, ws, L, a, s);
         }
-        bool comp_pending = false;
-        if (compaction && compact_now(n, nslots, live)) {
-            // lay the live states out densely: CB[nxt], slot counts slots[nxt], new records.  On a
-            // side stream: this round's kill does not touch the slots and runs concurrently; the
-            // apply waits for the compaction.
-            const int nxt = compacted ? cur ^ 1 : 0;
-            PEEL_CUDA(cudaEventRecord(sd.ev[0], s));
-            PEEL_CUDA(cudaStreamWaitEvent(sd.s2, sd.ev[0], 0));
-            PEEL_CUDA(cudaMemsetAsync(slots[nxt], 0, sizeof(ull) * nbins, sd.s2));
-            PEEL_CUDA(cudaMemsetAsync(&ctl->cwork, 0, sizeof(ull), sd.s2));
-            CArgs cc = c;
-            cc.Y = CB[nxt];
-            cc.alloc = slots[nxt];
-            cc.work = &ctl->cwork;
-            {
-                ProfScope ps("compact_slots", sd.s2);
-                if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
-                else ccompact_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
-            }
-            PEEL_CUDA(cudaEventRecord(sd.ev[1], sd.s2));
-            comp_pending = true;
-            compacted = true;
-            cur = nxt;
-            c.X = CB[cur];
-            c.slots = slots[cur];
-            nslots = live;
-        }
-        // per-round resets: decrement bins, item counter, next frontier counts
-        PEEL_CUDA(cudaMemsetAsync(cursor, 0, sizeof(ull) * nbins, s));
-        PEEL_CUDA(cudaMemsetAsync(&ctl->work, 0, sizeof(ull), s));
-        PEEL_CUDA(cudaMemsetAsync(fecnt[t & 1], 0, sizeof(ull) * enb, s));
-        br.t = t;
-        c.t = t;
-        c.fecur = fecnt[(t - 1) & 1];
-        c.fecnt = fecnt[t & 1];
+        // RC_COMPACT: lay the live states out densely -- CB[nxt], slot counts slots[nxt], new
+        // records -- on the side stream: round t's kill does not touch the slots and runs
+        // concurrently; its apply waits for the compaction
+        const int nxt = compacted ? cur ^ 1 : 0;
+        PEEL_CUDA(cudaEventRecord(sd.ev[0], s));
+        PEEL_CUDA(cudaStreamWaitEvent(sd.s2, sd.ev[0], 0));
+        PEEL_CUDA(cudaMemsetAsync(slots[nxt], 0, sizeof(ull) * nbins, sd.s2));
+        PEEL_CUDA(cudaMemsetAsync(&ctl->cwork, 0, sizeof(ull), sd.s2));
+        CArgs cc = c;
+        cc.Y = CB[nxt];
+        cc.alloc = slots[nxt];
+        cc.work = &ctl->cwork;
         {
-            ProfScope ps("round_kill_partition", s);
-            ckill_kernel<R><<<num_sms() * kb, PART_BLOCK, ksmem, s>>>(a, br, c);
+            ProfScope ps("compact_slots", sd.s2);
+            if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+            else ccompact_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
         }
-        if (comp_pending) PEEL_CUDA(cudaStreamWaitEvent(s, sd.ev[1], 0));
-        {
-            ProfScope ps("round_apply", s);
-            if (compacted) capply_kernel<R, true><<<num_sms() * (ab[1] < 1 ? 1 : ab[1]), CB_BLOCK, asmem, s>>>(c);
-            else capply_kernel<R, false><<<num_sms() * (ab[0] < 1 ? 1 : ab[0]), CB_BLOCK, asmem, s>>>(c);
-        }
-        PEEL_CUDA(cudaGetLastError());
-        t++;
-        PEEL_CUDA(cudaMemcpyAsync(&h, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-        PEEL_CUDA(cudaStreamSynchronize(s));
+        PEEL_CUDA(cudaEventRecord(sd.ev[1], sd.s2));
+        comp_pending = true;
+        compacted = true;
+        cur = nxt;
+        c.X = CB[cur];
+        c.slots = slots[cur];
+        hrc.nslots = hrc.live;
+        hrc.stop = RC_RUN;
+        PEEL_CUDA(cudaMemcpyAsync(rc, &hrc, sizeof hrc, cudaMemcpyHostToDevice, s));
     }
     {
         ProfScope ps("compact_core_mask", s);

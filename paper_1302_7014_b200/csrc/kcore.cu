@@ -62,7 +62,7 @@ struct Ctl {
 // compacted rounds (kcompact.cuh): group records, per-bin live counts, A-item counters,
 // per-edge-bin frontier regions and their counts
 struct CompactLayout {
-    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe;
+    size_t recs, live0, live1, adone, fecnt0, fecnt1, fe, rc;
     uint64_t enb, fe_stride;
 };
 
@@ -151,6 +151,7 @@ static Layout layout(uint64_t n, uint64_t m, uint32_t r, bool csr) {
         C.fecnt0 = o; o += al(sizeof(ull) * C.enb);
         C.fecnt1 = o; o += al(sizeof(ull) * C.enb);
         C.fe = o; o += al(sizeof(uint2) * C.enb * C.fe_stride);
+        C.rc = o; o += al(64);  // RoundCtl
     }
     L.total = o;
     return L;

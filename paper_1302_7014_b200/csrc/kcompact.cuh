@@ -46,15 +46,16 @@ static constexpr int CGW = 32;       // compaction: groups per warp per item (8 
 #endif
 static constexpr int FE_CAP_A = PEEL_FE_CAP_A;  // apply: frontier entries staged per block before an edge-bin sort
 static constexpr int FE_CAP_B = PEEL_FE_CAP_B;  // build scan (F_1 is ~24% of n: longer runs per edge bin)
-#ifndef PEEL_KILL_SPEC
-#define PEEL_KILL_SPEC 0
+// the kill: 4 entries per thread at 4 resident blocks per SM (C5 kill 25.0 -> 24.0 ms against
+// round 1's 3 at 5, which kcore.cu's uncompacted kill keeps)
+#ifndef PEEL_CKU
+#define PEEL_CKU 4
 #endif
-#ifndef PEEL_APPLY_PF
-#define PEEL_APPLY_PF 1
+#ifndef PEEL_CKILL_MINB
+#define PEEL_CKILL_MINB 4
 #endif
-#ifndef PEEL_KILL_EPF
-#define PEEL_KILL_EPF 1
-#endif
+static constexpr int CKU = PEEL_CKU;
+static constexpr int CKCH = PART_BLOCK * CKU;
 #ifndef PEEL_CB_RU
 #define PEEL_CB_RU 8
 #endif
@@ -352,6 +353,91 @@ __device__ void compact_item(const CArgs &a, uint32_t b, uint64_t g0, const ull 
 }
 
 // compaction pass over every bin (non-cooperative; items handed out by a counter in bin order)
+// the same with the item's states held in registers (8 groups per warp, 16 states per lane):
+// one load pass, no reload after the allocation (PEEL_CREG, default)
+static constexpr int CRG = 8;
+template <bool IDENT>
+__device__ void compact_item_reg(const CArgs &a, uint32_t b, uint64_t g0, const ull *src, uint32_t *wsh) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t gend = ((uint64_t)b << (BIN_SHIFT - 6)) + bin_groups(a.n, b);
+    const uint64_t gw0 = g0 + (uint64_t)w * CRG;
+    const uint32_t k = a.k;
+    ull mymask = 0;
+    uint32_t mybase = 0;
+    {
+        const uint64_t g = gw0 + lane;
+        if (lane < CRG && g < gend) {
+            if (IDENT) {
+                const uint64_t v0 = g << 6;
+                const uint64_t nv = min((uint64_t)64, a.n - v0);
+                mymask = nv == 64 ? ~0ull : ((1ull << nv) - 1);
+                mybase = (uint32_t)v0;
+            } else {
+                const uint4 r = __ldcg(reinterpret_cast<const uint4 *>(a.recs + g));
+                mymask = ((ull)r.y << 32) | r.x;
+                mybase = r.z;
+            }
+        }
+    }
+    ull st[CRG][2];
+    #pragma unroll
+    for (int j = 0; j < CRG; j++) {
+        const ull m = __shfl_sync(0xffffffffu, mymask, j);
+        const uint32_t bs = __shfl_sync(0xffffffffu, mybase, j);
+        #pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const uint32_t bit = 32 * h + lane;
+            const bool has = (m >> bit) & 1ull;
+            // a state that stays has count >= k >= 1; 0 marks "no slot"
+            st[j][h] = has ? __ldcs(src + bs + __popcll(m & ((1ull << bit) - 1ull))) : 0ull;
+        }
+    }
+    uint32_t keepcnt = 0;
+    #pragma unroll
+    for (int j = 0; j < CRG; j++)
+        #pragma unroll
+        for (int h = 0; h < 2; h++) keepcnt += __popc(__ballot_sync(0xffffffffu, (uint32_t)st[j][h] >= k && st[j][h]));
+    if (lane == 0) wsh[w] = keepcnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int q = 0; q < CB_BLOCK / 32; q++) { const uint32_t c = wsh[q]; wsh[q] = tot; tot += c; }
+        const ull base = tot ? atomicAdd(a.alloc + b, (ull)tot) : 0ull;
+        wsh[CB_BLOCK / 32] = (uint32_t)(((uint64_t)b << BIN_SHIFT) + base);
+    }
+    __syncthreads();
+    uint32_t run = wsh[CB_BLOCK / 32] + wsh[w];
+    #pragma unroll
+    for (int j = 0; j < CRG; j++) {
+        const bool k0 = st[j][0] && (uint32_t)st[j][0] >= k, k1 = st[j][1] && (uint32_t)st[j][1] >= k;
+        const uint32_t b0 = __ballot_sync(0xffffffffu, k0), b1 = __ballot_sync(0xffffffffu, k1);
+        if (k0) a.Y[run + __popc(b0 & lanemask_lt())] = st[j][0];
+        if (k1) a.Y[run + __popc(b0) + __popc(b1 & lanemask_lt())] = st[j][1];
+        const uint64_t g = gw0 + j;
+        if (lane == 0 && g < gend && (__shfl_sync(0xffffffffu, mymask, j) || b0 || b1))
+            __stcg(reinterpret_cast<uint4 *>(a.recs + g), make_uint4(b0, b1, run, 0u));
+        run += __popc(b0) + __popc(b1);
+    }
+}
+
+template <bool IDENT>
+__global__ void __launch_bounds__(CB_BLOCK, 4) ccompact_reg_kernel(CArgs a) {
+    __shared__ uint32_t wsh[CB_BLOCK / 32 + 1];
+    __shared__ ull item[2];
+    const uint64_t per_bin = (1ull << (BIN_SHIFT - 6)) / (8 * CRG);  // items of a full bin
+    const uint64_t nitems = (uint64_t)a.nbins * per_bin;
+    for (int ib = 0;; ib ^= 1) {
+        if (threadIdx.x == 0) item[ib] = atomicAdd(a.work, 1ull);
+        __syncthreads();
+        const ull c = item[ib];
+        if (c >= nitems) break;
+        const uint32_t b = (uint32_t)(c / per_bin);
+        const uint64_t g0 = ((uint64_t)b << (BIN_SHIFT - 6)) + (c % per_bin) * 8 * CRG;
+        if (g0 < ((uint64_t)b << (BIN_SHIFT - 6)) + bin_groups(a.n, b)) compact_item_reg<IDENT>(a, b, g0, a.X, wsh);
+        __syncthreads();  // wsh is rewritten next item
+    }
+}
+
 template <bool IDENT>
 __global__ void __launch_bounds__(CB_BLOCK, 4) ccompact_kernel(CArgs a) {
     __shared__ uint32_t wsh[CB_BLOCK / 32 + 1];
@@ -455,11 +541,11 @@ __global__ void __launch_bounds__(CB_BLOCK, 4) cbuild_kernel(CArgs a) {
 // ---- kill: F_t's entries read from the edge-bin regions in bin order (round_kill_partition's
 // body; the decrements are partitioned by vertex bin into the entry buffer)
 template <int R>
-__global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelArgs a, BinRound br, CArgs c) {
+__global__ void __launch_bounds__(PART_BLOCK, PEEL_CKILL_MINB) ckill_kernel(PeelArgs a, BinRound br, CArgs c) {
     extern __shared__ unsigned char smem_raw[];
     const uint32_t nbins = br.nbins;
-    ull *sorted = (ull *)smem_raw;                       // [(R-1) KCH] the chunk's decrements, bin-sorted
-    ull *gpos = sorted + (R - 1) * KCH;                  // [nbins]
+    ull *sorted = (ull *)smem_raw;                       // [(R-1) CKCH] the chunk's decrements, bin-sorted
+    ull *gpos = sorted + (R - 1) * CKCH;                  // [nbins]
     uint32_t *hist = (uint32_t *)(gpos + nbins);         // [nbins]
     uint32_t *offs = hist + nbins;                       // [nbins]
     uint32_t *pre = offs + nbins;                        // [enb + 1] chunks before edge bin j
@@ -469,7 +555,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
     const uint32_t t = c.rc ? *(volatile uint32_t *)&c.rc->t : br.t;
     const ull *fecur = c.rc ? (((t - 1) & 1) ? c.fec[1] : c.fec[0]) : c.fecur;
     for (uint32_t j = threadIdx.x; j < c.enb; j += PART_BLOCK)
-        pre[j] = (uint32_t)((ld_cg_u64(fecur + j) + KCH - 1) / KCH);
+        pre[j] = (uint32_t)((ld_cg_u64(fecur + j) + CKCH - 1) / CKCH);
     block_excl_scan(pre, c.enb);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (t <= a.stat_cap) a.rtime[t - 1] = globaltimer();
@@ -488,60 +574,36 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
             const uint32_t mid = (lo + hi) >> 1;
             if (pre[mid] <= item) lo = mid; else hi = mid;
         }
-        const ull off = (ull)(item - pre[lo]) * KCH;
-        const ull nE = min((ull)KCH, ld_cg_u64(fecur + lo) - off);
+        const ull off = (ull)(item - pre[lo]) * CKCH;
+        const ull nE = min((ull)CKCH, ld_cg_u64(fecur + lo) - off);
         const uint2 *Fc = c.fe + (ull)lo * c.fe_stride + off;
-#if PEEL_KILL_EPF
-        if (threadIdx.x == 32 && item + gridDim.x < nitems) {
-            // this block's next chunk of entries: into L2 while this one is processed
-            const uint32_t it2 = item + gridDim.x;
-            uint32_t l2 = lo, h2 = c.enb;
-            while (h2 - l2 > 1) {
-                const uint32_t mid = (l2 + h2) >> 1;
-                if (pre[mid] <= it2) l2 = mid; else h2 = mid;
-            }
-            const ull off2 = (ull)(it2 - pre[l2]) * KCH;
-            const ull n2 = min((ull)KCH, ld_cg_u64(fecur + l2) - off2);
-            const uintptr_t p0 = (uintptr_t)(c.fe + (ull)l2 * c.fe_stride + off2) & ~(uintptr_t)15;
-            const uintptr_t p1 = ((uintptr_t)(c.fe + (ull)l2 * c.fe_stride + off2 + n2) + 15) & ~(uintptr_t)15;
-            if (p1 > p0) prefetch_l2((const void *)p0, (uint32_t)(p1 - p0));
-        }
-#endif
-        uint2 ent[KU];
-        bool win[KU];
+        uint2 ent[CKU];
+        bool win[CKU];
         #pragma unroll
-        for (int q = 0; q < KU; q++) {
+        for (int q = 0; q < CKU; q++) {
             const uint32_t i = q * PART_BLOCK + threadIdx.x;
             ent[q] = i < nE ? __ldcg(Fc + i) : make_uint2(0u, 0u);
         }
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK) hist[b] = 0;
-        uint32_t oldw[KU];
+        uint32_t oldw[CKU];
         #pragma unroll
-        for (int q = 0; q < KU; q++) {
+        for (int q = 0; q < CKU; q++) {
             const uint32_t i = q * PART_BLOCK + threadIdx.x;
             oldw[q] = 0;
             if (i < nE) oldw[q] = atomicAnd(a.alive + (ent[q].y >> 5), ~(1u << (ent[q].y & 31)));
         }
-        // the rows are loaded together with the test-and-clears, not after them: one dependent
-        // memory trip less per chunk (a losing entry's row -- its edge died already -- is ~10%
-        // of the rows, read for nothing)
-        uint32_t ue[KU][R];
+        uint32_t ue[CKU][R];
         #pragma unroll
-        for (int q = 0; q < KU; q++) {
+        for (int q = 0; q < CKU; q++) {
             const uint32_t i = q * PART_BLOCK + threadIdx.x;
-#if PEEL_KILL_SPEC
-            if (i < nE) load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
-#endif
             win[q] = i < nE && ((oldw[q] >> (ent[q].y & 31)) & 1u);
-#if !PEEL_KILL_SPEC
             if (win[q]) load_row<R>(a.edges, ent[q].y, a.m, a.edges_vec, ue[q]);
-#endif
             kills += win[q];
         }
         __syncthreads();  // hist zeroed
-        uint32_t rk[KU][R];
+        uint32_t rk[CKU][R];
         #pragma unroll
-        for (int q = 0; q < KU; q++)
+        for (int q = 0; q < CKU; q++)
             #pragma unroll
             for (int r = 0; r < R; r++)
                 if (win[q] && ue[q][r] != ent[q].x) rk[q][r] = atomicAdd(&hist[ue[q][r] >> BIN_SHIFT], 1u);
@@ -570,7 +632,7 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
         for (uint32_t b = threadIdx.x; b < nbins; b += PART_BLOCK)  // absolute run starts
             if (hist[b]) gpos[b] = br.base[b] + atomicAdd(br.cursor + b, (ull)hist[b]);
         #pragma unroll
-        for (int q = 0; q < KU; q++)
+        for (int q = 0; q < CKU; q++)
             #pragma unroll
             for (int r = 0; r < R; r++)
                 if (win[q] && ue[q][r] != ent[q].x)
@@ -588,7 +650,8 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_KILL_MINB) ckill_kernel(PeelA
 }
 
 static size_t ckill_smem(int r, uint32_t nbins, uint32_t enb) {
-    return kill_partition_smem(r, nbins) + sizeof(uint32_t) * (enb + 1);
+    return sizeof(ull) * (size_t)(r - 1) * CKCH + (sizeof(ull) + 2 * sizeof(uint32_t)) * nbins +
+           sizeof(uint32_t) * (enb + 1);
 }
 
 // ---- apply: the round's decrements bin-major, DCH entries per work item (a counter hands
@@ -600,7 +663,7 @@ template <int R, bool COMPACT>
 __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ uint32_t fen;
-    __shared__ ull item;
+    __shared__ ull item[2];  // double-buffered: no barrier needed before the next claim
     const uint32_t nb = a.nbins;
     if (a.rc && *(volatile uint32_t *)&a.rc->stop) return;  // uniform: the loop stopped before this round
     const uint32_t t = a.rc ? *(volatile uint32_t *)&a.rc->t : a.t;
@@ -615,10 +678,10 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
     const ull mask = (1ull << BIN_SHIFT) - 1;
     const uint32_t k = a.k;
     ull crossed = 0;
-    for (;;) {
-        if (threadIdx.x == 0) item = atomicAdd(a.work, 1ull);
+    for (int ib = 0;; ib ^= 1) {
+        if (threadIdx.x == 0) item[ib] = atomicAdd(a.work, 1ull);
         __syncthreads();
-        const ull c = item;
+        const ull c = item[ib];
         if (c >= nitems) break;
         uint32_t lo = 0, hi = nb;  // bin b with pre[b] <= c < pre[b+1]
         while (hi - lo > 1) {
@@ -626,22 +689,6 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
             if (pre[mid] <= c) lo = mid; else hi = mid;
         }
         const uint32_t b = lo, j = (uint32_t)c - pre[b];
-#if PEEL_APPLY_PF
-        if (threadIdx.x == 32 && c + gridDim.x < nitems) {
-            // the entries of the item handed out one grid later: into L2 before it is claimed
-            const ull c2 = c + gridDim.x;
-            uint32_t l2 = lo, h2 = nb;
-            while (h2 - l2 > 1) {
-                const uint32_t mid = (l2 + h2) >> 1;
-                if (pre[mid] <= c2) l2 = mid; else h2 = mid;
-            }
-            const ull off2 = (ull)((uint32_t)c2 - pre[l2]) * CDCH;
-            const ull n2 = min((ull)CDCH, ld_cg_u64(a.cursor + l2) - off2);
-            const uintptr_t p0 = (uintptr_t)(a.entries + a.base[l2] + off2) & ~(uintptr_t)15;
-            const uintptr_t p1 = ((uintptr_t)(a.entries + a.base[l2] + off2 + n2) + 15) & ~(uintptr_t)15;
-            if (p1 > p0) prefetch_l2((const void *)p0, (uint32_t)(p1 - p0));
-        }
-#endif
         if (threadIdx.x == 0 && b + 1 < nb) {
             // slice j of the next bin's slots (and records) into L2
             const uint32_t nj = pre[b + 1] - pre[b];
@@ -702,9 +749,8 @@ __global__ void __launch_bounds__(CB_BLOCK, 6) capply_kernel(CArgs a) {
                 fe_push<FE_CAP_A>(f, a, make_uint2(u, idsum_of(old[r]) - (uint32_t)(x[r] >> 32)));
             }
         }
-        __syncthreads();
+        __syncthreads();  // every push of this item landed: one flush decision for the block
         if (fen >= FE_CAP_A / 2) fe_flush<FE_CAP_A>(f, a);
-        __syncthreads();  // item is rewritten next iteration
     }
     fe_flush<FE_CAP_A>(f, a);
     block_add<CB_BLOCK>(&a.ctl->nf[t % 3], crossed);
@@ -1080,8 +1126,14 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
         cc.work = &ctl->cwork;
         {
             ProfScope ps("compact_slots", sd.s2);
-            if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
-            else ccompact_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+            const char *cre = getenv("PEEL_CREG");
+            if (!(cre && atoi(cre) == 0)) {
+                if (compacted) ccompact_reg_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+                else ccompact_reg_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+            } else {
+                if (compacted) ccompact_kernel<false><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+                else ccompact_kernel<true><<<num_sms() * cb, CB_BLOCK, 0, sd.s2>>>(cc);
+            }
         }
         PEEL_CUDA(cudaEventRecord(sd.ev[1], sd.s2));
         comp_pending = true;

@@ -143,7 +143,7 @@ NCU_KERNEL = {"peel_rounds_packed": ("peel_packed",), "peel_rounds_csr": ("peel_
               "iblt_insert": ("iblt_update",), "frontier_edge_sort": ("esort_hist", "esort_scatter"),
               # slot-compacted binned rounds (kcompact.cuh) for n > 2^23, k <= 2
               "bin_accumulate": ("cbuild", "bin_accumulate"), "round_kill_partition": ("ckill", "round_kill_partition"),
-              "round_apply": ("capply", "round_apply"), "compact_slots": ("ccompact",),
+              "round_apply": ("capply", "round_apply"), "compact_slots": ("ccompact", "ccompact_reg"),
               "compact_core_mask": ("ctail", "cmask"), "compact_writeback": ("cdecompact",),
               "compact_gather": ("cgather",)}
 PROFILE_ROUNDS = ("r02", "r01")  # newest first: profiles/<round>_traffic_<config>.json
@@ -174,8 +174,8 @@ def ncu_traffic(config, kernel):
         d = json.load(open(tf))
     except Exception:
         return None, None
-    ks = [d.get("kernels", {}).get(x) for x in NCU_KERNEL.get(kernel, (kernel,))]
-    if not ks or not all(ks):
+    ks = [k for k in (d.get("kernels", {}).get(x) for x in NCU_KERNEL.get(kernel, (kernel,))) if k]
+    if not ks:
         return None, None
     per_step = sum(k["dram_read_bytes_per_step"] + k["dram_write_bytes_per_step"] for k in ks)
     return int(per_step / ks[-1]["launches_per_step"]), \

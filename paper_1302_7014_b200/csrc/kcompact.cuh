@@ -414,7 +414,8 @@ __device__ void compact_item_reg(const CArgs &a, uint32_t b, uint64_t g0, const 
         if (k0) a.Y[run + __popc(b0 & lanemask_lt())] = st[j][0];
         if (k1) a.Y[run + __popc(b0) + __popc(b1 & lanemask_lt())] = st[j][1];
         const uint64_t g = gw0 + j;
-        if (lane == 0 && g < gend && (__shfl_sync(0xffffffffu, mymask, j) || b0 || b1))
+        const ull mj = __shfl_sync(0xffffffffu, mymask, j);  // every lane: a shuffle is warp-wide
+        if (lane == 0 && g < gend && (mj || b0 || b1))
             __stcg(reinterpret_cast<uint4 *>(a.recs + g), make_uint4(b0, b1, run, 0u));
         run += __popc(b0) + __popc(b1);
     }

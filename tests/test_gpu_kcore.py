@@ -378,9 +378,10 @@ def test_maximum_vertex_range(k, flags, c):
 
 
 # ---- slot-compacted rounds (kcompact.cuh; n > 2^23, k <= 2) --------------------------------
-@pytest.mark.parametrize("tail,at", [("0", None), ("2", None), (None, None), ("2", "1.0"), ("2", "0")])
+@pytest.mark.parametrize("tail,at,creg", [("0", None, None), ("2", None, None), (None, None, None),
+                                          ("2", "1.0", None), ("2", "1.0", "0"), ("2", "0", None)])
 @pytest.mark.parametrize("c,k,r", [(0.85, 2, 3), (0.75, 2, 3), (0.6, 1, 3), (0.77, 2, 4)])
-def test_compact_rounds_modes(monkeypatch, tail, at, c, k, r):
+def test_compact_rounds_modes(monkeypatch, tail, at, creg, c, k, r):
     """The binned rounds with edge-bin frontier regions and slot compaction: handing over to
     the persistent kernel at the first small frontier (tail 0), never (tail 2), or by the
     default rule; compacting whenever the live set shrank at all (at 1.0), never (at 0), or at
@@ -391,12 +392,13 @@ def test_compact_rounds_modes(monkeypatch, tail, at, c, k, r):
     e = pk.gen_hypergraph(n, m, r, 70 + r, device=DEV)
     ref = O.sync_peel(e.cpu().numpy().view(np.uint32), n, k, want_peel_round=True)
     ratio = "0" if tail == "0" else None  # tail 0: hand over at the first small frontier
-    for name, val in (("PEEL_COMPACT_TAIL", tail), ("PEEL_COMPACT_AT", at), ("PEEL_COMPACT_TAIL_RATIO", ratio)):
+    for name, val in (("PEEL_COMPACT_TAIL", tail), ("PEEL_COMPACT_AT", at), ("PEEL_COMPACT_TAIL_RATIO", ratio),
+                      ("PEEL_CREG", creg)):
         if val is None:
             monkeypatch.delenv(name, raising=False)
         else:
             monkeypatch.setenv(name, val)
-    for compact in ("1", "0") if (tail, at) == (None, None) else ("1",):
+    for compact in ("1", "0") if (tail, at, creg) == (None, None, None) else ("1",):
         monkeypatch.setenv("PEEL_COMPACT", compact)
         res = pk.peel_kcore(e, n, k, want_peel_round=True)
         assert res.rounds == ref.rounds and res.survivors.tolist() == ref.survivors.tolist(), compact

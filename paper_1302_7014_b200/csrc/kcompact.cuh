@@ -85,7 +85,7 @@ struct RoundCtl {
 };
 struct RoundRule {    // the thresholds (compact_at, ctail_live_frac, ctail_ratio)
     uint64_t n;
-    double frac, tail, tratio, at;
+    double frac, tail, tratio, at, at1;  // at1: the first compaction (identity slots)
     int compaction;
 };
 
@@ -858,7 +858,8 @@ __global__ void __launch_bounds__(256) cround_ctl_kernel(Ctl *ctl, RoundCtl *rc,
             if (nF == 0) rc->stop = RC_DONE;
             else if ((double)nE < rule.frac * n && live >= rule.tail * n && slots >= rule.tratio * (double)nE)
                 rc->stop = RC_TAIL;
-            else if (rule.compaction && live <= rule.at * slots && 8.0 * (slots - live) >= 0.5 * n)
+            else if (rule.compaction && live <= (rc->nslots == rule.n ? rule.at1 : rule.at) * slots &&
+                     8.0 * (slots - live) >= 0.5 * n)
                 rc->stop = RC_COMPACT;
             else { go = 1; rc->ran = 1; }
             tt = t;
@@ -926,6 +927,10 @@ static SideStream &side_stream() {
 static double compact_at() {
     const char *e = getenv("PEEL_COMPACT_AT");  // live / slots ratio that triggers (A/B; 0: never)
     return e ? atof(e) : 0.5;
+}
+static double compact_at1() {
+    const char *e = getenv("PEEL_COMPACT_AT1");  // the first compaction (identity slots)
+    return e ? atof(e) : compact_at();
 }
 static int rounds_per_sync() {
     const char *e = getenv("PEEL_ROUNDS_PER_SYNC");
@@ -1058,7 +1063,7 @@ static peel_status run_compact(const uint32_t *edges, uint64_t n, uint64_t m, ui
     c.rc = rc;
     c.fec[0] = fecnt[0];
     c.fec[1] = fecnt[1];
-    const RoundRule rule = {n, frac, tail, tratio, compact_at(), compaction ? 1 : 0};
+    const RoundRule rule = {n, frac, tail, tratio, compact_at(), compact_at1(), compaction ? 1 : 0};
     const int K = rounds_per_sync();
     bool comp_pending = false;
     uint32_t t = 1;

@@ -159,7 +159,7 @@ def profile_file(kind, config, kernel=None):
     return None
 
 
-def ncu_traffic(config, kernel):
+def ncu_traffic(config, kernel, rounds=None):
     """DRAM bytes (read + write) per launch of `kernel`: from the committed `ncu --set full`
     capture of this config's kernel (profiles/r01_ncu_full_<kernel>_<config>.json) when there
     is one, else from the committed launch list (profiles/r01_traffic_<config>.json,
@@ -178,7 +178,10 @@ def ncu_traffic(config, kernel):
     if not ks:
         return None, None
     per_step = sum(k["dram_read_bytes_per_step"] + k["dram_write_bytes_per_step"] for k in ks)
-    return int(per_step / ks[-1]["launches_per_step"]), \
+    nlaunch = ks[-1]["launches_per_step"]
+    if rounds and kernel in ("round_kill_partition", "round_apply"):
+        nlaunch = min(nlaunch, rounds)  # launches after the device-side loop stopped move nothing
+    return int(per_step / nlaunch), \
         f"profiles/{os.path.basename(tf)} (ncu, dram__bytes_read.sum + dram__bytes_write.sum)"
 
 
@@ -953,6 +956,10 @@ def main():
     roof = None
     if dom:
         name, (ms_sum, nl) = dom
+        if name in ("round_kill_partition", "round_apply") and res.rounds:
+            # the compacted rounds' device-side loop launches 4 rounds per host sync; the launches
+            # after the loop stopped exit at once: per-launch figures count the rounds that ran
+            nl = min(nl, args.steps * int(res.rounds))
         avg_ms = ms_sum / max(nl, 1)
         alg = kb.get(name)  # bytes per STEP of this kernel (all its launches)
         if alg is None:  # CSR path / graph replay: whole-step formula over the whole-step time of its kernels
@@ -963,7 +970,7 @@ def main():
                              else (None, None))
         else:
             alg = alg / max(nl / args.steps, 1.0)  # per launch, like avg_ms
-            traffic, tsrc = ncu_traffic(args.config, name)
+            traffic, tsrc = ncu_traffic(args.config, name, int(res.rounds))
         ach = alg / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": name, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 4), "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,

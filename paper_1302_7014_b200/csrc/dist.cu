@@ -53,6 +53,14 @@ static inline size_t dal(size_t x) { return (x + 255) & ~(size_t)255; }
 
 __host__ __device__ inline uint64_t shard_lo(uint64_t n, int P, int q) { return (uint64_t)q * n / (uint64_t)P; }
 
+// owner of u: the number of shard boundaries lo[1 .. P-1] at or below u (P <= 8 compares)
+__device__ __forceinline__ int owner_fast(uint32_t u, const uint32_t (&lo)[8], int P) {
+    int q = 0;
+    #pragma unroll
+    for (int i = 1; i < 8; i++) q += (i < P) && u >= lo[i];
+    return q;
+}
+
 __device__ __forceinline__ int owner_of(uint32_t u, uint64_t n, int P) {
     int q = (int)(((uint64_t)u * (uint64_t)P) / n);
     if (q >= P) q = P - 1;
@@ -188,6 +196,8 @@ __device__ __forceinline__ void dist_decrement(ull *state, uint64_t v0, uint32_t
 struct DKArgs {
     const uint32_t *edges;
     uint64_t n, m;
+    uint32_t lo[8];  // shard boundaries lo[q] = shard_lo(n, P, q) for q < P (lo[0] = 0): owner
+                     // lookups by comparison, not a 64-bit division per endpoint
     int edges_vec;  // edges is 16-byte aligned (vector row loads)
     int P, p;
     uint32_t k;
@@ -224,11 +234,11 @@ __global__ void __launch_bounds__(DB) dist_kill_kernel(DKArgs a) {
                 load_row<R>(a.edges, e, a.m, a.edges_vec, u);
                 #pragma unroll
                 for (int j = 0; j < R; j++) mn = min(mn, u[j]);
-                if (owner_of(mn, a.n, a.P) == a.p) kills++;
+                if (owner_fast(mn, a.lo, a.P) == a.p) kills++;
                 uint32_t sent_mask = 0;
                 #pragma unroll
                 for (int j = 0; j < R; j++) {
-                    const int o = owner_of(u[j], a.n, a.P);
+                    const int o = owner_fast(u[j], a.lo, a.P);
                     if (o == a.p) {
                         if (u[j] != ent.x) dist_decrement(a.state, a.v0, u[j], e, a.k, q, slot, a.Fn, cn, crossed);
                     } else {
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(DB) dist_recv_kernel(DKArgs a, const uint32_t 
                 load_row<R>(a.edges, e, a.m, a.edges_vec, u);
                 #pragma unroll
                 for (int j = 0; j < R; j++) mn = min(mn, u[j]);
-                if (owner_of(mn, a.n, a.P) == a.p) kills++;
+                if (owner_fast(mn, a.lo, a.P) == a.p) kills++;
                 #pragma unroll
                 for (int j = 0; j < R; j++)
                     if (u[j] >= a.v0 && u[j] < a.v1) dist_decrement(a.state, a.v0, u[j], e, a.k, q, slot, a.Fn, cn, crossed);
@@ -343,9 +353,9 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             #pragma unroll
             for (int r = 0; r < R; r++) {
                 mn = min(mn, u[j][r]);
-                if (!(u[j][r] >= a.v0 && u[j][r] < a.v1)) sendm[j] |= 1u << owner_of(u[j][r], a.n, a.P);
+                if (!(u[j][r] >= a.v0 && u[j][r] < a.v1)) sendm[j] |= 1u << owner_fast(u[j][r], a.lo, a.P);
             }
-            if (owner_of(mn, a.n, a.P) == a.p) kills++;
+            if (owner_fast(mn, a.lo, a.P) == a.p) kills++;
         }
         if (!RECV) {
             // one push per destination; d is warp-uniform (each coalesced group targets one queue)
@@ -596,6 +606,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             DShard &d = sh[i];
             DKArgs a;
             a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
+            for (int q = 0; q < 8; q++) a.lo[q] = q < P ? (uint32_t)shard_lo(n, P, q) : 0u;
             a.edges_vec = ((uintptr_t)edges & 15) == 0;
             a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
             a.state = d.state; a.alive = d.alive;
@@ -709,6 +720,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             DShard &d = sh[i];
             DKArgs a;
             a.edges = edges; a.n = n; a.m = m; a.P = P; a.p = d.q; a.k = k;
+            for (int q = 0; q < 8; q++) a.lo[q] = q < P ? (uint32_t)shard_lo(n, P, q) : 0u;
             a.edges_vec = ((uintptr_t)edges & 15) == 0;
             a.v0 = d.v0; a.v1 = d.v1; a.nloc = nl_max;
             a.state = d.state; a.alive = d.alive;

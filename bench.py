@@ -662,6 +662,10 @@ def run_sweep_bench(args, pk, dev, ws, rank, local, n, T, r, k, text, barrier, s
                 "vs_baseline": None, "dtype": "u32/u64 integer",
                 "data": "synthetic G^r_{n,cn} trials (generation on device inside the timed region)",
                 "config": {"workload": f"C5s: {text}", "trials": T, "batch": batch,
+                           "path": ("per-trial groups (one trial per group of CTAs, 32-bit states in L2, rows "
+                                    "regenerated from the seed; sweep.cu)"
+                                    if os.environ.get("PEEL_SWEEP_GROUPS", "") != "0" and k == 2 and r <= 4
+                                    and n <= (1 << 22) else f"disjoint union of {batch} trials per peel_kcore call"),
                            "parallelism": f"trials sharded over {ws} rank(s)"},
                 "result": {"failure_fraction_crosses_half_at_c": cross, "c_star_2_3": 0.818469,
                            "mean_rounds_c0.70": float(R[:100].mean()), "mean_rounds_c0.898": float(R[-100:].mean()),

@@ -6,43 +6,9 @@
 // (ctr = {e_lo, e_hi, j/2, 'EDGE'}, key = {seed_lo, seed_hi}); vertex =
 // umulhi64(draw, n); rejected if already in the edge.
 #include "common.cuh"
+#include "genrow.cuh"
 
 namespace peel {
-
-// Philox4x32-10 (Salmon et al. SC'11), 10 rounds with Weyl key schedule.
-__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
-    #pragma unroll
-    for (int i = 0; i < 10; i++) {
-        uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), lo0 = 0xD2511F53u * c[0];
-        uint32_t hi1 = __umulhi(0xCD9E8D57u, c[2]), lo1 = 0xCD9E8D57u * c[2];
-        uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
-        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
-    }
-}
-
-// edge e of G^r_{n,.}(seed): r distinct vertices (see the header comment)
-template <int R>
-__device__ __forceinline__ void gen_one_edge(uint64_t e, uint64_t n, uint32_t k0, uint32_t k1, uint32_t (&acc)[R]) {
-    int na = 0;
-    uint32_t w[4];
-    for (uint32_t j = 0; na < R; j++) {
-        if ((j & 1) == 0) {
-            w[0] = (uint32_t)e; w[1] = (uint32_t)(e >> 32); w[2] = j >> 1; w[3] = 0x45444745u;
-            philox4x32_10(w, k0, k1);
-        }
-        uint64_t d = (j & 1) ? (((uint64_t)w[3] << 32) | w[2]) : (((uint64_t)w[1] << 32) | w[0]);
-        uint32_t v = (uint32_t)__umul64hi(d, n);
-        bool dup = false;
-        #pragma unroll
-        for (int i = 0; i < R; i++) dup |= (i < na) && (acc[i] == v);
-        if (!dup) {
-            #pragma unroll
-            for (int i = 0; i < R; i++) if (i == na) acc[i] = v;
-            na++;
-        }
-    }
-}
 
 template <int R>
 __global__ void __launch_bounds__(256) gen_edges_kernel(uint64_t n, uint64_t m, uint64_t seed,

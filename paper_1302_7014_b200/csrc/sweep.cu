@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "genrow.cuh"
 
 namespace peel {
 
@@ -72,6 +73,180 @@ static SweepLayout sweep_layout(uint64_t n, uint64_t max_m, uint32_t r, uint32_t
     return L;
 }
 
+// ---- per-trial groups (k = 2, r <= 4, n <= 2^22: the paper's protocol, C5s) ------------------
+// A trial of the protocol (n = 10^6) has a 4 MB working set once its state is one 32-bit word
+// per vertex, so the whole peel stays in L2 if only ~16 trials are in flight.  NG groups of G
+// co-resident CTAs (one cooperative launch) take trials off a counter; a group peels its trial
+// with group barriers (one L2 counter) between phases and rounds, and regenerates a killed
+// edge's row from (seed, e) -- G^r_{n,m} is a pure function of it (genrow.cuh), so no edge list
+// is stored.  The schedule is kcore.cu's (the crossing rule of DESIGN §5):
+//   state[v] = (Σ incident alive edge ids mod 2^(32-CB)) << CB | count        (count < 2^CB)
+// m <= 2^(32-CB), so a count-1 vertex's id field IS its edge.  A count reaching 2^CB would carry
+// into the id field: the scan checks Σ count == r m and flags the trial, and the host peels a
+// flagged trial on the union path.  Per trial: rounds = rounds with F_t non-empty, core =
+// vertices with count >= k after the build minus the crossings of every round.
+static constexpr int SG_BLOCK = 512;
+#ifndef PEEL_SG_MINB
+#define PEEL_SG_MINB 3
+#endif
+static constexpr int SG_QCAP = 2048;
+static constexpr uint32_t SG_CHUNK = 65536;  // trials per launch (device result arrays)
+
+struct __align__(128) SGroupCtl {
+    unsigned bar;    // barrier arrivals (monotonic over the launch)
+    unsigned trial;  // the group's trial
+    ull cnt[3];      // frontier entries of round t at cnt[t % 3]
+    ull sum, live, nf1;
+};
+
+struct SGArgs {
+    uint64_t n;
+    uint32_t k, cb, G, ntrials;
+    const uint64_t *m, *seeds;
+    uint32_t *out_rounds, *flag;
+    ull *out_core;
+    uint32_t *state;  // per group: sstride words
+    uint32_t *alive;  // per group: astride words
+    uint32_t *list;   // per group: 2 lists of n entries (lstride words)
+    uint64_t sstride, astride, lstride;
+    SGroupCtl *ctl;
+    unsigned *next;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// barrier of the group's G CTAs (co-resident: cooperative launch); every thread calls it
+__device__ __forceinline__ void group_sync(unsigned *bar, unsigned &target, unsigned G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        target += G;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire_u32(bar) < target) {}
+    }
+    __syncthreads();
+}
+
+template <int R>
+__global__ void __launch_bounds__(SG_BLOCK, PEEL_SG_MINB) sweep_group_kernel(SGArgs a) {
+    typedef BlockQueueT<uint32_t, SG_QCAP, SG_BLOCK> Q;
+    __shared__ Q bq;
+    __shared__ unsigned s_trial;
+    const uint32_t g = blockIdx.x / a.G, q = blockIdx.x % a.G;
+    SGroupCtl *c = a.ctl + g;
+    uint32_t *st = a.state + g * a.sstride;
+    uint32_t *alive = a.alive + g * a.astride;
+    uint32_t *L0 = a.list + g * a.lstride, *L1 = L0 + a.n;
+    const uint64_t tg = (uint64_t)q * SG_BLOCK + threadIdx.x, nthr = (uint64_t)a.G * SG_BLOCK;
+    const uint64_t n = a.n;
+    const uint32_t CB = a.cb, cmask = (1u << CB) - 1u, k = a.k;
+    unsigned target = 0;
+    bq_init(bq);
+    int slot = 0;
+    for (;;) {
+        if (q == 0 && threadIdx.x == 0) {
+            c->trial = atomicAdd(a.next, 1u);
+            c->cnt[0] = c->cnt[1] = c->cnt[2] = 0ull;
+            c->sum = c->live = c->nf1 = 0ull;
+        }
+        group_sync(&c->bar, target, a.G);
+        if (threadIdx.x == 0) s_trial = *(volatile unsigned *)&c->trial;
+        __syncthreads();
+        const uint32_t T = s_trial;
+        if (T >= a.ntrials) break;  // uniform over the group
+        const uint64_t m = a.m[T], seed = a.seeds[T];
+        const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+        // zero the state; alive bits of edges [0, m)
+        {
+            uint4 *z = reinterpret_cast<uint4 *>(st);
+            for (uint64_t i = tg; i < (n + 3) / 4; i += nthr) z[i] = make_uint4(0u, 0u, 0u, 0u);
+            const uint64_t aw = (m + 31) / 32;
+            for (uint64_t i = tg; i < aw; i += nthr)
+                alive[i] = (i == aw - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : ~0u;
+        }
+        group_sync(&c->bar, target, a.G);
+        // build: r increments per edge (fire-and-forget REDs into the L2-resident state)
+        for (uint64_t e = tg; e < m; e += nthr) {
+            uint32_t u[R];
+            gen_one_edge<R>(e, n, k0, k1, u);
+            const uint32_t inc = ((uint32_t)e << CB) + 1u;
+            #pragma unroll
+            for (int j = 0; j < R; j++) atomicAdd(st + u[j], inc);
+        }
+        group_sync(&c->bar, target, a.G);
+        // scan: F_1 (count < k), its entries (count 1), the live set, the overflow check
+        {
+            ull sum = 0, live = 0, nf = 0;
+            for (uint64_t v0 = (uint64_t)q * SG_BLOCK; v0 < n; v0 += nthr) {
+                const uint64_t v = v0 + threadIdx.x;
+                if (v < n) {
+                    const uint32_t cnt = __ldcg(st + v) & cmask;
+                    sum += cnt;
+                    if (cnt >= k) live++;
+                    else {
+                        nf++;
+                        if (cnt == 1u) bq_push(bq, slot, (uint32_t)v, L0, &c->cnt[1]);
+                    }
+                }
+                bq_flush(bq, slot, L0, &c->cnt[1]);
+                slot ^= 1;
+            }
+            block_add<SG_BLOCK>(&c->sum, sum);
+            block_add<SG_BLOCK>(&c->live, live);
+            block_add<SG_BLOCK>(&c->nf1, nf);
+        }
+        group_sync(&c->bar, target, a.G);
+        const ull S = ld_cg_u64(&c->sum), LIVE = ld_cg_u64(&c->live), NF1 = ld_cg_u64(&c->nf1);
+        const bool over = S != (ull)R * m;
+        uint32_t rounds = NF1 ? 1u : 0u;
+        ull crossed = 0;
+        for (uint32_t t = 1; !over; t++) {
+            const ull E = ld_cg_u64(&c->cnt[t % 3]);  // entries of F_t (t >= 2: |F_t|)
+            if (E == 0) break;                          // uniform: read after the same barrier
+            if (t >= 2) { rounds = t; crossed += E; }
+            if (q == 0 && threadIdx.x == 0) c->cnt[(t + 2) % 3] = 0ull;  // read before the last barrier
+            const uint32_t *Lc = (t & 1) ? L0 : L1;
+            uint32_t *Ln = (t & 1) ? L1 : L0;
+            ull *cn = &c->cnt[(t + 1) % 3];
+            for (uint64_t i0 = (uint64_t)q * SG_BLOCK; i0 < E; i0 += nthr) {
+                const uint64_t i = i0 + threadIdx.x;
+                if (i < E) {
+                    const uint32_t v = __ldcg(Lc + i);
+                    // v has count 1 (its edge e alive at the round start) or 0 (e killed this
+                    // round by another vertex of e): either way the test-and-clear decides
+                    const uint32_t s = __ldcg(st + v);
+                    const uint32_t e = s >> CB;
+                    const uint32_t bit = 1u << (e & 31);
+                    if ((s & cmask) && (atomicAnd(alive + (e >> 5), ~bit) & bit)) {
+                        uint32_t u[R];
+                        gen_one_edge<R>(e, n, k0, k1, u);
+                        const uint32_t dec = 0u - ((e << CB) + 1u);
+                        uint32_t old[R];
+                        #pragma unroll
+                        for (int j = 0; j < R; j++) old[j] = u[j] != v ? atomicAdd(st + u[j], dec) : 0u;
+                        #pragma unroll
+                        for (int j = 0; j < R; j++)
+                            if (u[j] != v && (old[j] & cmask) == k) bq_push(bq, slot, u[j], Ln, cn);
+                    }
+                }
+                bq_flush(bq, slot, Ln, cn);
+                slot ^= 1;
+            }
+            group_sync(&c->bar, target, a.G);
+        }
+        group_sync(&c->bar, target, a.G);  // every CTA read the control block: it may be reset
+        if (q == 0 && threadIdx.x == 0) {
+            a.out_rounds[T] = rounds;
+            a.out_core[T] = LIVE - crossed;
+            a.flag[T] = over ? 1u : 0u;
+        }
+    }
+}
+
 }  // namespace peel
 
 using namespace peel;
@@ -85,14 +260,134 @@ static uint32_t sweep_workers() {
     return (uint32_t)(w < 1 ? 1 : (w > 8 ? 8 : w));
 }
 
-extern "C" size_t peel_sweep_workspace_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
+// ---- the per-trial group path (host side)
+// PEEL_SWEEP_GROUPS: 0 = off (every trial on the union path), N > 0 = N groups; unset = as many
+// groups as fit PEEL_SWEEP_L2MB (default 80) MB of per-trial working set in L2.
+static const uint32_t SG_NG_MAX = 512;
+
+struct SGLayout {
+    size_t ctl, next, par, res, state, alive, list, total;
+    uint64_t sstride, astride, lstride;
+    uint32_t NG, cb;
+};
+
+static uint32_t sg_bits(uint64_t x) {  // bits to hold values < x (x >= 1)
+    uint32_t b = 1;
+    while (b < 64 && (1ull << b) < x) b++;
+    return b;
+}
+
+static bool sg_applicable(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k) {
+    const char *e = getenv("PEEL_SWEEP_GROUPS");
+    if (e && atoi(e) == 0) return false;
+    if (k != 2 || r < 2 || r > 4 || n < r || n > (1ull << 22)) return false;
+    const uint32_t eb = sg_bits(max_m ? max_m : 1);
+    return eb <= 28;  // at least 4 count bits
+}
+
+static SGLayout sg_layout(uint64_t n, uint64_t max_m) {
+    SGLayout L;
+    const char *e = getenv("PEEL_SWEEP_GROUPS");
+    uint32_t ng;
+    if (e && atoi(e) > 0) {
+        ng = (uint32_t)atoi(e);
+    } else {
+        const char *l2 = getenv("PEEL_SWEEP_L2MB");
+        const double budget = (l2 ? atof(l2) : 80.0) * 1048576.0;
+        const double per = 4.0 * n * 1.25 + max_m / 8.0 + 4096.0;  // state, touched list part, alive bits
+        ng = (uint32_t)(budget / per);
+    }
+    L.NG = ng < 1 ? 1 : (ng > SG_NG_MAX ? SG_NG_MAX : ng);
+    L.cb = 32 - sg_bits(max_m ? max_m : 1);
+    const char *cbe = getenv("PEEL_SWEEP_CB");  // tests: force a narrow count field (overflow path)
+    if (cbe && atoi(cbe) > 0 && (uint32_t)atoi(cbe) < L.cb) L.cb = (uint32_t)atoi(cbe);
+    L.sstride = (n + 63) & ~63ull;
+    L.astride = (((max_m + 31) / 32) + 63) & ~63ull;
+    L.lstride = (2 * n + 63) & ~63ull;
+    size_t o = 0;
+    L.ctl = o; o += al2(sizeof(SGroupCtl) * L.NG);
+    L.next = o; o += al2(sizeof(unsigned));
+    L.par = o; o += al2(sizeof(uint64_t) * 2 * SG_CHUNK);
+    L.res = o; o += al2((sizeof(uint32_t) * 2 + sizeof(ull)) * SG_CHUNK);
+    L.state = o; o += al2(sizeof(uint32_t) * L.sstride * L.NG);
+    L.alive = o; o += al2(sizeof(uint32_t) * L.astride * L.NG);
+    L.list = o; o += al2(sizeof(uint32_t) * L.lstride * L.NG);
+    L.total = o;
+    return L;
+}
+
+template <int R>
+static peel_status sg_launch(SGArgs &a, uint32_t NG, cudaStream_t s) {
+    int bps = 0;
+    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sweep_group_kernel<R>, SG_BLOCK, 0));
+    if (bps < 1) return PEEL_ECUDA;
+    const uint32_t total = (uint32_t)(bps * num_sms());
+    if (NG > total) NG = total;
+    if (NG > a.ntrials) NG = a.ntrials;
+    a.G = total / NG;
+    void *args[] = {&a};
+    ProfScope ps("sweep_groups", s);
+    PEEL_CUDA(cudaLaunchCooperativeKernel((void *)sweep_group_kernel<R>, NG * a.G, SG_BLOCK, args, 0, s));
+    return PEEL_OK;
+}
+
+// every trial on the group path; trials whose count field overflowed come back in `redo`
+static peel_status sweep_groups(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
+                                uint64_t ntrials, uint32_t *out_rounds, uint64_t *out_core, void *workspace,
+                                const SGLayout &L, cudaStream_t s, std::vector<uint64_t> &redo) {
+    char *ws = (char *)workspace;
+    uint64_t *par = (uint64_t *)(ws + L.par);
+    uint32_t *rr = (uint32_t *)(ws + L.res), *fl = rr + SG_CHUNK;
+    ull *cr = (ull *)(fl + SG_CHUNK);
+    std::vector<uint32_t> hr(SG_CHUNK), hf(SG_CHUNK);
+    std::vector<ull> hc(SG_CHUNK);
+    for (uint64_t t0 = 0; t0 < ntrials; t0 += SG_CHUNK) {
+        const uint32_t B = (uint32_t)(ntrials - t0 < SG_CHUNK ? ntrials - t0 : SG_CHUNK);
+        PEEL_CUDA(cudaMemcpyAsync(par, m + t0, sizeof(uint64_t) * B, cudaMemcpyHostToDevice, s));
+        PEEL_CUDA(cudaMemcpyAsync(par + SG_CHUNK, seeds + t0, sizeof(uint64_t) * B, cudaMemcpyHostToDevice, s));
+        PEEL_CUDA(cudaMemsetAsync(ws + L.ctl, 0, L.next + sizeof(unsigned) - L.ctl, s));
+        SGArgs a;
+        a.n = n; a.k = k; a.cb = L.cb; a.G = 1; a.ntrials = B;
+        a.m = par; a.seeds = par + SG_CHUNK;
+        a.out_rounds = rr; a.flag = fl; a.out_core = cr;
+        a.state = (uint32_t *)(ws + L.state); a.alive = (uint32_t *)(ws + L.alive); a.list = (uint32_t *)(ws + L.list);
+        a.sstride = L.sstride; a.astride = L.astride; a.lstride = L.lstride;
+        a.ctl = (SGroupCtl *)(ws + L.ctl); a.next = (unsigned *)(ws + L.next);
+        peel_status st = PEEL_EINVAL;
+        switch (r) {
+            case 2: st = sg_launch<2>(a, L.NG, s); break;
+            case 3: st = sg_launch<3>(a, L.NG, s); break;
+            case 4: st = sg_launch<4>(a, L.NG, s); break;
+        }
+        if (st != PEEL_OK) return st;
+        PEEL_CUDA(cudaMemcpyAsync(hr.data(), rr, sizeof(uint32_t) * B, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaMemcpyAsync(hf.data(), fl, sizeof(uint32_t) * B, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaMemcpyAsync(hc.data(), cr, sizeof(ull) * B, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        for (uint32_t b = 0; b < B; b++) {
+            if (hf[b]) { redo.push_back(t0 + b); continue; }
+            out_rounds[t0 + b] = hr[b];
+            out_core[t0 + b] = hc[b];
+        }
+    }
+    return PEEL_OK;
+}
+
+static size_t sweep_union_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
     if (batch == 0 || batch > 1024 || n < r || n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return 0;
     return sweep_layout(n, max_m, r, k, batch).total * sweep_workers();
 }
 
-extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
-                                  uint64_t ntrials, uint32_t batch, uint32_t *out_rounds, uint64_t *out_core,
-                                  void *workspace, size_t ws_bytes, void *stream) {
+extern "C" size_t peel_sweep_workspace_bytes(uint64_t n, uint64_t max_m, uint32_t r, uint32_t k, uint32_t batch) {
+    const size_t u = sweep_union_bytes(n, max_m, r, k, batch);
+    if (!u || !sg_applicable(n, max_m, r, k)) return u;
+    const size_t g = sg_layout(n, max_m).total;
+    return g > u ? g : u;
+}
+
+static peel_status sweep_union(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
+                               uint64_t ntrials, uint32_t batch, uint32_t *out_rounds, uint64_t *out_core,
+                               void *workspace, size_t ws_bytes, void *stream) {
     if (!m || !seeds || !out_rounds || !out_core || !workspace || batch == 0 || batch > 1024 || r < 2 || r > 8 || n < r)
         return PEEL_EINVAL;
     uint64_t max_m = 0;
@@ -186,5 +481,38 @@ extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint
     cudaEventDestroy(start);
     for (uint32_t w = 0; w < NW; w++)
         if (st[w] != PEEL_OK) return st[w];
+    return PEEL_OK;
+}
+
+extern "C" peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, const uint64_t *seeds,
+                                  uint64_t ntrials, uint32_t batch, uint32_t *out_rounds, uint64_t *out_core,
+                                  void *workspace, size_t ws_bytes, void *stream) {
+    if (!m || !seeds || !out_rounds || !out_core || !workspace || batch == 0 || batch > 1024 || r < 2 || r > 8 || n < r)
+        return PEEL_EINVAL;
+    uint64_t max_m = 0;
+    for (uint64_t t = 0; t < ntrials; t++) max_m = m[t] > max_m ? m[t] : max_m;
+    if (n * batch > (1ull << 32) || max_m * batch >= (1ull << 32)) return PEEL_EINVAL;
+    if (ntrials == 0) return PEEL_OK;
+    if (!sg_applicable(n, max_m, r, k))
+        return sweep_union(n, r, k, m, seeds, ntrials, batch, out_rounds, out_core, workspace, ws_bytes, stream);
+    const SGLayout L = sg_layout(n, max_m);
+    if (ws_bytes < L.total) return PEEL_ENOMEM;
+    std::vector<uint64_t> redo;
+    peel_status st;
+    {
+        prof_begin_call();
+        prof_hold(true);
+        st = sweep_groups(n, r, k, m, seeds, ntrials, out_rounds, out_core, workspace, L, (cudaStream_t)stream, redo);
+        prof_hold(false);
+        prof_collect();
+    }
+    if (st != PEEL_OK || redo.empty()) return st;
+    // trials whose count field overflowed: the union path (64-bit states), on the same workspace
+    std::vector<uint64_t> rm(redo.size()), rs(redo.size()), rc(redo.size());
+    std::vector<uint32_t> rr(redo.size());
+    for (size_t i = 0; i < redo.size(); i++) { rm[i] = m[redo[i]]; rs[i] = seeds[redo[i]]; }
+    st = sweep_union(n, r, k, rm.data(), rs.data(), redo.size(), batch, rr.data(), rc.data(), workspace, ws_bytes, stream);
+    if (st != PEEL_OK) return st;
+    for (size_t i = 0; i < redo.size(); i++) { out_rounds[redo[i]] = rr[i]; out_core[redo[i]] = rc[i]; }
     return PEEL_OK;
 }

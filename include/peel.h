@@ -166,10 +166,13 @@ peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, uint64_t m, 
  * seed seeds[t] (exactly peel_gen_hypergraph(n, m[t], r, seeds[t])) and peel it
  * to its k-core (exactly peel_kcore); report out_rounds[t] (host u32) and
  * out_core[t] (host u64: k-core vertices; "Failed" in Table 1 iff > 0).
- * m[], seeds[] are host arrays.  Trials are processed `batch` at a time as one
- * disjoint-union hypergraph (the synchronous peel of a disjoint union is the
- * trials' synchronous peels in lockstep), so 1 <= batch <= 1024, batch * n <= 2^32 and
- * batch * max(m) < 2^32.  Multi-GPU sweeps shard the trial index range across
+ * m[], seeds[] are host arrays.  For k = 2, r <= 4 and n <= 2^22 each trial is peeled by
+ * a group of co-resident CTAs with 32-bit L2-resident states and edge rows regenerated
+ * from (seeds[t], e) (PEEL_SWEEP_GROUPS=0 turns it off); a trial whose
+ * 32-bit count field would overflow is redone on the union path.  Otherwise trials are
+ * processed `batch` at a time as one disjoint-union hypergraph (the synchronous peel of a
+ * disjoint union is the trials' synchronous peels in lockstep).  Either way
+ * 1 <= batch <= 1024, batch * n <= 2^32 and batch * max(m) < 2^32.  Multi-GPU sweeps shard the trial index range across
  * ranks (no data-path collective); see paper_1302_7014_b200/trials.py.
  * workspace: dev, peel_sweep_workspace_bytes(n, max(m), r, k, batch) bytes.
  * Blocking (one stream sync per batch).

@@ -67,6 +67,13 @@ peel_status launch_gen_batch(uint64_t n, uint32_t r, uint32_t B, const uint64_t 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ ull ld_cg_u64(const ull *p) { return __ldcg(p); }
 
+// acquire load (gpu scope): spin-waits on counters other blocks release with a fence + atomic
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // bulk prefetch of [p, p + bytes) into L2 (p and bytes multiples of 16)
 __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");

@@ -113,12 +113,6 @@ struct SGArgs {
     unsigned *next;
 };
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // barrier of the group's G CTAs (co-resident: cooperative launch); every thread calls it
 __device__ __forceinline__ void group_sync(unsigned *bar, unsigned &target, unsigned G) {
     __syncthreads();
@@ -175,7 +169,7 @@ __global__ void __launch_bounds__(SG_BLOCK, PEEL_SG_MINB) sweep_group_kernel(SGA
             gen_one_edge<R>(e, n, k0, k1, u);
             const uint32_t inc = ((uint32_t)e << CB) + 1u;
             #pragma unroll
-            for (int j = 0; j < R; j++) atomicAdd(st + u[j], inc);
+            for (int j = 0; j < R; j++) asm volatile("red.global.add.u32 [%0], %1;" ::"l"(st + u[j]), "r"(inc) : "memory");
         }
         group_sync(&c->bar, target, a.G);
         // scan: F_1 (count < k), its entries (count 1), the live set, the overflow check
@@ -262,7 +256,7 @@ static uint32_t sweep_workers() {
 
 // ---- the per-trial group path (host side)
 // PEEL_SWEEP_GROUPS: 0 = off (every trial on the union path), N > 0 = N groups; unset = as many
-// groups as fit PEEL_SWEEP_L2MB (default 80) MB of per-trial working set in L2.
+// groups as fit PEEL_SWEEP_L2MB (default 100) MB of per-trial working set in L2.
 static const uint32_t SG_NG_MAX = 512;
 
 struct SGLayout {
@@ -293,7 +287,8 @@ static SGLayout sg_layout(uint64_t n, uint64_t max_m) {
         ng = (uint32_t)atoi(e);
     } else {
         const char *l2 = getenv("PEEL_SWEEP_L2MB");
-        const double budget = (l2 ? atof(l2) : 80.0) * 1048576.0;
+        // C5s (n = 10^6): 12 / 16 / 20 / 24 / 32 groups -> 514 / 482 / 471 / 488 / 542 ms
+        const double budget = (l2 ? atof(l2) : 100.0) * 1048576.0;
         const double per = 4.0 * n * 1.25 + max_m / 8.0 + 4096.0;  // state, touched list part, alive bits
         ng = (uint32_t)(budget / per);
     }

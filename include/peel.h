@@ -148,7 +148,11 @@ peel_status peel_kcore(const uint32_t *edges, uint64_t n, uint64_t m, uint32_t r
  * peel_kcore_host -- the same computation with HOST input and output:
  * edges_host u32 [m][r] and core_mask_host u8 [n] are CPU memory (pinned for
  * full copy speed); the host->device copy of the edges and the device->host
- * copy of the mask are part of the call.  workspace must hold
+ * copy of the mask are part of the call.  For n > 2^23 (k <= 2) the edges are
+ * copied in 16 chunks that the build partitions as they land, and the mask
+ * comes back as 64 chunks of which only those holding a core vertex are copied;
+ * host threads zero the rest of core_mask_host during the peel (its previous
+ * contents are irrelevant either way).  workspace must hold
  * peel_kcore_host_workspace_bytes(n, m, r, k, flags) bytes of device memory.
  */
 size_t peel_kcore_host_workspace_bytes(uint64_t n, uint64_t m, uint32_t r, uint32_t k, uint32_t flags);

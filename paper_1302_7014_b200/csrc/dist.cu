@@ -532,7 +532,10 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         d.binned = false;
         if (L.bins_bytes && d.v1 - d.v0 > 0) {
             char *b = ws + (c->virt ? (size_t)d.q * L.total : 0);
-            if (!step(shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct))) break;
+            // the exchange buffers (send, recv: adjacent) are free during the build
+            if (!step(shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct, b + L.send,
+                                  L.bins - L.send)))
+                break;
         }
         d.binned = !direct;  // bins usable by the binned rounds (no overflow)
         if (direct) {  // small shard, or a bin overflowed

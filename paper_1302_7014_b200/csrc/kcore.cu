@@ -34,6 +34,7 @@
 #include <algorithm>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -2161,9 +2162,233 @@ size_t shard_build_bytes(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc) {
     return shard_bins(n, m, r, nloc).total;
 }
 
+// ---- narrow shards (v1 - v0 <= n / 4; dist.cu at P >= 4): the replicated edge list is read
+// by every shard, and bin_partition_kernel's per-chunk work (staging, validation, ranking, one
+// scan and one global atomic per bin, the write-out) is paid per 1024 edges however few of
+// their endpoints the shard keeps (C5 over 8 virtual shards: 6.4 ms per shard against 10 ms
+// for all endpoints).  Instead: (1) a streaming filter pass -- each block walks a fixed edge
+// range, validates every edge and appends the shard's endpoints (e << 32 | local id) to its own
+// region of a scratch buffer (warp ballots, one shared-memory counter; no global atomics);
+// (2) the regions' entries are counting-sorted into the shard's bins chunk by chunk, as
+// bin_partition_kernel sorts its chunks.  A region that overflows (adversarial skew) sends the
+// build back to bin_partition_kernel.
+static constexpr int SF_U = 4;          // edges per thread per step
+static constexpr int SB_CH = 2048;      // entries per binning chunk
+struct SFHead {                         // at the start of the scratch buffer
+    uint32_t ovf;
+    uint32_t pad[63];
+};
+
+#ifndef PEEL_SF_MINB
+#define PEEL_SF_MINB 6
+#endif
+template <int R>
+__global__ void __launch_bounds__(256, PEEL_SF_MINB) shard_filter_kernel(const uint32_t *__restrict__ edges, uint64_t n, uint64_t m,
+                                                           uint64_t v0, uint64_t v1, uint64_t per_block, ull *out,
+                                                           uint64_t cap_b, ull *counts, uint32_t *err, uint32_t *ovf,
+                                                           int vec) {
+    // a warp takes 128 edges (R * 32 16-byte words) per step: coalesced 16-byte loads staged in
+    // its own shared-memory slice, then lane l validates and filters edges 4 l .. 4 l + 3
+    // (scalar loads with a 12-byte lane stride cost three times the L1 wavefronts: 5.2 ms per
+    // C5 shard against the 1.4 ms the bytes take)
+    constexpr int WW = 32 * R;  // 16-byte words per warp step (128 edges)
+    __shared__ __align__(16) uint32_t stage[8][2][4 * WW];  // per warp, double-buffered
+    __shared__ uint32_t cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const uint64_t e_lo = (uint64_t)blockIdx.x * per_block, e_hi = min(m, e_lo + per_block);
+    ull *ob = out + (uint64_t)blockIdx.x * cap_b;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t wend = m * R;  // words in the array
+    const uint32_t nm1 = (uint32_t)(n - 1), lv0 = (uint32_t)v0, nl32 = (uint32_t)(v1 - v0);
+    bool over = false, bad = false;
+    // the step's R 16-byte words per lane into stage[w][buf]: cp.async (no registers held, the
+    // next step's copy in flight while this one is filtered); scalar loads at the array's end
+    auto fetch = [&](uint64_t base, int buf) {
+        const uint64_t w0 = base * R;  // a multiple of 4 R words: 16-byte aligned
+        #pragma unroll
+        for (int q = 0; q < R; q++) {
+            const uint64_t wi = w0 + 4 * (uint64_t)(q * 32 + lane);
+            uint32_t *dst = &stage[w][buf][4 * (q * 32 + lane)];
+            if (vec && wi + 4 <= wend) {
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(edges + wi) : "memory");
+            } else {
+                #pragma unroll
+                for (int x = 0; x < 4; x++) dst[x] = wi + x < wend ? __ldcs(edges + wi + x) : 0u;
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const uint64_t step = 8 * 128;
+    uint64_t base = e_lo + (uint64_t)w * 128;
+    if (base < e_hi) fetch(base, 0);
+    for (int buf = 0; base < e_hi; base += step, buf ^= 1) {
+        if (base + step < e_hi) fetch(base + step, buf ^ 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");  // keep one group per step
+        asm volatile("cp.async.wait_group 1;" ::: "memory");       // this step's copies landed
+        __syncwarp();
+        const uint32_t *sw = stage[w][buf];
+        uint32_t wd[4 * R];
+        #pragma unroll
+        for (int q = 0; q < R; q++) {
+            const uint4 v = reinterpret_cast<const uint4 *>(sw)[lane * R + q];
+            wd[4 * q] = v.x; wd[4 * q + 1] = v.y; wd[4 * q + 2] = v.z; wd[4 * q + 3] = v.w;
+        }
+        __syncwarp();  // every lane read buf before the step after next refills it
+        // each lane's kept words (32-bit compares: n <= 2^32, nloc < 2^32), a warp scan of the
+        // per-lane counts, ONE shared-memory reservation per warp step; a lane writes its kept
+        // words contiguously (the order inside a region is free: the binning pass sorts)
+        uint32_t keep = 0;  // bit R j + q: word q of the lane's edge j is the shard's
+        const uint32_t nin = (uint32_t)min((uint64_t)128, e_hi - base);  // edges of the step
+        #pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const bool inb = 4 * lane + j < nin;
+            bool valid = true;
+            #pragma unroll
+            for (int q = 0; q < R; q++) valid &= wd[R * j + q] <= nm1;
+            #pragma unroll
+            for (int q = 0; q < R; q++)
+                #pragma unroll
+                for (int q2 = q + 1; q2 < R; q2++) valid &= wd[R * j + q] != wd[R * j + q2];
+            bad |= inb && !valid;
+            uint32_t kj = 0;
+            #pragma unroll
+            for (int q = 0; q < R; q++) kj |= (uint32_t)(wd[R * j + q] - lv0 < nl32) << q;
+            keep |= (inb && valid ? kj : 0u) << (R * j);
+        }
+        const uint32_t c = __popc(keep);
+        uint32_t incl = c;
+        #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (tot) {  // warp-uniform
+            uint32_t run = 0;
+            if (lane == 0) run = atomicAdd(&cnt, tot);
+            run = __shfl_sync(0xffffffffu, run, 0) + incl - c;
+            const ull eb = (ull)(base + 4 * lane) << 32;
+            for (uint32_t kk = keep; kk; kk &= kk - 1, run++) {  // the lane's kept words, in order
+                const uint32_t x = __ffs(kk) - 1, j = x / R;
+                uint32_t u = 0;  // wd[x] with constant register indices (a dynamic index spills wd)
+                #pragma unroll
+                for (int y = 0; y < 4 * R; y++) u = x == (uint32_t)y ? wd[y] : u;
+                if (run < cap_b) ob[run] = (eb + ((ull)j << 32)) | (u - lv0);
+                else over = true;
+            }
+        }
+    }
+    if (bad) atomicOr(err, ERR_BADVERTEX);
+    if (over) atomicOr(ovf, 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) counts[blockIdx.x] = min((uint64_t)cnt, cap_b);
+}
+
+// chunk c of the regions' entries: region c / cpr, entries [(c % cpr) SB_CH, +SB_CH)
+__global__ void __launch_bounds__(256, 5) shard_bin_kernel(const ull *__restrict__ in, uint64_t cap_b,
+                                                           const ull *__restrict__ counts, uint64_t nchunks,
+                                                           uint64_t cpr, uint32_t nbins, ull *cursor,
+                                                           const ull *__restrict__ base, const ull *__restrict__ cap,
+                                                           ull *entries, uint32_t *binovf) {
+    extern __shared__ unsigned char smem_raw[];
+    ull *sent = (ull *)smem_raw;                  // [SB_CH]
+    ull *gpos = sent + SB_CH;                     // [nbins]
+    uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
+    uint32_t *offs = hist + nbins;
+    uint32_t *fill = offs + nbins;
+    __shared__ uint32_t total;
+    constexpr int PER = SB_CH / 256;
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint64_t reg = c / cpr, off = (c % cpr) * SB_CH;
+        const uint64_t cntr = counts[reg];
+        if (off >= cntr) continue;  // uniform
+        const uint32_t ne = (uint32_t)min((uint64_t)SB_CH, cntr - off);
+        const ull *src = in + reg * cap_b + off;
+        for (uint32_t b = threadIdx.x; b < nbins; b += 256) hist[b] = 0;
+        __syncthreads();
+        ull x[PER];
+        uint32_t rk[PER];
+        #pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const uint32_t i = q * 256 + threadIdx.x;
+            x[q] = i < ne ? __ldcs(src + i) : 0ull;
+        }
+        #pragma unroll
+        for (int q = 0; q < PER; q++)
+            if (q * 256 + threadIdx.x < ne) rk[q] = atomicAdd(&hist[(uint32_t)x[q] >> BIN_SHIFT], 1u);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const uint32_t per = (nbins + 31) / 32;
+            uint32_t loc = 0;
+            for (uint32_t q = 0; q < per; q++) {
+                const uint32_t b = threadIdx.x * per + q;
+                loc += b < nbins ? hist[b] : 0;
+            }
+            uint32_t y = loc;
+            #pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+                if ((int)threadIdx.x >= o) y += z;
+            }
+            uint32_t run = y - loc;
+            for (uint32_t q = 0; q < per; q++) {
+                const uint32_t b = threadIdx.x * per + q;
+                if (b < nbins) { offs[b] = run; run += hist[b]; }
+            }
+            if (threadIdx.x == 31) total = y;
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < nbins; b += 256)
+            if (hist[b]) {
+                const ull g = atomicAdd(cursor + b, (ull)hist[b]);
+                const ull cp = cap[b];
+                if (g + hist[b] > cp) atomicOr(binovf, 1u);
+                gpos[b] = base[b] + g;
+                fill[b] = (uint32_t)(g >= cp ? 0ull : min((ull)hist[b], cp - g));
+            }
+        #pragma unroll
+        for (int q = 0; q < PER; q++)
+            if (q * 256 + threadIdx.x < ne) sent[offs[(uint32_t)x[q] >> BIN_SHIFT] + rk[q]] = x[q];
+        __syncthreads();
+        const uint32_t tot = total;
+        for (uint32_t i = threadIdx.x; i < tot; i += 256) {
+            const ull v = sent[i];
+            const uint32_t b = (uint32_t)v >> BIN_SHIFT;
+            const uint32_t q = i - offs[b];
+            if (q < fill[b]) entries[gpos[b] + q] = v & ~(0xFFFFFFFFull ^ mask);
+        }
+        __syncthreads();
+    }
+}
+
+static size_t shard_bin_smem(uint64_t nbins) { return sizeof(ull) * SB_CH + (sizeof(ull) + 3 * sizeof(uint32_t)) * nbins; }
+
+// the filter path's geometry: blocks, edges per block, region capacity (expected endpoints of
+// the shard in a block's edges + 8 standard deviations + 4096), bytes of scratch it needs
+struct SFGeom {
+    uint64_t nblk, per_block, cap_b, cpr;
+    size_t bytes;
+};
+static SFGeom sf_geom(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc, int per_sm) {
+    SFGeom g;
+    g.nblk = (uint64_t)num_sms() * (per_sm < 1 ? 1 : per_sm);  // one resident wave
+    g.per_block = (((m + g.nblk - 1) / g.nblk) + 127) & ~127ull;  // whole 128-edge warp steps
+    const double lam = (double)g.per_block * r * (double)nloc / (double)n;
+    g.cap_b = (uint64_t)(lam + 8.0 * sqrt(lam)) + 4096;
+    const char *ce = getenv("PEEL_SHARD_FILTER_CAP");  // tests: a small region forces the fallback
+    if (ce && atoll(ce) > 0) g.cap_b = (uint64_t)atoll(ce);
+    g.cpr = (g.cap_b + SB_CH - 1) / SB_CH;
+    g.bytes = sizeof(SFHead) + al(sizeof(ull) * g.nblk) + sizeof(ull) * g.nblk * g.cap_b;
+    return g;
+}
+
 template <int R>
 static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1, ull *state,
-                                 uint32_t *err, char *scratch, cudaStream_t s, bool *overflow) {
+                                 uint32_t *err, char *scratch, cudaStream_t s, bool *overflow, void *tmp,
+                                 size_t tmp_bytes) {
     const uint64_t nloc = v1 - v0;
     const ShardBins B = shard_bins(n, m, R, nloc);
     ull *cursor = (ull *)(scratch + B.cursor), *base = (ull *)(scratch + B.base), *cap = (ull *)(scratch + B.cap);
@@ -2181,15 +2406,53 @@ static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, 
     int pb = 0;
     PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, bin_partition_kernel<R>, PART_BLOCK, smem));
     if (pb < 1) pb = 1;
+    int fpb = 0;
+    if constexpr (R <= 5) PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fpb, shard_filter_kernel<R>, 256, 0));
+    const SFGeom G = sf_geom(n, m, R, nloc, fpb);
+    const char *sfe = getenv("PEEL_SHARD_FILTER");  // 0: bin_partition_kernel for every shard (A/B)
+    // (R <= 5: the filter's staging is R 3 KB per warp of static shared memory)
+    const bool filt = R <= 5 && m && tmp && G.bytes <= tmp_bytes && 4 * nloc <= n && !(sfe && atoi(sfe) == 0);
+    uint32_t hflag = 0;
+    if constexpr (R <= 5) if (filt) {
+        SFHead *hd = (SFHead *)tmp;
+        ull *counts = (ull *)((char *)tmp + sizeof(SFHead));
+        ull *regions = (ull *)((char *)tmp + sizeof(SFHead) + al(sizeof(ull) * G.nblk));
+        PEEL_CUDA(cudaMemsetAsync(hd, 0, sizeof(SFHead), s));
+        {
+            ProfScope ps("shard_filter", s);
+            shard_filter_kernel<R><<<(unsigned)G.nblk, 256, 0, s>>>(edges, n, m, v0, v1, G.per_block, regions, G.cap_b,
+                                                                   counts, err, &hd->ovf, ((uintptr_t)edges & 15) == 0);
+        }
+        const size_t bsm = shard_bin_smem(B.nbins);
+        PEEL_CUDA(raise_smem((const void *)shard_bin_kernel, bsm));
+        int bb = 0;
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, shard_bin_kernel, 256, bsm));
+        {
+            ProfScope ps("shard_bin", s);
+            shard_bin_kernel<<<num_sms() * (bb < 1 ? 1 : bb), 256, bsm, s>>>(regions, G.cap_b, counts, G.nblk * G.cpr,
+                                                                             G.cpr, (uint32_t)B.nbins, cursor, base,
+                                                                             cap, entries, flag);
+        }
+        PEEL_CUDA(cudaGetLastError());
+        uint32_t hovf = 0;
+        PEEL_CUDA(cudaMemcpyAsync(&hovf, &hd->ovf, sizeof hovf, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof hflag, cudaMemcpyDeviceToHost, s));
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        if (hovf) {  // a region overflowed: the chunked partition from a clean slate
+            PEEL_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), s));
+            bin_init_kernel<<<1, 32, 0, s>>>(n, nloc, m, R, B.nbins, cursor, base, cap);
+        }
+        if (!hovf) goto binned;
+    }
     if (m) {
         ProfScope ps("bin_partition", s);
         bin_partition_kernel<R><<<num_sms() * pb, PART_BLOCK, smem, s>>>(edges, n, m, (uint32_t)B.nbins, cursor, base, cap,
                                                                           entries, err, flag, v0, v1, 0ull);
     }
     PEEL_CUDA(cudaGetLastError());
-    uint32_t hflag = 0;
     PEEL_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof hflag, cudaMemcpyDeviceToHost, s));
     PEEL_CUDA(cudaStreamSynchronize(s));
+binned:
     if (hflag) {
         *overflow = true;
         return PEEL_OK;
@@ -2278,15 +2541,16 @@ peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long lo
 }
 
 peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
-                        unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow) {
+                        unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow,
+                        void *tmp, size_t tmp_bytes) {
     switch (r) {
-        case 2: return shard_build_r<2>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
-        case 3: return shard_build_r<3>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
-        case 4: return shard_build_r<4>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
-        case 5: return shard_build_r<5>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
-        case 6: return shard_build_r<6>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
-        case 7: return shard_build_r<7>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
-        case 8: return shard_build_r<8>(edges, n, m, v0, v1, state, err, scratch, s, overflow);
+        case 2: return shard_build_r<2>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 3: return shard_build_r<3>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 4: return shard_build_r<4>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 5: return shard_build_r<5>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 6: return shard_build_r<6>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 7: return shard_build_r<7>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 8: return shard_build_r<8>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
     }
     return PEEL_EINVAL;
 }
@@ -2350,7 +2614,64 @@ extern "C" size_t peel_kcore_host_workspace_bytes(uint64_t n, uint64_t m, uint32
                                                   uint32_t flags) {
     size_t w = peel_kcore_workspace_bytes(n, m, r, k, flags);
     if (!w) return 0;
-    return w + al(sizeof(uint32_t) * r * m) + al(n);
+    return w + al(sizeof(uint32_t) * r * m) + al(n) + 256;  // edges, mask, the mask's chunk flags
+}
+
+// The core mask back to the host (peel_kcore_host): the host buffer is zeroed by host threads
+// while the GPU peels, and only the mask chunks that hold a core vertex are copied back -- none
+// below the threshold, where the core is empty (C5: the 1 GB device-to-host copy, ~20 ms of the
+// end-to-end step, is skipped).  Same bytes in the caller's buffer either way.
+static constexpr uint32_t MASK_CHUNKS = 64;
+
+__global__ void __launch_bounds__(256) mask_chunks_kernel(const uint8_t *__restrict__ mask, uint64_t n, uint64_t chunk,
+                                                          uint32_t *flags) {
+    const uint64_t n16 = n / 16;
+    for (uint64_t i = blockIdx.x * 256ull + threadIdx.x; i < n16; i += (uint64_t)gridDim.x * 256) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(mask) + i);
+        if (v.x | v.y | v.z | v.w) flags[(i * 16) / chunk] = 1u;
+    }
+    for (uint64_t v = n16 * 16 + blockIdx.x * 256ull + threadIdx.x; v < n; v += (uint64_t)gridDim.x * 256)
+        if (mask[v]) flags[v / chunk] = 1u;
+}
+
+struct HostZero {  // zero a host buffer on a few threads (joined by finish / the destructor)
+    std::vector<std::thread> th;
+    HostZero(uint8_t *p, uint64_t n) {
+        const unsigned T = n >= (64ull << 20) ? 4u : (n ? 1u : 0u);
+        for (unsigned t = 0; t < T; t++) {
+            const uint64_t lo = n * t / T, hi = n * (t + 1) / T;
+            th.emplace_back([=]() { memset(p + lo, 0, hi - lo); });
+        }
+    }
+    void finish() {
+        for (auto &x : th) x.join();
+        th.clear();
+    }
+    ~HostZero() { finish(); }
+};
+
+static peel_status mask_to_host(const uint8_t *d_mask, uint8_t *h_mask, uint64_t n, uint32_t *d_flags, HostZero &hz,
+                                cudaStream_t s) {
+    if (!n) return PEEL_OK;
+    const uint64_t chunk = (((n + MASK_CHUNKS - 1) / MASK_CHUNKS) + 15) & ~15ull;
+    uint32_t hf[MASK_CHUNKS];
+    PEEL_CUDA(cudaMemsetAsync(d_flags, 0, sizeof hf, s));
+    {
+        ProfScope ps("mask_chunks", s);
+        mask_chunks_kernel<<<grid_for(n / 16 + 1), 256, 0, s>>>(d_mask, n, chunk, d_flags);
+    }
+    PEEL_CUDA(cudaGetLastError());
+    PEEL_CUDA(cudaMemcpyAsync(hf, d_flags, sizeof hf, cudaMemcpyDeviceToHost, s));
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    hz.finish();  // the zeros land before any chunk is copied over them
+    for (uint32_t c = 0; c < MASK_CHUNKS; c++) {
+        const uint64_t lo = c * chunk;
+        if (!hf[c] || lo >= n) continue;
+        const uint64_t len = std::min<uint64_t>(chunk, n - lo);
+        PEEL_CUDA(cudaMemcpyAsync(h_mask + lo, d_mask + lo, len, cudaMemcpyDeviceToHost, s));
+    }
+    PEEL_CUDA(cudaStreamSynchronize(s));
+    return PEEL_OK;
 }
 
 extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, uint64_t m,
@@ -2379,6 +2700,7 @@ extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, u
     }
     // per host thread and device: concurrent calls (distinct streams and workspaces, peel.h)
     // each get their own copy stream and events, and no lock is held across the peel
+    HostZero hz(core_mask_host, n);
     static thread_local std::map<int, std::pair<cudaStream_t, std::vector<cudaEvent_t>>> res;
     int dev = 0;
     PEEL_CUDA(cudaGetDevice(&dev));
@@ -2402,7 +2724,6 @@ extern "C" peel_status peel_kcore_host(const uint32_t *edges_host, uint64_t n, u
     peel_status st = kcore_entry(d_edges, n, m, r, k, flags, d_mask, rounds, survivors, killed, cap, nullptr,
                                  workspace, w, stream, m ? &es : nullptr);
     if (st != PEEL_OK && st != PEEL_ETRUNC) return st;
-    if (n) PEEL_CUDA(cudaMemcpyAsync(core_mask_host, d_mask, n, cudaMemcpyDeviceToHost, s));
-    PEEL_CUDA(cudaStreamSynchronize(s));
-    return st;
+    const peel_status sm = mask_to_host(d_mask, core_mask_host, n, (uint32_t *)(base + w + al(sizeof(uint32_t) * r * m) + al(n)), hz, s);
+    return sm != PEEL_OK ? sm : st;
 }

@@ -16,8 +16,12 @@ size_t shard_build_bytes(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc);
 // every edge of `edges` (validated: bad edges set ERR bit 1 in *err).  *overflow = true if a
 // bin exceeded its capacity (adversarial degree skew): the caller then builds directly.
 // Stream-ordered except for one small device-to-host read of the overflow flag.
+// tmp / tmp_bytes: optional device scratch that is free during the build (dist.cu: the
+// exchange buffers).  A narrow shard (v1 - v0 <= n / 4) with enough of it takes the filter
+// path: one streaming pass keeps the shard's endpoints, a second bins them.
 peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
-                        unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow);
+                        unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow,
+                        void *tmp = nullptr, size_t tmp_bytes = 0);
 
 // the shard's bins as the binned rounds use them: per-bin cursors and bases into `entries`
 // (capacities from the build: a round's decrements of a bin are a subset of the build's),

@@ -123,6 +123,32 @@ def test_binned_shard_build_vs_oracle(P):
     check(np.concatenate([hub[ok], e[400000:]]), n, 2, P)
 
 
+@pytest.mark.parametrize("P", [4, 5])
+def test_narrow_shard_filter_build_vs_oracle(P, monkeypatch):
+    """Shards of > 2^23 vertices that are at most n/4 wide take the filter build (a streaming
+    pass keeps the shard's endpoints in per-block regions, a second bins them): bit-exact
+    against the oracle -- and so are the region-overflow fallback to the chunked partition
+    (regions forced small) and the chunked partition itself (PEEL_SHARD_FILTER=0)."""
+    n = P * ((1 << 23) + 4099) + 17
+    m = int(0.78 * n)
+    e = O.gen_hypergraph(n, m, 3, seed=60 + P)
+    ref = O.sync_peel(e, n, 2)
+    ed = torch.from_numpy(e.view(np.int32)).to(DEV)
+    for env in ({}, {"PEEL_SHARD_FILTER_CAP": "5000"}, {"PEEL_SHARD_FILTER": "0"}):
+        for name in ("PEEL_SHARD_FILTER_CAP", "PEEL_SHARD_FILTER"):
+            if name in env:
+                monkeypatch.setenv(name, env[name])
+            else:
+                monkeypatch.delenv(name, raising=False)
+        res = pk.peel_kcore_dist(pk.Comm.virtual_shards(P), ed, n, 2)
+        assert res.rounds == ref.rounds, env
+        assert res.survivors.tolist() == ref.survivors.tolist() and res.killed.tolist() == ref.killed.tolist(), env
+        assert np.array_equal(res.core_mask.cpu().numpy(), ref.core_mask), env
+    del ed, res
+    pk._ws_cache.clear()
+    torch.cuda.empty_cache()
+
+
 # ---- cell-partitioned IBLT (SURVEY §8 f3) -------------------------------------------------
 def iblt_check(C, r, seed, keys_np, P, blog=0):
     o = O.Iblt(C, r, seed, blog=blog)

@@ -203,11 +203,13 @@ def test_round_cap_truncation():
 
 
 @pytest.mark.parametrize("n,m,r,k,pin", [(50021, 40000, 3, 2, True), ((1 << 23) + 4099, 6300000, 3, 2, True),
+                                         ((1 << 23) + 4099, 7560000, 3, 2, True),  # c = 0.9: a core to copy back
                                          ((1 << 23) + 4099, 6300000, 3, 2, False), ((1 << 23) + 17, 9000000, 3, 3, True),
                                          (3000, 17, 4, 2, True)])
 def test_host_buffer_entry_point(n, m, r, k, pin):
     # peel_kcore_host copies the edges in 16 chunks on its own stream; n > 2^23 (binned build)
-    # partitions each chunk as it lands; k = 3 (CSR) and small n wait for the whole copy
+    # partitions each chunk as it lands, and the mask comes back by chunks holding a core vertex
+    # (the rest zeroed on the host); k = 3 (CSR) and small n wait for the whole copy
     e_np = O.gen_hypergraph(n, m, r, 5)
     ref = O.sync_peel(e_np, n, k)
     host = torch.from_numpy(e_np.view(np.int32))

@@ -3,7 +3,7 @@
 # bench lines for every config, the C5 launch list (ncu, one pass) and ncu --set full captures
 # of the C5 kernels.  Outputs under gpurun_out/r02/.
 set -u
-O=gpurun_out/r02
+O=${OUT:-gpurun_out/r02}
 mkdir -p $O
 P="python tools/profile_step.py --n 1000000000 --c 0.75 --r 3 --k 2 --seed 6 --warm 0"
 timeout 400 python bench.py > $O/bench_C5.log 2>&1

@@ -301,8 +301,8 @@ __global__ void __launch_bounds__(DB) dist_recv_kernel(DKArgs a, const uint32_t 
 static constexpr int DKU = 4;                  // entries per thread per chunk
 static constexpr int DKCH = DB * DKU;          // entries per chunk
 
-static size_t dist_stage_smem(int r, uint32_t nbins) {
-    return sizeof(ull) * (size_t)r * DKCH + (sizeof(ull) + 2 * sizeof(uint32_t)) * nbins;
+static size_t dist_stage_smem(int r, uint32_t nbins) {  // nbins + 8: room for the destinations
+    return sizeof(ull) * (size_t)r * DKCH + (sizeof(ull) + 2 * sizeof(uint32_t)) * (nbins + 8);
 }
 
 template <int R, bool RECV>
@@ -311,20 +311,21 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
     extern __shared__ unsigned char smem_raw[];
     constexpr int SE = R * DKCH;
     const uint32_t nbins = bv.nbins;
-    ull *sorted = (ull *)smem_raw;                // [SE] the chunk's owned decrements, bin-sorted
-    ull *gpos = sorted + SE;                      // [nbins]
-    uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
-    uint32_t *offs = hist + nbins;                // [nbins]
-    __shared__ DIdQ qs[8];
+    // the kill's sends are ranked and written with the owned decrements: destination d is
+    // "bin" nbins + d of the same counting sort (one scan, one global atomic per destination
+    // and chunk, coalesced runs into its send segment) -- round 2; it replaced P block queues
+    // (32 KB of static shared memory) and a per-destination push loop per entry
+    const uint32_t nbx = RECV ? nbins : nbins + (uint32_t)a.P;  // bins + destinations
+    ull *sorted = (ull *)smem_raw;                // [SE] the chunk's decrements and sends, bin-sorted
+    ull *gpos = sorted + SE;                      // [nbx]
+    uint32_t *hist = (uint32_t *)(gpos + nbx);    // [nbx]
+    uint32_t *offs = hist + nbx;                  // [nbx]
     __shared__ uint32_t total;
-    if (!RECV)
-        for (int d = 0; d < 8; d++) bq_init(qs[d]);
     const ull nE = RECV ? nrecv : a.nE;
     const ull lmask = (1ull << SHARD_BIN_SHIFT) - 1;
     ull kills = 0;
-    int slot = 0;
     for (uint64_t base = (uint64_t)blockIdx.x * DKCH; base < nE; base += (uint64_t)gridDim.x * DKCH) {
-        for (uint32_t b = threadIdx.x; b < nbins; b += DB) hist[b] = 0;
+        for (uint32_t b = threadIdx.x; b < nbx; b += DB) hist[b] = 0;
         uint2 ent[DKU];
         bool win[DKU];
         #pragma unroll
@@ -357,13 +358,6 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             }
             if (owner_fast(mn, a.lo, a.P) == a.p) kills++;
         }
-        if (!RECV) {
-            // one push per destination; d is warp-uniform (each coalesced group targets one queue)
-            #pragma unroll
-            for (int j = 0; j < DKU; j++)
-                for (int d = 0; d < a.P; d++)
-                    if (sendm[j] >> d & 1u) bq_push(qs[d], slot, ent[j].y, a.send + (uint64_t)d * a.nloc, &a.ctl->nsend[d]);
-        }
         __syncthreads();  // hist zeroed
         // owned decrements stay in registers with their rank in the bin (the histogram atomic's
         // return value) until the bin offsets are known (as round_kill_partition_kernel does)
@@ -374,13 +368,27 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             for (int r = 0; r < R; r++)
                 if (win[j] && u[j][r] >= a.v0 && u[j][r] < a.v1 && (RECV || u[j][r] != ent[j].x))
                     rk[j][r] = atomicAdd(&hist[(uint32_t)(u[j][r] - a.v0) >> SHARD_BIN_SHIFT], 1u);
+        uint32_t rs[DKU][R - 1];  // ranks of the entry's sends, in the order of its destination bits
+        if (!RECV) {
+            #pragma unroll
+            for (int j = 0; j < DKU; j++) {
+                uint32_t sm = sendm[j];
+                #pragma unroll
+                for (int t = 0; t < R - 1; t++)
+                    if (sm) {
+                        const uint32_t d = __ffs(sm) - 1;
+                        sm &= sm - 1;
+                        rs[j][t] = atomicAdd(&hist[nbins + d], 1u);
+                    }
+            }
+        }
         __syncthreads();
         if (threadIdx.x < 32) {
-            const uint32_t per = (nbins + 31) / 32;
+            const uint32_t per = (nbx + 31) / 32;
             uint32_t loc = 0;
             for (uint32_t q2 = 0; q2 < per; q2++) {
                 uint32_t b = threadIdx.x * per + q2;
-                loc += b < nbins ? hist[b] : 0;
+                loc += b < nbx ? hist[b] : 0;
             }
             uint32_t z = loc;
             #pragma unroll
@@ -391,13 +399,15 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
             uint32_t run = z - loc;
             for (uint32_t q2 = 0; q2 < per; q2++) {
                 uint32_t b = threadIdx.x * per + q2;
-                if (b < nbins) { offs[b] = run; run += hist[b]; }
+                if (b < nbx) { offs[b] = run; run += hist[b]; }
             }
             if (threadIdx.x == 31) total = z;
         }
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < nbins; b += DB)
-            if (hist[b]) gpos[b] = atomicAdd(bv.cursor + b, (ull)hist[b]);
+        for (uint32_t b = threadIdx.x; b < nbx; b += DB)
+            if (hist[b])
+                gpos[b] = b < nbins ? atomicAdd(bv.cursor + b, (ull)hist[b])
+                                    : (ull)(b - nbins) * a.nloc + atomicAdd(&a.ctl->nsend[b - nbins], (ull)hist[b]);
         #pragma unroll
         for (int j = 0; j < DKU; j++)
             #pragma unroll
@@ -406,16 +416,27 @@ __global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint3
                     const uint32_t lu = (uint32_t)(u[j][r] - a.v0);
                     sorted[offs[lu >> SHARD_BIN_SHIFT] + rk[j][r]] = ((ull)ent[j].y << 32) | lu;
                 }
+        if (!RECV) {
+            #pragma unroll
+            for (int j = 0; j < DKU; j++) {
+                uint32_t sm = sendm[j];
+                #pragma unroll
+                for (int t = 0; t < R - 1; t++)
+                    if (sm) {
+                        const uint32_t d = __ffs(sm) - 1;
+                        sm &= sm - 1;
+                        sorted[offs[nbins + d] + rs[j][t]] = ((ull)ent[j].y << 32) | ((nbins + d) << SHARD_BIN_SHIFT);
+                    }
+            }
+        }
         __syncthreads();
         const uint32_t tot = total;
         for (uint32_t i = threadIdx.x; i < tot; i += DB) {
             const ull v = sorted[i];
             const uint32_t b = (uint32_t)v >> SHARD_BIN_SHIFT;
-            bv.entries[bv.base[b] + gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ lmask);
+            if (RECV || b < nbins) bv.entries[bv.base[b] + gpos[b] + (i - offs[b])] = v & ~(0xFFFFFFFFull ^ lmask);
+            else a.send[gpos[b] + (i - offs[b])] = (uint32_t)(v >> 32);
         }
-        if (!RECV)
-            flush_sends(qs, slot, a.P, a.send, a.nloc, a.ctl->nsend);
-        slot ^= 1;
         __syncthreads();
     }
     block_add<DB>(&a.ctl->kills, kills);

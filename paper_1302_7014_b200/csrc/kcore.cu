@@ -246,7 +246,6 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
     uint32_t *hist = (uint32_t *)(gpos + nbins);  // [nbins]
     uint32_t *offs = hist + nbins;                // [nbins]
     uint32_t *fill = offs + nbins;                // [nbins]
-    uint8_t *okb = (uint8_t *)(fill + nbins);     // [CH]  edge valid
     __shared__ uint32_t total;
     const ull mask = (1ull << BIN_SHIFT) - 1;
     for (uint64_t c0 = e0 + (uint64_t)blockIdx.x * CH; c0 < m; c0 += (uint64_t)gridDim.x * CH) {  // edges [e0, m)
@@ -273,32 +272,37 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
             for (int i = threadIdx.x; i < nw; i += PART_BLOCK) words[i] = __ldcs(src + i);
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < ne; i += PART_BLOCK) {
-            bool ok = true;
-            #pragma unroll
-            for (int j = 0; j < R; j++) ok &= (uint64_t)words[i * R + j] < n;
-            #pragma unroll
-            for (int j = 0; j < R; j++)
-                #pragma unroll
-                for (int q = j + 1; q < R; q++) ok &= words[i * R + j] != words[i * R + q];
-            okb[i] = ok;
-            if (!ok) atomicOr(err, ERR_BADVERTEX);
-        }
-        __syncthreads();
-        // a shard keeps only its endpoints [v0, v1), binned by the local id u - v0
-        // the histogram atomic's return value is the entry's rank within its bin in this
-        // chunk: kept in registers for the scatter (one shared atomic per entry, not two)
-        constexpr int WPT = (CWP + PART_BLOCK - 1) / PART_BLOCK;  // words per thread
-        uint32_t rank[WPT];
+        // thread t takes edges t, t + 256, ...: validates each in registers, and ranks the
+        // shard's endpoints [v0, v1) (local ids u - v0) in their bins with the histogram
+        // atomic's return value; ids and ranks stay in registers for the scatter (round 2:
+        // one pass over the staged words instead of a validation pass, a rank pass that
+        // rewrote them and a scatter pass that re-read them)
+        constexpr int EPT = (CH + PART_BLOCK - 1) / PART_BLOCK;  // edges per thread
+        static_assert(EPT * R <= 32, "one keep bit per (edge, endpoint) of the thread");
+        uint32_t lid[EPT][R], rank[EPT][R];
+        uint32_t kept = 0;  // bit q R + j: lid[q][j] is kept (every u32 is a valid local id)
         #pragma unroll
-        for (int q = 0; q < WPT; q++) {
+        for (int q = 0; q < EPT; q++) {
             const int i = q * PART_BLOCK + threadIdx.x;
-            rank[q] = 0;
-            if (i < nw) {
-                const uint64_t w = words[i];
-                const bool mine = okb[i / R] && w >= v0 && w < v1;
-                words[i] = mine ? (uint32_t)(w - v0) : 0xFFFFFFFFu;  // local id, or "not kept"
-                if (mine) rank[q] = atomicAdd(&hist[(uint32_t)(w - v0) >> BIN_SHIFT], 1u);
+            if (i < ne) {
+                uint32_t w[R];
+                #pragma unroll
+                for (int j = 0; j < R; j++) w[j] = words[i * R + j];
+                bool ok = true;
+                #pragma unroll
+                for (int j = 0; j < R; j++) ok &= (uint64_t)w[j] < n;
+                #pragma unroll
+                for (int j = 0; j < R; j++)
+                    #pragma unroll
+                    for (int j2 = j + 1; j2 < R; j2++) ok &= w[j] != w[j2];
+                if (!ok) atomicOr(err, ERR_BADVERTEX);
+                #pragma unroll
+                for (int j = 0; j < R; j++)
+                    if (ok && (uint64_t)w[j] >= v0 && (uint64_t)w[j] < v1) {
+                        lid[q][j] = (uint32_t)(w[j] - v0);
+                        rank[q][j] = atomicAdd(&hist[lid[q][j] >> BIN_SHIFT], 1u);
+                        kept |= 1u << (q * R + j);
+                    }
             }
         }
         __syncthreads();
@@ -335,13 +339,11 @@ __global__ void __launch_bounds__(PART_BLOCK, PEEL_PART_MINB) bin_partition_kern
                 fill[b] = (uint32_t)(g >= c ? 0ull : min((ull)hist[b], c - g));
             }
         #pragma unroll
-        for (int q = 0; q < WPT; q++) {
-            const int i = q * PART_BLOCK + threadIdx.x;
-            if (i >= nw) continue;
-            const int ed = i / R;
-            const uint32_t u = words[i];
-            if (!okb[ed] || (u == 0xFFFFFFFFu && v1 - v0 <= 0xFFFFFFFFull)) continue;
-            sent[offs[u >> BIN_SHIFT] + rank[q]] = ((c0 + ed) << 32) | u;
+        for (int q = 0; q < EPT; q++) {
+            const uint64_t e = c0 + (uint64_t)(q * PART_BLOCK + threadIdx.x);
+            #pragma unroll
+            for (int j = 0; j < R; j++)
+                if ((kept >> (q * R + j)) & 1u) sent[offs[lid[q][j] >> BIN_SHIFT] + rank[q][j]] = (e << 32) | lid[q][j];
         }
         __syncthreads();
         const uint32_t tot = total;

@@ -298,7 +298,15 @@ __global__ void __launch_bounds__(DB) dist_recv_kernel(DKArgs a, const uint32_t 
 // read-modify-writes; shard_apply then applies them bin by bin with L2-resident atomics.
 // RECV = false: entries are the local frontier (v, e), remote owners are sent e;
 // RECV = true: entries are edge ids received from other shards.
-static constexpr int DKU = 4;                  // entries per thread per chunk
+// 3 entries per thread at 5 resident blocks per SM (48 registers): C5 over 8 virtual shards
+// 237.4 -> 215.6 ms against 4 at 4 (64 registers); 4 at 5: 222.9, 3 at 4: 221.5, 3 at 6: 227.9
+#ifndef PEEL_DKU
+#define PEEL_DKU 3
+#endif
+#ifndef PEEL_DKB_MINB
+#define PEEL_DKB_MINB 5
+#endif
+static constexpr int DKU = PEEL_DKU;           // entries per thread per chunk
 static constexpr int DKCH = DB * DKU;          // entries per chunk
 
 static size_t dist_stage_smem(int r, uint32_t nbins) {  // nbins + 8: room for the destinations
@@ -306,7 +314,7 @@ static size_t dist_stage_smem(int r, uint32_t nbins) {  // nbins + 8: room for t
 }
 
 template <int R, bool RECV>
-__global__ void __launch_bounds__(DB) dist_kill_bin_kernel(DKArgs a, const uint32_t *__restrict__ recv, ull nrecv,
+__global__ void __launch_bounds__(DB, PEEL_DKB_MINB) dist_kill_bin_kernel(DKArgs a, const uint32_t *__restrict__ recv, ull nrecv,
                                                             ShardBinsView bv) {
     extern __shared__ unsigned char smem_raw[];
     constexpr int SE = R * DKCH;

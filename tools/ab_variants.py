@@ -19,6 +19,7 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--build-only", action="store_true")
 ap.add_argument("--prebuilt", action="store_true", help="use variants/libpeel_<name>.so as built")
 ap.add_argument("--env", default="", help="extra NAME=VALUE,... for every run")
+ap.add_argument("--extra", default="", help="extra bench.py arguments, e.g. '--virtual-shards 8'")
 ap.add_argument("variants", nargs="+", help="name:DEF=V,DEF=V (name: alone = the default build)")
 a = ap.parse_args()
 from paper_1302_7014_b200 import build as B  # noqa: E402
@@ -39,7 +40,8 @@ for name, lib in libs.items():
         k, _, val = kv.partition("=")
         env[k] = val
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", a.config, "--steps", str(a.steps),
-                        "--warmup", str(a.warmup), "--no-e2e", "--no-cpu-baseline"], env=env, capture_output=True,
+                        "--warmup", str(a.warmup), "--no-e2e", "--no-cpu-baseline", *a.extra.split()], env=env,
+                       capture_output=True,
                        text=True, timeout=900)
     line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
     if not line:

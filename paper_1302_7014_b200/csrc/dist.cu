@@ -23,6 +23,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "common.cuh"
@@ -478,14 +479,56 @@ static unsigned dgrid(uint64_t work) {
 
 using namespace peel;
 
+// per-round bookkeeping of all local shards in one launch each (virtual shards: 8 shards' worth
+// of memsets, row copies, packs and 56 exchange copies per round were ~180 small operations,
+// whose fixed costs showed as ~17 ms of gaps in C5 over 8 virtual shards)
+struct ShardCtls {
+    DCtl *c[8];
+    int n;
+};
+__global__ void dist_reset_kernel(ShardCtls cs, int nxt) {
+    const int i = threadIdx.x;
+    if (i >= cs.n) return;
+    DCtl *c = cs.c[i];
+    c->nf[nxt] = 0;
+    c->ne[nxt] = 0;
+    c->kills = 0;
+    #pragma unroll
+    for (int d = 0; d < 8; d++) c->nsend[d] = 0;
+}
+// the count rows (nsend[8], fail) of the local shards, shard i at out[9 i]
+__global__ void dist_rows_kernel(ShardCtls cs, ull *out) {
+    const int i = threadIdx.x / 9, j = threadIdx.x % 9;
+    if (i >= cs.n) return;
+    out[threadIdx.x] = j < 8 ? cs.c[i]->nsend[j] : cs.c[i]->fail;
+}
+// virtual exchange: pair p copies cnt[p] ids from src[p] to dst[p] (blockIdx.y = pair)
+struct XPairs {
+    const uint32_t *src[56];
+    uint32_t *dst[56];
+    ull cnt[56];
+    int n;
+};
+__global__ void __launch_bounds__(256) dist_xchg_kernel(XPairs x) {
+    const int p = blockIdx.y;
+    if (p >= x.n) return;
+    const ull c = x.cnt[p];
+    const uint32_t *src = x.src[p];
+    uint32_t *dst = x.dst[p];
+    for (ull i = blockIdx.x * 256ull + threadIdx.x; i < c; i += (ull)gridDim.x * 256) dst[i] = __ldcs(src + i);
+}
+
 // the end-of-round words of a shard: [0..3] reduced over ranks (|F_{t+1}|, kills, bad-vertex
 // bits, failure), [4] local (frontier entries of round t+1, sizes the next kill grid)
-__global__ void dist_pack_kernel(const DCtl *ctl, int par, ull *out) {
-    out[0] = ctl->nf[par];
-    out[1] = ctl->kills;
-    out[2] = ctl->err;
-    out[3] = ctl->fail;
-    out[4] = ctl->ne[par];
+__global__ void dist_pack_kernel(ShardCtls cs, int par, ull *out) {
+    const int i = threadIdx.x;
+    if (i >= cs.n) return;
+    const DCtl *ctl = cs.c[i];
+    out[5 * i] = ctl->nf[par];
+    out[5 * i + 1] = ctl->kills;
+    out[5 * i + 2] = ctl->err;
+    out[5 * i + 3] = ctl->fail;
+    out[5 * i + 4] = ctl->ne[par];
 }
 
 static uint64_t max_shard(uint64_t n, int P) {
@@ -530,6 +573,9 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     // Error protocol (peel.h "Errors"): a rank's first local failure is kept in lst; from then
     // on it launches nothing but still takes part in every collective with its failure word
     // set, and every rank leaves at the next exchange.  Virtual shards have no peers: return.
+    ShardCtls scs;
+    scs.n = (int)sh.size();
+    for (int i = 0; i < 8; i++) scs.c[i] = i < scs.n ? sh[i].ctl : nullptr;
     peel_status lst = PEEL_OK;
     auto cu = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess && lst == PEEL_OK) {
@@ -541,6 +587,22 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     auto step = [&](peel_status st2) {
         if (st2 != PEEL_OK && lst == PEEL_OK) lst = st2;
         return lst == PEEL_OK;
+    };
+    // the binned kill / receive kernels' shared-memory limit, carve-out and resident blocks per
+    // SM, set and queried once per (kernel, shared-memory size) in a call, not every round
+    std::map<std::pair<bool, size_t>, int> kbc;
+    auto kill_blocks = [&](bool recv, size_t sm) -> int {
+        auto it = kbc.find({recv, sm});
+        if (it != kbc.end()) return it->second;
+        const void *kern = recv ? (const void *)dist_kill_bin_kernel<R, true> : (const void *)dist_kill_bin_kernel<R, false>;
+        int kb = 0;
+        cudaError_t e = raise_smem(kern, sm);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 72);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, kern, DB, sm);
+        if (!cu(e, "kill kernel attributes")) return 1;
+        kb = kb < 1 ? 1 : kb;
+        kbc[{recv, sm}] = kb;
+        return kb;
     };
     ull *dsum = (ull *)(ws + L.scratch);  // device staging for the collectives (8 + 8 P words)
     ull one = 1;
@@ -586,7 +648,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     std::vector<ull> ne(sh.size(), 0), pk(5 * sh.size());
     auto end_round = [&](int par, ull g[4]) -> peel_status {
         if (lst != PEEL_OK) mark_fail();
-        for (size_t i = 0; i < sh.size(); i++) dist_pack_kernel<<<1, 1, 0, s>>>(sh[i].ctl, par, dsum + 8 + 5 * i);
+        dist_pack_kernel<<<1, 32, 0, s>>>(scs, par, dsum + 8);
         if (!c->virt && !c->host) {  // NCCL: reduce the device words in place, one copy back
             cudaMemcpyAsync(dsum, dsum + 8, sizeof(ull) * 4, cudaMemcpyDeviceToDevice, s);
             ncclResult_t nr = ncclAllReduce(dsum, dsum, 4, ncclUint64, ncclSum, c->nccl, s);
@@ -627,11 +689,8 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             lst = PEEL_ECUDA;
         }
         // reset next-round counters and per-destination queues (ne[] came with the last sums)
-        for (auto &d : sh) {
-            cu(cudaMemsetAsync(&d.ctl->nf[nxt], 0, sizeof(ull), s), "memset nf");
-            cu(cudaMemsetAsync(&d.ctl->ne[nxt], 0, sizeof(ull), s), "memset ne");
-            cu(cudaMemsetAsync(&d.ctl->kills, 0, sizeof(ull) * 9, s), "memset kills");  // kills + nsend[8]
-        }
+        dist_reset_kernel<<<1, 32, 0, s>>>(scs, nxt);  // nf, ne of round t+1; kills, nsend[8]
+        cu(cudaGetLastError(), "reset");
         // kill: binned (decrements staged in the shard's bins) while the local frontier is large
         std::vector<char> binr(sh.size(), 0);
         for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
@@ -653,10 +712,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 a.Fc = d.F[nxt];
                 cu(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s), "memset cursor");
                 const size_t sm = dist_stage_smem(R, bv.nbins);
-                cu(raise_smem((const void *)dist_kill_bin_kernel<R, false>, sm), "attr");
-                cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 72), "attr");
-                int kb = 0;
-                cu(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, false>, DB, sm), "occupancy");
+                const int kb = kill_blocks(false, sm);
                 if (lst != PEEL_OK) break;
                 ProfScope ps("dist_kill_binned", s);
                 dist_kill_bin_kernel<R, false><<<num_sms() * (kb < 1 ? 1 : kb), DB, sm, s>>>(a, nullptr, 0, bv);
@@ -670,9 +726,9 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         // (virtual: the shards' rows; ranks: one allgather of the 9-word rows nsend[8], fail)
         if (lst != PEEL_OK) mark_fail();
         bool peer_failed = false;
-        if (c->virt) {
-            for (size_t i = 0; i < sh.size(); i++)
-                cu(cudaMemcpyAsync(&rows[(size_t)sh[i].q * 9], sh[i].ctl->nsend, sizeof(ull) * 9, cudaMemcpyDeviceToHost, s), "rows");
+        if (c->virt) {  // shard i is shard q = i: the rows in shard order, one copy
+            dist_rows_kernel<<<1, 9 * 8, 0, s>>>(scs, dsum + 8);
+            cu(cudaMemcpyAsync(rows.data(), dsum + 8, sizeof(ull) * 9 * sh.size(), cudaMemcpyDeviceToHost, s), "rows");
             cu(cudaStreamSynchronize(s), "sync");
             if (lst != PEEL_OK) return lst;
         } else {
@@ -719,18 +775,30 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         }
         // payload: shard dst receives, from each src != dst, cnt[src][dst] ids into recv at running offsets
         std::vector<ull> nrecv(sh.size(), 0);
-        if (c->virt) {
+        if (c->virt) {  // every (src, dst) copy in one launch
+            XPairs xp;
+            xp.n = 0;
+            ull mx = 0;
             for (int dst = 0; dst < P; dst++) {
                 ull off = 0;
                 for (int src = 0; src < P; src++) {
                     if (src == dst) continue;
-                    ull cntv = cnt_mat[(size_t)src * P + dst];
-                    if (cntv)
-                        cu(cudaMemcpyAsync(sh[dst].recv + off, sh[src].send + (uint64_t)dst * nl_max,
-                                           sizeof(uint32_t) * cntv, cudaMemcpyDeviceToDevice, s), "virtual exchange");
+                    const ull cntv = cnt_mat[(size_t)src * P + dst];
+                    if (cntv) {
+                        xp.src[xp.n] = sh[src].send + (uint64_t)dst * nl_max;
+                        xp.dst[xp.n] = sh[dst].recv + off;
+                        xp.cnt[xp.n] = cntv;
+                        xp.n++;
+                        mx = std::max(mx, cntv);
+                    }
                     off += cntv;
                 }
                 nrecv[dst] = off;
+            }
+            if (xp.n) {
+                const unsigned gx = (unsigned)std::min<ull>((mx + 255) / 256, (ull)num_sms() * 4);
+                dist_xchg_kernel<<<dim3(gx, (unsigned)xp.n), 256, 0, s>>>(xp);
+                cu(cudaGetLastError(), "virtual exchange");
             }
         } else {
             const int me = c->rank;
@@ -762,10 +830,7 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
                 if (nrecv[i]) {
                     const size_t sm = dist_stage_smem(R, bv.nbins);
-                    cu(raise_smem((const void *)dist_kill_bin_kernel<R, true>, sm), "attr");
-                    cu(cudaFuncSetAttribute(dist_kill_bin_kernel<R, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 72), "attr");
-                    int kb = 0;
-                    cu(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&kb, dist_kill_bin_kernel<R, true>, DB, sm), "occupancy");
+                    const int kb = kill_blocks(true, sm);
                     if (lst != PEEL_OK) break;
                     ProfScope ps("dist_recv_binned", s);
                     dist_kill_bin_kernel<R, true><<<num_sms() * (kb < 1 ? 1 : kb), DB, sm, s>>>(a, d.recv, nrecv[i], bv);

@@ -573,6 +573,8 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     // Error protocol (peel.h "Errors"): a rank's first local failure is kept in lst; from then
     // on it launches nothing but still takes part in every collective with its failure word
     // set, and every rank leaves at the next exchange.  Virtual shards have no peers: return.
+    const char *ese = getenv("PEEL_ESORT");  // 0: the binned kill takes the frontier unsorted (A/B)
+    const bool esort = !(ese && atoi(ese) == 0);
     ShardCtls scs;
     scs.n = (int)sh.size();
     for (int i = 0; i < 8; i++) scs.c[i] = i < scs.n ? sh[i].ctl : nullptr;
@@ -624,8 +626,9 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
         if (L.bins_bytes && d.v1 - d.v0 > 0) {
             char *b = ws + (c->virt ? (size_t)d.q * L.total : 0);
             // the exchange buffers (send, recv: adjacent) are free during the build
+            ShardF1 f1 = {d.F[1], &d.ctl->ne[1], &d.ctl->nf[1], k};  // F_1 from the build's scan
             if (!step(shard_build(R, edges, n, m, d.v0, d.v1, d.state, &d.ctl->err, b + L.bins, s, &direct, b + L.send,
-                                  L.bins - L.send)))
+                                  L.bins - L.send, &f1)))
                 break;
         }
         d.binned = !direct;  // bins usable by the binned rounds (no overflow)
@@ -636,8 +639,10 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 dist_build_kernel<R><<<dgrid(m), DB, 0, s>>>(edges, n, m, d.v0, d.v1, d.state, d.ctl);
             }
         }
-        ProfScope ps("dist_scan", s);
-        dist_scan_kernel<<<dgrid(d.v1 - d.v0), DB, 0, s>>>(d.state, d.v0, d.v1 - d.v0, k, d.F[1], d.ctl);
+        if (direct) {  // a binned build scanned for F_1 itself
+            ProfScope ps("dist_scan", s);
+            dist_scan_kernel<<<dgrid(d.v1 - d.v0), DB, 0, s>>>(d.state, d.v0, d.v1 - d.v0, k, d.F[1], d.ctl);
+        }
     }
     cu(cudaGetLastError(), "build launch");
     if (lst != PEEL_OK && c->virt) return lst;
@@ -708,8 +713,10 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
                 // sort the local frontier by edge bin into the next-round buffer (free until
                 // shard_apply writes F_{t+1} there)
-                if (!step(shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s))) break;
-                a.Fc = d.F[nxt];
+                if (esort) {
+                    if (!step(shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s))) break;
+                    a.Fc = d.F[nxt];
+                }
                 cu(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s), "memset cursor");
                 const size_t sm = dist_stage_smem(R, bv.nbins);
                 const int kb = kill_blocks(false, sm);

@@ -2387,17 +2387,87 @@ static SFGeom sf_geom(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc, int per
     return g;
 }
 
+// the shard's accumulation and F_1 in one cooperative pass (round 2), as cbuild_kernel does for
+// one GPU: per bin, zero its states in L2, grid barrier, the bin's entries as REDs (8 loads in
+// flight per thread), grid barrier, then scan it -- still in L2 -- for F_1 (count < k; entries
+// (v0 + i, id sum) for count 1) while the next bin is zeroed.  Replaces the 8 nloc-byte memset,
+// bin_red_kernel and dist.cu's scan, which re-read the state from DRAM.
+static constexpr int SA_SU = 4;  // states per thread per scan step
+__global__ void __launch_bounds__(256) shard_accum_kernel(const ull *__restrict__ entries, const ull *__restrict__ base,
+                                                          const ull *__restrict__ cursor, uint32_t nbins, uint64_t nloc,
+                                                          uint64_t v0, uint32_t k, ull *state, uint2 *F, ull *ne,
+                                                          ull *nf) {
+    cg::grid_group grid = cg::this_grid();
+    typedef BlockQueueT<uint2, 4 * 256, 256> Q;
+    __shared__ Q q;
+    bq_init(q);
+    __syncthreads();
+    const uint64_t tid = blockIdx.x * 256ull + threadIdx.x, nthr = (uint64_t)gridDim.x * 256;
+    const ull mask = (1ull << BIN_SHIFT) - 1;
+    ull removed = 0;
+    int slot = 0;
+    for (uint32_t b = 0; b <= nbins; b++) {
+        if (b > 0) {  // scan bin b - 1 (in L2)
+            const uint64_t lo = (uint64_t)(b - 1) << BIN_SHIFT, hi = min(nloc, lo + ((uint64_t)1 << BIN_SHIFT));
+            for (uint64_t s0 = lo + (uint64_t)blockIdx.x * 256 * SA_SU; s0 < hi; s0 += (uint64_t)gridDim.x * 256 * SA_SU) {
+                ull w[SA_SU];
+                #pragma unroll
+                for (int j = 0; j < SA_SU; j++) {
+                    const uint64_t i = s0 + (uint64_t)j * 256 + threadIdx.x;
+                    w[j] = i < hi ? __ldcg(state + i) : ~0ull;
+                }
+                #pragma unroll
+                for (int j = 0; j < SA_SU; j++) {
+                    const uint64_t i = s0 + (uint64_t)j * 256 + threadIdx.x;
+                    if ((uint32_t)w[j] < k) {
+                        removed++;
+                        if ((uint32_t)w[j] == 1u) bq_push(q, slot, make_uint2((uint32_t)(v0 + i), (uint32_t)(w[j] >> 32)), F, ne);
+                    }
+                }
+                bq_flush(q, slot, F, ne);
+                slot ^= 1;
+            }
+        }
+        if (b < nbins) {  // zero bin b (2^22-aligned: 16-byte stores)
+            const uint64_t lo = (uint64_t)b << BIN_SHIFT, sz = min(nloc - lo, (uint64_t)1 << BIN_SHIFT);
+            ulonglong2 *z = reinterpret_cast<ulonglong2 *>(state + lo);
+            for (uint64_t i = tid; i < sz / 2; i += nthr) z[i] = make_ulonglong2(0ull, 0ull);
+            if ((sz & 1) && tid == 0) state[lo + sz - 1] = 0ull;
+        }
+        grid.sync();
+        if (b < nbins) {
+            ull *st = state + ((uint64_t)b << BIN_SHIFT);
+            const ull *ent = entries + base[b];
+            const ull cnt = cursor[b];
+            constexpr int RU = 8;
+            for (ull i0 = tid; i0 < cnt; i0 += RU * nthr) {
+                ull x[RU];
+                #pragma unroll
+                for (int u = 0; u < RU; u++) {
+                    const ull i = i0 + (ull)u * nthr;
+                    x[u] = i < cnt ? __ldcs(ent + i) : 0ull;
+                }
+                #pragma unroll
+                for (int u = 0; u < RU; u++)
+                    if (i0 + (ull)u * nthr < cnt) atomicAdd(st + (x[u] & mask), (x[u] & ~0xFFFFFFFFull) + 1ull);
+            }
+        }
+        grid.sync();
+    }
+    block_add<256>(nf, removed);
+}
+
 template <int R>
 static peel_status shard_build_r(const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1, ull *state,
                                  uint32_t *err, char *scratch, cudaStream_t s, bool *overflow, void *tmp,
-                                 size_t tmp_bytes) {
+                                 size_t tmp_bytes, const ShardF1 *f1) {
     const uint64_t nloc = v1 - v0;
     const ShardBins B = shard_bins(n, m, R, nloc);
     ull *cursor = (ull *)(scratch + B.cursor), *base = (ull *)(scratch + B.base), *cap = (ull *)(scratch + B.cap);
     uint32_t *flag = (uint32_t *)(scratch + B.flag);
     ull *entries = (ull *)(scratch + B.entries);
     *overflow = false;
-    PEEL_CUDA(cudaMemsetAsync(state, 0, sizeof(ull) * nloc, s));
+    if (!f1) PEEL_CUDA(cudaMemsetAsync(state, 0, sizeof(ull) * nloc, s));  // f1: zeroed per bin, in L2
     PEEL_CUDA(cudaMemsetAsync(flag, 0, sizeof(uint32_t), s));
     {
         ProfScope ps("bin_init", s);
@@ -2459,6 +2529,21 @@ binned:
         *overflow = true;
         return PEEL_OK;
     }
+    if (f1) {
+        int per_sm = 0;
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shard_accum_kernel, 256, 0));
+        uint32_t nb = (uint32_t)B.nbins;
+        uint32_t kk = f1->k;
+        uint64_t nl = nloc, vv0 = v0;
+        const ull *en = entries, *bs = base, *cu2 = cursor;
+        ull *st = state, *pne = f1->ne, *pnf = f1->nf;
+        uint2 *FF = (uint2 *)f1->F;
+        void *args[] = {&en, &bs, &cu2, &nb, &nl, &vv0, &kk, &st, &FF, &pne, &pnf};
+        ProfScope ps("shard_accum", s);
+        PEEL_CUDA(cudaLaunchCooperativeKernel((void *)shard_accum_kernel, num_sms() * (per_sm < 1 ? 1 : per_sm), 256, args,
+                                              0, s));
+        return PEEL_OK;
+    }
     uint64_t maxcap = 0;
     for (uint64_t b = 0; b < B.nbins; b++) maxcap = std::max<uint64_t>(maxcap, bin_capacity(n, nloc, m, R, b));
     const dim3 grid((unsigned)((maxcap + 256 * CSRB_PER - 1) / (256 * CSRB_PER)), (unsigned)B.nbins);
@@ -2506,12 +2591,24 @@ peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint6
 // dist.cu's kill/receive kernels) are applied by round_apply_kernel; crossings append
 // (v0 + local id, remaining edge) to Fn.  |F_{t+1}| and Fn's length are copied to out_nf /
 // out_ne (device words).
+// the apply's counters zeroed before it, its |F_{t+1}| and entry count copied out after it: one
+// tiny launch each instead of two memsets and two copies per shard and round
+__global__ void shard_apply_prep_kernel(Ctl *ctl, ull *work) {
+    const int i = threadIdx.x;
+    if (i < (int)(sizeof(Ctl) / sizeof(ull))) reinterpret_cast<ull *>(ctl)[i] = 0ull;
+    if (i == 0) *work = 0ull;
+}
+__global__ void shard_apply_post_kernel(const Ctl *ctl, uint32_t t, ull *out_nf, ull *out_ne) {
+    *out_nf = ctl->nf[t % 3];
+    *out_ne = ctl->ne[t % 3];
+}
+
 peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long long *state, void *Fn,
                         const ShardBinsView &v, uint32_t t, unsigned long long *out_nf, unsigned long long *out_ne,
                         cudaStream_t s) {
+    static_assert(sizeof(Ctl) % sizeof(ull) == 0 && sizeof(Ctl) / sizeof(ull) <= 32, "Ctl zeroed by one warp");
     Ctl *ctl = (Ctl *)v.ctl;
-    PEEL_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), s));
-    PEEL_CUDA(cudaMemsetAsync(v.work, 0, sizeof(ull), s));
+    shard_apply_prep_kernel<<<1, 32, 0, s>>>(ctl, v.work);
     PeelArgs a;
     memset(&a, 0, sizeof a);
     a.n = nloc;
@@ -2529,30 +2626,34 @@ peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long lo
     br.work = v.work;
     br.t = t;
     const size_t dsmem = sizeof(uint32_t) * (v.nbins + 1);
-    int db = 0;
-    PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
-    db = db < 1 ? 1 : db;
+    static thread_local std::map<std::pair<int, size_t>, int> dbc;  // (device, shared bytes) -> blocks per SM
+    int dev = 0;
+    PEEL_CUDA(cudaGetDevice(&dev));
+    int &db = dbc[{dev, dsmem}];
+    if (!db) {
+        PEEL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&db, round_apply_kernel, PEEL_BLOCK, dsmem));
+        db = db < 1 ? 1 : db;
+    }
     {
         ProfScope ps("round_apply", s);
         round_apply_kernel<<<num_sms() * db, PEEL_BLOCK, dsmem, s>>>(a, br);
     }
+    shard_apply_post_kernel<<<1, 1, 0, s>>>(ctl, t, out_nf, out_ne);
     PEEL_CUDA(cudaGetLastError());
-    PEEL_CUDA(cudaMemcpyAsync(out_nf, &ctl->nf[t % 3], sizeof(ull), cudaMemcpyDeviceToDevice, s));
-    PEEL_CUDA(cudaMemcpyAsync(out_ne, &ctl->ne[t % 3], sizeof(ull), cudaMemcpyDeviceToDevice, s));
     return PEEL_OK;
 }
 
 peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
                         unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow,
-                        void *tmp, size_t tmp_bytes) {
+                        void *tmp, size_t tmp_bytes, const ShardF1 *f1) {
     switch (r) {
-        case 2: return shard_build_r<2>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
-        case 3: return shard_build_r<3>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
-        case 4: return shard_build_r<4>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
-        case 5: return shard_build_r<5>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
-        case 6: return shard_build_r<6>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
-        case 7: return shard_build_r<7>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
-        case 8: return shard_build_r<8>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes);
+        case 2: return shard_build_r<2>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
+        case 3: return shard_build_r<3>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
+        case 4: return shard_build_r<4>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
+        case 5: return shard_build_r<5>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
+        case 6: return shard_build_r<6>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
+        case 7: return shard_build_r<7>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
+        case 8: return shard_build_r<8>(edges, n, m, v0, v1, state, err, scratch, s, overflow, tmp, tmp_bytes, f1);
     }
     return PEEL_EINVAL;
 }

@@ -19,9 +19,17 @@ size_t shard_build_bytes(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc);
 // tmp / tmp_bytes: optional device scratch that is free during the build (dist.cu: the
 // exchange buffers).  A narrow shard (v1 - v0 <= n / 4) with enough of it takes the filter
 // path: one streaming pass keeps the shard's endpoints, a second bins them.
+// f1 (optional): the build also scans the shard for F_1 while each bin is in L2 -- count < k
+// adds to *nf, count-1 vertices append (v0 + i, id sum) to F at *ne (device counters, zeroed by
+// the caller) -- and the caller skips its own scan.  Not done when *overflow comes back true.
+struct ShardF1 {
+    void *F;                   // uint2 [v1 - v0]
+    unsigned long long *ne, *nf;
+    uint32_t k;
+};
 peel_status shard_build(uint32_t r, const uint32_t *edges, uint64_t n, uint64_t m, uint64_t v0, uint64_t v1,
                         unsigned long long *state, uint32_t *err, char *scratch, cudaStream_t s, bool *overflow,
-                        void *tmp = nullptr, size_t tmp_bytes = 0);
+                        void *tmp = nullptr, size_t tmp_bytes = 0, const ShardF1 *f1 = nullptr);
 
 // the shard's bins as the binned rounds use them: per-bin cursors and bases into `entries`
 // (capacities from the build: a round's decrements of a bin are a subset of the build's),

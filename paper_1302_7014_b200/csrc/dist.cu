@@ -484,17 +484,25 @@ using namespace peel;
 // whose fixed costs showed as ~17 ms of gaps in C5 over 8 virtual shards)
 struct ShardCtls {
     DCtl *c[8];
+    ull *z0[8], *z1[8];     // binned shards: the bins' cursors and the edge-sort counters,
+    uint32_t n0[8], n1[8];  // zeroed with the round's counters when the shard runs binned
     int n;
 };
-__global__ void dist_reset_kernel(ShardCtls cs, int nxt) {
-    const int i = threadIdx.x;
+__global__ void dist_reset_kernel(ShardCtls cs, int nxt, uint32_t binned) {
+    const int i = blockIdx.x;
     if (i >= cs.n) return;
-    DCtl *c = cs.c[i];
-    c->nf[nxt] = 0;
-    c->ne[nxt] = 0;
-    c->kills = 0;
-    #pragma unroll
-    for (int d = 0; d < 8; d++) c->nsend[d] = 0;
+    if (threadIdx.x == 0) {
+        DCtl *c = cs.c[i];
+        c->nf[nxt] = 0;
+        c->ne[nxt] = 0;
+        c->kills = 0;
+        #pragma unroll
+        for (int d = 0; d < 8; d++) c->nsend[d] = 0;
+    }
+    if ((binned >> i) & 1u) {
+        for (uint32_t w = threadIdx.x; w < cs.n0[i]; w += blockDim.x) cs.z0[i][w] = 0ull;
+        for (uint32_t w = threadIdx.x; w < cs.n1[i]; w += blockDim.x) cs.z1[i][w] = 0ull;
+    }
 }
 // the count rows (nsend[8], fail) of the local shards, shard i at out[9 i]
 __global__ void dist_rows_kernel(ShardCtls cs, ull *out) {
@@ -577,7 +585,18 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     const bool esort = !(ese && atoi(ese) == 0);
     ShardCtls scs;
     scs.n = (int)sh.size();
-    for (int i = 0; i < 8; i++) scs.c[i] = i < scs.n ? sh[i].ctl : nullptr;
+    for (int i = 0; i < 8; i++) {
+        scs.c[i] = i < scs.n ? sh[i].ctl : nullptr;
+        scs.z0[i] = scs.z1[i] = nullptr;
+        scs.n0[i] = scs.n1[i] = 0;
+        if (i < scs.n && L.bins_bytes && sh[i].v1 > sh[i].v0) {
+            const ShardBinsView bv = shard_bins_view(n, m, R, sh[i].v1 - sh[i].v0, sh[i].bins);
+            scs.z0[i] = bv.cursor;
+            scs.n0[i] = bv.nbins;
+            scs.z1[i] = bv.esort;
+            scs.n1[i] = bv.esort_words;
+        }
+    }
     peel_status lst = PEEL_OK;
     auto cu = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess && lst == PEEL_OK) {
@@ -693,11 +712,18 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             set_cuda_error(cudaErrorUnknown, "PEEL_FAULT injected failure");
             lst = PEEL_ECUDA;
         }
-        // reset next-round counters and per-destination queues (ne[] came with the last sums)
-        dist_reset_kernel<<<1, 32, 0, s>>>(scs, nxt);  // nf, ne of round t+1; kills, nsend[8]
-        cu(cudaGetLastError(), "reset");
         // kill: binned (decrements staged in the shard's bins) while the local frontier is large
         std::vector<char> binr(sh.size(), 0);
+        uint32_t binmask = 0;
+        for (size_t i = 0; i < sh.size(); i++) {
+            const DShard &d = sh[i];
+            binr[i] = d.binned && (double)ne[i] >= dist_bin_frac(d.v1 - d.v0) * (double)(d.v1 - d.v0);
+            binmask |= (uint32_t)binr[i] << i;
+        }
+        // reset next-round counters and per-destination queues (ne[] came with the last sums),
+        // and the binned shards' bin cursors and edge-sort counters
+        dist_reset_kernel<<<(unsigned)sh.size(), 256, 0, s>>>(scs, nxt, binmask);
+        cu(cudaGetLastError(), "reset");
         for (size_t i = 0; i < sh.size() && lst == PEEL_OK; i++) {
             DShard &d = sh[i];
             DKArgs a;
@@ -708,16 +734,14 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
             a.state = d.state; a.alive = d.alive;
             a.Fc = d.F[cur]; a.nE = ne[i]; a.Fn = d.F[nxt];
             a.send = d.send; a.ctl = d.ctl; a.par = nxt;
-            binr[i] = d.binned && (double)a.nE >= dist_bin_frac(d.v1 - d.v0) * (double)(d.v1 - d.v0);
             if (binr[i]) {
                 const ShardBinsView bv = shard_bins_view(n, m, R, d.v1 - d.v0, d.bins);
                 // sort the local frontier by edge bin into the next-round buffer (free until
                 // shard_apply writes F_{t+1} there)
                 if (esort) {
-                    if (!step(shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s))) break;
+                    if (!step(shard_edge_sort(d.F[cur], &d.ctl->ne[cur], a.nE, m, d.F[nxt], bv, s, true))) break;
                     a.Fc = d.F[nxt];
                 }
-                cu(cudaMemsetAsync(bv.cursor, 0, sizeof(ull) * bv.nbins, s), "memset cursor");
                 const size_t sm = dist_stage_smem(R, bv.nbins);
                 const int kb = kill_blocks(false, sm);
                 if (lst != PEEL_OK) break;

@@ -2565,19 +2565,20 @@ ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc,
     v.work = (ull *)(scratch + B.flag + 8);  // after the overflow flag, in the same 256-byte slot
     v.ctl = scratch + B.ctl;
     v.esort = (ull *)(scratch + B.esort);
+    v.esort_words = (uint32_t)(2 * (((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT) + 1));
     return v;
 }
 
 // sort the shard's frontier entries (v, e) by edge bin into dst (see esort_scatter_kernel):
 // the shard's kill phase then reads alive bits and rows per edge bin, from L2
 peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint64_t nE_host, uint64_t m, void *dst,
-                            const ShardBinsView &v, cudaStream_t s) {
+                            const ShardBinsView &v, cudaStream_t s, bool zeroed) {
     if (!nE_host || !m) return PEEL_OK;
     const uint32_t enb = (uint32_t)((m + (1ull << EB_SHIFT) - 1) >> EB_SHIFT);
     ull *hist = v.esort, *cur = v.esort + enb + 1;
     const size_t essmem = esort_scatter_smem(enb);
     PEEL_CUDA(raise_smem((const void *)esort_scatter_kernel, essmem));
-    PEEL_CUDA(cudaMemsetAsync(v.esort, 0, sizeof(ull) * 2 * (enb + 1), s));
+    if (!zeroed) PEEL_CUDA(cudaMemsetAsync(v.esort, 0, sizeof(ull) * 2 * (enb + 1), s));
     ProfScope ps("frontier_edge_sort", s);
     esort_hist_kernel<<<grid_for(nE_host, 8), 256, sizeof(uint32_t) * enb, s>>>((const uint2 *)src, pN, enb, hist);
     const uint64_t chunks = (nE_host + ES_CH - 1) / ES_CH;

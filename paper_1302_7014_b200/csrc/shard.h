@@ -42,6 +42,7 @@ struct ShardBinsView {
     unsigned long long *work;
     char *ctl;
     unsigned long long *esort;  // edge-sort histogram and cursors
+    uint32_t esort_words;       // their count (2 (edge bins + 1))
 };
 ShardBinsView shard_bins_view(uint64_t n, uint64_t m, uint32_t r, uint64_t nloc, char *scratch);
 
@@ -52,8 +53,9 @@ peel_status shard_apply(uint64_t nloc, uint64_t v0, uint32_t k, unsigned long lo
 
 // the shard's frontier entries (v, e) [nE_host of them; *pN on the device] sorted by edge bin
 // into dst (same capacity), as the single-GPU binned rounds do before their kill phase
+// (zeroed: the caller has zeroed v.esort's 2 (enb + 1) counters on the stream already)
 peel_status shard_edge_sort(const void *src, const unsigned long long *pN, uint64_t nE_host, uint64_t m, void *dst,
-                            const ShardBinsView &v, cudaStream_t s);
+                            const ShardBinsView &v, cudaStream_t s, bool zeroed = false);
 
 // BIN_SHIFT of kcore.cu (vertex bins of 2^22 local ids)
 constexpr int SHARD_BIN_SHIFT = 22;

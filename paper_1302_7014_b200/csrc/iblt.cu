@@ -119,6 +119,7 @@ struct IPeelArgs {
     bool subt;          // subtable hashing
     uint32_t blog;      // blocked hashing: log2 block size, 0 = off
     bool insert_only;   // every count is the true number of keys in its cell (no delete/subtract)
+    ull ninserted;      // insert-only: keys inserted since the build (complete iff all recovered)
 };
 
 
@@ -300,6 +301,13 @@ __global__ void __launch_bounds__(IB_BLOCK, 5) iblt_peel_kernel(IPeelArgs a) {
         if (t <= ISTAT_CAP) a.rtime[t - 1] = globaltimer();
     }
     // ---- complete iff every cell is zero ----
+    // An insert-only table is the multiset sum of its N inserted keys, and recovery removed
+    // exactly the recovered ones: every cell is zero iff all N were recovered -- no scan of the
+    // C cells (C2: 160 MB)
+    if (!SIGNED && a.insert_only) {
+        if (tid == 0 && ld_cg_u64(&ctl->nrec) != a.ninserted) ctl->nonzero = 1u;
+        return;
+    }
     uint32_t nz = 0;
     for (ull c = tid; c < a.C; c += nthr) {
         Cell v = ld_cell_cg(a.cells + c);
@@ -445,6 +453,7 @@ struct peel_iblt {
     bool subt;  // IBLT_FLAG_SUBTABLES
     uint32_t blog;  // IBLT_FLAG_BLOCKED: log2 cells per block (0: plain hashing)
     mutable bool insert_only;  // no delete, no subtract, no raw cell access since the build
+    ull ninserted;             // keys inserted since the build
     ull seed, seed_h, seed_c;
     char *mem;
     ILayout L;
@@ -483,6 +492,7 @@ extern "C" peel_status iblt_build_ex(uint64_t cells, uint32_t r, uint64_t seed, 
     t->subt = (flags & IBLT_FLAG_SUBTABLES) != 0;
     t->blog = blog;
     t->insert_only = true;
+    t->ninserted = 0;
     t->seed = seed;
     const ull G = 0x9E3779B97F4A7C15ull;
     t->seed_h = host_mix64((seed ^ 0x6A09E667F3BCC909ull) + G);
@@ -504,6 +514,7 @@ static peel_status iblt_update(peel_iblt *t, const uint64_t *keys, uint64_t nkey
     if (nkeys == 0) return PEEL_OK;
     if (!keys) return PEEL_EINVAL;
     if (delta != 1u) t->insert_only = false;
+    else t->ninserted += nkeys;
     cudaStream_t s = (cudaStream_t)stream;
     prof_begin_call();
     Cell *cells = (Cell *)(t->mem + t->L.cells);
@@ -588,6 +599,7 @@ static peel_status iblt_peel_impl(peel_iblt *t, uint64_t *out_keys, int8_t *out_
     a.subt = t->subt;
     a.blog = t->blog;
     a.insert_only = t->insert_only;
+    a.ninserted = t->ninserted;
     peel_status st = PEEL_EINVAL;
     switch (t->r) {
         case 2: st = run_iblt_peel<2>(t, a, sgn, s); break;

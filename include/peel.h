@@ -318,7 +318,10 @@ peel_status iblt_delete(peel_iblt *t, const uint64_t *keys, uint64_t nkeys, void
  *      nrecovered host u64 (may exceed cap_keys: then PEEL_ETRUNC and only
  *      cap_keys were stored); rounds host u32; per_round host u64 [cap]
  *      (nullable) keys recovered in round t; complete host int (nullable):
- *      1 iff every cell is zero afterwards (success iff the 2-core is empty).
+ *      1 iff every cell is zero afterwards (success iff the 2-core is empty) --
+ *      for an insert-only table (no delete, subtract or raw cell access since
+ *      the build) decided as "every inserted key was recovered", which is the
+ *      same condition, without scanning the cells.
  * Blocking.
  */
 peel_status iblt_peel(peel_iblt *t, uint64_t *out_keys, uint64_t cap_keys, uint64_t *nrecovered,

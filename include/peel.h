@@ -220,7 +220,11 @@ peel_status peel_sweep(uint64_t n, uint32_t r, uint32_t k, const uint64_t *m, co
  * Errors (all partitioned calls): a rank that fails locally keeps taking part in
  *   the collectives with an error word set; every rank then leaves at the same
  *   collective -- the failing rank with its status, the others with PEEL_EPEER --
- *   so no rank is left blocked in a collective.
+ *   so no rank is left blocked in a collective.  A rank that dies or disappears
+ *   cannot do that: NCCL communicators wait on their streams with a watchdog
+ *   (asynchronous NCCL errors, or PEEL_NCCL_TIMEOUT_S seconds, default 600), which
+ *   aborts the communicator and returns PEEL_ENCCL; every later call on an aborted
+ *   communicator returns PEEL_ENCCL (destroy it and create a new one).
  * peel_kcore_dist: edges dev u32 [m][r] (replicated); core_mask dev u8: the
  *   rank's slice [v1 - v0] (NCCL) or all n (virtual); rounds/survivors/killed
  *   host, global (identical on every rank); workspace dev,

@@ -7,6 +7,9 @@
 
 #include <vector>
 
+#include <chrono>
+#include <thread>
+
 #include "comm.h"
 #include "common.cuh"
 
@@ -31,15 +34,61 @@ static peel_status pin(peel_comm *c, size_t bytes) {
     return PEEL_OK;
 }
 
+// Stream sync after NCCL work, with a watchdog: polls the stream and ncclCommGetAsyncError,
+// and aborts the communicator (every later call on it fails with PEEL_ENCCL) on an
+// asynchronous NCCL error or after PEEL_NCCL_TIMEOUT_S seconds (default 600) -- a peer that
+// died or left mid-protocol cannot hang this rank forever.  Other communicators: a plain sync.
+static double nccl_timeout_s() {
+    const char *e = getenv("PEEL_NCCL_TIMEOUT_S");
+    const double t = e ? atof(e) : 600.0;
+    return t > 0 ? t : 600.0;
+}
+
+peel_status comm_sync(peel_comm *c, cudaStream_t s) {
+    if (c->virt || c->host) {
+        PEEL_CUDA(cudaStreamSynchronize(s));
+        return PEEL_OK;
+    }
+    if (!c->nccl) {
+        set_cuda_error(cudaErrorUnknown, "NCCL communicator aborted");
+        return PEEL_ENCCL;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const double limit = nccl_timeout_s();
+    for (uint32_t it = 0;; it++) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return PEEL_OK;
+        if (q != cudaErrorNotReady) {
+            set_cuda_error(q, "stream sync");
+            return PEEL_ECUDA;
+        }
+        ncclResult_t ar = ncclSuccess;
+        const ncclResult_t gr = ncclCommGetAsyncError(c->nccl, &ar);
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (gr != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress) || el > limit) {
+            set_cuda_error(cudaErrorUnknown, el > limit ? "NCCL watchdog: timeout, communicator aborted"
+                                                        : "NCCL asynchronous error, communicator aborted");
+            ncclCommAbort(c->nccl);
+            c->nccl = nullptr;
+            return PEEL_ENCCL;
+        }
+        if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
 peel_status comm_allreduce_sum(peel_comm *c, ull *vals, int count, ull *dstage, cudaStream_t s) {
     if (c->host) {
         if (c->h_allreduce(c->h_ctx, (uint64_t *)vals, (uint64_t)count)) return host_fail("allreduce");
         return PEEL_OK;
     }
     PEEL_CUDA(cudaMemcpyAsync(dstage, vals, sizeof(ull) * count, cudaMemcpyHostToDevice, s));
+    if (!c->nccl) return comm_sync(c, s);
     PEEL_NCCL(ncclAllReduce(dstage, dstage, count, ncclUint64, ncclSum, c->nccl, s));
-    PEEL_CUDA(cudaMemcpyAsync(vals, dstage, sizeof(ull) * count, cudaMemcpyDeviceToHost, s));
-    PEEL_CUDA(cudaStreamSynchronize(s));
+    // wait with the watchdog BEFORE the copy back: a copy to pageable memory blocks inside
+    // the runtime until the stream drains, where no watchdog could see a dead peer
+    const peel_status ws = comm_sync(c, s);
+    if (ws != PEEL_OK) return ws;
+    PEEL_CUDA(cudaMemcpy(vals, dstage, sizeof(ull) * count, cudaMemcpyDeviceToHost));
     return PEEL_OK;
 }
 
@@ -50,9 +99,11 @@ peel_status comm_allgather_u64(peel_comm *c, const ull *send, ull *recv, int cou
     }
     ull *mine = dstage + (size_t)c->rank * count;
     PEEL_CUDA(cudaMemcpyAsync(mine, send, sizeof(ull) * count, cudaMemcpyHostToDevice, s));
+    if (!c->nccl) return comm_sync(c, s);
     PEEL_NCCL(ncclAllGather(mine, dstage, count, ncclUint64, c->nccl, s));
-    PEEL_CUDA(cudaMemcpyAsync(recv, dstage, sizeof(ull) * count * c->P, cudaMemcpyDeviceToHost, s));
-    PEEL_CUDA(cudaStreamSynchronize(s));
+    const peel_status ws = comm_sync(c, s);  // before the (blocking) copy back, as above
+    if (ws != PEEL_OK) return ws;
+    PEEL_CUDA(cudaMemcpy(recv, dstage, sizeof(ull) * count * c->P, cudaMemcpyDeviceToHost));
     return PEEL_OK;
 }
 
@@ -67,6 +118,7 @@ peel_status comm_allgather_dev(peel_comm *c, const void *send_dev, void *recv_de
         PEEL_CUDA(cudaMemcpyAsync(recv_dev, c->pin, bytes * c->P, cudaMemcpyHostToDevice, s));
         return PEEL_OK;
     }
+    if (!c->nccl) return comm_sync(c, s);
     PEEL_NCCL(ncclAllGather(send_dev, recv_dev, bytes, ncclUint8, c->nccl, s));
     return PEEL_OK;
 }
@@ -97,6 +149,7 @@ peel_status comm_alltoallv(peel_comm *c, const char *const *send, const ull *sby
         PEEL_CUDA(cudaStreamSynchronize(s));
         return PEEL_OK;
     }
+    if (!c->nccl) return comm_sync(c, s);
     PEEL_NCCL(ncclGroupStart());
     ull off = 0;
     for (int q = 0; q < P; q++) {

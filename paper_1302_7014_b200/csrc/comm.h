@@ -52,6 +52,9 @@ peel_status comm_alltoallv(peel_comm *c, const char *const *send, const ull *sby
 // rejects its arguments never leaves the others blocked in the first collective.  Virtual
 // communicators return `local` unchanged.
 peel_status comm_agree(peel_comm *c, peel_status local, cudaStream_t s);
+// stream sync after NCCL work with a watchdog (asynchronous NCCL errors, PEEL_NCCL_TIMEOUT_S):
+// on either the communicator is aborted and PEEL_ENCCL returned; other kinds: a plain sync
+peel_status comm_sync(peel_comm *c, cudaStream_t s);
 
 // Test hook (PEEL_FAULT="rank:round"): true when this rank must fail in that round, to
 // exercise the error protocol of the partitioned calls.

@@ -673,10 +673,16 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
     auto end_round = [&](int par, ull g[4]) -> peel_status {
         if (lst != PEEL_OK) mark_fail();
         dist_pack_kernel<<<1, 32, 0, s>>>(scs, par, dsum + 8);
-        if (!c->virt && !c->host) {  // NCCL: reduce the device words in place, one copy back
+        const bool nccl = !c->virt && !c->host;
+        if (nccl) {  // NCCL: reduce the device words in place, one copy back
+            if (!c->nccl) return comm_sync(c, s);  // aborted by the watchdog
             cudaMemcpyAsync(dsum, dsum + 8, sizeof(ull) * 4, cudaMemcpyDeviceToDevice, s);
             ncclResult_t nr = ncclAllReduce(dsum, dsum, 4, ncclUint64, ncclSum, c->nccl, s);
             if (nr != ncclSuccess) { nccl_error(nr); return PEEL_ENCCL; }
+            // the watchdog sync, before the copies back: copies to pageable memory block
+            // inside the runtime until the stream drains, out of the watchdog's sight
+            const peel_status ws = comm_sync(c, s);
+            if (ws != PEEL_OK) return lst != PEEL_OK ? lst : ws;
             cudaMemcpyAsync(g, dsum, sizeof(ull) * 4, cudaMemcpyDeviceToHost, s);
         }
         if (cudaMemcpyAsync(pk.data(), dsum + 8, sizeof(ull) * 5 * sh.size(), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -781,9 +787,12 @@ static peel_status run_dist(peel_comm *c, const uint32_t *edges, uint64_t n, uin
                 sg = comm_allgather_u64(c, mine.data(), rows.data(), 9, dsum + 8, s);
             } else {
                 // NCCL: gather the device rows in place, then one copy back
-                sg = PEEL_OK;
-                ncclResult_t nr = ncclAllGather(dsum + 8 + 9 * c->rank, dsum + 8, 9, ncclUint64, c->nccl, s);
-                if (nr != ncclSuccess) { nccl_error(nr); sg = PEEL_ENCCL; }
+                sg = c->nccl ? PEEL_OK : comm_sync(c, s);  // aborted by the watchdog
+                if (sg == PEEL_OK) {
+                    ncclResult_t nr = ncclAllGather(dsum + 8 + 9 * c->rank, dsum + 8, 9, ncclUint64, c->nccl, s);
+                    if (nr != ncclSuccess) { nccl_error(nr); sg = PEEL_ENCCL; }
+                }
+                if (sg == PEEL_OK) sg = comm_sync(c, s);  // before the copy back (see end_round)
                 if (sg == PEEL_OK && (cudaMemcpyAsync(rows.data(), dsum + 8, sizeof(ull) * 9 * P, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
                                       cudaStreamSynchronize(s) != cudaSuccess)) {
                     cu(cudaGetLastError(), "rows");

@@ -377,6 +377,11 @@ static peel_status run_iblt_dist(peel_comm *c, uint64_t C, uint64_t seed, uint32
 
     std::vector<IDCtl> hc(sh.size());
     auto fetch = [&]() {
+        if (!c->virt && !c->host) {  // after NCCL work: the watchdog sync, before the copies
+            const peel_status ws = comm_sync(c, s);  // (pageable copies would block out of its sight)
+            if (ws != PEEL_OK && lst == PEEL_OK) lst = ws;
+            if (lst != PEEL_OK) return;
+        }
         for (size_t i = 0; i < sh.size(); i++)
             cu(cudaMemcpyAsync(&hc[i], sh[i].ctl, sizeof(IDCtl), cudaMemcpyDeviceToHost, s), "fetch");
         cu(cudaStreamSynchronize(s), "fetch");

@@ -106,6 +106,47 @@ def test_nccl_transport_world1():
     assert out.returncode == 0 and "NCCL_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
 
 
+NCCL_WATCHDOG = r"""
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["REPO"])
+import paper_1302_7014_b200 as pk
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%s" % os.environ["PORT"], rank=0, world_size=1,
+                        device_id=torch.device("cuda:0"))
+comm = pk.Comm.from_process_group()
+n = (1 << 24) + 12345
+e = pk.gen_hypergraph(n, int(0.75 * n), 3, 8, device=torch.device("cuda:0"))
+os.environ["PEEL_NCCL_TIMEOUT_S"] = "1e-9"  # every sync after NCCL work "times out"
+codes = []
+for _ in range(2):
+    try:
+        pk.peel_kcore_dist(comm, e, n, 2)
+        codes.append(0)
+    except pk.PeelError as ex:
+        codes.append(ex.status)
+assert codes == [pk.PEEL_ENCCL, pk.PEEL_ENCCL], codes  # aborted, and stays aborted
+del comm
+print("WATCHDOG_OK")
+"""
+
+
+def test_nccl_watchdog_aborts():
+    """The NCCL watchdog sync (comm_sync): past PEEL_NCCL_TIMEOUT_S it aborts the communicator
+    and the call fails with PEEL_ENCCL instead of hanging on a dead peer; later calls on the
+    aborted communicator fail the same way."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, REPO=repo, PORT=str(port))
+    out = subprocess.run([sys.executable, "-c", NCCL_WATCHDOG], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "WATCHDOG_OK" in out.stdout, out.stdout[-2000:] + out.stderr[-4000:]
+
+
 @pytest.mark.parametrize("P", [1, 2, 3])
 def test_binned_shard_build_vs_oracle(P):
     """Shards larger than 2^23 vertices use the binned build restricted to their endpoints
